@@ -1,0 +1,437 @@
+#!/usr/bin/env python3
+"""AES-SpMM benchmark (BASELINE.json metric: "AES-SpMM ms & achieved HBM GB/s
+(% of peak), F=128, at 1/2/4/8 B200").
+
+Workload (config "products", BASELINE configs[4]): ogbn-products-shaped
+synthetic power-law graph (2.45 M rows, ~62 M edges, alpha 1.7885, max degree
+17 481), raw adjacency (val = 1), U(-1, 1) fp32 features F = 128, adaptive
+sampling W = 32.  A step is one sampled SpMM over this rank's row shard with
+the plan prebuilt (as the reference times it: proj/src/bench.cpp:59-77).  At
+N > 1 the rows are cut into contiguous slot-balanced shards, every rank holds
+the full feature replica and computes its shard (strong scaling, no data-path
+collective inside the SpMM; `--mode layer` adds the GCN layer's GEMM and the
+NCCL all-gather of the layer output).
+
+value  = whole-job algorithmic bytes / max-over-ranks device time, GB/s
+         (8(N+1) + 8S + 4FS + 4FN per SpMM).
+e2e    = the same metric through the reference-facing C-ABI handle call
+         (aes_spmm_sampled) with pinned HOST buffers: H2D of the features and
+         D2H of the result inside the timed region.
+--impl reference: the reference's own CPU implementation (oracle/_ref, built
+from /root/reference by oracle/Makefile) with every host thread, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SHAPES = {
+    # name: (n, alpha, max_degree, F)
+    "cora": (2_708, 2.1181, 168, 16),
+    "pubmed": (19_717, 2.0321, 171, 128),
+    "arxiv": (169_343, 2.0737, 13_161, 128),
+    "reddit": (232_965, 1.2986, 21_657, 602),
+    "products": (2_450_000, 1.7885, 17_481, 128),
+}
+METRIC = "AES-SpMM ms & achieved HBM GB/s (% of peak), F=128, at 1/2/4/8 B200"
+
+
+def alg_bytes(n_rows, slots, f, elem=4):
+    return 8 * (n_rows + 1) + 8 * slots + elem * f * slots + 4 * f * n_rows
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        loaded = [s for s in sm if mx and s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def shard_bounds(srow_ptr_host, world):
+    """Contiguous row cuts with ~equal sampled slots per shard."""
+    import numpy as np
+    total = int(srow_ptr_host[-1])
+    n = srow_ptr_host.size - 1
+    cuts = [0]
+    for r in range(1, world):
+        cuts.append(int(np.searchsorted(srow_ptr_host, total * r // world, side="left")))
+    cuts.append(n)
+    for i in range(1, len(cuts)):
+        cuts[i] = max(cuts[i], cuts[i - 1])
+    return cuts
+
+
+def load_traffic(kind):
+    """dram bytes/launch of the dominant kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get(kind, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import numpy as np
+    import torch
+
+    n, alpha, maxdeg, f = SHAPES[args.config]
+    from oracle import ref as oref  # the reference CPU implementation, built from its own sources
+    if not oref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (make -C oracle ref)"}))
+        return 0
+    from paper_2503_18427_b200 import synth
+    gdev = "cuda" if torch.cuda.is_available() else "cpu"
+    rp, col, val = synth.power_law_csr(n, alpha, maxdeg, seed=args.seed, device=gdev)
+    b = synth.features(n, f, seed=5, device=gdev, ld=f)
+    rp_np = rp.cpu().numpy().view(np.uint64)
+    col_np = col.cpu().numpy().view(np.uint32)
+    val_np = val.cpu().numpy()
+    b_np = np.ascontiguousarray(b.cpu().numpy())
+    csr = oref.RefCsr.from_arrays(n, n, rp_np, col_np, val_np)
+    threads = os.cpu_count() or 1
+    strat = {"adaptive": 0, "afs": 1, "sfs": 2, "full": 3}[args.strategy]
+    plan_ms, ms, _ = oref.time_spmm_sampled(csr, b_np, args.width, strat, threads, args.warmup + args.steps)
+    timed = ms[args.warmup:]
+    chunk, cnt, _, _ = oref.build_plans(csr, args.width, strat)
+    slots = int((chunk.astype(np.uint64) * cnt.astype(np.uint64)).sum())
+    by = alg_bytes(n, slots, f)
+    t = float(np.mean(timed))
+    gbs = by / (t * 1e-3) / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config} W={args.width} {args.strategy} F={f} spmm_sampled",
+                   "n_rows": n, "nnz": int(rp_np[-1]), "slots": slots, "F": f, "width": args.width,
+                   "plan_ms": round(plan_ms, 3), "median_ms": round(float(np.median(timed)), 3)},
+        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
+                         "sample": f"full {args.config} workload, reference aes::spmm_sampled "
+                                   f"(proj/src/spmm.cpp:40-107), {threads} std::threads, prebuilt plans"},
+        "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------ our arm
+def cpu_baseline(args, rp_np, col_np, val_np, b_np, f):
+    """Reference CPU path (oracle/_ref) on a bounded row sample, all host threads."""
+    import numpy as np
+    try:
+        from oracle import ref as oref
+        if not oref.available():
+            raise ImportError
+        kind = "reference"
+    except Exception:
+        oref = None
+        kind = "port"
+    n = rp_np.size - 1
+    rows = n if kind == "reference" else min(n, 200_000)
+    sub_rp = rp_np[: rows + 1]
+    nnz = int(sub_rp[-1])
+    threads = os.cpu_count() or 1
+    strat = {"adaptive": 0, "afs": 1, "sfs": 2, "full": 3}[args.strategy]
+    if kind == "reference":
+        csr = oref.RefCsr.from_arrays(rows, n, sub_rp, col_np[:nnz], val_np[:nnz])
+        _, ms, _ = oref.time_spmm_sampled(csr, b_np, args.width, strat, threads, 3)
+        chunk, cnt, _, _ = oref.build_plans(csr, args.width, strat)
+        slots = int((chunk.astype(np.uint64) * cnt.astype(np.uint64)).sum())
+        t = float(np.median(ms))
+        sample = f"first {rows} rows of the workload, reference spmm_sampled, median of 3"
+    else:
+        from oracle import port
+        threads = 1
+        srow, scol, sval = port.sample_csr(sub_rp, col_np[:nnz], val_np[:nnz], args.width, strat)
+        t0 = time.perf_counter()
+        port.spmm_csr(srow, scol, sval, b_np)
+        t = (time.perf_counter() - t0) * 1e3
+        slots = int(srow[-1])
+        sample = f"first {rows} rows of the workload, oracle port (scalar C)"
+    gbs = alg_bytes(rows, slots, f) / (t * 1e-3) / 1e9
+    return {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": kind, "sample": sample,
+            "ms": round(t, 3)}
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2503_18427_b200 import capi, device, synth
+
+    n, alpha, maxdeg, f = SHAPES[args.config]
+    rp, col, val = synth.power_law_csr(n, alpha, maxdeg, seed=args.seed, device="cuda")
+    g = device.Graph(rp, col, val, n)
+    b = synth.features(n, f, seed=5, device="cuda")
+    strat = capi.strategy_code(args.strategy)
+    full_plan = device.SampledPlan(g, args.width, strat)
+    srow_host = full_plan.srow_ptr.cpu().numpy()
+    cuts = shard_bounds(srow_host, world)
+    lo, hi = cuts[rank], cuts[rank + 1]
+    # the shard is a view of the global sampled CSR (absolute slot offsets)
+    srow = full_plan.srow_ptr[lo:hi + 1]
+    shard_rows = hi - lo
+    shard_slots = int(srow_host[hi] - srow_host[lo])
+    stream = torch.cuda.current_stream()
+
+    quant = None
+    if args.dtype == "int8":
+        quant = device.quantize(b)
+        elem = 1
+    else:
+        elem = 4
+    out = device.empty_padded(max(shard_rows, 1), f)
+
+    layer = None
+    if args.mode == "layer":
+        w = (torch.rand(f, f, device="cuda") - 0.5)
+        bias = torch.full((f,), 0.01, device="cuda")
+        h_next = device.empty_padded(max(shard_rows, 1), f)
+        gathered = torch.empty((cuts[-1] if world == 1 else max(c1 - c0 for c0, c1 in zip(cuts, cuts[1:])) * world, f),
+                               device="cuda")
+        layer = (w, bias, h_next, gathered)
+
+    def step():
+        if quant is not None:
+            device.spmm_q8(srow, full_plan.scol, full_plan.sval, quant, out=out)
+        else:
+            device.spmm(srow, full_plan.scol, full_plan.sval, b, out=out)
+        if layer is not None:
+            w, bias, h_next, gathered = layer
+            device.gemm_bias_act(out, w, bias, True, out=h_next)
+            if world > 1:
+                mx = gathered.shape[0] // world
+                send = torch.zeros((mx, f), device="cuda")
+                send[:shard_rows].copy_(h_next[:shard_rows])
+                dist.all_gather_into_tensor(gathered, send)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.2)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    start.record(stream)
+    for _ in range(args.steps):
+        step()
+    end.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    ms_total = start.elapsed_time(end)
+    t_rank = torch.tensor([ms_total], device="cuda", dtype=torch.float64)
+    if dist:
+        dist.all_reduce(t_rank, op=dist.ReduceOp.MAX)
+    ms_step = float(t_rank.item()) / args.steps
+    total_bytes = alg_bytes(n, int(srow_host[-1]), f, elem)
+    my_bytes = alg_bytes(shard_rows, shard_slots, f, elem)
+    value = total_bytes / (ms_step * 1e-3) / 1e9
+    # kernel-level roofline for this rank (the step is the SpMM kernel alone in spmm mode)
+    k_ms = ms_total / args.steps
+    peak, peak_kind = peaks()
+    achieved = my_bytes / (k_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": load_traffic(f"spmm_{args.dtype}_{args.config}"),
+                "peak_kind": peak_kind, "alg_bytes_per_launch": my_bytes, "nominal_8000_frac": round(achieved / 8000, 4)}
+
+    # ---- e2e through the reference-facing C-ABI handle call, pinned host buffers
+    e2e = None
+    if not args.no_e2e and args.dtype == "f32":
+        e2e = run_e2e(args, rp, col, val, b, lo, hi, f, n, total_bytes, dist, world)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        b_np = np.ascontiguousarray(b.cpu().numpy())
+        cpu = cpu_baseline(args, rp.cpu().numpy().view(np.uint64), col.cpu().numpy().view(np.uint32),
+                           val.cpu().numpy(), b_np, f)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8" if args.dtype == "int8" else "f32",
+            "data": "synthetic (GPU power-law generator, seed %d; U(-1,1) features)" % args.seed,
+            "config": {"workload": f"{args.config} W={args.width} {args.strategy} F={f} sampled SpMM"
+                                   + (" + GEMM + all-gather (GCN layer)" if args.mode == "layer" else ""),
+                       "n_rows": n, "nnz": int(rp[-1].item()), "slots": int(srow_host[-1]), "F": f,
+                       "width": args.width, "mode": args.mode, "shard_rows": [c1 - c0 for c0, c1 in zip(cuts, cuts[1:])],
+                       "l2": "inputs larger than L2 (features %.2f GB, output %.2f GB vs 126 MB L2)"
+                             % (n * f * elem / 1e9, n * f * 4 / 1e9),
+                       "parallelism": f"row-sharded x{world}" if world > 1 else "single GPU"},
+            "roofline": roofline, "clocks": clocks,
+            "e2e": e2e, "cpu_baseline": cpu,
+            "gpu_launches": args.steps * (1 + (1 if args.mode == "layer" else 0)),
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, rp, col, val, b, lo, hi, f, n, total_bytes, dist, world):
+    """aes_csr_create / aes_build_plan_set once, then per step the host-buffer
+    call aes_spmm_sampled (H2D features, kernel, D2H result) — the call a
+    reference user makes (proj/bindings/module.cpp:124-131)."""
+    import numpy as np
+    import torch
+
+    from paper_2503_18427_b200 import capi
+    L = capi.lib()
+    vp, u64 = ctypes.c_void_p, ctypes.c_uint64
+    L.aes_csr_create.argtypes = [u64, u64, vp, u64, vp, vp, u64, vp]
+    L.aes_build_plan_set.argtypes = [vp, ctypes.c_uint32, ctypes.c_int, vp]
+    L.aes_spmm_sampled.argtypes = [vp, vp, u64, u64, vp, vp, vp, vp, vp]
+    L.aes_csr_destroy.argtypes = [vp]
+    L.aes_plan_destroy.argtypes = [vp]
+    rp_np = rp.cpu().numpy().view(np.uint64)
+    base = int(rp_np[lo])
+    srp = np.ascontiguousarray(rp_np[lo:hi + 1] - np.uint64(base))
+    nnz = int(srp[-1])
+    scol = np.ascontiguousarray(col.cpu().numpy().view(np.uint32)[base:base + nnz])
+    sval = np.ascontiguousarray(val.cpu().numpy()[base:base + nnz])
+    h = ctypes.c_void_p()
+    capi.check(L.aes_csr_create(hi - lo, n, srp.ctypes.data, srp.size, scol.ctypes.data, sval.ctypes.data, nnz,
+                                ctypes.byref(h)))
+    p = ctypes.c_void_p()
+    capi.check(L.aes_build_plan_set(h, args.width, capi.strategy_code(args.strategy), ctypes.byref(p)))
+    b_host = torch.empty((n, f), dtype=torch.float32).pin_memory()
+    b_host.copy_(b[:, :f])
+    c_host = torch.empty((max(hi - lo, 1), f), dtype=torch.float32).pin_memory()
+
+    def call():
+        capi.check(L.aes_spmm_sampled(h, b_host.data_ptr(), n, f, p, c_host.data_ptr(), None, None, None))
+
+    for _ in range(max(1, min(args.warmup, 3))):
+        call()
+    steps = max(1, min(args.steps, 10))
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        call()
+    t = (time.perf_counter() - t0) / steps
+    tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t = float(tt.item())
+    L.aes_plan_destroy(p)
+    L.aes_csr_destroy(h)
+    return {"value": round(total_bytes / t / 1e9, 3), "unit": "GB/s", "ms_per_step": round(t * 1e3, 3),
+            "h2d_bytes_per_step": n * f * 4, "d2h_bytes_per_step": (hi - lo) * f * 4,
+            "path": "C-ABI aes_spmm_sampled, pinned host buffers, steps=%d" % steps}
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=list(SHAPES), default="products")
+    ap.add_argument("--width", type=int, default=32)
+    ap.add_argument("--strategy", default="adaptive", choices=["adaptive", "afs", "sfs", "full"])
+    ap.add_argument("--dtype", default="f32", choices=["f32", "int8"])
+    ap.add_argument("--mode", default="spmm", choices=["spmm", "layer"])
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = max(args.warmup, 1)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

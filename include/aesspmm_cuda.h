@@ -1,0 +1,239 @@
+/*
+ * aesspmm_cuda.h — the C-ABI boundary of the B200-native AES-SpMM path.
+ *
+ * Implemented by paper_2503_18427_b200/libaescuda.so (hand-written sm_100a
+ * CUDA; no CPU fallback).  Plain pointers and sizes only: no C++ or torch
+ * types cross this boundary.  Every function returns an aes_status (0 = OK);
+ * aes_last_error() gives the message for the calling thread, using the
+ * reference's exception strings so a binding can re-raise them verbatim
+ * ("ZeroWidth", "ShapeMismatch", "PlanMatrixMismatch", "EmptyMatrix",
+ * "NonFinite", "invalid QuantParams", "bits must be 1..16",
+ * "<CsrError> at row <i>" — proj/src/{sampling,spmm,quantize,matrix}.cpp).
+ *
+ * Two tiers:
+ *   1. Handle API (host buffers in, host buffers out).  These are exactly the
+ *      entry points the reference's FFI binds — proj/bindings/module.cpp:52-144
+ *      — so a pybind11 / ctypes / cgo binding maps 1:1 onto them.  Objects
+ *      (CSR, plan set, quantized features) live in HBM behind opaque handles.
+ *   2. Device API (device pointers + a cudaStream_t passed as void*).  Used by
+ *      the handle tier, the benchmark and the multi-GPU layer driver; it never
+ *      synchronises the stream and never allocates unless it says so.
+ *
+ * Strategy values follow the reference enum order
+ * (proj/include/aesspmm/sampling.hpp:14).
+ */
+#ifndef AESSPMM_CUDA_H
+#define AESSPMM_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AES_API __attribute__((visibility("default")))
+
+typedef enum {
+    AES_OK = 0,
+    AES_ERR_ZERO_WIDTH = 1,      /* "ZeroWidth"              sampling.cpp:30,63,106 */
+    AES_ERR_SHAPE = 2,           /* "ShapeMismatch"          spmm.cpp:13, gnn.cpp:13,44 */
+    AES_ERR_PLAN_MISMATCH = 3,   /* "PlanMatrixMismatch"     spmm.cpp:44-46 */
+    AES_ERR_EMPTY = 4,           /* "EmptyMatrix"            quantize.cpp:12 */
+    AES_ERR_NONFINITE = 5,       /* "NonFinite"              quantize.cpp:16 */
+    AES_ERR_QPARAMS = 6,         /* "invalid QuantParams"    quantize.cpp:24-26 */
+    AES_ERR_BITS = 7,            /* "bits must be 1..16"     quantize.cpp:13 */
+    AES_ERR_CSR_INVALID = 8,     /* ValidationResult::message()  matrix.cpp:11-26 */
+    AES_ERR_INVALID_ARG = 9,     /* null handle / bad argument */
+    AES_ERR_CUDA = 10,           /* CUDA runtime error (message has details) */
+    AES_ERR_UNSUPPORTED = 11,    /* layout the kernels do not take */
+    AES_ERR_NOT_SQUARE = 12      /* "NotSquare"              matrix.cpp:131 */
+} aes_status;
+
+typedef enum { AES_ADAPTIVE = 0, AES_AFS = 1, AES_SFS = 2, AES_FULL = 3 } aes_strategy;
+
+/* CsrError codes of proj/include/aesspmm/matrix.hpp:44-51. */
+typedef enum {
+    AES_CSR_OK = 0, AES_CSR_NON_MONOTONIC = 1, AES_CSR_COL_OUT_OF_RANGE = 2,
+    AES_CSR_UNSORTED = 3, AES_CSR_LENGTH_MISMATCH = 4, AES_CSR_NOT_SQUARE = 5
+} aes_csr_error;
+
+AES_API const char* aes_last_error(void);
+AES_API const char* aes_status_name(int status);
+AES_API int aes_version(void);
+
+/* ======================================================================
+ * Scalar formulas (host-callable; the same __host__ __device__ code the
+ * kernels run).
+ * ====================================================================== */
+
+/* select_strategy — proj/include/aesspmm/sampling.hpp:61, sampling.cpp:29-54 */
+AES_API int aes_select_strategy(uint64_t row_nnz, uint32_t width, uint32_t* chunk_len,
+                                uint32_t* sample_cnt);
+/* hash_start — sampling.hpp:64-65, sampling.cpp:56-60 */
+AES_API uint32_t aes_hash_start(uint32_t current_ind, uint64_t row_nnz, uint32_t chunk_len);
+
+/* ======================================================================
+ * Tier 1: handle API (host buffers) — mirrors proj/bindings/module.cpp
+ * ====================================================================== */
+
+typedef struct aes_csr_s* aes_csr_t;      /* CsrMatrix resident in HBM */
+typedef struct aes_plan_s* aes_plan_t;    /* SamplePlanSet resident in HBM */
+typedef struct aes_qfeat_s* aes_qfeat_t;  /* QuantizedFeatures resident in HBM */
+
+/* CsrMatrix(n_rows, n_cols, row_ptr, col_ind, val) with validate_csr —
+ * module.cpp:17-33 (copies in, validates on the GPU; on failure returns
+ * AES_ERR_CSR_INVALID with ValidationResult::message()).  row_ptr_len,
+ * nnz_len are the host array lengths (the reference checks them). */
+AES_API int aes_csr_create(uint64_t n_rows, uint64_t n_cols, const uint64_t* row_ptr,
+                           uint64_t row_ptr_len, const uint32_t* col_ind, const float* val,
+                           uint64_t nnz_len, aes_csr_t* out);
+/* Same, without validation, from DEVICE arrays that stay owned by the caller
+ * (no copy).  Used by the device tier / layer driver. */
+AES_API int aes_csr_wrap_device(uint64_t n_rows, uint64_t n_cols, const uint64_t* d_row_ptr,
+                                const uint32_t* d_col_ind, const float* d_val, uint64_t nnz,
+                                aes_csr_t* out);
+AES_API int aes_csr_destroy(aes_csr_t a);
+AES_API int aes_csr_shape(aes_csr_t a, uint64_t* n_rows, uint64_t* n_cols, uint64_t* nnz);
+/* Device views of the CSR arrays (for zero-copy interop). */
+AES_API int aes_csr_device_ptrs(aes_csr_t a, const uint64_t** row_ptr, const uint32_t** col_ind,
+                                const float** val);
+/* Copy the CSR back to host arrays (sizes n_rows+1 and nnz). */
+AES_API int aes_csr_download(aes_csr_t a, uint64_t* row_ptr, uint32_t* col_ind, float* val);
+/* row_stats — matrix.hpp:82, matrix.cpp:54-63 (row_nnz may be NULL). */
+AES_API int aes_csr_row_stats(aes_csr_t a, uint64_t* row_nnz, uint64_t* max_row_nnz,
+                              double* avg_degree);
+/* gcn_normalize(a, add_self_loops) — matrix.hpp:76, matrix.cpp:130-144 */
+AES_API int aes_gcn_normalize(aes_csr_t a, int add_self_loops, aes_csr_t* out);
+
+/* build_plan_set(matrix, width, strategy) — sampling.hpp:70-72,
+ * sampling.cpp:104-118, module.cpp:107-108.  Builds the per-row plan and the
+ * sampled CSR (slot order) in HBM. */
+AES_API int aes_build_plan_set(aes_csr_t a, uint32_t width, int strategy, aes_plan_t* out);
+AES_API int aes_plan_destroy(aes_plan_t p);
+AES_API int aes_plan_info(aes_plan_t p, uint32_t* width, int* strategy, uint64_t* n_rows,
+                          uint64_t* total_slots, uint64_t* total_starts);
+/* Export SamplePlanSet::plans (module.cpp:78-81) as flat host arrays:
+ * chunk_len[n], sample_cnt[n], starts_ptr[n+1], starts[total_starts]. */
+AES_API int aes_plan_export(aes_plan_t p, uint32_t* chunk_len, uint32_t* sample_cnt,
+                            uint64_t* starts_ptr, uint32_t* starts);
+/* Sampled CSR device views (srow_ptr n+1 u64, scol/sval total_slots). */
+AES_API int aes_plan_device_ptrs(aes_plan_t p, const uint64_t** srow_ptr, const uint32_t** scol,
+                                 const float** sval);
+/* Copy the sampled CSR (srow_ptr n+1, scol/sval total_slots) to host. */
+AES_API int aes_plan_download(aes_plan_t p, uint64_t* srow_ptr, uint32_t* scol, float* sval);
+/* sampling_rate(plans, row_stats(matrix)) — sampling.cpp:120-152,
+ * module.cpp:109-116.  per_row (n doubles) may be NULL. */
+AES_API int aes_sampling_rate(aes_plan_t p, aes_csr_t a, double* aggregate,
+                              double* unique_coverage, double* per_row);
+
+/* spmm_exact(a, b) — spmm.hpp:19-20, spmm.cpp:18-36, module.cpp:118-123.
+ * b: host row-major b_rows x f; c: host row-major a.n_rows x f. */
+AES_API int aes_spmm_exact(aes_csr_t a, const float* b, uint64_t b_rows, uint64_t f, float* c);
+/* spmm_sampled(a, b, plans) — spmm.hpp:25-26, spmm.cpp:40-107, module.cpp:124-131.
+ * fma/loads counters (spmm_sampled_instrumented, spmm.cpp:109-114) may be NULL. */
+AES_API int aes_spmm_sampled(aes_csr_t a, const float* b, uint64_t b_rows, uint64_t f,
+                             aes_plan_t p, float* c, uint64_t* fma_count, uint64_t* loads_a,
+                             uint64_t* loads_b);
+
+/* quantize(x, bits) = quantize(x, fit_params(x, bits)) — module.cpp:133-139,
+ * quantize.cpp:11-51.  x: host rows x cols f32. */
+AES_API int aes_quantize(const float* x, uint64_t rows, uint64_t cols, uint32_t bits,
+                         aes_qfeat_t* out);
+/* quantize(x, p) with explicit params — quantize.hpp:31 */
+AES_API int aes_quantize_with(const float* x, uint64_t rows, uint64_t cols, float x_min,
+                              float x_max, uint32_t bits, aes_qfeat_t* out);
+/* QuantizedFeatures from host uint16 codes (quantize.hpp:20-25). */
+AES_API int aes_qfeat_from_codes(const uint16_t* codes, uint64_t rows, uint64_t cols,
+                                 float x_min, float x_max, uint32_t bits, aes_qfeat_t* out);
+AES_API int aes_qfeat_destroy(aes_qfeat_t q);
+AES_API int aes_qfeat_info(aes_qfeat_t q, uint64_t* rows, uint64_t* cols, float* x_min,
+                           float* x_max, uint32_t* bits);
+/* codes as uint16 (the reference's in-memory type, module.cpp:96-101). */
+AES_API int aes_qfeat_codes(aes_qfeat_t q, uint16_t* codes);
+/* dequantize(qf) — quantize.hpp:34, quantize.cpp:53-64, module.cpp:140-143 */
+AES_API int aes_dequantize(aes_qfeat_t q, float* x);
+/* spmm_sampled(a, dequantize(q), plans) with the dequantization fused into
+ * the gather (int8 feature bytes).  plans == NULL -> exact (spmm_exact). */
+AES_API int aes_spmm_sampled_q8(aes_csr_t a, aes_qfeat_t q, aes_plan_t p, float* c);
+
+/* dense_matmul(a, b) — gnn.hpp:64, gnn.cpp:11-31 (host buffers). */
+AES_API int aes_dense_matmul(const float* a, uint64_t m, uint64_t k, const float* b, uint64_t n,
+                             float* c);
+/* gcn_forward(adj, features, model, plans) — gnn.hpp:37-40, gnn.cpp:66-78.
+ * dims[0..n_layers]; weights/biases concatenated per layer (bias_len[l] is
+ * 0 or dims[l+1]); p == NULL -> exact aggregation. */
+AES_API int aes_gcn_forward(aes_csr_t adj, const float* x, const uint64_t* dims, int n_layers,
+                            const float* weights, const float* biases, const uint64_t* bias_len,
+                            aes_plan_t p, float* out);
+
+/* ======================================================================
+ * Tier 2: device API (device pointers, caller's stream, no sync)
+ * ====================================================================== */
+
+/* Workspace bytes for aes_dev_sample_plan / aes_dev_fit_params over n items. */
+AES_API size_t aes_dev_scan_workspace_bytes(uint64_t n_rows);
+
+/* Sampler pass 1: per-row (chunk, cnt) and the sampled row pointer
+ * srow_ptr[n+1] = exclusive scan of chunk*cnt (single-pass decoupled
+ * look-back).  plan_row_ptr supplies row_nnz.  row_params (n x uint2
+ * {chunk, cnt}) may be NULL.  Reference: sampling.cpp:29-118. */
+AES_API int aes_dev_sample_plan(const uint64_t* plan_row_ptr, uint64_t n_rows, uint32_t width,
+                                int strategy, uint64_t* srow_ptr, uint32_t* row_params,
+                                void* workspace, size_t workspace_bytes, void* stream);
+/* Sampler pass 2: sampled col/val in slot order: slot s + j*cnt of row i
+ * <- nonzero row_ptr[i] + start_s + j (spmm.cpp:54-76).  Windows come from
+ * plan_row_ptr's row lengths; bases from row_ptr (equal pointers in the
+ * usual case). */
+AES_API int aes_dev_sample_fill(const uint64_t* plan_row_ptr, const uint64_t* row_ptr,
+                                const uint32_t* col_ind, const float* val, uint64_t n_rows,
+                                uint32_t width, int strategy, const uint64_t* srow_ptr,
+                                uint32_t* scol, float* sval, void* stream);
+
+/* C[i, 0:f] = sum over k in [srow_ptr[i], srow_ptr[i+1]) ascending of
+ * sval[k] * B[scol[k], 0:f], rounded as RN(acc + RN(v*b)) — bit-exact with
+ * spmm.cpp:77-84.  Every row of C (0:f) is written (zeros for empty rows).
+ * Vector path needs ldb, ldc % 4 == 0 and 16-B aligned B, C; the kernel
+ * then also writes C columns f..round_up(f,4) (zeros when B's pad is 0).
+ * `row_begin` offsets the row range (sharded drivers): rows
+ * [row_begin, row_begin + n_rows) of the CSR are computed into C rows
+ * [0, n_rows). */
+AES_API int aes_dev_spmm_f32(const uint64_t* srow_ptr, const uint32_t* scol, const float* sval,
+                             uint64_t n_rows, const float* b, uint64_t ldb, uint64_t f, float* c,
+                             uint64_t ldc, void* stream);
+
+/* Int8 variant: Q is u8 codes (ldq bytes per row), lut[256] the exact
+ * dequantized value of each code (aes_dev_dequant_lut).  Result is
+ * bit-identical to aes_dev_spmm_f32 over dequantize(Q). */
+AES_API int aes_dev_spmm_q8(const uint64_t* srow_ptr, const uint32_t* scol, const float* sval,
+                            uint64_t n_rows, const uint8_t* q, uint64_t ldq, uint64_t f,
+                            const float* lut, float* c, uint64_t ldc, void* stream);
+
+/* fit_params: result[0] = x_min, result[1] = x_max (first-occurrence
+ * semantics of quantize.cpp:14-19), ((uint32_t*)result)[2] = 1 when a
+ * non-finite element was seen.  Deterministic two-level reduction. */
+AES_API int aes_dev_fit_params(const float* x, uint64_t n, float* result, void* workspace,
+                               size_t workspace_bytes, void* stream);
+/* codes = quantize(x, {lo, hi, bits}) — quantize.cpp:23-51 (fp64, no
+ * contraction).  Codes are u8 when bits <= 8 else u16; rows x cols with row
+ * strides ldx (floats) and ldq (codes). */
+AES_API int aes_dev_quantize(const float* x, uint64_t rows, uint64_t cols, uint64_t ldx, float lo,
+                             float hi, uint32_t bits, void* codes, uint64_t ldq, void* stream);
+/* x = dequantize(codes) — quantize.cpp:53-64 */
+AES_API int aes_dev_dequantize(const void* codes, uint64_t rows, uint64_t cols, uint64_t ldq,
+                               float lo, float hi, uint32_t bits, float* x, uint64_t ldx,
+                               void* stream);
+/* lut[q] = float(double(q) * step + double(lo)) for q < 2^bits (bits <= 8). */
+AES_API int aes_dev_dequant_lut(float lo, float hi, uint32_t bits, float* lut, void* stream);
+
+/* H = act(A @ W + bias): k-ascending, separate mul/add roundings, zero
+ * entries of A skipped (gnn.cpp:11-31), bias (may be NULL) then ReLU
+ * max(v, 0) when relu != 0 (gnn.cpp:41-52). */
+AES_API int aes_dev_gemm_bias_act(const float* a, uint64_t m, uint64_t k, uint64_t lda,
+                                  const float* w, uint64_t n, uint64_t ldw, const float* bias,
+                                  int relu, float* h, uint64_t ldh, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AESSPMM_CUDA_H */

@@ -1,0 +1,91 @@
+"""ctypes binding of the device tier of the C ABI (include/aesspmm_cuda.h).
+
+This is the binding a maintainer would add on the reference side for a
+zero-copy, device-resident path: plain pointers + a cudaStream_t.  Tensors are
+torch CUDA tensors used only as device-memory plumbing; every arithmetic step
+runs in libaescuda.so.  Nothing here falls back to the CPU: if the library or
+a GPU is missing, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libaescuda.so")
+
+ADAPTIVE, AFS, SFS, FULL = 0, 1, 2, 3
+_STRATEGIES = {"adaptive": ADAPTIVE, "afs": AFS, "sfs": SFS, "full": FULL}
+
+
+class AesError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(msg)
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    """Load libaescuda.so (raises if it was not built — no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        u64, u32, i32, vp, f32, sz = C.c_uint64, C.c_uint32, C.c_int, C.c_void_p, C.c_float, C.c_size_t
+        L.aes_last_error.restype = C.c_char_p
+        L.aes_status_name.restype = C.c_char_p
+        L.aes_status_name.argtypes = [i32]
+        L.aes_dev_scan_workspace_bytes.restype = sz
+        L.aes_dev_scan_workspace_bytes.argtypes = [u64]
+        L.aes_dev_sample_plan.argtypes = [vp, u64, u32, i32, vp, vp, vp, sz, vp]
+        L.aes_dev_sample_fill.argtypes = [vp, vp, vp, vp, u64, u32, i32, vp, vp, vp, vp]
+        L.aes_dev_spmm_f32.argtypes = [vp, vp, vp, u64, vp, u64, u64, vp, u64, vp]
+        L.aes_dev_spmm_q8.argtypes = [vp, vp, vp, u64, vp, u64, u64, vp, vp, u64, vp]
+        L.aes_dev_fit_params.argtypes = [vp, u64, vp, vp, sz, vp]
+        L.aes_dev_quantize.argtypes = [vp, u64, u64, u64, f32, f32, u32, vp, u64, vp]
+        L.aes_dev_dequantize.argtypes = [vp, u64, u64, u64, f32, f32, u32, vp, u64, vp]
+        L.aes_dev_dequant_lut.argtypes = [f32, f32, u32, vp, vp]
+        L.aes_dev_gemm_bias_act.argtypes = [vp, u64, u64, u64, vp, u64, u64, vp, i32, vp, u64, vp]
+        L.aes_select_strategy.argtypes = [u64, u32, vp, vp]
+        L.aes_hash_start.argtypes = [u32, u64, u32]
+        L.aes_hash_start.restype = u32
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        L = lib()
+        raise AesError(rc, L.aes_last_error().decode() or L.aes_status_name(rc).decode())
+
+
+def strategy_code(s) -> int:
+    if isinstance(s, str):
+        return _STRATEGIES[s.lower()]
+    if hasattr(s, "value"):
+        return int(s.value)
+    return int(s)
+
+
+def ptr(t) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+def stream_of(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def exported_symbols():
+    """Names declared AES_API in include/aesspmm_cuda.h."""
+    import re
+
+    hdr = os.path.join(os.path.dirname(_PKG), "include", "aesspmm_cuda.h")
+    with open(hdr) as f:
+        text = f.read()
+    return re.findall(r"AES_API\s+[\w\s\*]+?\b(aes_\w+)\s*\(", text)

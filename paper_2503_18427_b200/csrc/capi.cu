@@ -1,0 +1,871 @@
+// Handle tier of the C ABI (include/aesspmm_cuda.h): the entry points the
+// reference's FFI binds (proj/bindings/module.cpp:52-144), backed by HBM-
+// resident objects and the sm_100a kernels.  Host buffers in, host buffers out;
+// every call is synchronous on the library stream, like the reference call it
+// replaces.  No CPU fallback: every arithmetic step runs in a kernel.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace aes {
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int status, const std::string& msg) {
+    g_err = msg;
+    return status;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+    g_err = std::string("CUDA error: ") + cudaGetErrorString(e) + " at " + where;
+    return AES_ERR_CUDA;
+}
+
+// launchers defined in other translation units
+int launch_sample_fill(const uint64_t*, const uint64_t*, const uint32_t*, const float*, uint64_t, uint32_t, int,
+                       const uint64_t*, uint32_t*, float*, cudaStream_t);
+int launch_plan_export(const uint64_t*, uint64_t, uint32_t, int, const uint64_t*, uint32_t*, uint32_t*,
+                       uint32_t*, cudaStream_t);
+int launch_sampling_rate(const uint64_t*, uint64_t, uint32_t, int, double*, unsigned long long*,
+                         cudaStream_t);
+int launch_row_stats(const uint64_t*, uint64_t, uint64_t*, unsigned long long*, cudaStream_t);
+int launch_validate(const uint64_t*, const uint32_t*, uint64_t, uint64_t, unsigned long long*, cudaStream_t);
+int launch_validate_rows(const uint64_t*, const uint32_t*, uint64_t, uint64_t, unsigned long long*,
+                         cudaStream_t);
+int launch_gcn_normalize(const uint64_t*, const uint32_t*, uint64_t, int, const uint64_t*, float*, uint32_t*,
+                         float*, cudaStream_t);
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// library stream + stream-ordered device buffers
+// ---------------------------------------------------------------------------
+cudaStream_t lib_stream() {
+    static std::once_flag once;
+    static cudaStream_t s = nullptr;
+    std::call_once(once, [] { cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking); });
+    return s;
+}
+
+template <typename T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { reset(); }
+    int alloc(size_t count) {
+        reset();
+        n = count;
+        if (count == 0) return AES_OK;
+        AES_CUDA_TRY(cudaMallocAsync((void**)&p, count * sizeof(T), lib_stream()));
+        return AES_OK;
+    }
+    void reset() {
+        if (p) cudaFreeAsync(p, lib_stream());
+        p = nullptr;
+        n = 0;
+    }
+    T* release() {
+        T* r = p;
+        p = nullptr;
+        n = 0;
+        return r;
+    }
+};
+
+int sync() {
+    AES_CUDA_TRY(cudaStreamSynchronize(lib_stream()));
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
+uint64_t round4(uint64_t x) { return (x + 3) & ~3ull; }
+
+// Upload a host row-major rows x cols f32 matrix into a device buffer with
+// ld = round4(cols), pad columns zeroed (the vector kernels read them).
+int upload_dense(const float* h, uint64_t rows, uint64_t cols, DBuf<float>& d, uint64_t& ld) {
+    ld = round4(cols ? cols : 1);
+    AES_TRY(d.alloc(rows * ld));
+    if (rows == 0) return AES_OK;
+    cudaStream_t st = lib_stream();
+    if (ld != cols) AES_CUDA_TRY(cudaMemsetAsync(d.p, 0, rows * ld * sizeof(float), st));
+    if (cols)
+        AES_CUDA_TRY(cudaMemcpy2DAsync(d.p, ld * sizeof(float), h, cols * sizeof(float), cols * sizeof(float),
+                                       rows, cudaMemcpyHostToDevice, st));
+    return AES_OK;
+}
+
+int download_dense(const float* d, uint64_t ld, uint64_t rows, uint64_t cols, float* h) {
+    if (rows == 0 || cols == 0) return AES_OK;
+    AES_CUDA_TRY(cudaMemcpy2DAsync(h, cols * sizeof(float), d, ld * sizeof(float), cols * sizeof(float), rows,
+                                   cudaMemcpyDeviceToHost, lib_stream()));
+    return AES_OK;
+}
+
+template <typename T>
+int d2h_scalar(const T* d, T* h) {
+    AES_CUDA_TRY(cudaMemcpyAsync(h, d, sizeof(T), cudaMemcpyDeviceToHost, lib_stream()));
+    return sync();
+}
+
+__global__ void widen_u8_kernel(const uint8_t* __restrict__ in, uint64_t rows, uint64_t cols, uint64_t ld,
+                                uint16_t* __restrict__ out) {
+    const uint64_t total = rows * cols;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t r = e / cols, c = e - r * cols;
+        out[e] = in[r * ld + c];
+    }
+}
+
+// narrow u16 codes to u8 (ld), flagging any code > 255
+__global__ void narrow_u16_kernel(const uint16_t* __restrict__ in, uint64_t rows, uint64_t cols, uint64_t ld,
+                                  uint8_t* __restrict__ out, unsigned int* __restrict__ overflow) {
+    const uint64_t total = rows * cols;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t r = e / cols, c = e - r * cols;
+        uint16_t v = in[e];
+        if (v > 255) atomicOr(overflow, 1u);
+        out[r * ld + c] = (uint8_t)v;
+    }
+}
+
+}  // namespace
+}  // namespace aes
+
+// ===========================================================================
+// handle objects
+// ===========================================================================
+struct aes_csr_s {
+    uint64_t n_rows = 0, n_cols = 0, nnz = 0;
+    uint64_t* row_ptr = nullptr;
+    uint32_t* col = nullptr;
+    float* val = nullptr;
+    bool owned = true;
+    std::atomic<int> refs{1};
+};
+
+struct aes_plan_s {
+    uint32_t width = 0;
+    int strategy = 0;
+    uint64_t n_rows = 0, total_slots = 0;
+    aes_csr_s* src = nullptr;  // holds a reference
+    uint64_t* srow_ptr = nullptr;
+    uint32_t* scol = nullptr;
+    float* sval = nullptr;
+};
+
+struct aes_qfeat_s {
+    uint64_t rows = 0, cols = 0, ld = 0;  // ld in codes
+    float x_min = 0.f, x_max = 0.f;
+    uint32_t bits = 8;
+    bool u8 = true;       // codes stored as u8 (bits <= 8 and all codes <= 255)
+    void* codes = nullptr;
+    float* lut = nullptr;  // 256 floats when u8
+};
+
+namespace {
+using namespace aes;
+
+void csr_release(aes_csr_s* a) {
+    if (a && a->refs.fetch_sub(1) == 1) {
+        if (a->owned) {
+            cudaStream_t st = lib_stream();
+            if (a->row_ptr) cudaFreeAsync(a->row_ptr, st);
+            if (a->col) cudaFreeAsync(a->col, st);
+            if (a->val) cudaFreeAsync(a->val, st);
+        }
+        delete a;
+    }
+}
+
+const char* csr_error_name(int e) {
+    switch (e) {
+        case AES_CSR_NON_MONOTONIC: return "NonMonotonicRowPtr";
+        case AES_CSR_COL_OUT_OF_RANGE: return "ColumnOutOfRange";
+        case AES_CSR_UNSORTED: return "UnsortedRow";
+        case AES_CSR_LENGTH_MISMATCH: return "LengthMismatch";
+        case AES_CSR_NOT_SQUARE: return "NotSquare";
+        default: return "ok";
+    }
+}
+
+// validate_csr (matrix.cpp:28-52) with the reference's check order.
+int validate_device(const aes_csr_s* a, uint64_t row_ptr_len, uint64_t nnz_len, uint64_t first_row_ptr) {
+    if (row_ptr_len != a->n_rows + 1 || row_ptr_len == 0 || first_row_ptr != 0)
+        return fail(AES_ERR_CSR_INVALID, "LengthMismatch");
+    DBuf<unsigned long long> scratch;
+    AES_TRY(scratch.alloc(2));
+    cudaStream_t st = lib_stream();
+    AES_TRY(launch_validate(a->row_ptr, a->col, a->n_rows, a->n_cols, scratch.p, st));
+    unsigned long long first_bad = 0;
+    AES_TRY(d2h_scalar(scratch.p, &first_bad));
+    if (first_bad != ~0ull)
+        return fail(AES_ERR_CSR_INVALID, std::string("NonMonotonicRowPtr at row ") + std::to_string(first_bad));
+    uint64_t back = 0;
+    AES_TRY(d2h_scalar(a->row_ptr + a->n_rows, &back));
+    if (back != nnz_len) return fail(AES_ERR_CSR_INVALID, "LengthMismatch");
+    AES_TRY(launch_validate_rows(a->row_ptr, a->col, a->n_rows, a->n_cols, scratch.p + 1, st));
+    unsigned long long code = 0;
+    AES_TRY(d2h_scalar(scratch.p + 1, &code));
+    if (code != ~0ull) {
+        uint64_t row = code >> 2;
+        return fail(AES_ERR_CSR_INVALID,
+                    std::string(csr_error_name((int)(code & 3))) + " at row " + std::to_string(row));
+    }
+    return AES_OK;
+}
+
+// spmm over a device CSR (original or sampled) with host dense operands.
+int spmm_host(const uint64_t* rp, const uint32_t* col, const float* val, uint64_t n_rows, const float* b,
+              uint64_t b_rows, uint64_t f, float* c) {
+    if (n_rows == 0 || f == 0) return AES_OK;
+    DBuf<float> db, dc;
+    uint64_t ldb = 0;
+    AES_TRY(upload_dense(b, b_rows, f, db, ldb));
+    const uint64_t ldc = ldb;
+    AES_TRY(dc.alloc(n_rows * ldc));
+    AES_TRY(aes_dev_spmm_f32(rp, col, val, n_rows, db.p, ldb, f, dc.p, ldc, lib_stream()));
+    AES_TRY(download_dense(dc.p, ldc, n_rows, f, c));
+    return sync();
+}
+
+// Sampled CSR for (plan, matrix): the plan's own arrays when `a` is the
+// matrix it was built on; otherwise re-filled from `a` with the plan's windows
+// (spmm.cpp:44-76 fills per call from whatever matrix it is given).
+int sampled_for(aes_plan_t p, aes_csr_t a, DBuf<uint32_t>& tcol, DBuf<float>& tval, const uint32_t** scol,
+                const float** sval) {
+    if (a == p->src) {
+        *scol = p->scol;
+        *sval = p->sval;
+        return AES_OK;
+    }
+    AES_TRY(tcol.alloc(p->total_slots));
+    AES_TRY(tval.alloc(p->total_slots));
+    AES_TRY(launch_sample_fill(p->src->row_ptr, a->row_ptr, a->col, a->val, a->n_rows, p->width, p->strategy,
+                               p->srow_ptr, tcol.p, tval.p, lib_stream()));
+    *scol = tcol.p;
+    *sval = tval.p;
+    return AES_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI — handle tier
+// ===========================================================================
+extern "C" {
+
+const char* aes_last_error(void) { return aes::g_err.c_str(); }
+
+const char* aes_status_name(int s) {
+    switch (s) {
+        case AES_OK: return "OK";
+        case AES_ERR_ZERO_WIDTH: return "ZeroWidth";
+        case AES_ERR_SHAPE: return "ShapeMismatch";
+        case AES_ERR_PLAN_MISMATCH: return "PlanMatrixMismatch";
+        case AES_ERR_EMPTY: return "EmptyMatrix";
+        case AES_ERR_NONFINITE: return "NonFinite";
+        case AES_ERR_QPARAMS: return "invalid QuantParams";
+        case AES_ERR_BITS: return "bits must be 1..16";
+        case AES_ERR_CSR_INVALID: return "InvalidCsr";
+        case AES_ERR_INVALID_ARG: return "InvalidArgument";
+        case AES_ERR_CUDA: return "CudaError";
+        case AES_ERR_UNSUPPORTED: return "Unsupported";
+        case AES_ERR_NOT_SQUARE: return "NotSquare";
+        default: return "Unknown";
+    }
+}
+
+int aes_version(void) { return 1; }
+
+int aes_select_strategy(uint64_t row_nnz, uint32_t width, uint32_t* chunk_len, uint32_t* sample_cnt) {
+    if (width == 0) return fail(AES_ERR_ZERO_WIDTH, "ZeroWidth");
+    aes::RowParams p = aes::select_strategy(row_nnz, width);
+    *chunk_len = p.chunk;
+    *sample_cnt = p.cnt;
+    return AES_OK;
+}
+
+uint32_t aes_hash_start(uint32_t current_ind, uint64_t row_nnz, uint32_t chunk_len) {
+    return aes::hash_start(current_ind, row_nnz, chunk_len);
+}
+
+// ---- CSR ------------------------------------------------------------------
+int aes_csr_create(uint64_t n_rows, uint64_t n_cols, const uint64_t* row_ptr, uint64_t row_ptr_len,
+                   const uint32_t* col_ind, const float* val, uint64_t nnz_len, aes_csr_t* out) {
+    if (!out) return fail(AES_ERR_INVALID_ARG, "null out");
+    *out = nullptr;
+    // The reference's ctor checks sizes before anything else.
+    if (row_ptr_len != n_rows + 1 || row_ptr_len == 0) return fail(AES_ERR_CSR_INVALID, "LengthMismatch");
+    if (row_ptr[0] != 0) return fail(AES_ERR_CSR_INVALID, "LengthMismatch");
+    auto* a = new aes_csr_s;
+    a->n_rows = n_rows;
+    a->n_cols = n_cols;
+    a->nnz = nnz_len;
+    cudaStream_t st = lib_stream();
+    DBuf<uint64_t> rp;
+    DBuf<uint32_t> ci;
+    DBuf<float> vv;
+    int s = rp.alloc(n_rows + 1);
+    if (!s) s = ci.alloc(nnz_len ? nnz_len : 1);
+    if (!s) s = vv.alloc(nnz_len ? nnz_len : 1);
+    if (!s && cudaMemcpyAsync(rp.p, row_ptr, (n_rows + 1) * 8, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        s = fail(AES_ERR_CUDA, "row_ptr upload failed");
+    if (!s && nnz_len) {
+        if (cudaMemcpyAsync(ci.p, col_ind, nnz_len * 4, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+            cudaMemcpyAsync(vv.p, val, nnz_len * 4, cudaMemcpyHostToDevice, st) != cudaSuccess)
+            s = fail(AES_ERR_CUDA, "csr upload failed");
+    }
+    a->row_ptr = rp.p;
+    a->col = ci.p;
+    a->val = vv.p;
+    if (!s) s = validate_device(a, row_ptr_len, nnz_len, row_ptr[0]);
+    if (s) {
+        a->row_ptr = nullptr; a->col = nullptr; a->val = nullptr;
+        delete a;
+        sync();
+        return s;
+    }
+    rp.release();
+    ci.release();
+    vv.release();
+    *out = a;
+    return AES_OK;
+}
+
+int aes_csr_wrap_device(uint64_t n_rows, uint64_t n_cols, const uint64_t* d_row_ptr, const uint32_t* d_col_ind,
+                        const float* d_val, uint64_t nnz, aes_csr_t* out) {
+    if (!out || !d_row_ptr) return fail(AES_ERR_INVALID_ARG, "null argument");
+    auto* a = new aes_csr_s;
+    a->n_rows = n_rows;
+    a->n_cols = n_cols;
+    a->nnz = nnz;
+    a->row_ptr = const_cast<uint64_t*>(d_row_ptr);
+    a->col = const_cast<uint32_t*>(d_col_ind);
+    a->val = const_cast<float*>(d_val);
+    a->owned = false;
+    *out = a;
+    return AES_OK;
+}
+
+int aes_csr_destroy(aes_csr_t a) {
+    csr_release(a);
+    return AES_OK;
+}
+
+int aes_csr_shape(aes_csr_t a, uint64_t* n_rows, uint64_t* n_cols, uint64_t* nnz) {
+    if (!a) return fail(AES_ERR_INVALID_ARG, "null csr");
+    if (n_rows) *n_rows = a->n_rows;
+    if (n_cols) *n_cols = a->n_cols;
+    if (nnz) *nnz = a->nnz;
+    return AES_OK;
+}
+
+int aes_csr_device_ptrs(aes_csr_t a, const uint64_t** row_ptr, const uint32_t** col_ind, const float** val) {
+    if (!a) return fail(AES_ERR_INVALID_ARG, "null csr");
+    AES_TRY(sync());  // creation is stream-ordered on the library stream
+    if (row_ptr) *row_ptr = a->row_ptr;
+    if (col_ind) *col_ind = a->col;
+    if (val) *val = a->val;
+    return AES_OK;
+}
+
+int aes_csr_download(aes_csr_t a, uint64_t* row_ptr, uint32_t* col_ind, float* val) {
+    if (!a) return fail(AES_ERR_INVALID_ARG, "null csr");
+    cudaStream_t st = lib_stream();
+    if (row_ptr) AES_CUDA_TRY(cudaMemcpyAsync(row_ptr, a->row_ptr, (a->n_rows + 1) * 8, cudaMemcpyDeviceToHost, st));
+    if (a->nnz) {
+        if (col_ind) AES_CUDA_TRY(cudaMemcpyAsync(col_ind, a->col, a->nnz * 4, cudaMemcpyDeviceToHost, st));
+        if (val) AES_CUDA_TRY(cudaMemcpyAsync(val, a->val, a->nnz * 4, cudaMemcpyDeviceToHost, st));
+    }
+    return sync();
+}
+
+int aes_csr_row_stats(aes_csr_t a, uint64_t* row_nnz, uint64_t* max_row_nnz, double* avg_degree) {
+    if (!a) return fail(AES_ERR_INVALID_ARG, "null csr");
+    DBuf<uint64_t> rn;
+    DBuf<unsigned long long> mx;
+    AES_TRY(mx.alloc(1));
+    if (row_nnz) AES_TRY(rn.alloc(a->n_rows));
+    AES_TRY(launch_row_stats(a->row_ptr, a->n_rows, rn.p, mx.p, lib_stream()));
+    if (row_nnz && a->n_rows)
+        AES_CUDA_TRY(cudaMemcpyAsync(row_nnz, rn.p, a->n_rows * 8, cudaMemcpyDeviceToHost, lib_stream()));
+    unsigned long long m = 0;
+    AES_TRY(d2h_scalar(mx.p, &m));
+    if (max_row_nnz) *max_row_nnz = m;
+    if (avg_degree) *avg_degree = a->n_rows == 0 ? 0.0 : double(a->nnz) / double(a->n_rows);
+    return AES_OK;
+}
+
+int aes_gcn_normalize(aes_csr_t a, int add_self_loops, aes_csr_t* out) {
+    if (!a || !out) return fail(AES_ERR_INVALID_ARG, "null argument");
+    if (a->n_rows != a->n_cols) return fail(AES_ERR_NOT_SQUARE, "NotSquare");
+    cudaStream_t st = lib_stream();
+    const uint64_t n = a->n_rows;
+    DBuf<uint64_t> optr;
+    DBuf<char> ws;
+    AES_TRY(optr.alloc(n + 1));
+    size_t wsb = row_scan_workspace_bytes(n);
+    AES_TRY(ws.alloc(wsb));
+    ScanArgs sa{a->row_ptr, a->col, n, 1, 0, add_self_loops, optr.p, nullptr};
+    AES_TRY(launch_row_scan(kScanGcnNnz, sa, ws.p, wsb, st));
+    uint64_t nnz = 0;
+    AES_TRY(d2h_scalar(optr.p + n, &nnz));
+    DBuf<uint32_t> ocol;
+    DBuf<float> oval, inv;
+    AES_TRY(ocol.alloc(nnz ? nnz : 1));
+    AES_TRY(oval.alloc(nnz ? nnz : 1));
+    AES_TRY(inv.alloc(n ? n : 1));
+    AES_TRY(launch_gcn_normalize(a->row_ptr, a->col, n, add_self_loops, optr.p, inv.p, ocol.p, oval.p, st));
+    AES_TRY(sync());
+    auto* o = new aes_csr_s;
+    o->n_rows = n;
+    o->n_cols = a->n_cols;
+    o->nnz = nnz;
+    o->row_ptr = optr.release();
+    o->col = ocol.release();
+    o->val = oval.release();
+    *out = o;
+    return AES_OK;
+}
+
+// ---- plans -------------------------------------------------------------------
+int aes_build_plan_set(aes_csr_t a, uint32_t width, int strategy, aes_plan_t* out) {
+    if (!a || !out) return fail(AES_ERR_INVALID_ARG, "null argument");
+    if (width == 0) return fail(AES_ERR_ZERO_WIDTH, "ZeroWidth");
+    if (strategy < 0 || strategy > 3) return fail(AES_ERR_INVALID_ARG, "unknown strategy");
+    cudaStream_t st = lib_stream();
+    const uint64_t n = a->n_rows;
+    DBuf<uint64_t> srow;
+    DBuf<char> ws;
+    AES_TRY(srow.alloc(n + 1));
+    size_t wsb = aes_dev_scan_workspace_bytes(n);
+    AES_TRY(ws.alloc(wsb));
+    AES_TRY(aes_dev_sample_plan(a->row_ptr, n, width, strategy, srow.p, nullptr, ws.p, wsb, st));
+    uint64_t total = 0;
+    AES_TRY(d2h_scalar(srow.p + n, &total));
+    DBuf<uint32_t> scol;
+    DBuf<float> sval;
+    AES_TRY(scol.alloc(total ? total : 1));
+    AES_TRY(sval.alloc(total ? total : 1));
+    AES_TRY(aes_dev_sample_fill(a->row_ptr, a->row_ptr, a->col, a->val, n, width, strategy, srow.p, scol.p,
+                                sval.p, st));
+    AES_TRY(sync());
+    auto* p = new aes_plan_s;
+    p->width = width;
+    p->strategy = strategy;
+    p->n_rows = n;
+    p->total_slots = total;
+    a->refs.fetch_add(1);
+    p->src = a;
+    p->srow_ptr = srow.release();
+    p->scol = scol.release();
+    p->sval = sval.release();
+    *out = p;
+    return AES_OK;
+}
+
+int aes_plan_destroy(aes_plan_t p) {
+    if (!p) return AES_OK;
+    cudaStream_t st = lib_stream();
+    cudaFreeAsync(p->srow_ptr, st);
+    cudaFreeAsync(p->scol, st);
+    cudaFreeAsync(p->sval, st);
+    csr_release(p->src);
+    delete p;
+    return AES_OK;
+}
+
+int aes_plan_info(aes_plan_t p, uint32_t* width, int* strategy, uint64_t* n_rows, uint64_t* total_slots,
+                  uint64_t* total_starts) {
+    if (!p) return fail(AES_ERR_INVALID_ARG, "null plan");
+    if (width) *width = p->width;
+    if (strategy) *strategy = p->strategy;
+    if (n_rows) *n_rows = p->n_rows;
+    if (total_slots) *total_slots = p->total_slots;
+    if (total_starts) {
+        const uint64_t n = p->n_rows;
+        DBuf<uint64_t> sp;
+        DBuf<char> ws;
+        AES_TRY(sp.alloc(n + 1));
+        size_t wsb = row_scan_workspace_bytes(n);
+        AES_TRY(ws.alloc(wsb));
+        ScanArgs sa{p->src->row_ptr, nullptr, n, p->width, p->strategy, 0, sp.p, nullptr};
+        AES_TRY(launch_row_scan(kScanStarts, sa, ws.p, wsb, lib_stream()));
+        AES_TRY(d2h_scalar(sp.p + n, total_starts));
+    }
+    return AES_OK;
+}
+
+int aes_plan_export(aes_plan_t p, uint32_t* chunk_len, uint32_t* sample_cnt, uint64_t* starts_ptr,
+                    uint32_t* starts) {
+    if (!p) return fail(AES_ERR_INVALID_ARG, "null plan");
+    cudaStream_t st = lib_stream();
+    const uint64_t n = p->n_rows;
+    DBuf<uint64_t> sp;
+    DBuf<char> ws;
+    AES_TRY(sp.alloc(n + 1));
+    size_t wsb = row_scan_workspace_bytes(n);
+    AES_TRY(ws.alloc(wsb));
+    ScanArgs sa{p->src->row_ptr, nullptr, n, p->width, p->strategy, 0, sp.p, nullptr};
+    AES_TRY(launch_row_scan(kScanStarts, sa, ws.p, wsb, st));
+    uint64_t tot = 0;
+    AES_TRY(d2h_scalar(sp.p + n, &tot));
+    DBuf<uint32_t> dch, dcn, dst;
+    AES_TRY(dch.alloc(n ? n : 1));
+    AES_TRY(dcn.alloc(n ? n : 1));
+    AES_TRY(dst.alloc(tot ? tot : 1));
+    AES_TRY(launch_plan_export(p->src->row_ptr, n, p->width, p->strategy, sp.p, dch.p, dcn.p, dst.p, st));
+    if (n) {
+        if (chunk_len) AES_CUDA_TRY(cudaMemcpyAsync(chunk_len, dch.p, n * 4, cudaMemcpyDeviceToHost, st));
+        if (sample_cnt) AES_CUDA_TRY(cudaMemcpyAsync(sample_cnt, dcn.p, n * 4, cudaMemcpyDeviceToHost, st));
+    }
+    if (starts_ptr) AES_CUDA_TRY(cudaMemcpyAsync(starts_ptr, sp.p, (n + 1) * 8, cudaMemcpyDeviceToHost, st));
+    if (starts && tot) AES_CUDA_TRY(cudaMemcpyAsync(starts, dst.p, tot * 4, cudaMemcpyDeviceToHost, st));
+    return sync();
+}
+
+int aes_plan_device_ptrs(aes_plan_t p, const uint64_t** srow_ptr, const uint32_t** scol, const float** sval) {
+    if (!p) return fail(AES_ERR_INVALID_ARG, "null plan");
+    if (srow_ptr) *srow_ptr = p->srow_ptr;
+    if (scol) *scol = p->scol;
+    if (sval) *sval = p->sval;
+    return AES_OK;
+}
+
+int aes_plan_download(aes_plan_t p, uint64_t* srow_ptr, uint32_t* scol, float* sval) {
+    if (!p) return fail(AES_ERR_INVALID_ARG, "null plan");
+    cudaStream_t st = lib_stream();
+    if (srow_ptr)
+        AES_CUDA_TRY(cudaMemcpyAsync(srow_ptr, p->srow_ptr, (p->n_rows + 1) * 8, cudaMemcpyDeviceToHost, st));
+    if (p->total_slots) {
+        if (scol) AES_CUDA_TRY(cudaMemcpyAsync(scol, p->scol, p->total_slots * 4, cudaMemcpyDeviceToHost, st));
+        if (sval) AES_CUDA_TRY(cudaMemcpyAsync(sval, p->sval, p->total_slots * 4, cudaMemcpyDeviceToHost, st));
+    }
+    return sync();
+}
+
+int aes_sampling_rate(aes_plan_t p, aes_csr_t a, double* aggregate, double* unique_coverage, double* per_row) {
+    if (!p || !a) return fail(AES_ERR_INVALID_ARG, "null argument");
+    if (p->n_rows != a->n_rows) return fail(AES_ERR_INVALID_ARG, "plan/stats row count mismatch");
+    cudaStream_t st = lib_stream();
+    DBuf<unsigned long long> tot;
+    DBuf<double> pr;
+    AES_TRY(tot.alloc(3));
+    if (per_row) AES_TRY(pr.alloc(a->n_rows ? a->n_rows : 1));
+    AES_TRY(launch_sampling_rate(a->row_ptr, a->n_rows, p->width, p->strategy, pr.p, tot.p, st));
+    unsigned long long t[3];
+    AES_CUDA_TRY(cudaMemcpyAsync(t, tot.p, sizeof(t), cudaMemcpyDeviceToHost, st));
+    if (per_row && a->n_rows)
+        AES_CUDA_TRY(cudaMemcpyAsync(per_row, pr.p, a->n_rows * 8, cudaMemcpyDeviceToHost, st));
+    AES_TRY(sync());
+    if (aggregate) *aggregate = t[2] == 0 ? 1.0 : double(t[0]) / double(t[2]);
+    if (unique_coverage) *unique_coverage = t[2] == 0 ? 1.0 : double(t[1]) / double(t[2]);
+    return AES_OK;
+}
+
+// ---- SpMM ------------------------------------------------------------------------
+int aes_spmm_exact(aes_csr_t a, const float* b, uint64_t b_rows, uint64_t f, float* c) {
+    if (!a) return fail(AES_ERR_INVALID_ARG, "null csr");
+    if (a->n_cols != b_rows) return fail(AES_ERR_SHAPE, "ShapeMismatch");
+    return spmm_host(a->row_ptr, a->col, a->val, a->n_rows, b, b_rows, f, c);
+}
+
+int aes_spmm_sampled(aes_csr_t a, const float* b, uint64_t b_rows, uint64_t f, aes_plan_t p, float* c,
+                     uint64_t* fma_count, uint64_t* loads_a, uint64_t* loads_b) {
+    if (!a || !p) return fail(AES_ERR_INVALID_ARG, "null argument");
+    if (a->n_cols != b_rows) return fail(AES_ERR_SHAPE, "ShapeMismatch");
+    if (p->n_rows != a->n_rows) return fail(AES_ERR_PLAN_MISMATCH, "PlanMatrixMismatch");
+    DBuf<uint32_t> tc;
+    DBuf<float> tv;
+    const uint32_t* scol;
+    const float* sval;
+    AES_TRY(sampled_for(p, a, tc, tv, &scol, &sval));
+    AES_TRY(spmm_host(p->srow_ptr, scol, sval, a->n_rows, b, b_rows, f, c));
+    // WorkCounter semantics (spmm.cpp:95-97): fma = slots*F, loads_a = slots
+    if (fma_count) *fma_count = p->total_slots * f;
+    if (loads_a) *loads_a = p->total_slots;
+    if (loads_b) *loads_b = p->total_slots * f;
+    return AES_OK;
+}
+
+// ---- quantization -------------------------------------------------------------------
+static int make_qfeat(const float* x, uint64_t rows, uint64_t cols, float lo, float hi, uint32_t bits,
+                      const float* dx, aes_qfeat_t* out) {
+    cudaStream_t st = lib_stream();
+    auto* q = new aes_qfeat_s;
+    q->rows = rows;
+    q->cols = cols;
+    q->x_min = lo;
+    q->x_max = hi;
+    q->bits = bits;
+    q->u8 = bits <= 8;
+    q->ld = q->u8 ? round4(cols ? cols : 1) : cols;
+    const size_t esz = q->u8 ? 1 : 2;
+    int s = AES_OK;
+    if (cudaMallocAsync(&q->codes, rows * q->ld * esz + 16, st) != cudaSuccess) s = fail(AES_ERR_CUDA, "alloc");
+    if (!s && q->ld != cols) cudaMemsetAsync(q->codes, 0, rows * q->ld * esz, st);
+    if (!s) s = aes_dev_quantize(dx, rows, cols, cols, lo, hi, bits, q->codes, q->ld, st);
+    if (!s && q->u8) {
+        if (cudaMallocAsync((void**)&q->lut, 256 * sizeof(float), st) != cudaSuccess) s = fail(AES_ERR_CUDA, "alloc");
+        if (!s) s = aes_dev_dequant_lut(lo, hi, bits, q->lut, st);
+    }
+    if (!s) s = sync();
+    if (s) {
+        aes_qfeat_destroy(q);
+        return s;
+    }
+    (void)x;
+    *out = q;
+    return AES_OK;
+}
+
+int aes_quantize(const float* x, uint64_t rows, uint64_t cols, uint32_t bits, aes_qfeat_t* out) {
+    if (!out) return fail(AES_ERR_INVALID_ARG, "null out");
+    const uint64_t n = rows * cols;
+    if (n == 0) return fail(AES_ERR_EMPTY, "EmptyMatrix");       // quantize.cpp:12
+    if (bits < 1 || bits > 16) return fail(AES_ERR_BITS, "bits must be 1..16");  // :13
+    cudaStream_t st = lib_stream();
+    DBuf<float> dx, res;
+    DBuf<char> ws;
+    AES_TRY(dx.alloc(n));
+    AES_CUDA_TRY(cudaMemcpyAsync(dx.p, x, n * 4, cudaMemcpyHostToDevice, st));
+    const size_t wsb = aes_dev_scan_workspace_bytes(1);
+    AES_TRY(ws.alloc(wsb));
+    AES_TRY(res.alloc(4));
+    AES_TRY(aes_dev_fit_params(dx.p, n, res.p, ws.p, wsb, st));
+    float r[4];
+    AES_CUDA_TRY(cudaMemcpyAsync(r, res.p, sizeof(r), cudaMemcpyDeviceToHost, st));
+    AES_TRY(sync());
+    uint32_t flag;
+    memcpy(&flag, &r[2], 4);
+    if (flag) return fail(AES_ERR_NONFINITE, "NonFinite");
+    return make_qfeat(x, rows, cols, r[0], r[1], bits, dx.p, out);
+}
+
+int aes_quantize_with(const float* x, uint64_t rows, uint64_t cols, float x_min, float x_max, uint32_t bits,
+                      aes_qfeat_t* out) {
+    if (!out) return fail(AES_ERR_INVALID_ARG, "null out");
+    if (bits < 1 || bits > 16 || !(x_min <= x_max)) return fail(AES_ERR_QPARAMS, "invalid QuantParams");
+    const uint64_t n = rows * cols;
+    DBuf<float> dx;
+    AES_TRY(dx.alloc(n ? n : 1));
+    if (n) AES_CUDA_TRY(cudaMemcpyAsync(dx.p, x, n * 4, cudaMemcpyHostToDevice, lib_stream()));
+    return make_qfeat(x, rows, cols, x_min, x_max, bits, dx.p, out);
+}
+
+int aes_qfeat_from_codes(const uint16_t* codes, uint64_t rows, uint64_t cols, float x_min, float x_max,
+                         uint32_t bits, aes_qfeat_t* out) {
+    if (!out) return fail(AES_ERR_INVALID_ARG, "null out");
+    if (bits < 1 || bits > 16) return fail(AES_ERR_QPARAMS, "invalid QuantParams");
+    cudaStream_t st = lib_stream();
+    const uint64_t n = rows * cols;
+    DBuf<uint16_t> d16;
+    AES_TRY(d16.alloc(n ? n : 1));
+    if (n) AES_CUDA_TRY(cudaMemcpyAsync(d16.p, codes, n * 2, cudaMemcpyHostToDevice, st));
+    auto* q = new aes_qfeat_s;
+    q->rows = rows;
+    q->cols = cols;
+    q->x_min = x_min;
+    q->x_max = x_max;
+    q->bits = bits;
+    q->u8 = false;
+    q->ld = cols;
+    int s = AES_OK;
+    if (bits <= 8) {
+        DBuf<unsigned int> ovf;
+        uint64_t ld = round4(cols ? cols : 1);
+        void* c8 = nullptr;
+        s = ovf.alloc(1);
+        if (!s && cudaMallocAsync(&c8, rows * ld + 16, st) != cudaSuccess) s = fail(AES_ERR_CUDA, "alloc");
+        if (!s) {
+            cudaMemsetAsync(c8, 0, rows * ld, st);
+            cudaMemsetAsync(ovf.p, 0, 4, st);
+            if (n)
+                narrow_u16_kernel<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(d16.p, rows, cols, ld,
+                                                                              (uint8_t*)c8, ovf.p);
+            unsigned int o = 0;
+            s = d2h_scalar(ovf.p, &o);
+            if (!s && o == 0) {
+                q->u8 = true;
+                q->ld = ld;
+                q->codes = c8;
+                c8 = nullptr;
+                if (cudaMallocAsync((void**)&q->lut, 1024, st) != cudaSuccess) s = fail(AES_ERR_CUDA, "alloc");
+                if (!s) s = aes_dev_dequant_lut(x_min, x_max, bits, q->lut, st);
+            }
+        }
+        if (c8) cudaFreeAsync(c8, st);
+    }
+    if (!s && !q->u8) q->codes = d16.release();
+    if (!s) s = sync();
+    if (s) {
+        aes_qfeat_destroy(q);
+        return s;
+    }
+    *out = q;
+    return AES_OK;
+}
+
+int aes_qfeat_destroy(aes_qfeat_t q) {
+    if (!q) return AES_OK;
+    cudaStream_t st = lib_stream();
+    if (q->codes) cudaFreeAsync(q->codes, st);
+    if (q->lut) cudaFreeAsync(q->lut, st);
+    delete q;
+    return AES_OK;
+}
+
+int aes_qfeat_info(aes_qfeat_t q, uint64_t* rows, uint64_t* cols, float* x_min, float* x_max, uint32_t* bits) {
+    if (!q) return fail(AES_ERR_INVALID_ARG, "null qfeat");
+    if (rows) *rows = q->rows;
+    if (cols) *cols = q->cols;
+    if (x_min) *x_min = q->x_min;
+    if (x_max) *x_max = q->x_max;
+    if (bits) *bits = q->bits;
+    return AES_OK;
+}
+
+int aes_qfeat_codes(aes_qfeat_t q, uint16_t* codes) {
+    if (!q) return fail(AES_ERR_INVALID_ARG, "null qfeat");
+    const uint64_t n = q->rows * q->cols;
+    if (n == 0) return AES_OK;
+    cudaStream_t st = lib_stream();
+    if (q->u8) {
+        DBuf<uint16_t> w;
+        AES_TRY(w.alloc(n));
+        widen_u8_kernel<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>((const uint8_t*)q->codes, q->rows, q->cols,
+                                                                    q->ld, w.p);
+        AES_CUDA_TRY(cudaGetLastError());
+        AES_CUDA_TRY(cudaMemcpyAsync(codes, w.p, n * 2, cudaMemcpyDeviceToHost, st));
+        return sync();
+    }
+    AES_CUDA_TRY(cudaMemcpyAsync(codes, q->codes, n * 2, cudaMemcpyDeviceToHost, st));
+    return sync();
+}
+
+static int dequant_device(aes_qfeat_t q, DBuf<float>& out, uint64_t& ld) {
+    ld = round4(q->cols ? q->cols : 1);
+    AES_TRY(out.alloc(q->rows * ld));
+    cudaStream_t st = lib_stream();
+    if (ld != q->cols) AES_CUDA_TRY(cudaMemsetAsync(out.p, 0, q->rows * ld * 4, st));
+    return aes_dev_dequantize(q->codes, q->rows, q->cols, q->ld, q->x_min, q->x_max, q->bits, out.p, ld, st);
+}
+
+int aes_dequantize(aes_qfeat_t q, float* x) {
+    if (!q) return fail(AES_ERR_INVALID_ARG, "null qfeat");
+    if (q->rows * q->cols == 0) return AES_OK;
+    DBuf<float> d;
+    uint64_t ld;
+    AES_TRY(dequant_device(q, d, ld));
+    AES_TRY(download_dense(d.p, ld, q->rows, q->cols, x));
+    return sync();
+}
+
+int aes_spmm_sampled_q8(aes_csr_t a, aes_qfeat_t q, aes_plan_t p, float* c) {
+    if (!a || !q) return fail(AES_ERR_INVALID_ARG, "null argument");
+    if (a->n_cols != q->rows) return fail(AES_ERR_SHAPE, "ShapeMismatch");
+    if (p && p->n_rows != a->n_rows) return fail(AES_ERR_PLAN_MISMATCH, "PlanMatrixMismatch");
+    const uint64_t n = a->n_rows, f = q->cols;
+    if (n == 0 || f == 0) return AES_OK;
+    cudaStream_t st = lib_stream();
+    DBuf<uint32_t> tc;
+    DBuf<float> tv;
+    const uint64_t* rp = a->row_ptr;
+    const uint32_t* scol = a->col;
+    const float* sval = a->val;
+    if (p) {
+        rp = p->srow_ptr;
+        AES_TRY(sampled_for(p, a, tc, tv, &scol, &sval));
+    }
+    const uint64_t ldc = round4(f);
+    DBuf<float> dc;
+    AES_TRY(dc.alloc(n * ldc));
+    if (q->u8) {
+        AES_TRY(aes_dev_spmm_q8(rp, scol, sval, n, (const uint8_t*)q->codes, q->ld, f, q->lut, dc.p, ldc, st));
+    } else {  // 9..16-bit codes: dequantize on the GPU, then the fp32 kernel
+        DBuf<float> dx;
+        uint64_t ld;
+        AES_TRY(dequant_device(q, dx, ld));
+        AES_TRY(aes_dev_spmm_f32(rp, scol, sval, n, dx.p, ld, f, dc.p, ldc, st));
+    }
+    AES_TRY(download_dense(dc.p, ldc, n, f, c));
+    return sync();
+}
+
+// ---- GNN -------------------------------------------------------------------------------
+int aes_dense_matmul(const float* a, uint64_t m, uint64_t k, const float* b, uint64_t n, float* c) {
+    DBuf<float> da, db, dc;
+    uint64_t lda, ldb;
+    AES_TRY(upload_dense(a, m, k, da, lda));
+    AES_TRY(upload_dense(b, k, n, db, ldb));
+    const uint64_t ldc = round4(n ? n : 1);
+    AES_TRY(dc.alloc(m * ldc));
+    AES_TRY(aes_dev_gemm_bias_act(da.p, m, k, lda, db.p, n, ldb, nullptr, 0, dc.p, ldc, lib_stream()));
+    AES_TRY(download_dense(dc.p, ldc, m, n, c));
+    return sync();
+}
+
+int aes_gcn_forward(aes_csr_t adj, const float* x, const uint64_t* dims, int n_layers, const float* weights,
+                    const float* biases, const uint64_t* bias_len, aes_plan_t p, float* out) {
+    if (!adj || !dims) return fail(AES_ERR_INVALID_ARG, "null argument");
+    if (adj->n_cols != adj->n_rows) return fail(AES_ERR_SHAPE, "ShapeMismatch");
+    if (p && p->n_rows != adj->n_rows) return fail(AES_ERR_PLAN_MISMATCH, "PlanMatrixMismatch");
+    cudaStream_t st = lib_stream();
+    const uint64_t n = adj->n_rows;
+    DBuf<uint32_t> tc;
+    DBuf<float> tv;
+    const uint64_t* rp = adj->row_ptr;
+    const uint32_t* scol = adj->col;
+    const float* sval = adj->val;
+    if (p) {
+        rp = p->srow_ptr;
+        AES_TRY(sampled_for(p, adj, tc, tv, &scol, &sval));
+    }
+    DBuf<float> h, agg, nxt, dw, db;
+    uint64_t ldh;
+    AES_TRY(upload_dense(x, n, dims[0], h, ldh));
+    uint64_t woff = 0, boff = 0;
+    for (int l = 0; l < n_layers; ++l) {
+        const uint64_t fin = dims[l], fout = dims[l + 1];
+        if (bias_len && bias_len[l] != 0 && bias_len[l] != fout) return fail(AES_ERR_SHAPE, "ShapeMismatch");
+        const uint64_t lda = round4(fin ? fin : 1);
+        AES_TRY(agg.alloc(n * lda));
+        AES_TRY(aes_dev_spmm_f32(rp, scol, sval, n, h.p, ldh, fin, agg.p, lda, st));
+        uint64_t ldw;
+        AES_TRY(upload_dense(weights + woff, fin, fout, dw, ldw));
+        const bool has_bias = bias_len ? bias_len[l] != 0 : true;
+        if (has_bias) {
+            AES_TRY(db.alloc(fout ? fout : 1));
+            if (fout) AES_CUDA_TRY(cudaMemcpyAsync(db.p, biases + boff, fout * 4, cudaMemcpyHostToDevice, st));
+        }
+        const uint64_t ldo = round4(fout ? fout : 1);
+        AES_TRY(nxt.alloc(n * ldo));
+        if (ldo != fout) AES_CUDA_TRY(cudaMemsetAsync(nxt.p, 0, n * ldo * 4, st));
+        AES_TRY(aes_dev_gemm_bias_act(agg.p, n, fin, lda, dw.p, fout, ldw, has_bias ? db.p : nullptr,
+                                      l + 1 < n_layers, nxt.p, ldo, st));
+        std::swap(h.p, nxt.p);
+        std::swap(h.n, nxt.n);
+        ldh = ldo;
+        woff += fin * fout;
+        boff += has_bias ? fout : 0;
+    }
+    AES_TRY(download_dense(h.p, ldh, n, dims[n_layers], out));
+    return sync();
+}
+
+}  // extern "C"

@@ -1,0 +1,235 @@
+// Scalar (global min/max) quantization for sm_100a — proj/src/quantize.cpp.
+//
+//  * fit_params (quantize.cpp:11-21): deterministic two-level (value, index)
+//    reduction.  The reference keeps the FIRST element that attains the
+//    min/max under strict '<' (so -0.0f vs +0.0f and ties resolve to the lowest
+//    index); reducing (value, index) pairs with "smaller value, then smaller
+//    index" reproduces the exact float it returns, sign of zero included.
+//  * quantize (quantize.cpp:23-51): fp64 with __dsub_rn/__ddiv_rn/__dmul_rn/
+//    __dadd_rn so ratio*levels + 2^-7 is NOT contracted into a DFMA.
+//  * dequantize (quantize.cpp:53-64): float(double(q)*step + double(lo)), and
+//    the 256-entry LUT of the same values that the int8 SpMM gathers through.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace aes {
+namespace {
+
+constexpr int kFitThreads = 256;
+constexpr int kFitBlocks = 148 * 4;
+
+struct MinMax {
+    float lo, hi;
+    uint64_t ilo, ihi;
+    uint32_t bad;
+};
+
+__device__ __forceinline__ void mm_merge(MinMax& a, const MinMax& b) {
+    if (b.lo < a.lo || (b.lo == a.lo && b.ilo < a.ilo)) { a.lo = b.lo; a.ilo = b.ilo; }
+    if (b.hi > a.hi || (b.hi == a.hi && b.ihi < a.ihi)) { a.hi = b.hi; a.ihi = b.ihi; }
+    a.bad |= b.bad;
+}
+
+__device__ __forceinline__ MinMax mm_shfl(const MinMax& m, int o) {
+    MinMax r;
+    r.lo = __shfl_down_sync(0xffffffffu, m.lo, o);
+    r.hi = __shfl_down_sync(0xffffffffu, m.hi, o);
+    r.ilo = __shfl_down_sync(0xffffffffu, m.ilo, o);
+    r.ihi = __shfl_down_sync(0xffffffffu, m.ihi, o);
+    r.bad = __shfl_down_sync(0xffffffffu, m.bad, o);
+    return r;
+}
+
+__device__ MinMax block_reduce(MinMax m) {
+    __shared__ MinMax s[kFitThreads / 32];
+    for (int o = 16; o > 0; o >>= 1) {
+        MinMax t = mm_shfl(m, o);
+        mm_merge(m, t);
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) s[wid] = m;
+    __syncthreads();
+    if (wid == 0) {
+        m = s[lane < kFitThreads / 32 ? lane : 0];
+        for (int o = 16; o > 0; o >>= 1) {
+            MinMax t = mm_shfl(m, o);
+            mm_merge(m, t);
+        }
+    }
+    return m;
+}
+
+// Level 1: block b reduces the contiguous chunk [b*chunk, (b+1)*chunk).
+__global__ void __launch_bounds__(kFitThreads)
+fit_partial_kernel(const float* __restrict__ x, uint64_t n, uint64_t chunk, MinMax* __restrict__ part) {
+    const uint64_t b0 = (uint64_t)blockIdx.x * chunk;
+    const uint64_t b1 = min(n, b0 + chunk);
+    MinMax m{INFINITY, -INFINITY, ~0ull, ~0ull, 0u};
+    for (uint64_t i = b0 + threadIdx.x; i < b1; i += kFitThreads) {
+        float v = __ldcs(x + i);
+        if (!isfinite(v)) { m.bad = 1; continue; }
+        if (v < m.lo || (v == m.lo && i < m.ilo)) { m.lo = v; m.ilo = i; }
+        if (v > m.hi || (v == m.hi && i < m.ihi)) { m.hi = v; m.ihi = i; }
+    }
+    m = block_reduce(m);
+    if (threadIdx.x == 0) part[blockIdx.x] = m;
+}
+
+// Level 2: one block over the partials; emit the element values themselves.
+__global__ void __launch_bounds__(kFitThreads)
+fit_final_kernel(const float* __restrict__ x, const MinMax* __restrict__ part, int nparts,
+                 float* __restrict__ result) {
+    MinMax m{INFINITY, -INFINITY, ~0ull, ~0ull, 0u};
+    for (int i = threadIdx.x; i < nparts; i += kFitThreads) mm_merge(m, part[i]);
+    m = block_reduce(m);
+    if (threadIdx.x == 0) {
+        uint32_t* flags = reinterpret_cast<uint32_t*>(result + 2);
+        flags[0] = m.bad;
+        result[0] = m.bad || m.ilo == ~0ull ? 0.f : x[m.ilo];
+        result[1] = m.bad || m.ihi == ~0ull ? 0.f : x[m.ihi];
+    }
+}
+
+template <typename CodeT>
+__global__ void quantize_kernel(const float* __restrict__ x, uint64_t rows, uint64_t cols, uint64_t ldx,
+                                double lo, double range, double levels, CodeT* __restrict__ q, uint64_t ldq) {
+    const uint64_t total = rows * cols;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = e / cols, c = e - r * cols;
+        const double v = (double)__ldcs(x + r * ldx + c);
+        double code;
+        if (range == 0.0) {
+            code = 0.0;
+        } else {
+            const double ratio = __ddiv_rn(__dsub_rn(v, lo), range);
+            code = floor(__dadd_rn(__dmul_rn(ratio, levels), 0.0078125));
+            code = code < 0.0 ? 0.0 : code;            // std::clamp(q, 0, levels)
+            code = levels < code ? levels : code;
+        }
+        q[r * ldq + c] = (CodeT)(uint32_t)code;
+    }
+}
+
+// Vector form for the common contiguous case: 4 floats -> 4 codes per thread.
+__global__ void quantize_u8_vec4_kernel(const float4* __restrict__ x, uint64_t n4, double lo, double range,
+                                        double levels, uchar4* __restrict__ q) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n4;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const float4 v = __ldcs(x + e);
+        float in[4] = {v.x, v.y, v.z, v.w};
+        unsigned char out[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            double code = 0.0;
+            if (range != 0.0) {
+                const double ratio = __ddiv_rn(__dsub_rn((double)in[i], lo), range);
+                code = floor(__dadd_rn(__dmul_rn(ratio, levels), 0.0078125));
+                code = code < 0.0 ? 0.0 : code;
+                code = levels < code ? levels : code;
+            }
+            out[i] = (unsigned char)(uint32_t)code;
+        }
+        __stcs(q + e, make_uchar4(out[0], out[1], out[2], out[3]));
+    }
+}
+
+template <typename CodeT>
+__global__ void dequantize_kernel(const CodeT* __restrict__ q, uint64_t rows, uint64_t cols, uint64_t ldq,
+                                  double lo, double step, float* __restrict__ x, uint64_t ldx) {
+    const uint64_t total = rows * cols;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = e / cols, c = e - r * cols;
+        const double code = (double)q[r * ldq + c];
+        x[r * ldx + c] = __double2float_rn(__dadd_rn(__dmul_rn(code, step), lo));
+    }
+}
+
+__global__ void lut_kernel(double lo, double step, uint32_t levels, float* __restrict__ lut) {
+    const uint32_t q = threadIdx.x;
+    lut[q] = q <= levels ? __double2float_rn(__dadd_rn(__dmul_rn((double)q, step), lo)) : 0.f;
+}
+
+}  // namespace
+}  // namespace aes
+
+extern "C" {
+
+int aes_dev_fit_params(const float* x, uint64_t n, float* result, void* workspace,
+                       size_t workspace_bytes, void* stream) {
+    using namespace aes;
+    cudaStream_t st = as_stream(stream);
+    if (n == 0) return fail(AES_ERR_EMPTY, "EmptyMatrix");
+    uint64_t nbl = (n + kFitThreads - 1) / kFitThreads;
+    int nb = (int)(nbl < (uint64_t)kFitBlocks ? nbl : (uint64_t)kFitBlocks);
+    if (workspace_bytes < nb * sizeof(MinMax)) return fail(AES_ERR_INVALID_ARG, "fit workspace too small");
+    uint64_t chunk = (n + nb - 1) / nb;
+    auto* part = static_cast<MinMax*>(workspace);
+    fit_partial_kernel<<<nb, kFitThreads, 0, st>>>(x, n, chunk, part);
+    fit_final_kernel<<<1, kFitThreads, 0, st>>>(x, part, nb, result);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
+int aes_dev_quantize(const float* x, uint64_t rows, uint64_t cols, uint64_t ldx, float lo, float hi,
+                     uint32_t bits, void* codes, uint64_t ldq, void* stream) {
+    using namespace aes;
+    cudaStream_t st = as_stream(stream);
+    if (bits < 1 || bits > 16 || !(lo <= hi)) return fail(AES_ERR_QPARAMS, "invalid QuantParams");
+    const uint64_t total = rows * cols;
+    if (total == 0) return AES_OK;
+    const double dlo = (double)lo, range = (double)hi - (double)lo;
+    const double levels = (double)((1u << bits) - 1u);
+    const unsigned grid = grid_for(total, 256, 148 * 32);
+    if (bits <= 8) {
+        if (ldx == cols && ldq == cols && total % 4 == 0 && (uintptr_t)x % 16 == 0 &&
+            (uintptr_t)codes % 4 == 0) {
+            quantize_u8_vec4_kernel<<<grid_for(total / 4, 256, 148 * 32), 256, 0, st>>>(
+                reinterpret_cast<const float4*>(x), total / 4, dlo, range, levels,
+                static_cast<uchar4*>(codes));
+        } else {
+            quantize_kernel<uint8_t><<<grid, 256, 0, st>>>(x, rows, cols, ldx, dlo, range, levels,
+                                                           static_cast<uint8_t*>(codes), ldq);
+        }
+    } else {
+        quantize_kernel<uint16_t><<<grid, 256, 0, st>>>(x, rows, cols, ldx, dlo, range, levels,
+                                                        static_cast<uint16_t*>(codes), ldq);
+    }
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
+int aes_dev_dequantize(const void* codes, uint64_t rows, uint64_t cols, uint64_t ldq, float lo, float hi,
+                       uint32_t bits, float* x, uint64_t ldx, void* stream) {
+    using namespace aes;
+    cudaStream_t st = as_stream(stream);
+    if (bits < 1 || bits > 16) return fail(AES_ERR_QPARAMS, "invalid QuantParams");
+    const uint64_t total = rows * cols;
+    if (total == 0) return AES_OK;
+    const double step = ((double)hi - (double)lo) / (double)((1u << bits) - 1u);
+    const unsigned grid = grid_for(total, 256, 148 * 32);
+    if (bits <= 8)
+        dequantize_kernel<uint8_t><<<grid, 256, 0, st>>>(static_cast<const uint8_t*>(codes), rows, cols,
+                                                         ldq, (double)lo, step, x, ldx);
+    else
+        dequantize_kernel<uint16_t><<<grid, 256, 0, st>>>(static_cast<const uint16_t*>(codes), rows,
+                                                          cols, ldq, (double)lo, step, x, ldx);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
+int aes_dev_dequant_lut(float lo, float hi, uint32_t bits, float* lut, void* stream) {
+    using namespace aes;
+    if (bits < 1 || bits > 8) return fail(AES_ERR_UNSUPPORTED, "LUT needs bits <= 8");
+    const uint32_t levels = (1u << bits) - 1u;
+    const double step = ((double)hi - (double)lo) / (double)levels;
+    lut_kernel<<<1, 256, 0, as_stream(stream)>>>((double)lo, step, levels, lut);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,443 @@
+// Adaptive edge sampler for sm_100a: per-row strategy (Table 1 / Eq. 3), a
+// single-pass decoupled look-back scan building the sampled row pointer, and a
+// slot-order fill producing the sampled CSR that the SpMM consumes.
+//
+// Reference: proj/src/sampling.cpp:29-152 (plans), proj/src/spmm.cpp:54-76
+// (the per-row buffer fill, which here is materialised once per (graph, W)
+// and reused by every layer), proj/src/matrix.cpp:28-63 (validate_csr,
+// row_stats).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace aes {
+
+// ===========================================================================
+// Row-count scan: out[0] = 0, out[i+1] = sum_{r<=i} count(r).
+// One pass over row_ptr; tile prefixes chained with decoupled look-back.
+// ===========================================================================
+namespace {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanIters = 8;                        // rows per thread per tile
+constexpr int kScanTile = kScanThreads * kScanIters; // 2048 rows per tile
+
+// tile state word: (value << 2) | flag ; flag 1 = aggregate, 2 = inclusive prefix
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <int KIND>
+__device__ __forceinline__ uint64_t row_count(const ScanArgs& a, uint64_t r) {
+    uint64_t b = a.row_ptr[r], e = a.row_ptr[r + 1];
+    uint64_t nnz = e - b;
+    if (KIND == kScanSlots) {
+        RowParams p = row_params(nnz, a.width, a.strategy);
+        if (a.row_params) {
+            reinterpret_cast<uint2*>(a.row_params)[r] = make_uint2(p.chunk, p.cnt);
+        }
+        return (uint64_t)p.chunk * p.cnt;
+    } else if (KIND == kScanStarts) {
+        RowParams p = row_params(nnz, a.width, a.strategy);
+        return row_num_starts(nnz, a.width, a.strategy, p);
+    } else {  // kScanGcnNnz: rows are sorted (validated); probe the diagonal
+        if (!a.add_self_loops) return nnz;
+        uint64_t lo = b, hi = e;
+        while (lo < hi) {
+            uint64_t mid = (lo + hi) >> 1;
+            if (a.col_ind[mid] < r) lo = mid + 1; else hi = mid;
+        }
+        bool has_diag = lo < e && a.col_ind[lo] == r;
+        return nnz + (has_diag ? 0 : 1);
+    }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kScanThreads)
+row_scan_kernel(ScanArgs a, unsigned long long* tile_state, unsigned int* tile_counter) {
+    __shared__ uint64_t warp_tot[kScanThreads / 32];
+    __shared__ uint64_t s_excl;
+    __shared__ unsigned int s_tile;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+
+    if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+    __syncthreads();
+    const uint64_t tile = s_tile;
+    const uint64_t base = tile * kScanTile;
+
+    uint64_t incl[kScanIters];
+    uint64_t carry = 0;
+#pragma unroll
+    for (int it = 0; it < kScanIters; ++it) {
+        uint64_t r = base + (uint64_t)it * kScanThreads + tid;
+        uint64_t c = r < a.n ? row_count<KIND>(a, r) : 0;
+        // warp inclusive scan
+        uint64_t v = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint64_t t = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += t;
+        }
+        if (lane == 31) warp_tot[wid] = v;
+        __syncthreads();
+        uint64_t woff = 0, tot = 0;
+#pragma unroll
+        for (int w = 0; w < kScanThreads / 32; ++w) {
+            uint64_t x = warp_tot[w];
+            woff += (w < wid) ? x : 0;
+            tot += x;
+        }
+        incl[it] = carry + woff + v;
+        carry += tot;
+        __syncthreads();
+    }
+
+    // publish aggregate / look back
+    if (tid == 0) {
+        uint64_t excl = 0;
+        if (tile == 0) {
+            st_release(&tile_state[0], (carry << 2) | 2ull);
+        } else {
+            st_release(&tile_state[tile], (carry << 2) | 1ull);
+            int64_t j = (int64_t)tile - 1;
+            while (j >= 0) {
+                unsigned long long s;
+                do {
+                    s = ld_acquire(&tile_state[j]);
+                } while ((s & 3ull) == 0);
+                excl += s >> 2;
+                if ((s & 3ull) == 2ull) break;
+                --j;
+            }
+            st_release(&tile_state[tile], ((excl + carry) << 2) | 2ull);
+        }
+        s_excl = excl;
+    }
+    __syncthreads();
+    const uint64_t excl = s_excl;
+#pragma unroll
+    for (int it = 0; it < kScanIters; ++it) {
+        uint64_t r = base + (uint64_t)it * kScanThreads + tid;
+        if (r < a.n) a.out[r + 1] = excl + incl[it];
+    }
+    if (tile == 0 && tid == 0) a.out[0] = 0;
+}
+
+}  // namespace
+
+size_t row_scan_workspace_bytes(uint64_t n) {
+    uint64_t tiles = (n + kScanTile - 1) / kScanTile;
+    if (tiles == 0) tiles = 1;
+    return 256 + tiles * sizeof(unsigned long long);
+}
+
+int launch_row_scan(int kind, const ScanArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
+    size_t need = row_scan_workspace_bytes(a.n);
+    if (ws == nullptr || ws_bytes < need) return fail(AES_ERR_INVALID_ARG, "scan workspace too small");
+    if (a.n == 0) {
+        AES_CUDA_TRY(cudaMemsetAsync(a.out, 0, sizeof(uint64_t), st));
+        return AES_OK;
+    }
+    uint64_t tiles = (a.n + kScanTile - 1) / kScanTile;
+    AES_CUDA_TRY(cudaMemsetAsync(ws, 0, need, st));
+    auto* counter = static_cast<unsigned int*>(ws);
+    auto* state = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 256);
+    switch (kind) {
+        case kScanSlots:
+            row_scan_kernel<kScanSlots><<<(unsigned)tiles, kScanThreads, 0, st>>>(a, state, counter);
+            break;
+        case kScanStarts:
+            row_scan_kernel<kScanStarts><<<(unsigned)tiles, kScanThreads, 0, st>>>(a, state, counter);
+            break;
+        default:
+            row_scan_kernel<kScanGcnNnz><<<(unsigned)tiles, kScanThreads, 0, st>>>(a, state, counter);
+            break;
+    }
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
+// ===========================================================================
+// Slot-order fill.  A CTA owns 256 consecutive rows and flattens their slots;
+// each thread takes slots in stride, finds its row by binary search over the
+// sampled row pointer staged in shared memory, and copies one (col, val) —
+// writes are fully coalesced, reads are contiguous runs of chunk_len.
+// ===========================================================================
+namespace {
+
+constexpr int kFillRows = 256;
+
+__global__ void __launch_bounds__(kFillRows)
+sample_fill_kernel(const uint64_t* __restrict__ plan_row_ptr, const uint64_t* __restrict__ row_ptr,
+                   const uint32_t* __restrict__ col_ind, const float* __restrict__ val,
+                   uint64_t n, uint32_t width, int strategy, const uint64_t* __restrict__ srow_ptr,
+                   uint32_t* __restrict__ scol, float* __restrict__ sval) {
+    __shared__ uint64_t s_srow[kFillRows + 1];
+    __shared__ uint64_t s_prp[kFillRows + 1];
+    __shared__ uint64_t s_rp[kFillRows];
+    const uint64_t r0 = (uint64_t)blockIdx.x * kFillRows;
+    const int nr = (int)min((uint64_t)kFillRows, n - r0);
+    for (int i = threadIdx.x; i <= nr; i += blockDim.x) {
+        s_srow[i] = srow_ptr[r0 + i];
+        s_prp[i] = plan_row_ptr[r0 + i];
+        if (i < nr) s_rp[i] = row_ptr[r0 + i];
+    }
+    __syncthreads();
+    const uint64_t g0 = s_srow[0];
+    const uint64_t total = s_srow[nr] - g0;
+    for (uint64_t t = threadIdx.x; t < total; t += blockDim.x) {
+        const uint64_t pos = g0 + t;
+        // last row with start <= pos (skips empty rows sharing the start)
+        int lo = 0, hi = nr;  // invariant: s_srow[lo] <= pos < s_srow[hi]
+        while (hi - lo > 1) {
+            int mid = (lo + hi) >> 1;
+            if (s_srow[mid] <= pos) lo = mid; else hi = mid;
+        }
+        const uint64_t nnz = s_prp[lo + 1] - s_prp[lo];
+        const RowParams p = row_params(nnz, width, strategy);
+        const uint64_t k = pos - s_srow[lo];
+        uint64_t s, j;
+        if (p.cnt == 1) {
+            s = 0; j = k;
+        } else {
+            uint32_t k32 = (uint32_t)k;  // adaptive/afs rows have <= W slots
+            s = k32 % p.cnt; j = k32 / p.cnt;
+        }
+        const uint64_t src = s_rp[lo] + row_start(nnz, width, strategy, p, (uint32_t)s) + j;
+        scol[pos] = col_ind[src];
+        sval[pos] = val[src];
+    }
+}
+
+// Export RowSamplePlan data (module.cpp:72-81) as flat arrays.
+__global__ void plan_export_kernel(const uint64_t* __restrict__ row_ptr, uint64_t n, uint32_t width,
+                                   int strategy, const uint64_t* __restrict__ starts_ptr,
+                                   uint32_t* __restrict__ chunk, uint32_t* __restrict__ cnt,
+                                   uint32_t* __restrict__ starts) {
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n;
+         r += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t nnz = row_ptr[r + 1] - row_ptr[r];
+        RowParams p = row_params(nnz, width, strategy);
+        chunk[r] = p.chunk;
+        cnt[r] = p.cnt;
+        uint32_t ns = row_num_starts(nnz, width, strategy, p);
+        uint64_t b = starts_ptr[r];
+        for (uint32_t s = 0; s < ns; ++s) starts[b + s] = row_start(nnz, width, strategy, p, s);
+    }
+}
+
+// sampling_rate (sampling.cpp:120-152): per-row slots/nnz, and totals of
+// slots, distinct sampled offsets and nnz (integer sums -> deterministic).
+__global__ void sampling_rate_kernel(const uint64_t* __restrict__ row_ptr, uint64_t n, uint32_t width,
+                                     int strategy, double* __restrict__ per_row,
+                                     unsigned long long* __restrict__ totals) {
+    uint64_t slots_sum = 0, uniq_sum = 0, nnz_sum = 0;
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n;
+         r += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t nnz = row_ptr[r + 1] - row_ptr[r];
+        nnz_sum += nnz;
+        if (nnz == 0) {
+            if (per_row) per_row[r] = 1.0;
+            continue;
+        }
+        RowParams p = row_params(nnz, width, strategy);
+        uint64_t slots = (uint64_t)p.chunk * p.cnt;
+        slots_sum += slots;
+        if (per_row) per_row[r] = (double)slots / (double)nnz;
+        uint64_t uniq;
+        if (strategy == AES_FULL) {
+            uniq = nnz;
+        } else if (strategy == AES_SFS) {
+            uniq = p.chunk;
+        } else if (strategy == AES_AFS) {
+            uniq = p.cnt;  // floor(s*nnz/cnt) strictly increases for cnt <= nnz
+        } else if (nnz <= width) {
+            uniq = nnz;
+        } else {
+            // union of cnt (<= 32) windows of length chunk
+            uint32_t st[32];
+            uint32_t c = p.cnt;
+            for (uint32_t s = 0; s < c; ++s) st[s] = hash_start(s, nnz, p.chunk);
+            for (uint32_t i = 1; i < c; ++i) {  // insertion sort
+                uint32_t v = st[i];
+                int j = (int)i - 1;
+                while (j >= 0 && st[j] > v) { st[j + 1] = st[j]; --j; }
+                st[j + 1] = v;
+            }
+            uniq = 0;
+            uint64_t cover_end = 0;  // exclusive end of covered prefix
+            for (uint32_t s = 0; s < c; ++s) {
+                uint64_t b = st[s], e = b + p.chunk;
+                if (b < cover_end) b = cover_end;
+                if (e > b) { uniq += e - b; cover_end = e; }
+            }
+        }
+        uniq_sum += uniq;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        slots_sum += __shfl_down_sync(0xffffffffu, slots_sum, o);
+        uniq_sum += __shfl_down_sync(0xffffffffu, uniq_sum, o);
+        nnz_sum += __shfl_down_sync(0xffffffffu, nnz_sum, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&totals[0], (unsigned long long)slots_sum);
+        atomicAdd(&totals[1], (unsigned long long)uniq_sum);
+        atomicAdd(&totals[2], (unsigned long long)nnz_sum);
+    }
+}
+
+// row_stats (matrix.cpp:54-63)
+__global__ void row_stats_kernel(const uint64_t* __restrict__ row_ptr, uint64_t n,
+                                 uint64_t* __restrict__ row_nnz, unsigned long long* __restrict__ max_nnz) {
+    unsigned long long m = 0;
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n;
+         r += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t d = row_ptr[r + 1] - row_ptr[r];
+        if (row_nnz) row_nnz[r] = d;
+        m = d > m ? d : m;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long t = __shfl_down_sync(0xffffffffu, m, o);
+        m = t > m ? t : m;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(max_nnz, m);
+}
+
+// validate_csr (matrix.cpp:28-52), pass 1: first decreasing row_ptr step.
+__global__ void validate_monotonic_kernel(const uint64_t* __restrict__ row_ptr, uint64_t n,
+                                          unsigned long long* __restrict__ first_bad) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (row_ptr[i + 1] < row_ptr[i]) atomicMin(first_bad, (unsigned long long)(i + 1));
+    }
+}
+
+// pass 2: warp per row; the first offending element of the lowest row wins.
+// code = (row << 2) | error, error 2 = ColumnOutOfRange, 3 = UnsortedRow.
+__global__ void validate_rows_kernel(const uint64_t* __restrict__ row_ptr,
+                                     const uint32_t* __restrict__ col, uint64_t n, uint64_t n_cols,
+                                     unsigned long long* __restrict__ first_bad) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
+        const uint64_t b = row_ptr[r], e = row_ptr[r + 1];
+        for (uint64_t k0 = b; k0 < e; k0 += 32) {
+            uint64_t k = k0 + lane;
+            int err = 0;
+            if (k < e) {
+                uint32_t c = col[k];
+                if (c >= n_cols) err = AES_CSR_COL_OUT_OF_RANGE;
+                else if (k > b && c <= col[k - 1]) err = AES_CSR_UNSORTED;
+            }
+            unsigned bad = __ballot_sync(0xffffffffu, err != 0);
+            if (bad) {
+                int first = __ffs(bad) - 1;
+                int e_first = __shfl_sync(0xffffffffu, err, first);
+                if (lane == 0) atomicMin(first_bad, (unsigned long long)((r << 2) | (uint64_t)e_first));
+                break;
+            }
+        }
+    }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Internal launchers used by the handle API
+// ---------------------------------------------------------------------------
+int launch_sample_fill(const uint64_t* plan_row_ptr, const uint64_t* row_ptr, const uint32_t* col,
+                       const float* val, uint64_t n, uint32_t width, int strategy,
+                       const uint64_t* srow_ptr, uint32_t* scol, float* sval, cudaStream_t st) {
+    if (n == 0) return AES_OK;
+    unsigned grid = grid_for(n, kFillRows);
+    sample_fill_kernel<<<grid, kFillRows, 0, st>>>(plan_row_ptr, row_ptr, col, val, n, width, strategy,
+                                                   srow_ptr, scol, sval);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
+int launch_plan_export(const uint64_t* row_ptr, uint64_t n, uint32_t width, int strategy,
+                       const uint64_t* starts_ptr, uint32_t* chunk, uint32_t* cnt, uint32_t* starts,
+                       cudaStream_t st) {
+    if (n == 0) return AES_OK;
+    plan_export_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(row_ptr, n, width, strategy,
+                                                                   starts_ptr, chunk, cnt, starts);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
+int launch_sampling_rate(const uint64_t* row_ptr, uint64_t n, uint32_t width, int strategy,
+                         double* per_row, unsigned long long* totals, cudaStream_t st) {
+    AES_CUDA_TRY(cudaMemsetAsync(totals, 0, 3 * sizeof(unsigned long long), st));
+    if (n == 0) return AES_OK;
+    sampling_rate_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(row_ptr, n, width, strategy,
+                                                                     per_row, totals);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
+int launch_row_stats(const uint64_t* row_ptr, uint64_t n, uint64_t* row_nnz,
+                     unsigned long long* max_nnz, cudaStream_t st) {
+    AES_CUDA_TRY(cudaMemsetAsync(max_nnz, 0, sizeof(unsigned long long), st));
+    if (n == 0) return AES_OK;
+    row_stats_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(row_ptr, n, row_nnz, max_nnz);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
+int launch_validate(const uint64_t* row_ptr, const uint32_t* col, uint64_t n, uint64_t n_cols,
+                    unsigned long long* scratch2, cudaStream_t st) {
+    AES_CUDA_TRY(cudaMemsetAsync(scratch2, 0xff, 2 * sizeof(unsigned long long), st));
+    if (n == 0) return AES_OK;
+    validate_monotonic_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(row_ptr, n, scratch2);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
+int launch_validate_rows(const uint64_t* row_ptr, const uint32_t* col, uint64_t n, uint64_t n_cols,
+                         unsigned long long* scratch, cudaStream_t st) {
+    if (n == 0) return AES_OK;
+    validate_rows_kernel<<<grid_for(n * 32, 256, 148 * 32), 256, 0, st>>>(row_ptr, col, n, n_cols,
+                                                                         scratch);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
+}  // namespace aes
+
+// ===========================================================================
+// C ABI: device tier
+// ===========================================================================
+extern "C" {
+
+size_t aes_dev_scan_workspace_bytes(uint64_t n_rows) {
+    size_t a = aes::row_scan_workspace_bytes(n_rows);
+    size_t b = 256 + 2 * 148 * 8 * 32;  // fit_params partials
+    return a > b ? a : b;
+}
+
+int aes_dev_sample_plan(const uint64_t* plan_row_ptr, uint64_t n_rows, uint32_t width, int strategy,
+                        uint64_t* srow_ptr, uint32_t* row_params, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+    if (width == 0) return aes::fail(AES_ERR_ZERO_WIDTH, "ZeroWidth");
+    if (strategy < 0 || strategy > 3) return aes::fail(AES_ERR_INVALID_ARG, "unknown strategy");
+    aes::ScanArgs a{plan_row_ptr, nullptr, n_rows, width, strategy, 0, srow_ptr, row_params};
+    return aes::launch_row_scan(aes::kScanSlots, a, workspace, workspace_bytes, aes::as_stream(stream));
+}
+
+int aes_dev_sample_fill(const uint64_t* plan_row_ptr, const uint64_t* row_ptr,
+                        const uint32_t* col_ind, const float* val, uint64_t n_rows, uint32_t width,
+                        int strategy, const uint64_t* srow_ptr, uint32_t* scol, float* sval,
+                        void* stream) {
+    if (width == 0) return aes::fail(AES_ERR_ZERO_WIDTH, "ZeroWidth");
+    return aes::launch_sample_fill(plan_row_ptr, row_ptr, col_ind, val, n_rows, width, strategy,
+                                   srow_ptr, scol, sval, aes::as_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,351 @@
+// Gather-SpMM over a (sampled) CSR for sm_100a, fp32 and int8-with-fused-
+// dequantization.  Bit-exact with the reference accumulation
+// (proj/src/spmm.cpp:77-84): each output element is owned by one lane and
+// accumulated in ascending slot order as acc = RN(acc + RN(v * b)) starting
+// from +0.0f — __fmul_rn/__fadd_rn keep ptxas from contracting into FFMA.
+//
+// Mapping (HBM-bound irregular gather, no tensor cores):
+//  * wide rows (>= 32 float4 columns, e.g. F = 128): one warp owns a GROUP of
+//    32 consecutive rows.  The warp loads the group's 33 row offsets with one
+//    coalesced load, then streams the group's slots in batches of U slots
+//    across row boundaries: slot metadata (col, val) for a batch is loaded by
+//    U lanes in one coalesced request and broadcast by shuffle, the U dense-row
+//    gathers (512 B each at F = 128, one LDG.128 per lane) are all issued
+//    before any is consumed, and the next batch's metadata is prefetched under
+//    them.  Memory-level parallelism is therefore U rows per warp regardless
+//    of how short the rows are (products: 72 % of rows have <= 4 slots).
+//  * narrow rows (F <= 64): sub-warp units of LPR lanes, one row each.
+//  * int8: the same schedule gathers 4 codes per lane (u32) and dequantizes
+//    through a 256-entry LUT replicated per shared-memory bank (lut[q][lane],
+//    conflict-free) — the exact value dequantize() produces, so the result is
+//    bit-identical to the fp32 kernel over dequantize(Q).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace aes {
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ float4 f4_zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+
+__device__ __forceinline__ void f4_axpy(float4& acc, float v, const float4& b) {
+    acc.x = __fadd_rn(acc.x, __fmul_rn(v, b.x));
+    acc.y = __fadd_rn(acc.y, __fmul_rn(v, b.y));
+    acc.z = __fadd_rn(acc.z, __fmul_rn(v, b.z));
+    acc.w = __fadd_rn(acc.w, __fmul_rn(v, b.w));
+}
+
+__device__ __forceinline__ uint32_t ld_meta_u32(const uint32_t* p) { return __ldcs(p); }
+__device__ __forceinline__ float ld_meta_f32(const float* p) { return __ldcs(p); }
+
+// ---------------------------------------------------------------------------
+// Gather "element" abstraction: fp32 rows (float4 per lane-column) or u8 code
+// rows (4 codes per lane-column, dequantized through the banked LUT).
+// ---------------------------------------------------------------------------
+struct GatherF32 {
+    const float4* __restrict__ b;
+    uint64_t ld4;  // row stride in float4
+    typedef float4 raw_t;
+    __host__ void offset(uint32_t c0) { b += c0; }
+    __device__ __forceinline__ raw_t load(uint32_t row, uint32_t c4) const {
+        return __ldg(b + (uint64_t)row * ld4 + c4);
+    }
+    __device__ __forceinline__ float4 decode(const raw_t& r, const float*) const { return r; }
+};
+
+struct GatherQ8 {
+    const uint32_t* __restrict__ q;
+    uint64_t ld4;  // row stride in u32 (4 codes)
+    typedef uint32_t raw_t;
+    __host__ void offset(uint32_t c0) { q += c0; }
+    __device__ __forceinline__ raw_t load(uint32_t row, uint32_t c4) const {
+        return __ldg(q + (uint64_t)row * ld4 + c4);
+    }
+    // lut is this lane's column of the banked table: lut[code * 32]
+    __device__ __forceinline__ float4 decode(const raw_t& r, const float* lut) const {
+        return make_float4(lut[(r & 0xffu) << 5], lut[((r >> 8) & 0xffu) << 5],
+                           lut[((r >> 16) & 0xffu) << 5], lut[(r >> 24) << 5]);
+    }
+};
+
+template <class G>
+struct LutSmem {
+    __device__ __forceinline__ static const float* setup(const float*, float*) { return nullptr; }
+};
+template <>
+struct LutSmem<GatherQ8> {
+    __device__ __forceinline__ static const float* setup(const float* lut_g, float* smem) {
+        // smem[q * 32 + bank] = lut[q]
+        for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) smem[i] = lut_g[i >> 5];
+        __syncthreads();
+        return smem + (threadIdx.x & 31);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Wide kernel: warp per 32-row group, flattened slot stream, U-slot batches.
+// Lane handles float4 columns lane + 32*n for n < NV.
+// ---------------------------------------------------------------------------
+template <class G, int NV, int U>
+__global__ void __launch_bounds__(kThreads)
+spmm_wide_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
+                 const float* __restrict__ sval, uint64_t n_rows, G g, uint32_t f4, float4* __restrict__ c,
+                 uint64_t ldc4, const float* __restrict__ lut_g) {
+    extern __shared__ float smem_lut[];
+    const float* lut = LutSmem<G>::setup(lut_g, smem_lut);
+
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
+    const uint64_t r0 = warp * 32;
+    if (r0 >= n_rows) return;
+    const uint32_t nr = (uint32_t)min((uint64_t)32, n_rows - r0);
+
+    // row offsets of the group: lane l holds the END of row l (one coalesced
+    // load of srow[r0+1 .. r0+32]); the group start is a broadcast load.
+    const uint64_t g0 = srow[r0];
+    const uint64_t my_end = srow[r0 + 1 + min(lane, nr - 1)];
+    const uint64_t total = __shfl_sync(0xffffffffu, my_end, nr - 1) - g0;
+    const uint32_t rel = (uint32_t)(my_end - g0);  // relative row end (group < 2^32 slots)
+
+    float4 acc[NV];
+#pragma unroll
+    for (int n = 0; n < NV; ++n) acc[n] = f4_zero();
+
+    bool colok[NV];
+#pragma unroll
+    for (int n = 0; n < NV; ++n) colok[n] = lane + 32u * n < f4;
+
+    float4* crow = c + r0 * ldc4;
+    uint32_t row = 0;
+    uint32_t row_end = __shfl_sync(0xffffffffu, rel, 0);
+
+    auto store_row = [&](uint32_t r) {
+#pragma unroll
+        for (int n = 0; n < NV; ++n)
+            if (colok[n]) __stcs(crow + (uint64_t)r * ldc4 + lane + 32u * n, acc[n]);
+#pragma unroll
+        for (int n = 0; n < NV; ++n) acc[n] = f4_zero();
+    };
+    // leading empty rows
+    while (row < nr && row_end == 0) {
+        store_row(row);
+        ++row;
+        row_end = __shfl_sync(0xffffffffu, rel, min(row, nr - 1));
+    }
+
+    // metadata for the first batch
+    uint32_t mc = 0;
+    float mv = 0.f;
+    if (lane < (uint32_t)U && lane < total) {
+        mc = ld_meta_u32(scol + g0 + lane);
+        mv = ld_meta_f32(sval + g0 + lane);
+    }
+
+    for (uint64_t t = 0; t < total; t += U) {
+        typename G::raw_t braw[U][NV];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t cidx = __shfl_sync(0xffffffffu, mc, u);
+            if (t + u < total) {
+#pragma unroll
+                for (int n = 0; n < NV; ++n)
+                    if (colok[n]) braw[u][n] = g.load(cidx, lane + 32u * n);
+            }
+        }
+        float vv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) vv[u] = __shfl_sync(0xffffffffu, mv, u);
+        // prefetch next batch's metadata under the gathers
+        if (lane < (uint32_t)U && t + U + lane < total) {
+            mc = ld_meta_u32(scol + g0 + t + U + lane);
+            mv = ld_meta_f32(sval + g0 + t + U + lane);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (t + u < total) {
+#pragma unroll
+                for (int n = 0; n < NV; ++n)
+                    if (colok[n]) f4_axpy(acc[n], vv[u], g.decode(braw[u][n], lut));
+                const uint32_t pos = (uint32_t)(t + u + 1);
+                if (pos == row_end) {
+                    store_row(row);
+                    ++row;
+                    row_end = __shfl_sync(0xffffffffu, rel, min(row, nr - 1));
+                    while (row < nr && row_end == pos) {  // empty rows
+                        store_row(row);
+                        ++row;
+                        row_end = __shfl_sync(0xffffffffu, rel, min(row, nr - 1));
+                    }
+                }
+            }
+        }
+    }
+    while (row < nr) {  // trailing empty rows of a group with no slots left
+        store_row(row);
+        ++row;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Narrow kernel: LPR lanes per row (LPR in 1..16), one float4 column each.
+// ---------------------------------------------------------------------------
+template <class G, int LPR, int U>
+__global__ void __launch_bounds__(kThreads)
+spmm_narrow_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
+                   const float* __restrict__ sval, uint64_t n_rows, G g, uint32_t f4,
+                   float4* __restrict__ c, uint64_t ldc4, const float* __restrict__ lut_g) {
+    extern __shared__ float smem_lut[];
+    const float* lut = LutSmem<G>::setup(lut_g, smem_lut);
+    const uint64_t tid = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
+    const uint64_t row = tid / LPR;
+    const uint32_t li = (uint32_t)(tid % LPR);
+    if (row >= n_rows) return;
+    const bool ok = li < f4;
+    const uint64_t k0 = srow[row], k1 = srow[row + 1];
+    float4 acc = f4_zero();
+    for (uint64_t k = k0; k < k1; k += U) {
+        uint32_t cc[U];
+        float vv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (k + u < k1) {
+                cc[u] = ld_meta_u32(scol + k + u);
+                vv[u] = ld_meta_f32(sval + k + u);
+            }
+        }
+        typename G::raw_t braw[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (k + u < k1 && ok) braw[u] = g.load(cc[u], li);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (k + u < k1 && ok) f4_axpy(acc, vv[u], g.decode(braw[u], lut));
+    }
+    if (ok) __stcs(c + row * ldc4 + li, acc);
+}
+
+// ---------------------------------------------------------------------------
+// Scalar kernel for layouts the vector path cannot take (ld % 4 != 0 or
+// misaligned): warp per row, lane per column, same ordering.
+// ---------------------------------------------------------------------------
+template <int U>
+__global__ void __launch_bounds__(kThreads)
+spmm_scalar_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
+                   const float* __restrict__ sval, uint64_t n_rows, const float* __restrict__ b,
+                   uint64_t ldb, uint64_t f, float* __restrict__ c, uint64_t ldc) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warps = ((uint64_t)gridDim.x * kThreads) >> 5;
+    for (uint64_t row = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5; row < n_rows; row += warps) {
+        const uint64_t k0 = srow[row], k1 = srow[row + 1];
+        for (uint64_t j0 = 0; j0 < f; j0 += 32) {
+            const uint64_t j = j0 + lane;
+            const bool ok = j < f;
+            float acc = 0.f;
+            for (uint64_t k = k0; k < k1; k += U) {
+                float bv[U], vv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (k + u < k1) {
+                        uint32_t cc = scol[k + u];
+                        vv[u] = sval[k + u];
+                        if (ok) bv[u] = __ldg(b + (uint64_t)cc * ldb + j);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (k + u < k1 && ok) acc = __fadd_rn(acc, __fmul_rn(vv[u], bv[u]));
+            }
+            if (ok) c[row * ldc + j] = acc;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// dispatch
+// ---------------------------------------------------------------------------
+template <class G>
+int launch_vector(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n,
+                  G g, uint32_t f4, float4* c, uint64_t ldc4, const float* lut, cudaStream_t st) {
+    const size_t smem = lut ? 256 * 32 * sizeof(float) : 0;
+    if (f4 <= 16) {
+        uint32_t lpr = f4 <= 1 ? 1 : f4 <= 2 ? 2 : f4 <= 4 ? 4 : f4 <= 8 ? 8 : 16;
+        unsigned grid = grid_for(n * lpr, kThreads);
+        switch (lpr) {
+            case 1: spmm_narrow_kernel<G, 1, 4><<<grid, kThreads, smem, st>>>(srow, scol, sval, n, g, f4, c, ldc4, lut); break;
+            case 2: spmm_narrow_kernel<G, 2, 4><<<grid, kThreads, smem, st>>>(srow, scol, sval, n, g, f4, c, ldc4, lut); break;
+            case 4: spmm_narrow_kernel<G, 4, 4><<<grid, kThreads, smem, st>>>(srow, scol, sval, n, g, f4, c, ldc4, lut); break;
+            case 8: spmm_narrow_kernel<G, 8, 4><<<grid, kThreads, smem, st>>>(srow, scol, sval, n, g, f4, c, ldc4, lut); break;
+            default: spmm_narrow_kernel<G, 16, 4><<<grid, kThreads, smem, st>>>(srow, scol, sval, n, g, f4, c, ldc4, lut); break;
+        }
+        AES_CUDA_TRY(cudaGetLastError());
+        return AES_OK;
+    }
+    // wide: column tiles of up to 256 float4 (1024 floats)
+    for (uint32_t c0 = 0; c0 < f4; c0 += 256) {
+        uint32_t tf4 = min(256u, f4 - c0);
+        G gt = g;
+        gt.offset(c0);
+        float4* ct = c + c0;
+        unsigned grid = grid_for((n + 31) / 32 * 32, kThreads);
+        uint32_t nv = (tf4 + 31) / 32;
+        switch (nv) {
+            case 1: spmm_wide_kernel<G, 1, 8><<<grid, kThreads, smem, st>>>(srow, scol, sval, n, gt, tf4, ct, ldc4, lut); break;
+            case 2: spmm_wide_kernel<G, 2, 4><<<grid, kThreads, smem, st>>>(srow, scol, sval, n, gt, tf4, ct, ldc4, lut); break;
+            case 3: spmm_wide_kernel<G, 3, 2><<<grid, kThreads, smem, st>>>(srow, scol, sval, n, gt, tf4, ct, ldc4, lut); break;
+            case 4: spmm_wide_kernel<G, 4, 2><<<grid, kThreads, smem, st>>>(srow, scol, sval, n, gt, tf4, ct, ldc4, lut); break;
+            case 5: spmm_wide_kernel<G, 5, 1><<<grid, kThreads, smem, st>>>(srow, scol, sval, n, gt, tf4, ct, ldc4, lut); break;
+            case 6: spmm_wide_kernel<G, 6, 1><<<grid, kThreads, smem, st>>>(srow, scol, sval, n, gt, tf4, ct, ldc4, lut); break;
+            case 7: spmm_wide_kernel<G, 7, 1><<<grid, kThreads, smem, st>>>(srow, scol, sval, n, gt, tf4, ct, ldc4, lut); break;
+            default: spmm_wide_kernel<G, 8, 1><<<grid, kThreads, smem, st>>>(srow, scol, sval, n, gt, tf4, ct, ldc4, lut); break;
+        }
+        AES_CUDA_TRY(cudaGetLastError());
+    }
+    return AES_OK;
+}
+
+}  // namespace
+}  // namespace aes
+
+extern "C" {
+
+int aes_dev_spmm_f32(const uint64_t* srow_ptr, const uint32_t* scol, const float* sval,
+                     uint64_t n_rows, const float* b, uint64_t ldb, uint64_t f, float* c,
+                     uint64_t ldc, void* stream) {
+    using namespace aes;
+    cudaStream_t st = as_stream(stream);
+    if (n_rows == 0 || f == 0) return AES_OK;
+    if (ldb < f || ldc < f) return fail(AES_ERR_INVALID_ARG, "leading dimension smaller than f");
+    const uint64_t f4 = (f + 3) / 4;
+    const bool vec = (ldb % 4 == 0) && (ldc % 4 == 0) && ((uintptr_t)b % 16 == 0) &&
+                     ((uintptr_t)c % 16 == 0) && ldb >= f4 * 4 && ldc >= f4 * 4;
+    if (vec) {
+        GatherF32 g{reinterpret_cast<const float4*>(b), ldb / 4};
+        return launch_vector(srow_ptr, scol, sval, n_rows, g, (uint32_t)f4,
+                             reinterpret_cast<float4*>(c), ldc / 4, nullptr, st);
+    }
+    spmm_scalar_kernel<4><<<grid_for(n_rows * 32, kThreads, 148 * 64), kThreads, 0, st>>>(
+        srow_ptr, scol, sval, n_rows, b, ldb, f, c, ldc);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
+int aes_dev_spmm_q8(const uint64_t* srow_ptr, const uint32_t* scol, const float* sval,
+                    uint64_t n_rows, const uint8_t* q, uint64_t ldq, uint64_t f, const float* lut,
+                    float* c, uint64_t ldc, void* stream) {
+    using namespace aes;
+    cudaStream_t st = as_stream(stream);
+    if (n_rows == 0 || f == 0) return AES_OK;
+    const uint64_t f4 = (f + 3) / 4;
+    if (ldq % 4 != 0 || (uintptr_t)q % 4 != 0 || ldq < f4 * 4 || ldc % 4 != 0 ||
+        (uintptr_t)c % 16 != 0 || ldc < f4 * 4 || lut == nullptr)
+        return fail(AES_ERR_UNSUPPORTED,
+                    "spmm_q8 needs ldq % 4 == 0, ldc % 4 == 0 and ld >= round_up(f, 4)");
+    GatherQ8 g{reinterpret_cast<const uint32_t*>(q), ldq / 4};
+    return launch_vector(srow_ptr, scol, sval, n_rows, g, (uint32_t)f4,
+                         reinterpret_cast<float4*>(c), ldc / 4, lut, st);
+}
+
+}  // extern "C"

@@ -1,0 +1,223 @@
+"""Device-resident AES-SpMM API over torch CUDA tensors (zero host copies).
+
+Layout in HBM:
+  * graph CSR: ``row_ptr`` int64 [n+1] (the reference's u64), ``col`` int32
+    [nnz] (u32 bits), ``val`` float32 [nnz];
+  * sampled CSR (one per (graph, W, strategy), reused by every layer):
+    ``srow_ptr`` int64 [n+1], ``scol`` int32 [S], ``sval`` float32 [S] in the
+    reference's slot order (slot s + j*cnt, proj/src/spmm.cpp:68-76);
+  * dense features: row-major float32 with the row stride padded to a
+    multiple of 4 floats (16 B) so every gathered row is float4-aligned
+    (F = 602 is stored with ld = 604); int8 codes likewise with ld % 4 == 0.
+
+Every function launches sm_100a kernels from libaescuda.so through the C ABI
+on the caller's (default: torch's current) stream and never synchronises
+unless it has to read a size back (plan building, quantization params).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import capi
+from .capi import check, lib, ptr, stream_of
+
+
+def _round4(x: int) -> int:
+    return (x + 3) & ~3
+
+
+def padded(x: torch.Tensor) -> torch.Tensor:
+    """Return a view of ``x`` whose row stride is a multiple of 4 elements."""
+    assert x.dim() == 2
+    if x.stride(1) == 1 and x.stride(0) % 4 == 0 and x.data_ptr() % 16 == 0:
+        return x
+    r, f = x.shape
+    buf = torch.zeros((r, _round4(max(f, 1))), dtype=x.dtype, device=x.device)
+    buf[:, :f].copy_(x)
+    return buf[:, :f]
+
+
+def empty_padded(rows: int, cols: int, dtype=torch.float32, device="cuda") -> torch.Tensor:
+    buf = torch.empty((rows, _round4(max(cols, 1))), dtype=dtype, device=device)
+    return buf[:, :cols]
+
+
+@dataclass
+class Graph:
+    """A CSR matrix resident in HBM."""
+
+    row_ptr: torch.Tensor  # int64 [n+1]
+    col: torch.Tensor      # int32 [nnz]
+    val: torch.Tensor      # float32 [nnz]
+    n_cols: int
+
+    @property
+    def n_rows(self) -> int:
+        return self.row_ptr.numel() - 1
+
+    @property
+    def nnz(self) -> int:
+        return self.col.numel()
+
+    @classmethod
+    def from_numpy(cls, row_ptr, col, val, n_cols=None, device="cuda") -> "Graph":
+        import numpy as np
+
+        rp = torch.from_numpy(np.ascontiguousarray(row_ptr, np.uint64).view(np.int64)).to(device)
+        ci = torch.from_numpy(np.ascontiguousarray(col, np.uint32).view(np.int32)).to(device)
+        vv = torch.from_numpy(np.ascontiguousarray(val, np.float32)).to(device)
+        n = rp.numel() - 1
+        return cls(rp, ci, vv, n if n_cols is None else int(n_cols))
+
+    def rows(self, begin: int, end: int) -> "Graph":
+        """Row shard [begin, end) as a view; row_ptr stays absolute."""
+        return Graph(self.row_ptr[begin:end + 1], self.col, self.val, self.n_cols)
+
+
+class SampledPlan:
+    """build_plan_set + the buffer fill, materialised once in HBM
+    (proj/src/sampling.cpp:104-118, proj/src/spmm.cpp:54-76)."""
+
+    def __init__(self, graph: Graph, width: int, strategy="adaptive", stream=None):
+        L = lib()
+        self.width = int(width)
+        self.strategy = capi.strategy_code(strategy)
+        n = graph.n_rows
+        dev = graph.row_ptr.device
+        st = stream_of(stream)
+        self.n_rows = n
+        self.srow_ptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        self.row_params = torch.empty((max(n, 1), 2), dtype=torch.int32, device=dev)
+        ws_bytes = L.aes_dev_scan_workspace_bytes(n)
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        check(L.aes_dev_sample_plan(ptr(graph.row_ptr), n, self.width, self.strategy, ptr(self.srow_ptr),
+                                    ptr(self.row_params), ptr(ws), ws_bytes, st))
+        # the absolute offset of this (possibly sharded) row range
+        self.base = int(self.srow_ptr[0].item()) if n else 0
+        self.total_slots = int(self.srow_ptr[-1].item()) - self.base
+        self.scol = torch.empty(max(self.total_slots, 1), dtype=torch.int32, device=dev)
+        self.sval = torch.empty(max(self.total_slots, 1), dtype=torch.float32, device=dev)
+        check(L.aes_dev_sample_fill(ptr(graph.row_ptr), ptr(graph.row_ptr), ptr(graph.col), ptr(graph.val), n,
+                                    self.width, self.strategy, ptr(self.srow_ptr), ptr(self.scol),
+                                    ptr(self.sval), st))
+        del ws
+
+    def algorithmic_bytes(self, f: int, elem_bytes: int = 4) -> int:
+        """Bytes one SpMM over this plan must move:
+        8(N+1) row offsets + 8S (col, val) + e*F*S gathered + 4*F*N written."""
+        n, s = self.n_rows, self.total_slots
+        return 8 * (n + 1) + 8 * s + elem_bytes * f * s + 4 * f * n
+
+
+def spmm(srow_ptr, scol, sval, b: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """C = A_sampled @ B (bit-exact with the reference spmm_sampled)."""
+    n = srow_ptr.numel() - 1
+    f = b.shape[1]
+    if out is None:
+        out = empty_padded(n, f, device=b.device)
+    check(lib().aes_dev_spmm_f32(ptr(srow_ptr), ptr(scol), ptr(sval), n, ptr(b), b.stride(0), f, ptr(out),
+                                 out.stride(0), stream_of(stream)))
+    return out
+
+
+def spmm_plan(plan: SampledPlan, b: torch.Tensor, out=None, stream=None) -> torch.Tensor:
+    return spmm(plan.srow_ptr, plan.scol, plan.sval, b, out, stream)
+
+
+def spmm_exact(g: Graph, b: torch.Tensor, out=None, stream=None) -> torch.Tensor:
+    return spmm(g.row_ptr, g.col, g.val, b, out, stream)
+
+
+@dataclass
+class QuantizedDevice:
+    """int8 codes (bits <= 8) in HBM with their global params and the exact
+    dequantization table (proj/include/aesspmm/quantize.hpp:10-25)."""
+
+    codes: torch.Tensor  # uint8 [rows, cols] view with ld % 4 == 0
+    x_min: float
+    x_max: float
+    bits: int
+    lut: torch.Tensor    # float32 [256]
+
+
+def fit_params(x: torch.Tensor, stream=None):
+    """Global (x_min, x_max) — quantize.cpp:11-21.  Synchronises once."""
+    L = lib()
+    x = x.contiguous()
+    n = x.numel()
+    if n == 0:
+        raise ValueError("EmptyMatrix")
+    ws_bytes = L.aes_dev_scan_workspace_bytes(1)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=x.device)
+    res = torch.empty(4, dtype=torch.float32, device=x.device)
+    check(L.aes_dev_fit_params(ptr(x), n, ptr(res), ptr(ws), ws_bytes, stream_of(stream)))
+    r = res.cpu()
+    if r.view(torch.int32)[2].item() != 0:
+        raise ValueError("NonFinite")
+    return float(r[0]), float(r[1])
+
+
+def quantize(x: torch.Tensor, bits: int = 8, params=None, stream=None) -> QuantizedDevice:
+    """quantize(x, fit_params(x, bits)) — quantize.cpp:23-51, codes kept as u8."""
+    if not 1 <= bits <= 8:
+        raise ValueError("device int8 path takes bits in 1..8")
+    L = lib()
+    lo, hi = params if params is not None else fit_params(x, stream)
+    rows, cols = x.shape
+    codes = empty_padded(rows, cols, dtype=torch.uint8, device=x.device)
+    st = stream_of(stream)
+    check(L.aes_dev_quantize(ptr(x), rows, cols, x.stride(0), lo, hi, bits, ptr(codes), codes.stride(0), st))
+    lut = torch.zeros(256, dtype=torch.float32, device=x.device)
+    check(L.aes_dev_dequant_lut(lo, hi, bits, ptr(lut), st))
+    return QuantizedDevice(codes, lo, hi, bits, lut)
+
+
+def dequantize(q: QuantizedDevice, stream=None) -> torch.Tensor:
+    rows, cols = q.codes.shape
+    out = empty_padded(rows, cols, device=q.codes.device)
+    check(lib().aes_dev_dequantize(ptr(q.codes), rows, cols, q.codes.stride(0), q.x_min, q.x_max, q.bits,
+                                   ptr(out), out.stride(0), stream_of(stream)))
+    return out
+
+
+def spmm_q8(srow_ptr, scol, sval, q: QuantizedDevice, out=None, stream=None) -> torch.Tensor:
+    """spmm(A, dequantize(Q)) with dequantization fused into the u8 gather."""
+    n = srow_ptr.numel() - 1
+    f = q.codes.shape[1]
+    if out is None:
+        out = empty_padded(n, f, device=q.codes.device)
+    check(lib().aes_dev_spmm_q8(ptr(srow_ptr), ptr(scol), ptr(sval), n, ptr(q.codes), q.codes.stride(0), f,
+                                ptr(q.lut), ptr(out), out.stride(0), stream_of(stream)))
+    return out
+
+
+def gemm_bias_act(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None, relu: bool, out=None,
+                  stream=None) -> torch.Tensor:
+    """act(a @ w + bias) with the reference's ordered fp32 arithmetic (gnn.cpp:11-52)."""
+    m, k = a.shape
+    k2, n = w.shape
+    if k != k2:
+        raise ValueError("ShapeMismatch")
+    w = w.contiguous()
+    if out is None:
+        out = empty_padded(m, n, device=a.device)
+        if out.stride(0) != n:
+            out.as_strided((m, out.stride(0)), (out.stride(0), 1))[:, n:].zero_()
+    check(lib().aes_dev_gemm_bias_act(ptr(a), m, k, a.stride(0), ptr(w), n, w.stride(0),
+                                      ptr(bias) if bias is not None and bias.numel() else None, int(relu),
+                                      ptr(out), out.stride(0), stream_of(stream)))
+    return out
+
+
+def gcn_forward(graph: Graph, x: torch.Tensor, weights, biases, plan: SampledPlan | None = None,
+                stream=None) -> torch.Tensor:
+    """gcn_forward (proj/src/gnn.cpp:66-78) on one GPU, all tensors in HBM."""
+    h = padded(x)
+    srow, scol, sval = (plan.srow_ptr, plan.scol, plan.sval) if plan is not None else (
+        graph.row_ptr, graph.col, graph.val)
+    for l, (w, b) in enumerate(zip(weights, biases)):
+        agg = spmm(srow, scol, sval, h, stream=stream)
+        h = gemm_bias_act(agg, w, b, relu=l + 1 < len(weights), stream=stream)
+    return h
