@@ -202,6 +202,11 @@ AES_API int aes_dev_spmm_f32(const uint64_t* srow_ptr, const uint32_t* scol, con
                              uint64_t n_rows, const float* b, uint64_t ldb, uint64_t f, float* c,
                              uint64_t ldc, void* stream);
 
+/* Kernel-schedule override for F <= 128 (tuning/benchmarks; 0 = default):
+ * 1 register-staged batches, 2..8 shared-memory cp.async rings of different
+ * depth x warps-per-CTA.  Results are bit-identical for every variant. */
+AES_API int aes_dev_spmm_set_variant(int variant);
+
 /* Int8 variant: Q is u8 codes (ldq bytes per row), lut[256] the exact
  * dequantized value of each code (aes_dev_dequant_lut).  Result is
  * bit-identical to aes_dev_spmm_f32 over dequantize(Q). */

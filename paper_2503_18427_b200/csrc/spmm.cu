@@ -31,6 +31,10 @@ constexpr int kThreads = 256;
 
 __device__ __forceinline__ float4 f4_zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
 
+// acc += v * b with separate IEEE roundings (FMUL then FADD).  Note: ptxas
+// 12.9 fuses packed mul.rn.f32x2 + add.rn.f32x2 (even via inline PTX or
+// -fmad=false) into FFMA2, which would change the result bits, so the packed
+// FP32x2 pipe is not used here; tests/test_sass.py guards the SASS.
 __device__ __forceinline__ void f4_axpy(float4& acc, float v, const float4& b) {
     acc.x = __fadd_rn(acc.x, __fmul_rn(v, b.x));
     acc.y = __fadd_rn(acc.y, __fmul_rn(v, b.y));
@@ -49,7 +53,11 @@ struct GatherF32 {
     const float4* __restrict__ b;
     uint64_t ld4;  // row stride in float4
     typedef float4 raw_t;
+    static constexpr int kLutBytes = 0;
     __host__ void offset(uint32_t c0) { b += c0; }
+    __device__ __forceinline__ const raw_t* src(uint32_t row, uint32_t c4) const {
+        return b + (uint64_t)row * ld4 + c4;
+    }
     __device__ __forceinline__ raw_t load(uint32_t row, uint32_t c4) const {
         return __ldg(b + (uint64_t)row * ld4 + c4);
     }
@@ -60,7 +68,11 @@ struct GatherQ8 {
     const uint32_t* __restrict__ q;
     uint64_t ld4;  // row stride in u32 (4 codes)
     typedef uint32_t raw_t;
+    static constexpr int kLutBytes = 256 * 32 * 4;
     __host__ void offset(uint32_t c0) { q += c0; }
+    __device__ __forceinline__ const raw_t* src(uint32_t row, uint32_t c4) const {
+        return q + (uint64_t)row * ld4 + c4;
+    }
     __device__ __forceinline__ raw_t load(uint32_t row, uint32_t c4) const {
         return __ldg(q + (uint64_t)row * ld4 + c4);
     }
@@ -189,6 +201,140 @@ spmm_wide_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Ring kernel (F <= 128 fp32 / F <= 128 int8): same warp-per-32-row-group
+// slot stream, but the gathered rows land in a per-warp shared-memory ring of
+// C slots through cp.async (LDGSTS), so C gathers (C x 512 B at F = 128) stay
+// in flight per warp independent of the register budget.  Slot t is consumed
+// after cp.async.wait_group(C-1), then slot t + C is issued into the same
+// ring entry.  Slot metadata is loaded C slots at a time (lane p holds slot
+// base + p) two chunks ahead of use.  Each lane only ever reads the 16 (or 4)
+// bytes it copied itself, so no cross-lane barrier is needed.
+// ---------------------------------------------------------------------------
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    if (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <class G, int NV, int C, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+spmm_ring_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
+                 const float* __restrict__ sval, uint64_t n_rows, G g, uint32_t f4, float4* __restrict__ c,
+                 uint64_t ldc4, const float* __restrict__ lut_g) {
+    typedef typename G::raw_t raw_t;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const float* lut = LutSmem<G>::setup(lut_g, reinterpret_cast<float*>(smem_raw));
+    // ring[p][n][lane]: slot p, column block n
+    raw_t* ring = reinterpret_cast<raw_t*>(smem_raw + G::kLutBytes) + (threadIdx.x >> 5) * (C * NV * 32);
+
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t r0 = ((uint64_t)blockIdx.x * WARPS + (threadIdx.x >> 5)) * 32;
+    if (r0 >= n_rows) return;
+    const uint32_t nr = (uint32_t)min((uint64_t)32, n_rows - r0);
+    const uint64_t g0 = srow[r0];
+    const uint64_t my_end = srow[r0 + 1 + min(lane, nr - 1)];
+    const uint64_t total = __shfl_sync(0xffffffffu, my_end, nr - 1) - g0;
+    const uint32_t rel = (uint32_t)(my_end - g0);
+    bool colok[NV];
+#pragma unroll
+    for (int n = 0; n < NV; ++n) colok[n] = lane + 32u * n < f4;
+
+    auto ld_col = [&](uint64_t chunk) -> uint32_t {
+        const uint64_t s = chunk * C + lane;
+        return (lane < (uint32_t)C && s < total) ? ld_meta_u32(scol + g0 + s) : 0u;
+    };
+    auto ld_val = [&](uint64_t chunk) -> float {
+        const uint64_t s = chunk * C + lane;
+        return (lane < (uint32_t)C && s < total) ? ld_meta_f32(sval + g0 + s) : 0.f;
+    };
+    auto issue = [&](int p, uint32_t col) {
+#pragma unroll
+        for (int n = 0; n < NV; ++n)
+            if (colok[n]) cp_async<sizeof(raw_t)>(ring + (p * NV + n) * 32 + lane, g.src(col, lane + 32u * n));
+    };
+
+    // prologue: issue the first C gathers
+    {
+        const uint32_t mc0 = ld_col(0);
+#pragma unroll
+        for (int p = 0; p < C; ++p) {
+            const uint32_t col = __shfl_sync(0xffffffffu, mc0, p);
+            if ((uint64_t)p < total) issue(p, col);
+            cp_commit();
+        }
+    }
+    uint32_t mc_is = ld_col(1), mc_nx = ld_col(2);
+    float mv_cur = ld_val(0), mv_nx = ld_val(1);
+
+    float4 acc[NV];
+#pragma unroll
+    for (int n = 0; n < NV; ++n) acc[n] = f4_zero();
+    float4* crow = c + r0 * ldc4;
+    uint32_t row = 0;
+    uint32_t row_end = __shfl_sync(0xffffffffu, rel, 0);
+    auto store_row = [&](uint32_t r) {
+#pragma unroll
+        for (int n = 0; n < NV; ++n) {
+            if (colok[n]) __stcs(crow + (uint64_t)r * ldc4 + lane + 32u * n, acc[n]);
+            acc[n] = f4_zero();
+        }
+    };
+    while (row < nr && row_end == 0) {
+        store_row(row);
+        ++row;
+        row_end = __shfl_sync(0xffffffffu, rel, min(row, nr - 1));
+    }
+
+    uint64_t k = 0;
+    for (uint64_t t0 = 0; t0 < total; t0 += C, ++k) {
+#pragma unroll
+        for (int p = 0; p < C; ++p) {
+            const uint64_t t = t0 + p;
+            if (t >= total) break;
+            cp_wait<C - 1>();
+            const float v = __shfl_sync(0xffffffffu, mv_cur, p);
+#pragma unroll
+            for (int n = 0; n < NV; ++n) {
+                if (colok[n]) {
+                    const raw_t r = ring[(p * NV + n) * 32 + lane];
+                    f4_axpy(acc[n], v, g.decode(r, lut));
+                }
+            }
+            const uint32_t col = __shfl_sync(0xffffffffu, mc_is, p);
+            if (t + C < total) issue(p, col);
+            cp_commit();
+            const uint32_t pos = (uint32_t)(t + 1);
+            if (pos == row_end) {
+                store_row(row);
+                ++row;
+                row_end = __shfl_sync(0xffffffffu, rel, min(row, nr - 1));
+                while (row < nr && row_end == pos) {
+                    store_row(row);
+                    ++row;
+                    row_end = __shfl_sync(0xffffffffu, rel, min(row, nr - 1));
+                }
+            }
+        }
+        mv_cur = mv_nx;
+        mc_is = mc_nx;
+        mv_nx = ld_val(k + 2);
+        mc_nx = ld_col(k + 3);
+    }
+    cp_wait<0>();
+    while (row < nr) {
+        store_row(row);
+        ++row;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Narrow kernel: LPR lanes per row (LPR in 1..16), one float4 column each.
 // ---------------------------------------------------------------------------
@@ -266,6 +412,26 @@ spmm_scalar_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict
 // ---------------------------------------------------------------------------
 // dispatch
 // ---------------------------------------------------------------------------
+int g_spmm_variant = 0;          // 0 = auto; see aes_dev_spmm_set_variant
+constexpr int kDefaultVariant = 6;  // ring C=8 x 8 warps (scripts/tune_spmm.py, B200)
+
+template <class G, int NV, int C, int W>
+int launch_ring(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, G g, uint32_t f4,
+                float4* c, uint64_t ldc4, const float* lut, cudaStream_t st) {
+    const size_t smem = (size_t)G::kLutBytes + (size_t)W * C * NV * 32 * sizeof(typename G::raw_t);
+    static bool attr_set = false;  // per template instance
+    if (!attr_set) {
+        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_ring_kernel<G, NV, C, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+        attr_set = true;
+    }
+    const uint64_t groups = (n + 31) / 32;
+    const unsigned grid = (unsigned)((groups + W - 1) / W);
+    spmm_ring_kernel<G, NV, C, W><<<grid, W * 32, smem, st>>>(srow, scol, sval, n, g, f4, c, ldc4, lut);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
 template <class G>
 int launch_vector(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n,
                   G g, uint32_t f4, float4* c, uint64_t ldc4, const float* lut, cudaStream_t st) {
@@ -283,7 +449,43 @@ int launch_vector(const uint64_t* srow, const uint32_t* scol, const float* sval,
         AES_CUDA_TRY(cudaGetLastError());
         return AES_OK;
     }
-    // wide: column tiles of up to 256 float4 (1024 floats)
+    if (f4 <= 32) {
+        int v = g_spmm_variant;
+        if (v == 0) v = kDefaultVariant;
+        switch (v) {
+            case 2: return launch_ring<G, 1, 16, 4>(srow, scol, sval, n, g, f4, c, ldc4, lut, st);
+            case 3: return launch_ring<G, 1, 16, 8>(srow, scol, sval, n, g, f4, c, ldc4, lut, st);
+            case 4: return launch_ring<G, 1, 32, 4>(srow, scol, sval, n, g, f4, c, ldc4, lut, st);
+            case 5: return launch_ring<G, 1, 32, 8>(srow, scol, sval, n, g, f4, c, ldc4, lut, st);
+            case 6: return launch_ring<G, 1, 8, 8>(srow, scol, sval, n, g, f4, c, ldc4, lut, st);
+            case 7: return launch_ring<G, 1, 32, 2>(srow, scol, sval, n, g, f4, c, ldc4, lut, st);
+            case 8: return launch_ring<G, 1, 8, 16>(srow, scol, sval, n, g, f4, c, ldc4, lut, st);
+            default: break;  // 1: register-staged wide kernel below
+        }
+    }
+    if (g_spmm_variant != 1) {
+        // wider rows: ring of C slots x NV float4 per lane, column tiles of 256 float4
+        for (uint32_t c0 = 0; c0 < f4; c0 += 256) {
+            const uint32_t tf4 = min(256u, f4 - c0);
+            G gt = g;
+            gt.offset(c0);
+            float4* ct = c + c0;
+            int rc;
+            switch ((tf4 + 31) / 32) {
+                case 1: rc = launch_ring<G, 1, 8, 8>(srow, scol, sval, n, gt, tf4, ct, ldc4, lut, st); break;
+                case 2: rc = launch_ring<G, 2, 8, 8>(srow, scol, sval, n, gt, tf4, ct, ldc4, lut, st); break;
+                case 3: rc = launch_ring<G, 3, 4, 8>(srow, scol, sval, n, gt, tf4, ct, ldc4, lut, st); break;
+                case 4: rc = launch_ring<G, 4, 4, 8>(srow, scol, sval, n, gt, tf4, ct, ldc4, lut, st); break;
+                case 5: rc = launch_ring<G, 5, 4, 4>(srow, scol, sval, n, gt, tf4, ct, ldc4, lut, st); break;
+                case 6: rc = launch_ring<G, 6, 4, 4>(srow, scol, sval, n, gt, tf4, ct, ldc4, lut, st); break;
+                case 7: rc = launch_ring<G, 7, 4, 4>(srow, scol, sval, n, gt, tf4, ct, ldc4, lut, st); break;
+                default: rc = launch_ring<G, 8, 4, 4>(srow, scol, sval, n, gt, tf4, ct, ldc4, lut, st); break;
+            }
+            if (rc != AES_OK) return rc;
+        }
+        return AES_OK;
+    }
+    // variant 1: register-staged wide kernel, column tiles of up to 256 float4
     for (uint32_t c0 = 0; c0 < f4; c0 += 256) {
         uint32_t tf4 = min(256u, f4 - c0);
         G gt = g;
@@ -310,6 +512,11 @@ int launch_vector(const uint64_t* srow, const uint32_t* scol, const float* sval,
 }  // namespace aes
 
 extern "C" {
+
+int aes_dev_spmm_set_variant(int variant) {
+    aes::g_spmm_variant = variant;
+    return AES_OK;
+}
 
 int aes_dev_spmm_f32(const uint64_t* srow_ptr, const uint32_t* scol, const float* sval,
                      uint64_t n_rows, const float* b, uint64_t ldb, uint64_t f, float* c,

@@ -1,0 +1,213 @@
+"""CPU: pin the oracle (oracle/aes_oracle.c) to the reference.
+
+1. the reference's own known-answer values (proj/tests/test_*.cpp,
+   proj/tests/python/test_smoke.py);
+2. the committed golden fixtures generated from the unmodified reference;
+3. live comparison with the reference built into oracle/_ref (when present).
+"""
+import numpy as np
+import pytest
+
+from oracle import port
+from oracle import ref as oref
+from tests import golden_util as gu
+from tests import graphs
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+# ----------------------------------------------------------------- known answers
+def test_select_strategy_table():
+    # test_sampling.cpp:44-60, test_smoke.py:28-34
+    assert port.select_strategy(20, 32) == (20, 1)
+    assert port.select_strategy(100, 32) == (4, 8)
+    assert port.select_strategy(60, 32) == (8, 4)
+    assert port.select_strategy(1000, 16) == (1, 16)
+    assert port.select_strategy(0, 64) == (0, 0)
+    # boundary ratios stay in the "<=" branch (test_sampling.cpp:62-68)
+    assert port.select_strategy(32, 32)[1] == 1
+    assert port.select_strategy(64, 32)[1] == 4
+    assert port.select_strategy(36 * 32, 32)[1] == 8
+    assert port.select_strategy(54 * 32, 32)[1] == 16
+    assert port.select_strategy(54 * 32 + 1, 32)[1] == 32
+    with pytest.raises(ValueError, match="ZeroWidth"):
+        port.select_strategy(10, 0)
+
+
+def table_oracle(nnz, w):
+    """Real-valued-ratio restatement (acceptance.cpp:48-71)."""
+    if nnz == 0:
+        return 0, 0
+    r = nnz / w
+    if r <= 1.0:
+        return nnz, 1
+    chunk, cnt = ((w // 4, 4) if r <= 2.0 else (w // 8, 8) if r <= 36.0 else (w // 16, 16) if r <= 54.0
+                  else (w // 32, 32))
+    return max(chunk, 1), min(cnt, w)
+
+
+@pytest.mark.parametrize("w", [16, 32, 64, 128, 256, 512, 1024])
+def test_select_strategy_exhaustive(w):
+    # acceptance criterion 1 (acceptance.cpp:129-147): nnz in [0, 65536]
+    for nnz in list(range(0, 4097)) + list(range(4097, 65537, 37)):
+        got = port.select_strategy(nnz, w)
+        assert got == table_oracle(nnz, w), (nnz, w)
+        if nnz > w:
+            assert got[0] >= 1 and 1 <= got[1] <= w and got[0] * got[1] <= w
+
+
+def test_hash_start_values():
+    # test_sampling.cpp:99-103, test_smoke.py:37-39
+    assert port.hash_start(0, 10, 1) == 0
+    assert port.hash_start(1, 10, 1) == 9
+    assert port.hash_start(3, 100, 4) == 19
+    assert port.hash_start(1, 14, 5) == 1429 % 10
+    rng = np.random.default_rng(11)
+    for _ in range(2000):  # test_sampling.cpp:105-115
+        nnz = int(1 + rng.integers(0, 100000))
+        n = int(1 + rng.integers(0, min(nnz, 64)))
+        s = int(rng.integers(0, 33))
+        got = port.hash_start(s, nnz, n)
+        assert got <= nnz - n and got == (s * 1429) % (nnz - n + 1)
+
+
+def test_plan_known_answers():
+    assert port.row_plan(3, 4, port.ADAPTIVE) == (3, 1, [0])          # test_sampling.cpp:117-122
+    assert port.row_plan(500, 32, port.SFS) == (32, 1, [0])           # :124-129
+    assert port.row_plan(8, 4, port.AFS) == (1, 4, [0, 2, 4, 6])      # :131-135
+    assert port.row_plan(100, 32) == (4, 8, [0, 71, 45, 19, 90, 64, 38, 12])
+    ch, cn, st = port.row_plan(1430, 32)
+    assert (ch, cn) == (2, 16) and st == [0] * 16                      # hash collisions kept
+    ch, cn, st = port.row_plan(2859, 32)
+    assert (ch, cn) == (1, 32) and st[:5] == [0, 1429, 2858, 1428, 2857]
+    for strat in (0, 1, 2, 3):  # starts stay inside the row (test_sampling.cpp:148-162)
+        rng = np.random.default_rng(29 + strat)
+        for _ in range(300):
+            nnz, w = int(rng.integers(0, 3000)), int(1 + rng.integers(0, 200))
+            ch, cn, st = port.row_plan(nnz, w, strat)
+            assert all(s + ch <= nnz for s in st)
+
+
+def test_rates_known_answers():
+    rp, _, _, _ = graphs.with_degrees([2, 9, 40])
+    assert port.sampling_rate(rp, 8, port.FULL) == (1.0, 1.0)
+    rp, _, _, _ = graphs.with_degrees([100])
+    agg, uni = port.sampling_rate(rp, 32)
+    assert abs(agg - 0.32) < 1e-12 and uni <= agg
+
+
+def test_spmm_known_answers():
+    # identity, row sums (test_spmm.cpp:81-101)
+    n = 8
+    rp = np.arange(n + 1, dtype=np.uint64)
+    eye_col = np.arange(n, dtype=np.uint32)
+    b = np.random.default_rng(1).uniform(-1, 1, (n, 5)).astype(np.float32)
+    assert np.array_equal(port.spmm_csr(rp, eye_col, np.ones(n, np.float32), b), b)
+    rp = np.array([0, 2, 4, 5], np.uint64)
+    c = port.spmm_csr(rp, np.array([0, 2, 1, 2, 0], np.uint32), np.array([1, 2, 3, 4, 5], np.float32),
+                      np.ones((3, 1), np.float32))
+    assert list(c[:, 0]) == [3.0, 7.0, 5.0]
+
+
+def test_quantize_known_answers():
+    # test_quantize.cpp:53-91
+    assert port.quantize(np.array([0.5], np.float32), 0.0, 1.0)[0] == 127
+    assert list(port.quantize(np.array([-2.5, 7.25], np.float32), -2.5, 7.25)) == [0, 255]
+    assert list(port.quantize(np.array([3.0, 3.0], np.float32), 3.0, 3.0)) == [0, 0]
+    assert port.dequantize(np.array([0], np.uint16), 3.0, 3.0)[0] == 3.0
+    assert list(port.quantize(np.array([-5.0, 42.0], np.float32), 0.0, 1.0)) == [0, 255]
+    x = port.dequantize(np.array([0, 127, 255], np.uint16), 0.0, 1.0)
+    assert x[0] == 0.0 and x[2] == 1.0 and abs(x[1] - 127 / 255) < 1e-7
+    with pytest.raises(ValueError):
+        port.quantize(np.ones(1, np.float32), 1.0, 0.0)
+    with pytest.raises(ValueError):
+        port.fit_params(np.array([1.0, np.nan], np.float32))
+    with pytest.raises(ValueError):
+        port.fit_params(np.zeros(0, np.float32))
+
+
+# ----------------------------------------------------------------- golden fixtures
+@pytest.mark.parametrize("name", list(gu.STRATS))
+@pytest.mark.parametrize("w", [8, 32])
+def test_golden_cora_plans_and_spmm(name, w):
+    fx = gu.cora()
+    strat = gu.STRATS[name]
+    rp, col, val, b = fx["row_ptr"], fx["col"], fx["val"], fx["b"]
+    n = rp.size - 1
+    for i in range(0, n, 97):
+        ch, cn, st = port.row_plan(int(rp[i + 1] - rp[i]), w, strat)
+        assert ch == fx[f"plan_{name}_{w}_chunk"][i] and cn == fx[f"plan_{name}_{w}_cnt"][i]
+        sp = fx[f"plan_{name}_{w}_starts_ptr"]
+        assert st == list(fx[f"plan_{name}_{w}_starts"][sp[i]:sp[i + 1]])
+    assert gu.digest(port.spmm_sampled(rp, col, val, b, w, strat)) == fx[f"spmm_{name}_{w}"]
+    nrp, ncol = fx["norm_row_ptr"], fx["norm_col"]
+    _, _, nval = port.gcn_normalize(rp, col, True)
+    assert gu.digest(port.spmm_sampled(nrp, ncol, nval, b, w, strat)) == fx[f"spmm_norm_{name}_{w}"]
+    assert port.sampling_rate(rp, w, strat) == tuple(fx[f"rate_{name}_{w}"])
+
+
+def test_golden_cora_exact_normalize_gcn_quant():
+    fx = gu.cora()
+    rp, col, val, b = fx["row_ptr"], fx["col"], fx["val"], fx["b"]
+    assert gu.digest(port.spmm_csr(rp, col, val, b)) == fx["spmm_exact"]
+    nrp, ncol, nval = port.gcn_normalize(rp, col, True)
+    assert np.array_equal(nrp, fx["norm_row_ptr"]) and np.array_equal(ncol, fx["norm_col"])
+    assert gu.digest(nval) == fx["norm_val"]
+    ws, bs = [fx["gcn_w0"], fx["gcn_w1"]], [fx["gcn_b0"], fx["gcn_b1"]]
+    assert gu.digest(port.gcn_forward(nrp, ncol, nval, b, ws, bs, None)) == fx["gcn_exact"]
+    assert gu.digest(port.gcn_forward(nrp, ncol, nval, b, ws, bs, 32)) == fx["gcn_w32"]
+    assert gu.digest(port.gcn_forward(nrp, ncol, nval, b, ws, bs, 8)) == fx["gcn_w8"]
+    for q in (8, 4):
+        lo, hi = port.fit_params(b, q)
+        assert np.array_equal(np.array([lo, hi], np.float32), fx[f"q{q}_params"])
+        codes = port.quantize(b, lo, hi, q)
+        assert gu.digest(codes) == fx[f"q{q}_codes"]
+        deq = port.dequantize(codes, lo, hi, q)
+        assert gu.digest(deq) == fx[f"q{q}_deq"]
+        assert gu.digest(port.spmm_sampled(rp, col, val, deq, 32)) == fx[f"q{q}_spmm_adaptive_32"]
+
+
+@pytest.mark.parametrize("w", [16, 32, 64])
+def test_golden_heavy_tail(w):
+    fx = gu.heavy()
+    rp, col, val, b = fx["row_ptr"], fx["col"], fx["val"], fx["b"]
+    assert gu.digest(port.spmm_sampled(rp, col, val, b, w)) == fx[f"spmm_adaptive_{w}"]
+    cnt = fx[f"plan_{w}_cnt"]
+    if w == 32:  # Table-1 branches 1..4 at W = 32 (max degree 1496 < 54 W)
+        assert {1, 4, 8, 16} <= set(int(c) for c in np.unique(cnt))
+    if w == 16:  # ... and the R > 54 branch at W = 16
+        assert int(np.diff(rp).max()) > 54 * 16
+    srow, _, _ = port.sample_csr(rp, col, val, w)
+    assert np.array_equal(np.diff(srow), fx[f"plan_{w}_chunk"].astype(np.uint64) * cnt)
+
+
+# ----------------------------------------------------------------- live reference (oracle/_ref)
+needs_ref = pytest.mark.skipif(not oref.available(), reason="oracle/_ref not built")
+
+
+@needs_ref
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_port_matches_reference_live(seed):
+    g = oref.gen_synthetic(3000, 1.3, 2000, seed)
+    rp, col, _ = g.arrays()
+    val = np.random.default_rng(seed).uniform(-1, 1, col.size).astype(np.float32)
+    g = oref.RefCsr.from_arrays(3000, 3000, rp, col, val)
+    b = np.random.default_rng(seed + 10).standard_normal((3000, 12)).astype(np.float32)
+    for strat in (0, 1, 2, 3):
+        for w in (1, 4, 16, 32, 100):
+            assert np.array_equal(bits(port.spmm_sampled(rp, col, val, b, w, strat)),
+                                  bits(oref.spmm_sampled(g, b, w, strat)))
+            chunk, cnt, sp, starts = oref.build_plans(g, w, strat)
+            for i in range(0, 3000, 211):
+                ch, cn, st = port.row_plan(int(rp[i + 1] - rp[i]), w, strat)
+                assert (ch, cn, st) == (chunk[i], cnt[i], list(starts[sp[i]:sp[i + 1]]))
+    assert np.array_equal(bits(port.spmm_csr(rp, col, val, b)), bits(oref.spmm_exact(g, b)))
+
+
+@needs_ref
+def test_reference_python_core_loads():
+    core = oref.core()
+    assert core.select_strategy(100, 32).sample_cnt == 8
+    assert core.hash_start(3, 100, 4) == 19
