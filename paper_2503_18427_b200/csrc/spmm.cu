@@ -55,6 +55,7 @@ struct GatherF32 {
     typedef float4 raw_t;
     static constexpr int kLutBytes = 0;
     __host__ void offset(uint32_t c0) { b += c0; }
+    __host__ const float4* base() const { return b; }
     __device__ __forceinline__ const raw_t* src(uint32_t row, uint32_t c4) const {
         return b + (uint64_t)row * ld4 + c4;
     }
@@ -70,6 +71,7 @@ struct GatherQ8 {
     typedef uint32_t raw_t;
     static constexpr int kLutBytes = 256 * 32 * 4;
     __host__ void offset(uint32_t c0) { q += c0; }
+    __host__ const uint32_t* base() const { return q; }
     __device__ __forceinline__ const raw_t* src(uint32_t row, uint32_t c4) const {
         return q + (uint64_t)row * ld4 + c4;
     }
@@ -224,50 +226,109 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-template <class G, int NV, int C, int WARPS>
+// Shared-memory helpers on 32-bit shared-window addresses (no generic->shared
+// conversion per access).  Volatile so they stay ordered after cp.async.wait.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float4 lds_f32x4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void cp_async_sa(uint32_t sa, const void* gmem, int bytes) {
+    if (bytes == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+// Ring element types: fp32 rows (float4 per lane) or u8 code rows (4 codes per
+// lane, decoded through the per-bank replicated LUT at smem offset 0).
+struct RingF32 {
+    typedef float4 raw_t;
+    static constexpr int kBytes = 16;
+    static constexpr int kLutBytes = 0;
+    __device__ __forceinline__ static float4 load_decode(uint32_t a, uint32_t) { return lds_f32x4(a); }
+};
+struct RingQ8 {
+    typedef uint32_t raw_t;
+    static constexpr int kBytes = 4;
+    static constexpr int kLutBytes = 256 * 32 * 4;
+    // lut_lane = smem address of lut[0][lane]; entry q is at lut_lane + q * 128
+    __device__ __forceinline__ static float4 load_decode(uint32_t a, uint32_t lut_lane) {
+        const uint32_t r = lds_u32(a);
+        return make_float4(lds_f32(lut_lane + (__byte_perm(r, 0, 0x4440) << 7)),
+                           lds_f32(lut_lane + (__byte_perm(r, 0, 0x4441) << 7)),
+                           lds_f32(lut_lane + (__byte_perm(r, 0, 0x4442) << 7)),
+                           lds_f32(lut_lane + (__byte_perm(r, 0, 0x4443) << 7)));
+    }
+};
+
+template <class R, int NV, int C, int WARPS, bool FULL>
 __global__ void __launch_bounds__(WARPS * 32)
 spmm_ring_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
-                 const float* __restrict__ sval, uint64_t n_rows, G g, uint32_t f4, float4* __restrict__ c,
-                 uint64_t ldc4, const float* __restrict__ lut_g) {
-    typedef typename G::raw_t raw_t;
+                 const float* __restrict__ sval, uint64_t n_rows, const typename R::raw_t* __restrict__ gsrc,
+                 uint32_t ld, uint32_t f4, float4* __restrict__ c, uint64_t ldc4, const float* __restrict__ lut_g) {
+    typedef typename R::raw_t raw_t;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const float* lut = LutSmem<G>::setup(lut_g, reinterpret_cast<float*>(smem_raw));
-    // ring[p][n][lane]: slot p, column block n
-    raw_t* ring = reinterpret_cast<raw_t*>(smem_raw + G::kLutBytes) + (threadIdx.x >> 5) * (C * NV * 32);
-
     const uint32_t lane = threadIdx.x & 31;
+    const uint32_t smem0 = smem_addr(smem_raw);
+    if (R::kLutBytes) {
+        float* lut = reinterpret_cast<float*>(smem_raw);
+        for (int i = threadIdx.x; i < 256 * 32; i += WARPS * 32) lut[i] = lut_g[i >> 5];
+        __syncthreads();
+    }
+    const uint32_t lut_lane = smem0 + lane * 4;
+    // ring entry (p, n) of this lane: ring0 + (p * NV + n) * 32 * kBytes
+    const uint32_t ring0 = smem0 + R::kLutBytes + (threadIdx.x >> 5) * (C * NV * 32 * R::kBytes) + lane * R::kBytes;
+
     const uint64_t r0 = ((uint64_t)blockIdx.x * WARPS + (threadIdx.x >> 5)) * 32;
     if (r0 >= n_rows) return;
     const uint32_t nr = (uint32_t)min((uint64_t)32, n_rows - r0);
     const uint64_t g0 = srow[r0];
     const uint64_t my_end = srow[r0 + 1 + min(lane, nr - 1)];
-    const uint64_t total = __shfl_sync(0xffffffffu, my_end, nr - 1) - g0;
+    // slot offsets inside a 32-row group fit in 32 bits
+    const uint32_t total = (uint32_t)(__shfl_sync(0xffffffffu, my_end, nr - 1) - g0);
     const uint32_t rel = (uint32_t)(my_end - g0);
+    const uint32_t* gcol = scol + g0;
+    const float* gval = sval + g0;
+    const char* glb = reinterpret_cast<const char*>(gsrc + lane);
+    const uint32_t ld_bytes = ld * (uint32_t)sizeof(raw_t);
     bool colok[NV];
 #pragma unroll
-    for (int n = 0; n < NV; ++n) colok[n] = lane + 32u * n < f4;
+    for (int n = 0; n < NV; ++n) colok[n] = FULL || lane + 32u * n < f4;
 
-    auto ld_col = [&](uint64_t chunk) -> uint32_t {
-        const uint64_t s = chunk * C + lane;
-        return (lane < (uint32_t)C && s < total) ? ld_meta_u32(scol + g0 + s) : 0u;
+    auto ld_col = [&](uint32_t chunk) -> uint32_t {
+        const uint32_t s = chunk * C + lane;
+        return (lane < (uint32_t)C && s < total) ? ld_meta_u32(gcol + s) : 0u;
     };
-    auto ld_val = [&](uint64_t chunk) -> float {
-        const uint64_t s = chunk * C + lane;
-        return (lane < (uint32_t)C && s < total) ? ld_meta_f32(sval + g0 + s) : 0.f;
+    auto ld_val = [&](uint32_t chunk) -> float {
+        const uint32_t s = chunk * C + lane;
+        return (lane < (uint32_t)C && s < total) ? ld_meta_f32(gval + s) : 0.f;
     };
     auto issue = [&](int p, uint32_t col) {
+        // one IMAD.WIDE.U32: lane base + col * row_bytes
+        const raw_t* src = reinterpret_cast<const raw_t*>(glb + (uint64_t)col * ld_bytes);
 #pragma unroll
         for (int n = 0; n < NV; ++n)
-            if (colok[n]) cp_async<sizeof(raw_t)>(ring + (p * NV + n) * 32 + lane, g.src(col, lane + 32u * n));
+            if (colok[n]) cp_async_sa(ring0 + (p * NV + n) * 32 * R::kBytes, src + 32 * n, R::kBytes);
     };
 
-    // prologue: issue the first C gathers
-    {
+    {  // prologue: first C gathers in flight
         const uint32_t mc0 = ld_col(0);
 #pragma unroll
         for (int p = 0; p < C; ++p) {
             const uint32_t col = __shfl_sync(0xffffffffu, mc0, p);
-            if ((uint64_t)p < total) issue(p, col);
+            if ((uint32_t)p < total) issue(p, col);
             cp_commit();
         }
     }
@@ -277,50 +338,47 @@ spmm_ring_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__
     float4 acc[NV];
 #pragma unroll
     for (int n = 0; n < NV; ++n) acc[n] = f4_zero();
-    float4* crow = c + r0 * ldc4;
+    float4* crow = c + r0 * ldc4 + lane;
     uint32_t row = 0;
     uint32_t row_end = __shfl_sync(0xffffffffu, rel, 0);
     auto store_row = [&](uint32_t r) {
 #pragma unroll
         for (int n = 0; n < NV; ++n) {
-            if (colok[n]) __stcs(crow + (uint64_t)r * ldc4 + lane + 32u * n, acc[n]);
+            if (colok[n]) __stcs(crow + (uint64_t)r * ldc4 + 32u * n, acc[n]);
             acc[n] = f4_zero();
         }
     };
-    while (row < nr && row_end == 0) {
-        store_row(row);
-        ++row;
-        row_end = __shfl_sync(0xffffffffu, rel, min(row, nr - 1));
-    }
+    auto advance_rows = [&](uint32_t pos) {  // rows ending at slot position pos
+        do {
+            store_row(row);
+            ++row;
+            row_end = __shfl_sync(0xffffffffu, rel, min(row, nr - 1));
+        } while (row < nr && row_end == pos);
+    };
+    if (row_end == 0) advance_rows(0);
 
-    uint64_t k = 0;
-    for (uint64_t t0 = 0; t0 < total; t0 += C, ++k) {
+    auto body = [&](int p, uint32_t t) {
+        cp_wait<C - 1>();
+        const float v = __shfl_sync(0xffffffffu, mv_cur, p);
 #pragma unroll
-        for (int p = 0; p < C; ++p) {
-            const uint64_t t = t0 + p;
-            if (t >= total) break;
-            cp_wait<C - 1>();
-            const float v = __shfl_sync(0xffffffffu, mv_cur, p);
+        for (int n = 0; n < NV; ++n)
+            if (colok[n]) f4_axpy(acc[n], v, R::load_decode(ring0 + (p * NV + n) * 32 * R::kBytes, lut_lane));
+        const uint32_t col = __shfl_sync(0xffffffffu, mc_is, p);
+        if (t + C < total) issue(p, col);
+        cp_commit();
+        if (t + 1 == row_end) advance_rows(t + 1);
+    };
+
+    uint32_t k = 0;
+    for (uint32_t t0 = 0; t0 < total; t0 += C, ++k) {
+        if (t0 + C <= total) {
 #pragma unroll
-            for (int n = 0; n < NV; ++n) {
-                if (colok[n]) {
-                    const raw_t r = ring[(p * NV + n) * 32 + lane];
-                    f4_axpy(acc[n], v, g.decode(r, lut));
-                }
-            }
-            const uint32_t col = __shfl_sync(0xffffffffu, mc_is, p);
-            if (t + C < total) issue(p, col);
-            cp_commit();
-            const uint32_t pos = (uint32_t)(t + 1);
-            if (pos == row_end) {
-                store_row(row);
-                ++row;
-                row_end = __shfl_sync(0xffffffffu, rel, min(row, nr - 1));
-                while (row < nr && row_end == pos) {
-                    store_row(row);
-                    ++row;
-                    row_end = __shfl_sync(0xffffffffu, rel, min(row, nr - 1));
-                }
+            for (int p = 0; p < C; ++p) body(p, t0 + p);
+        } else {
+#pragma unroll
+            for (int p = 0; p < C; ++p) {
+                if (t0 + p >= total) break;
+                body(p, t0 + p);
             }
         }
         mv_cur = mv_nx;
@@ -413,23 +471,39 @@ spmm_scalar_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict
 // dispatch
 // ---------------------------------------------------------------------------
 int g_spmm_variant = 0;          // 0 = auto; see aes_dev_spmm_set_variant
-constexpr int kDefaultVariant = 6;  // ring C=8 x 8 warps (scripts/tune_spmm.py, B200)
+// Measured on B200 (scripts/tune_spmm.py, products W=32): fp32 best with a
+// 16-slot ring x 4 warps (1.18 ms), int8 with an 8-slot ring x 16 warps (0.89 ms).
+constexpr int kDefaultVariantF32 = 2;
+constexpr int kDefaultVariantQ8 = 8;
 
-template <class G, int NV, int C, int W>
-int launch_ring(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, G g, uint32_t f4,
-                float4* c, uint64_t ldc4, const float* lut, cudaStream_t st) {
-    const size_t smem = (size_t)G::kLutBytes + (size_t)W * C * NV * 32 * sizeof(typename G::raw_t);
+template <class G> struct RingOf;
+template <> struct RingOf<GatherF32> { typedef RingF32 type; };
+template <> struct RingOf<GatherQ8> { typedef RingQ8 type; };
+
+template <class G, int NV, int C, int W, bool FULL>
+int launch_ring_t(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, G g, uint32_t f4,
+                  float4* c, uint64_t ldc4, const float* lut, cudaStream_t st) {
+    typedef typename RingOf<G>::type R;
+    const size_t smem = (size_t)R::kLutBytes + (size_t)W * C * NV * 32 * R::kBytes;
     static bool attr_set = false;  // per template instance
     if (!attr_set) {
-        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_ring_kernel<G, NV, C, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)smem));
+        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_ring_kernel<R, NV, C, W, FULL>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set = true;
     }
     const uint64_t groups = (n + 31) / 32;
     const unsigned grid = (unsigned)((groups + W - 1) / W);
-    spmm_ring_kernel<G, NV, C, W><<<grid, W * 32, smem, st>>>(srow, scol, sval, n, g, f4, c, ldc4, lut);
+    spmm_ring_kernel<R, NV, C, W, FULL><<<grid, W * 32, smem, st>>>(srow, scol, sval, n, g.base(), (uint32_t)g.ld4,
+                                                                    f4, c, ldc4, lut);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
+}
+
+template <class G, int NV, int C, int W>
+int launch_ring(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, G g, uint32_t f4,
+                float4* c, uint64_t ldc4, const float* lut, cudaStream_t st) {
+    if (f4 == 32u * NV) return launch_ring_t<G, NV, C, W, true>(srow, scol, sval, n, g, f4, c, ldc4, lut, st);
+    return launch_ring_t<G, NV, C, W, false>(srow, scol, sval, n, g, f4, c, ldc4, lut, st);
 }
 
 template <class G>
@@ -451,7 +525,7 @@ int launch_vector(const uint64_t* srow, const uint32_t* scol, const float* sval,
     }
     if (f4 <= 32) {
         int v = g_spmm_variant;
-        if (v == 0) v = kDefaultVariant;
+        if (v == 0) v = G::kLutBytes ? kDefaultVariantQ8 : kDefaultVariantF32;
         switch (v) {
             case 2: return launch_ring<G, 1, 16, 4>(srow, scol, sval, n, g, f4, c, ldc4, lut, st);
             case 3: return launch_ring<G, 1, 16, 8>(srow, scol, sval, n, g, f4, c, ldc4, lut, st);
@@ -472,7 +546,9 @@ int launch_vector(const uint64_t* srow, const uint32_t* scol, const float* sval,
             float4* ct = c + c0;
             int rc;
             switch ((tf4 + 31) / 32) {
-                case 1: rc = launch_ring<G, 1, 8, 8>(srow, scol, sval, n, gt, tf4, ct, ldc4, lut, st); break;
+                case 1: rc = G::kLutBytes ? launch_ring<G, 1, 8, 16>(srow, scol, sval, n, gt, tf4, ct, ldc4, lut, st)
+                                      : launch_ring<G, 1, 16, 4>(srow, scol, sval, n, gt, tf4, ct, ldc4, lut, st);
+                    break;
                 case 2: rc = launch_ring<G, 2, 8, 8>(srow, scol, sval, n, gt, tf4, ct, ldc4, lut, st); break;
                 case 3: rc = launch_ring<G, 3, 4, 8>(srow, scol, sval, n, gt, tf4, ct, ldc4, lut, st); break;
                 case 4: rc = launch_ring<G, 4, 4, 8>(srow, scol, sval, n, gt, tf4, ct, ldc4, lut, st); break;
