@@ -301,10 +301,12 @@ def run_ours(args):
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
+    torch.cuda.nvtx.range_push("timed")
     start.record(stream)
     for _ in range(args.steps):
         step()
     end.record(stream)
+    torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     clocks = sampler.stop()
     ms_total = start.elapsed_time(end)

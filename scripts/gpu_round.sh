@@ -1,17 +1,23 @@
 #!/bin/bash
-# One GPU verification pass: tests, smoke, bench lines, ncu launch list + full capture.
+# One GPU verification pass: tests, smoke, bench lines, ncu launch list + full captures.
 cd ${GRAFT_REPO_ROOT:-.}
 mkdir -p gpurun_out
-nproc; lscpu | grep "Model name"
-python -m pytest tests -m gpu -q 2>&1 | tail -6
+nproc; lscpu | grep "Model name"; nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv,noheader
+python -m pytest tests -m gpu -q 2>&1 | tail -4
 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err; cat gpurun_out/bench.json
 timeout 300 python bench.py --dtype int8 --no-e2e --no-cpu-baseline > gpurun_out/bench_int8.json 2>&1; cat gpurun_out/bench_int8.json
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2>&1; cat gpurun_out/bench_ref.json
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
-    python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:spmm_ring -s 2 -c 1 -o gpurun_out/prof_spmm_f32 -f \
-    python bench.py --steps 2 --warmup 2 --no-e2e --no-cpu-baseline > gpurun_out/ncu_f32.log 2>&1; tail -1 gpurun_out/ncu_f32.log
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:spmm_ring -s 2 -c 1 -o gpurun_out/prof_spmm_int8 -f \
-    python bench.py --steps 2 --warmup 2 --dtype int8 --no-e2e --no-cpu-baseline > gpurun_out/ncu_int8.log 2>&1; tail -1 gpurun_out/ncu_int8.log
+# launch list of the timed region only (NVTX range "timed")
+timeout 300 ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/launches_timed.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_all.csv \
+    python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+for dt in f32 int8; do
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:spmm_ring -s 2 -c 1 -o gpurun_out/prof_spmm_$dt -f \
+      python bench.py --steps 2 --warmup 2 --dtype $dt --no-e2e --no-cpu-baseline > gpurun_out/ncu_$dt.log 2>&1; tail -1 gpurun_out/ncu_$dt.log
+done
+python scripts/ncu_summary.py gpurun_out/prof_spmm_f32.ncu-rep gpurun_out/prof_spmm_int8.ncu-rep > gpurun_out/ncu_full_summary.json
+python scripts/launch_summary.py gpurun_out/launches_timed.csv > gpurun_out/launches_timed_summary.json
+python scripts/launch_summary.py gpurun_out/launches_all.csv > gpurun_out/launches_all_summary.json
 ls gpurun_out
