@@ -37,5 +37,4 @@ def summarize(path):
 
 
 if __name__ == "__main__":
-    for p in sys.argv[1:]:
-        print(json.dumps(summarize(p), indent=1))
+    print(json.dumps({p.split("/")[-1]: summarize(p) for p in sys.argv[1:]}, indent=1))
