@@ -1,0 +1,182 @@
+// B200-native implementation of the reference's C++ operator API for the
+// AES-SpMM hot path.  The reference headers proj/include/aesspmm/{matrix,
+// sampling,spmm,quantize,gnn}.hpp are mirrored here with identical type and
+// function signatures, so code written against them recompiles unchanged
+// (include "aesspmm/<same name>.hpp", link libaescuda.so).  Every operation
+// runs on the GPU through the C ABI in aesspmm_cuda.h; the structs stay the
+// reference's host-side value types (std::vector storage, results returned by
+// value), and host<->device copies happen at each call exactly where the
+// reference would copy.
+//
+// Differences, all documented in DESIGN.md:
+//  * SamplePlanSet additionally carries an opaque handle to the plan built in
+//    HBM by build_plan_set (the `plans` vector is still filled, eagerly).
+//  * n_threads parameters are accepted and ignored (results never depend on
+//    them, in the reference or here).
+//  * Out of scope for the B200 hot path (not declared): csr_from_triplets,
+//    row_mean_normalize, sage_forward, argmax_rows, evaluate.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#define AES_CXX_API __attribute__((visibility("default")))
+
+namespace aes {
+
+// ---------------------------------------------------------------- matrix.hpp
+/// Canonical CSR (proj/include/aesspmm/matrix.hpp:11-26): u64 row offsets,
+/// strictly increasing u32 columns within a row, f32 values.
+struct CsrMatrix {
+    std::size_t n_rows = 0;
+    std::size_t n_cols = 0;
+    std::vector<std::uint64_t> row_ptr;
+    std::vector<std::uint32_t> col_ind;
+    std::vector<float> val;
+
+    CsrMatrix() : row_ptr{0} {}
+    CsrMatrix(std::size_t rows, std::size_t cols) : n_rows(rows), n_cols(cols), row_ptr(rows + 1, 0) {}
+    std::size_t nnz() const { return col_ind.size(); }
+    std::size_t row_nnz(std::size_t i) const { return static_cast<std::size_t>(row_ptr[i + 1] - row_ptr[i]); }
+};
+
+/// Row-major f32 matrix (matrix.hpp:29-42).
+struct DenseMatrix {
+    std::size_t n_rows = 0;
+    std::size_t n_cols = 0;
+    std::vector<float> data;
+
+    DenseMatrix() = default;
+    DenseMatrix(std::size_t rows, std::size_t cols, float fill = 0.0f)
+        : n_rows(rows), n_cols(cols), data(rows * cols, fill) {}
+    float& at(std::size_t i, std::size_t j) { return data[i * n_cols + j]; }
+    float at(std::size_t i, std::size_t j) const { return data[i * n_cols + j]; }
+    const float* row(std::size_t i) const { return data.data() + i * n_cols; }
+    float* row(std::size_t i) { return data.data() + i * n_cols; }
+};
+
+struct RowStats {
+    std::vector<std::uint64_t> row_nnz;
+    std::uint64_t max_row_nnz = 0;
+    double avg_degree = 0.0;
+};
+
+enum class CsrError { Ok, NonMonotonicRowPtr, ColumnOutOfRange, UnsortedRow, LengthMismatch, NotSquare };
+
+struct ValidationResult {
+    CsrError error = CsrError::Ok;
+    std::size_t row = 0;
+    bool ok() const { return error == CsrError::Ok; }
+    AES_CXX_API std::string message() const;
+};
+
+AES_CXX_API ValidationResult validate_csr(const CsrMatrix& m);
+AES_CXX_API RowStats row_stats(const CsrMatrix& m);
+/// D^-1/2 (A [+ I]) D^-1/2 (matrix.cpp:130-144), on the GPU.
+AES_CXX_API CsrMatrix gcn_normalize(const CsrMatrix& a, bool add_self_loops);
+
+// -------------------------------------------------------------- sampling.hpp
+inline constexpr std::uint64_t kHashPrime = 1429;
+
+enum class Strategy { Adaptive, Afs, Sfs, Full };
+
+AES_CXX_API Strategy strategy_from_string(const std::string& s);
+AES_CXX_API std::string to_string(Strategy s);
+
+struct StrategyParams {
+    std::uint32_t chunk_len = 0;
+    std::uint32_t sample_cnt = 0;
+};
+
+struct RowSamplePlan {
+    std::uint32_t row_id = 0;
+    StrategyParams params;
+    std::vector<std::uint32_t> starts;
+    std::uint64_t slots() const { return std::uint64_t(params.chunk_len) * params.sample_cnt; }
+    bool empty() const { return params.sample_cnt == 0; }
+};
+
+struct SamplePlanSet {
+    std::uint32_t width = 0;
+    Strategy strategy = Strategy::Full;
+    std::vector<RowSamplePlan> plans;
+    /// HBM-resident plan + sampled CSR built by build_plan_set (opaque).
+    std::shared_ptr<void> device;
+};
+
+AES_CXX_API StrategyParams select_strategy(std::uint64_t row_nnz, std::uint32_t width);
+AES_CXX_API std::uint32_t hash_start(std::uint32_t current_ind, std::uint64_t row_nnz, std::uint32_t chunk_len);
+AES_CXX_API RowSamplePlan build_plan(std::uint32_t row_id, std::uint64_t row_nnz, std::uint32_t width,
+                                     Strategy strategy);
+AES_CXX_API SamplePlanSet build_plan_set(const CsrMatrix& m, std::uint32_t width, Strategy strategy);
+
+struct SamplingRates {
+    std::vector<double> per_row;
+    double aggregate = 0.0;
+    double unique_coverage = 0.0;
+};
+
+AES_CXX_API SamplingRates sampling_rate(const SamplePlanSet& plans, const RowStats& stats);
+
+// ------------------------------------------------------------------ spmm.hpp
+struct WorkCounter {
+    std::uint64_t fma_count = 0;
+    std::uint64_t loads_a = 0;
+    std::uint64_t loads_b = 0;
+};
+
+AES_CXX_API DenseMatrix spmm_exact(const CsrMatrix& a, const DenseMatrix& b, unsigned n_threads = 0);
+AES_CXX_API DenseMatrix spmm_sampled(const CsrMatrix& a, const DenseMatrix& b, const SamplePlanSet& plans,
+                                     unsigned n_threads = 0);
+AES_CXX_API DenseMatrix spmm_sampled_instrumented(const CsrMatrix& a, const DenseMatrix& b,
+                                                  const SamplePlanSet& plans, WorkCounter& counter,
+                                                  unsigned n_threads = 0);
+AES_CXX_API WorkCounter exact_work(const CsrMatrix& a, const DenseMatrix& b);
+
+// -------------------------------------------------------------- quantize.hpp
+struct QuantParams {
+    float x_min = 0.0f;
+    float x_max = 0.0f;
+    std::uint32_t bits = 8;
+    std::uint32_t levels() const { return (1u << bits) - 1u; }
+};
+
+struct QuantizedFeatures {
+    std::size_t n_rows = 0;
+    std::size_t n_cols = 0;
+    std::vector<std::uint16_t> codes;
+    QuantParams params;
+};
+
+AES_CXX_API QuantParams fit_params(const DenseMatrix& x, std::uint32_t bits = 8);
+AES_CXX_API QuantizedFeatures quantize(const DenseMatrix& x, const QuantParams& p);
+AES_CXX_API DenseMatrix dequantize(const QuantizedFeatures& qf);
+/// spmm_sampled(a, dequantize(qf), plans) with dequantization fused into the
+/// int8 gather (B200 extension; plans == nullptr -> exact).
+AES_CXX_API DenseMatrix spmm_sampled_q8(const CsrMatrix& a, const QuantizedFeatures& qf,
+                                        const SamplePlanSet* plans = nullptr);
+
+// ------------------------------------------------------------------- gnn.hpp
+enum class ModelKind { Gcn, SageMean };
+
+struct GnnLayer {
+    DenseMatrix weight;       // in_dim x out_dim
+    std::vector<float> bias;  // out_dim, may be empty
+};
+
+struct GnnModel {
+    ModelKind kind = ModelKind::Gcn;
+    std::vector<GnnLayer> layers;
+};
+
+AES_CXX_API DenseMatrix gcn_forward(const CsrMatrix& adj, const DenseMatrix& features, const GnnModel& model,
+                                    const SamplePlanSet* plans = nullptr, unsigned n_threads = 0);
+/// Dispatches on model.kind; SageMean is outside the B200 hot path and throws.
+AES_CXX_API DenseMatrix gnn_forward(const CsrMatrix& adj, const DenseMatrix& features, const GnnModel& model,
+                                    const SamplePlanSet* plans = nullptr, unsigned n_threads = 0);
+AES_CXX_API DenseMatrix dense_matmul(const DenseMatrix& a, const DenseMatrix& b, unsigned n_threads = 0);
+
+}  // namespace aes

@@ -93,6 +93,15 @@ AES_API int aes_csr_create(uint64_t n_rows, uint64_t n_cols, const uint64_t* row
 AES_API int aes_csr_wrap_device(uint64_t n_rows, uint64_t n_cols, const uint64_t* d_row_ptr,
                                 const uint32_t* d_col_ind, const float* d_val, uint64_t nnz,
                                 aes_csr_t* out);
+/* validate_csr on host arrays (matrix.cpp:28-52): *error = CsrError code,
+ * *row = offending row; returns AES_ERR_CSR_INVALID with the message. */
+AES_API int aes_validate_csr(uint64_t n_rows, uint64_t n_cols, const uint64_t* row_ptr,
+                             uint64_t row_ptr_len, const uint32_t* col_ind, uint64_t nnz_len,
+                             int* error, uint64_t* row);
+/* Structure-only CSR (row_ptr only): enough for row_stats, sampling_rate and
+ * plan export; not for SpMM. */
+AES_API int aes_csr_structure(uint64_t n_rows, uint64_t n_cols, const uint64_t* row_ptr,
+                              aes_csr_t* out);
 AES_API int aes_csr_destroy(aes_csr_t a);
 AES_API int aes_csr_shape(aes_csr_t a, uint64_t* n_rows, uint64_t* n_cols, uint64_t* nnz);
 /* Device views of the CSR arrays (for zero-copy interop). */
@@ -110,6 +119,12 @@ AES_API int aes_gcn_normalize(aes_csr_t a, int add_self_loops, aes_csr_t* out);
  * sampling.cpp:104-118, module.cpp:107-108.  Builds the per-row plan and the
  * sampled CSR (slot order) in HBM. */
 AES_API int aes_build_plan_set(aes_csr_t a, uint32_t width, int strategy, aes_plan_t* out);
+/* A plan set given as host data (SamplePlanSet built or edited by the
+ * caller): per-row chunk_len/sample_cnt and starts in CSR form (starts_ptr
+ * n+1).  Filled in slot order exactly like a built plan (spmm.cpp:54-76). */
+AES_API int aes_plan_from_host(aes_csr_t a, uint32_t width, int strategy, const uint32_t* chunk_len,
+                               const uint32_t* sample_cnt, const uint64_t* starts_ptr,
+                               const uint32_t* starts, aes_plan_t* out);
 AES_API int aes_plan_destroy(aes_plan_t p);
 AES_API int aes_plan_info(aes_plan_t p, uint32_t* width, int* strategy, uint64_t* n_rows,
                           uint64_t* total_slots, uint64_t* total_starts);
@@ -140,6 +155,9 @@ AES_API int aes_spmm_sampled(aes_csr_t a, const float* b, uint64_t b_rows, uint6
  * quantize.cpp:11-51.  x: host rows x cols f32. */
 AES_API int aes_quantize(const float* x, uint64_t rows, uint64_t cols, uint32_t bits,
                          aes_qfeat_t* out);
+/* fit_params(x, bits) — quantize.hpp:28, quantize.cpp:11-21 */
+AES_API int aes_fit_params(const float* x, uint64_t rows, uint64_t cols, uint32_t bits, float* x_min,
+                           float* x_max);
 /* quantize(x, p) with explicit params — quantize.hpp:31 */
 AES_API int aes_quantize_with(const float* x, uint64_t rows, uint64_t cols, float x_min,
                               float x_max, uint32_t bits, aes_qfeat_t* out);

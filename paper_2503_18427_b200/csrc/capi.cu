@@ -44,6 +44,10 @@ int launch_validate_rows(const uint64_t*, const uint32_t*, uint64_t, uint64_t, u
                          cudaStream_t);
 int launch_gcn_normalize(const uint64_t*, const uint32_t*, uint64_t, int, const uint64_t*, float*, uint32_t*,
                          float*, cudaStream_t);
+int launch_explicit_fill(const uint64_t*, const uint32_t*, const uint64_t*, const uint32_t*, const uint32_t*,
+                         const float*, uint64_t, const uint64_t*, uint32_t*, float*, cudaStream_t);
+int launch_explicit_rate(const uint64_t*, const uint32_t*, const uint64_t*, const uint32_t*, uint64_t, uint64_t,
+                         unsigned char*, double*, unsigned long long*, cudaStream_t);
 
 namespace {
 
@@ -166,6 +170,12 @@ struct aes_plan_s {
     uint64_t* srow_ptr = nullptr;
     uint32_t* scol = nullptr;
     float* sval = nullptr;
+    // host-supplied plans (aes_plan_from_host): per-row (chunk, cnt) and starts
+    bool explicit_plan = false;
+    uint32_t* params = nullptr;       // uint2 per row
+    uint64_t* starts_ptr = nullptr;   // n+1
+    uint32_t* starts = nullptr;
+    uint64_t total_starts = 0;
 };
 
 struct aes_qfeat_s {
@@ -204,28 +214,35 @@ const char* csr_error_name(int e) {
 }
 
 // validate_csr (matrix.cpp:28-52) with the reference's check order.
-int validate_device(const aes_csr_s* a, uint64_t row_ptr_len, uint64_t nnz_len, uint64_t first_row_ptr) {
+// validate_csr (matrix.cpp:28-52) with the reference's check order; the
+// first violation is reported as (CsrError, row) and as the message text.
+int validate_device(const aes_csr_s* a, uint64_t row_ptr_len, uint64_t nnz_len, uint64_t first_row_ptr,
+                    int* err_out = nullptr, uint64_t* row_out = nullptr) {
+    auto bad = [&](int e, uint64_t row, bool with_row) {
+        if (err_out) *err_out = e;
+        if (row_out) *row_out = row;
+        std::string msg = csr_error_name(e);
+        if (with_row) msg += " at row " + std::to_string(row);
+        return fail(AES_ERR_CSR_INVALID, msg);
+    };
+    if (err_out) *err_out = AES_CSR_OK;
+    if (row_out) *row_out = 0;
     if (row_ptr_len != a->n_rows + 1 || row_ptr_len == 0 || first_row_ptr != 0)
-        return fail(AES_ERR_CSR_INVALID, "LengthMismatch");
+        return bad(AES_CSR_LENGTH_MISMATCH, 0, false);
     DBuf<unsigned long long> scratch;
     AES_TRY(scratch.alloc(2));
     cudaStream_t st = lib_stream();
     AES_TRY(launch_validate(a->row_ptr, a->col, a->n_rows, a->n_cols, scratch.p, st));
     unsigned long long first_bad = 0;
     AES_TRY(d2h_scalar(scratch.p, &first_bad));
-    if (first_bad != ~0ull)
-        return fail(AES_ERR_CSR_INVALID, std::string("NonMonotonicRowPtr at row ") + std::to_string(first_bad));
+    if (first_bad != ~0ull) return bad(AES_CSR_NON_MONOTONIC, first_bad, true);
     uint64_t back = 0;
     AES_TRY(d2h_scalar(a->row_ptr + a->n_rows, &back));
-    if (back != nnz_len) return fail(AES_ERR_CSR_INVALID, "LengthMismatch");
+    if (back != nnz_len) return bad(AES_CSR_LENGTH_MISMATCH, 0, false);
     AES_TRY(launch_validate_rows(a->row_ptr, a->col, a->n_rows, a->n_cols, scratch.p + 1, st));
     unsigned long long code = 0;
     AES_TRY(d2h_scalar(scratch.p + 1, &code));
-    if (code != ~0ull) {
-        uint64_t row = code >> 2;
-        return fail(AES_ERR_CSR_INVALID,
-                    std::string(csr_error_name((int)(code & 3))) + " at row " + std::to_string(row));
-    }
+    if (code != ~0ull) return bad((int)(code & 3), code >> 2, true);
     return AES_OK;
 }
 
@@ -255,8 +272,12 @@ int sampled_for(aes_plan_t p, aes_csr_t a, DBuf<uint32_t>& tcol, DBuf<float>& tv
     }
     AES_TRY(tcol.alloc(p->total_slots));
     AES_TRY(tval.alloc(p->total_slots));
-    AES_TRY(launch_sample_fill(p->src->row_ptr, a->row_ptr, a->col, a->val, a->n_rows, p->width, p->strategy,
-                               p->srow_ptr, tcol.p, tval.p, lib_stream()));
+    if (p->explicit_plan)
+        AES_TRY(launch_explicit_fill(a->row_ptr, p->params, p->starts_ptr, p->starts, a->col, a->val, a->n_rows,
+                                     p->srow_ptr, tcol.p, tval.p, lib_stream()));
+    else
+        AES_TRY(launch_sample_fill(p->src->row_ptr, a->row_ptr, a->col, a->val, a->n_rows, p->width, p->strategy,
+                                   p->srow_ptr, tcol.p, tval.p, lib_stream()));
     *scol = tcol.p;
     *sval = tval.p;
     return AES_OK;
@@ -443,6 +464,72 @@ int aes_gcn_normalize(aes_csr_t a, int add_self_loops, aes_csr_t* out) {
     return AES_OK;
 }
 
+int aes_validate_csr(uint64_t n_rows, uint64_t n_cols, const uint64_t* row_ptr, uint64_t row_ptr_len,
+                     const uint32_t* col_ind, uint64_t nnz_len, int* error, uint64_t* row) {
+    if (error) *error = AES_CSR_OK;
+    if (row) *row = 0;
+    if (row_ptr_len != n_rows + 1 || row_ptr_len == 0 || row_ptr[0] != 0) {
+        if (error) *error = AES_CSR_LENGTH_MISMATCH;
+        return fail(AES_ERR_CSR_INVALID, "LengthMismatch");
+    }
+    aes_csr_s tmp;
+    tmp.n_rows = n_rows;
+    tmp.n_cols = n_cols;
+    tmp.owned = false;
+    DBuf<uint64_t> rp;
+    DBuf<uint32_t> ci;
+    AES_TRY(rp.alloc(n_rows + 1));
+    AES_TRY(ci.alloc(nnz_len ? nnz_len : 1));
+    cudaStream_t st = lib_stream();
+    AES_CUDA_TRY(cudaMemcpyAsync(rp.p, row_ptr, (n_rows + 1) * 8, cudaMemcpyHostToDevice, st));
+    if (nnz_len) AES_CUDA_TRY(cudaMemcpyAsync(ci.p, col_ind, nnz_len * 4, cudaMemcpyHostToDevice, st));
+    tmp.row_ptr = rp.p;
+    tmp.col = ci.p;
+    int s = validate_device(&tmp, row_ptr_len, nnz_len, row_ptr[0], error, row);
+    tmp.row_ptr = nullptr;
+    tmp.col = nullptr;
+    return s;
+}
+
+int aes_csr_structure(uint64_t n_rows, uint64_t n_cols, const uint64_t* row_ptr, aes_csr_t* out) {
+    if (!out || !row_ptr) return fail(AES_ERR_INVALID_ARG, "null argument");
+    DBuf<uint64_t> rp;
+    AES_TRY(rp.alloc(n_rows + 1));
+    AES_CUDA_TRY(cudaMemcpyAsync(rp.p, row_ptr, (n_rows + 1) * 8, cudaMemcpyHostToDevice, lib_stream()));
+    AES_TRY(sync());
+    auto* a = new aes_csr_s;
+    a->n_rows = n_rows;
+    a->n_cols = n_cols;
+    a->nnz = row_ptr[n_rows];
+    a->row_ptr = rp.release();
+    *out = a;
+    return AES_OK;
+}
+
+int aes_fit_params(const float* x, uint64_t rows, uint64_t cols, uint32_t bits, float* x_min, float* x_max) {
+    const uint64_t n = rows * cols;
+    if (n == 0) return fail(AES_ERR_EMPTY, "EmptyMatrix");
+    if (bits < 1 || bits > 16) return fail(AES_ERR_BITS, "bits must be 1..16");
+    cudaStream_t st = lib_stream();
+    DBuf<float> dx, res;
+    DBuf<char> ws;
+    AES_TRY(dx.alloc(n));
+    AES_CUDA_TRY(cudaMemcpyAsync(dx.p, x, n * 4, cudaMemcpyHostToDevice, st));
+    const size_t wsb = aes_dev_scan_workspace_bytes(1);
+    AES_TRY(ws.alloc(wsb));
+    AES_TRY(res.alloc(4));
+    AES_TRY(aes_dev_fit_params(dx.p, n, res.p, ws.p, wsb, st));
+    float r[4];
+    AES_CUDA_TRY(cudaMemcpyAsync(r, res.p, sizeof(r), cudaMemcpyDeviceToHost, st));
+    AES_TRY(sync());
+    uint32_t flag;
+    memcpy(&flag, &r[2], 4);
+    if (flag) return fail(AES_ERR_NONFINITE, "NonFinite");
+    *x_min = r[0];
+    *x_max = r[1];
+    return AES_OK;
+}
+
 // ---- plans -------------------------------------------------------------------
 int aes_build_plan_set(aes_csr_t a, uint32_t width, int strategy, aes_plan_t* out) {
     if (!a || !out) return fail(AES_ERR_INVALID_ARG, "null argument");
@@ -462,8 +549,9 @@ int aes_build_plan_set(aes_csr_t a, uint32_t width, int strategy, aes_plan_t* ou
     DBuf<float> sval;
     AES_TRY(scol.alloc(total ? total : 1));
     AES_TRY(sval.alloc(total ? total : 1));
-    AES_TRY(aes_dev_sample_fill(a->row_ptr, a->row_ptr, a->col, a->val, n, width, strategy, srow.p, scol.p,
-                                sval.p, st));
+    if (a->col)  // structure-only CSRs get the plan (row pointer) without a sampled CSR
+        AES_TRY(aes_dev_sample_fill(a->row_ptr, a->row_ptr, a->col, a->val, n, width, strategy, srow.p, scol.p,
+                                    sval.p, st));
     AES_TRY(sync());
     auto* p = new aes_plan_s;
     p->width = width;
@@ -479,12 +567,72 @@ int aes_build_plan_set(aes_csr_t a, uint32_t width, int strategy, aes_plan_t* ou
     return AES_OK;
 }
 
+int aes_plan_from_host(aes_csr_t a, uint32_t width, int strategy, const uint32_t* chunk_len,
+                       const uint32_t* sample_cnt, const uint64_t* starts_ptr, const uint32_t* starts,
+                       aes_plan_t* out) {
+    if (!a || !out || (a->n_rows && (!chunk_len || !sample_cnt || !starts_ptr)))
+        return fail(AES_ERR_INVALID_ARG, "null argument");
+    cudaStream_t st = lib_stream();
+    const uint64_t n = a->n_rows;
+    const uint64_t tot_starts = starts_ptr ? starts_ptr[n] : 0;
+    // interleave (chunk, cnt) on the host side of the copy: plain data marshaling
+    std::vector<uint32_t> params(2 * (n ? n : 1));
+    for (uint64_t i = 0; i < n; ++i) {
+        params[2 * i] = chunk_len[i];
+        params[2 * i + 1] = sample_cnt[i];
+    }
+    DBuf<uint32_t> dpar, dst;
+    DBuf<uint64_t> dsp, srow;
+    DBuf<char> ws;
+    AES_TRY(dpar.alloc(params.size()));
+    AES_TRY(dsp.alloc(n + 1));
+    AES_TRY(dst.alloc(tot_starts ? tot_starts : 1));
+    AES_CUDA_TRY(cudaMemcpyAsync(dpar.p, params.data(), params.size() * 4, cudaMemcpyHostToDevice, st));
+    if (starts_ptr) AES_CUDA_TRY(cudaMemcpyAsync(dsp.p, starts_ptr, (n + 1) * 8, cudaMemcpyHostToDevice, st));
+    if (tot_starts) AES_CUDA_TRY(cudaMemcpyAsync(dst.p, starts, tot_starts * 4, cudaMemcpyHostToDevice, st));
+    AES_TRY(srow.alloc(n + 1));
+    size_t wsb = row_scan_workspace_bytes(n);
+    AES_TRY(ws.alloc(wsb));
+    ScanArgs sa{nullptr, nullptr, n, width, strategy, 0, srow.p, dpar.p};
+    AES_TRY(launch_row_scan(kScanExplicit, sa, ws.p, wsb, st));
+    uint64_t total = 0;
+    AES_TRY(d2h_scalar(srow.p + n, &total));
+    DBuf<uint32_t> scol;
+    DBuf<float> sval;
+    AES_TRY(scol.alloc(total ? total : 1));
+    AES_TRY(sval.alloc(total ? total : 1));
+    if (a->col)  // structure-only CSRs (aes_csr_structure) carry plans for rates only
+        AES_TRY(launch_explicit_fill(a->row_ptr, dpar.p, dsp.p, dst.p, a->col, a->val, n, srow.p, scol.p, sval.p,
+                                     st));
+    AES_TRY(sync());
+    auto* p = new aes_plan_s;
+    p->width = width;
+    p->strategy = strategy;
+    p->n_rows = n;
+    p->total_slots = total;
+    a->refs.fetch_add(1);
+    p->src = a;
+    p->srow_ptr = srow.release();
+    p->scol = scol.release();
+    p->sval = sval.release();
+    p->explicit_plan = true;
+    p->params = dpar.release();
+    p->starts_ptr = dsp.release();
+    p->starts = dst.release();
+    p->total_starts = tot_starts;
+    *out = p;
+    return AES_OK;
+}
+
 int aes_plan_destroy(aes_plan_t p) {
     if (!p) return AES_OK;
     cudaStream_t st = lib_stream();
     cudaFreeAsync(p->srow_ptr, st);
     cudaFreeAsync(p->scol, st);
     cudaFreeAsync(p->sval, st);
+    if (p->params) cudaFreeAsync(p->params, st);
+    if (p->starts_ptr) cudaFreeAsync(p->starts_ptr, st);
+    if (p->starts) cudaFreeAsync(p->starts, st);
     csr_release(p->src);
     delete p;
     return AES_OK;
@@ -497,7 +645,9 @@ int aes_plan_info(aes_plan_t p, uint32_t* width, int* strategy, uint64_t* n_rows
     if (strategy) *strategy = p->strategy;
     if (n_rows) *n_rows = p->n_rows;
     if (total_slots) *total_slots = p->total_slots;
-    if (total_starts) {
+    if (total_starts && p->explicit_plan) {
+        *total_starts = p->total_starts;
+    } else if (total_starts) {
         const uint64_t n = p->n_rows;
         DBuf<uint64_t> sp;
         DBuf<char> ws;
@@ -516,6 +666,22 @@ int aes_plan_export(aes_plan_t p, uint32_t* chunk_len, uint32_t* sample_cnt, uin
     if (!p) return fail(AES_ERR_INVALID_ARG, "null plan");
     cudaStream_t st = lib_stream();
     const uint64_t n = p->n_rows;
+    if (p->explicit_plan) {  // stored as given
+        if (n) {
+            DBuf<uint32_t> ch, cn;
+            AES_TRY(ch.alloc(n));
+            AES_TRY(cn.alloc(n));
+            AES_CUDA_TRY(cudaMemcpy2DAsync(ch.p, 4, p->params, 8, 4, n, cudaMemcpyDeviceToDevice, st));
+            AES_CUDA_TRY(cudaMemcpy2DAsync(cn.p, 4, p->params + 1, 8, 4, n, cudaMemcpyDeviceToDevice, st));
+            if (chunk_len) AES_CUDA_TRY(cudaMemcpyAsync(chunk_len, ch.p, n * 4, cudaMemcpyDeviceToHost, st));
+            if (sample_cnt) AES_CUDA_TRY(cudaMemcpyAsync(sample_cnt, cn.p, n * 4, cudaMemcpyDeviceToHost, st));
+            AES_TRY(sync());
+        }
+        if (starts_ptr) AES_CUDA_TRY(cudaMemcpyAsync(starts_ptr, p->starts_ptr, (n + 1) * 8, cudaMemcpyDeviceToHost, st));
+        if (starts && p->total_starts)
+            AES_CUDA_TRY(cudaMemcpyAsync(starts, p->starts, p->total_starts * 4, cudaMemcpyDeviceToHost, st));
+        return sync();
+    }
     DBuf<uint64_t> sp;
     DBuf<char> ws;
     AES_TRY(sp.alloc(n + 1));
@@ -567,7 +733,14 @@ int aes_sampling_rate(aes_plan_t p, aes_csr_t a, double* aggregate, double* uniq
     DBuf<double> pr;
     AES_TRY(tot.alloc(3));
     if (per_row) AES_TRY(pr.alloc(a->n_rows ? a->n_rows : 1));
-    AES_TRY(launch_sampling_rate(a->row_ptr, a->n_rows, p->width, p->strategy, pr.p, tot.p, st));
+    DBuf<unsigned char> seen;
+    if (p->explicit_plan) {
+        AES_TRY(seen.alloc(a->nnz ? a->nnz : 1));
+        AES_TRY(launch_explicit_rate(a->row_ptr, p->params, p->starts_ptr, p->starts, a->n_rows, a->nnz, seen.p,
+                                     pr.p, tot.p, st));
+    } else {
+        AES_TRY(launch_sampling_rate(a->row_ptr, a->n_rows, p->width, p->strategy, pr.p, tot.p, st));
+    }
     unsigned long long t[3];
     AES_CUDA_TRY(cudaMemcpyAsync(t, tot.p, sizeof(t), cudaMemcpyDeviceToHost, st));
     if (per_row && a->n_rows)

@@ -112,7 +112,7 @@ inline unsigned grid_for(uint64_t work, unsigned per_block, unsigned cap = 1u <<
 // Internal launchers shared between translation units.
 // ---------------------------------------------------------------------------
 // Exclusive scan of per-row counts produced by a functor kind, writing out[n+1].
-enum ScanKind : int { kScanSlots = 0, kScanStarts = 1, kScanGcnNnz = 2 };
+enum ScanKind : int { kScanSlots = 0, kScanStarts = 1, kScanGcnNnz = 2, kScanExplicit = 3 };
 struct ScanArgs {
     const uint64_t* row_ptr;  // row lengths from here
     const uint32_t* col_ind;  // for kScanGcnNnz (diagonal probe)
@@ -121,7 +121,7 @@ struct ScanArgs {
     int strategy;
     int add_self_loops;
     uint64_t* out;           // n+1
-    uint32_t* row_params;    // optional (kScanSlots)
+    uint32_t* row_params;    // kScanSlots: optional output; kScanExplicit: input (uint2 per row)
 };
 int launch_row_scan(int kind, const ScanArgs& a, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t row_scan_workspace_bytes(uint64_t n);

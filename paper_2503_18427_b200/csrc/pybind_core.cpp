@@ -356,12 +356,12 @@ PYBIND11_MODULE(_core, mod) {
         "fit_params",
         [](F32In x, uint32_t bits) {
             x = as_2d(x);
-            aes_qfeat_t h = nullptr;
+            QuantParams p;
+            p.bits = bits;
             uint64_t r = x.shape(0), c = x.shape(1);
             const float* px = x.data();
-            check(nogil([&] { return aes_quantize(px, r, c, bits, &h); }));
-            QFeat q(h);
-            return q.params;
+            check(nogil([&] { return aes_fit_params(px, r, c, bits, &p.x_min, &p.x_max); }));
+            return p;
         },
         py::arg("x"), py::arg("bits") = 8);
     mod.def(

@@ -35,6 +35,10 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 
 template <int KIND>
 __device__ __forceinline__ uint64_t row_count(const ScanArgs& a, uint64_t r) {
+    if (KIND == kScanExplicit) {  // host-supplied plans: slots = chunk * cnt
+        const uint2 p = reinterpret_cast<const uint2*>(a.row_params)[r];
+        return (uint64_t)p.x * p.y;
+    }
     uint64_t b = a.row_ptr[r], e = a.row_ptr[r + 1];
     uint64_t nnz = e - b;
     if (KIND == kScanSlots) {
@@ -155,6 +159,9 @@ int launch_row_scan(int kind, const ScanArgs& a, void* ws, size_t ws_bytes, cuda
         case kScanStarts:
             row_scan_kernel<kScanStarts><<<(unsigned)tiles, kScanThreads, 0, st>>>(a, state, counter);
             break;
+        case kScanExplicit:
+            row_scan_kernel<kScanExplicit><<<(unsigned)tiles, kScanThreads, 0, st>>>(a, state, counter);
+            break;
         default:
             row_scan_kernel<kScanGcnNnz><<<(unsigned)tiles, kScanThreads, 0, st>>>(a, state, counter);
             break;
@@ -212,6 +219,90 @@ sample_fill_kernel(const uint64_t* __restrict__ plan_row_ptr, const uint64_t* __
         const uint64_t src = s_rp[lo] + row_start(nnz, width, strategy, p, (uint32_t)s) + j;
         scol[pos] = col_ind[src];
         sval[pos] = val[src];
+    }
+}
+
+// Fill from host-supplied plans (RowSamplePlan objects built outside
+// build_plan_set): chunk/cnt per row as uint2, starts in CSR form.  Same slot
+// order as spmm.cpp:68-76.
+__global__ void __launch_bounds__(kFillRows)
+explicit_fill_kernel(const uint64_t* __restrict__ row_ptr, const uint2* __restrict__ params,
+                     const uint64_t* __restrict__ starts_ptr, const uint32_t* __restrict__ starts,
+                     const uint32_t* __restrict__ col_ind, const float* __restrict__ val, uint64_t n,
+                     const uint64_t* __restrict__ srow_ptr, uint32_t* __restrict__ scol, float* __restrict__ sval) {
+    __shared__ uint64_t s_srow[kFillRows + 1];
+    const uint64_t r0 = (uint64_t)blockIdx.x * kFillRows;
+    const int nr = (int)min((uint64_t)kFillRows, n - r0);
+    for (int i = threadIdx.x; i <= nr; i += blockDim.x) s_srow[i] = srow_ptr[r0 + i];
+    __syncthreads();
+    const uint64_t g0 = s_srow[0];
+    const uint64_t total = s_srow[nr] - g0;
+    for (uint64_t t = threadIdx.x; t < total; t += blockDim.x) {
+        const uint64_t pos = g0 + t;
+        int lo = 0, hi = nr;
+        while (hi - lo > 1) {
+            int mid = (lo + hi) >> 1;
+            if (s_srow[mid] <= pos) lo = mid; else hi = mid;
+        }
+        const uint64_t row = r0 + lo;
+        const uint2 p = params[row];
+        const uint64_t k = pos - s_srow[lo];
+        const uint64_t s = k % p.y, j = k / p.y;
+        const uint64_t src = row_ptr[row] + starts[starts_ptr[row] + s] + j;
+        scol[pos] = col_ind[src];
+        sval[pos] = val[src];
+    }
+}
+
+// Coverage of explicit plans (sampling_rate's unique count, sampling.cpp:136-147):
+// mark every sampled offset, then count marks per matrix.
+__global__ void explicit_mark_kernel(const uint64_t* __restrict__ row_ptr, const uint2* __restrict__ params,
+                                     const uint64_t* __restrict__ starts_ptr, const uint32_t* __restrict__ starts,
+                                     uint64_t n, unsigned char* __restrict__ seen) {
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
+        const uint2 p = params[r];
+        const uint64_t slots = (uint64_t)p.x * p.y;
+        const uint64_t sp = starts_ptr[r], base = row_ptr[r];
+        for (uint64_t k = lane; k < slots; k += 32) {
+            const uint64_t s = k % p.y, j = k / p.y;
+            seen[base + starts[sp + s] + j] = 1;
+        }
+    }
+}
+
+__global__ void count_marks_kernel(const unsigned char* __restrict__ seen, uint64_t nnz,
+                                   unsigned long long* __restrict__ total) {
+    unsigned long long c = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nnz; i += (uint64_t)gridDim.x * blockDim.x)
+        c += seen[i];
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(total, c);
+}
+
+__global__ void explicit_slots_kernel(const uint64_t* __restrict__ row_ptr, const uint2* __restrict__ params,
+                                      uint64_t n, double* __restrict__ per_row, unsigned long long* __restrict__ totals) {
+    unsigned long long slots = 0, nnz_sum = 0;
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t nnz = row_ptr[r + 1] - row_ptr[r];
+        const uint2 p = params[r];
+        nnz_sum += nnz;
+        if (nnz == 0) {
+            if (per_row) per_row[r] = 1.0;
+            continue;
+        }
+        const uint64_t sl = (uint64_t)p.x * p.y;
+        slots += sl;
+        if (per_row) per_row[r] = (double)sl / (double)nnz;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        slots += __shfl_down_sync(0xffffffffu, slots, o);
+        nnz_sum += __shfl_down_sync(0xffffffffu, nnz_sum, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&totals[0], slots);
+        atomicAdd(&totals[2], nnz_sum);
     }
 }
 
@@ -358,6 +449,32 @@ int launch_sample_fill(const uint64_t* plan_row_ptr, const uint64_t* row_ptr, co
     unsigned grid = grid_for(n, kFillRows);
     sample_fill_kernel<<<grid, kFillRows, 0, st>>>(plan_row_ptr, row_ptr, col, val, n, width, strategy,
                                                    srow_ptr, scol, sval);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
+int launch_explicit_fill(const uint64_t* row_ptr, const uint32_t* params, const uint64_t* starts_ptr,
+                         const uint32_t* starts, const uint32_t* col, const float* val, uint64_t n,
+                         const uint64_t* srow_ptr, uint32_t* scol, float* sval, cudaStream_t st) {
+    if (n == 0) return AES_OK;
+    explicit_fill_kernel<<<grid_for(n, kFillRows), kFillRows, 0, st>>>(
+        row_ptr, reinterpret_cast<const uint2*>(params), starts_ptr, starts, col, val, n, srow_ptr, scol, sval);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
+int launch_explicit_rate(const uint64_t* row_ptr, const uint32_t* params, const uint64_t* starts_ptr,
+                         const uint32_t* starts, uint64_t n, uint64_t nnz, unsigned char* seen, double* per_row,
+                         unsigned long long* totals, cudaStream_t st) {
+    AES_CUDA_TRY(cudaMemsetAsync(totals, 0, 3 * sizeof(unsigned long long), st));
+    if (n == 0) return AES_OK;
+    const uint2* pp = reinterpret_cast<const uint2*>(params);
+    explicit_slots_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(row_ptr, pp, n, per_row, totals);
+    if (nnz) {
+        AES_CUDA_TRY(cudaMemsetAsync(seen, 0, nnz, st));
+        explicit_mark_kernel<<<grid_for(n * 32, 256, 148 * 32), 256, 0, st>>>(row_ptr, pp, starts_ptr, starts, n, seen);
+        count_marks_kernel<<<grid_for(nnz, 256, 148 * 16), 256, 0, st>>>(seen, nnz, totals + 1);
+    }
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
 }
