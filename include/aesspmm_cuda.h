@@ -256,6 +256,32 @@ AES_API int aes_dev_gemm_bias_act(const float* a, uint64_t m, uint64_t k, uint64
                                   const float* w, uint64_t n, uint64_t ldw, const float* bias,
                                   int relu, float* h, uint64_t ldh, void* stream);
 
+/* Extended layer GEMM: as aes_dev_gemm_bias_act, writing rows
+ * [row_offset, row_offset + m) of the replica(s) dsts[0..n_dst) (ld ldh).
+ * finite_w != 0 asserts W has no inf/NaN (check with aes_dev_all_finite), which
+ * makes the reference's zero-skip result-neutral and lets the kernel drop it.
+ * counters != NULL turns on the fused exchange: dsts are every rank's replica
+ * (CUDA-IPC peer pointers), and each CTA, after its stores, does a
+ * system-scope fence and one release-add on counters[d] for every d — a rank
+ * waits for sum-over-producers aes_gemm_ctas(m_p, n) arrivals
+ * (aes_dev_wait_counter) before reading its replica.  This replaces the
+ * layer's all-gather (gnn.cpp:66-78 run row-sharded). */
+AES_API int aes_dev_gemm_bias_act_ex(const float* a, uint64_t m, uint64_t k, uint64_t lda,
+                                     const float* w, uint64_t n, uint64_t ldw, const float* bias,
+                                     int relu, int finite_w, float* const* dsts,
+                                     unsigned long long* const* counters, int n_dst,
+                                     uint64_t row_offset, uint64_t ldh, void* stream);
+/* Number of CTAs (= arrivals per destination) the GEMM above launches. */
+AES_API uint64_t aes_gemm_ctas(uint64_t m, uint64_t n);
+/* Spin (one thread, ld.acquire.sys) until *counter >= target. */
+AES_API int aes_dev_wait_counter(const unsigned long long* counter, unsigned long long target,
+                                 void* stream);
+/* Device-side barrier arrival: system-scope fence, then +1 on every
+ * counters[d] (host array of device pointers, e.g. all ranks' counters). */
+AES_API int aes_dev_signal_all(unsigned long long* const* counters, int n, void* stream);
+/* *bad_flag = 1 if any of x[0..count) is inf/NaN (stream-ordered). */
+AES_API int aes_dev_all_finite(const float* x, uint64_t count, unsigned int* bad_flag, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -49,6 +49,13 @@ def lib():
         L.aes_dev_dequantize.argtypes = [vp, u64, u64, u64, f32, f32, u32, vp, u64, vp]
         L.aes_dev_dequant_lut.argtypes = [f32, f32, u32, vp, vp]
         L.aes_dev_gemm_bias_act.argtypes = [vp, u64, u64, u64, vp, u64, u64, vp, i32, vp, u64, vp]
+        L.aes_dev_gemm_bias_act_ex.argtypes = [vp, u64, u64, u64, vp, u64, u64, vp, i32, i32, vp, vp, i32, u64,
+                                               u64, vp]
+        L.aes_gemm_ctas.argtypes = [u64, u64]
+        L.aes_gemm_ctas.restype = u64
+        L.aes_dev_wait_counter.argtypes = [vp, u64, vp]
+        L.aes_dev_all_finite.argtypes = [vp, u64, vp, vp]
+        L.aes_dev_signal_all.argtypes = [vp, i32, vp]
         L.aes_select_strategy.argtypes = [u64, u32, vp, vp]
         L.aes_hash_start.argtypes = [u32, u64, u32]
         L.aes_hash_start.restype = u32

@@ -1,13 +1,18 @@
-// Ordered fp32 layer GEMM + bias + ReLU epilogue for the GCN layer driver.
+// Ordered fp32 layer GEMM + bias + ReLU epilogue for the GCN layer driver,
+// optionally fused with the layer's exchange: the epilogue stores every output
+// tile into ALL ranks' next-layer replicas over peer memory (NVLink P2P
+// stores to CUDA-IPC-mapped buffers) and each CTA then publishes a
+// system-scope arrival on every destination's counter — the all-gather
+// disappears into the GEMM (no NCCL call, transfer overlapped tile by tile).
 //
 // Bit-exact with the reference dense_matmul (proj/src/gnn.cpp:11-31): every
 // output element accumulates k in ascending order as acc = RN(acc + RN(a*w))
-// from +0.0f, skipping a == 0 exactly as the reference does (which also keeps
-// 0*inf from producing NaN).  Bias then ReLU follow gnn.cpp:41-52 with
-// std::max(v, 0.0f) semantics ((v < 0) ? 0 : v, so -0.0f and NaN pass through).
-// Tensor cores are deliberately not used: their reduction order and fused
-// rounding cannot reproduce the reference's result bits.  (A tcgen05 TF32/BF16
-// "fast mode" with a stated tolerance is listed as next work in DESIGN.md.)
+// from +0.0f, skipping a == 0 as the reference does.  When W is known to be
+// finite the skip is provably result-neutral (acc is never -0 and RN(0*w) is
+// +-0), so the `finite_w` form drops the select.  Bias then ReLU follow
+// gnn.cpp:41-52 with std::max(v, 0.0f) semantics ((v < 0) ? 0 : v).  Tensor
+// cores are not used: their reduction order and fused rounding cannot
+// reproduce the reference's result bits.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -16,15 +21,24 @@
 namespace aes {
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4;
+constexpr int BM = 128, BN = 128, BK = 8, TM = 8, TN = 8;
 constexpr int kThreads = (BM / TM) * (BN / TN);  // 256
+constexpr int kMaxDst = 16;
 
-__global__ void __launch_bounds__(kThreads)
+struct Bcast {
+    float* dst[kMaxDst];                   // replica base pointers (own + peers)
+    unsigned long long* ctr[kMaxDst];      // arrival counters (one per destination rank)
+    int n;
+    uint64_t row_off;                      // this shard's first row in the replica
+};
+
+template <bool SKIP, bool BCAST>
+__global__ void __launch_bounds__(kThreads, 2)
 gemm_ordered_kernel(const float* __restrict__ a, uint64_t m, uint64_t k, uint64_t lda,
-                    const float* __restrict__ w, uint64_t n, uint64_t ldw,
-                    const float* __restrict__ bias, int relu, float* __restrict__ h, uint64_t ldh) {
-    __shared__ float As[BK][BM + 4];
-    __shared__ float Ws[BK][BN + 4];
+                    const float* __restrict__ w, uint64_t n, uint64_t ldw, const float* __restrict__ bias,
+                    int relu, float* __restrict__ h, uint64_t ldh, Bcast bc) {
+    __shared__ __align__(16) float As[2][BK][BM + 4];  // +4: conflict-free transposed stores
+    __shared__ __align__(16) float Ws[2][BK][BN];
     const int tid = threadIdx.x;
     const int tx = tid % (BN / TN), ty = tid / (BN / TN);
     const uint64_t m0 = (uint64_t)blockIdx.y * BM, n0 = (uint64_t)blockIdx.x * BN;
@@ -35,79 +49,222 @@ gemm_ordered_kernel(const float* __restrict__ a, uint64_t m, uint64_t k, uint64_
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
 
+    // staging: A tile BM x BK (4 elements / thread), W tile BK x BN (4 / thread)
+    float ra[4], rw[4];
+    auto load_tiles = [&](uint64_t k0) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int e = tid + r * kThreads;      // 0..1023
+            const int mm = e / BK, kk = e % BK;
+            const uint64_t gm = m0 + mm, gk = k0 + kk;
+            ra[r] = (gm < m && gk < k) ? __ldg(a + gm * lda + gk) : 0.f;  // zero fill is neutral
+            const int kw = e / BN, nn = e % BN;
+            const uint64_t gkw = k0 + kw, gn = n0 + nn;
+            rw[r] = (gkw < k && gn < n) ? __ldg(w + gkw * ldw + gn) : 0.f;
+        }
+    };
+    auto store_tiles = [&](int buf) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int e = tid + r * kThreads;
+            As[buf][e % BK][e / BK] = ra[r];
+            Ws[buf][e / BN][e % BN] = rw[r];
+        }
+    };
+
+    load_tiles(0);
+    store_tiles(0);
+    __syncthreads();
+    int buf = 0;
     for (uint64_t k0 = 0; k0 < k; k0 += BK) {
-        // A tile (BM x BK) -> As[kk][mm]; zero fill is neutral (a == 0 skipped)
-#pragma unroll
-        for (int e = tid; e < BM * BK; e += kThreads) {
-            int mm = e / BK, kk = e % BK;
-            uint64_t gm = m0 + mm, gk = k0 + kk;
-            As[kk][mm] = (gm < m && gk < k) ? a[gm * lda + gk] : 0.f;
-        }
-#pragma unroll
-        for (int e = tid; e < BK * BN; e += kThreads) {
-            int kk = e / BN, nn = e % BN;
-            uint64_t gk = k0 + kk, gn = n0 + nn;
-            Ws[kk][nn] = (gk < k && gn < n) ? w[gk * ldw + gn] : 0.f;
-        }
-        __syncthreads();
+        const bool more = k0 + BK < k;
+        if (more) load_tiles(k0 + BK);  // prefetch the next K slab into registers
 #pragma unroll
         for (int kk = 0; kk < BK; ++kk) {
-            float av[TM], wv[TN];
-#pragma unroll
-            for (int i = 0; i < TM; ++i) av[i] = As[kk][ty * TM + i];
-#pragma unroll
-            for (int j = 0; j < TN; ++j) wv[j] = Ws[kk][tx * TN + j];
+            const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * TM]);
+            const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * TM + 4]);
+            const float4 w0 = *reinterpret_cast<const float4*>(&Ws[buf][kk][tx * TN]);
+            const float4 w1 = *reinterpret_cast<const float4*>(&Ws[buf][kk][tx * TN + 4]);
+            const float av[TM] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float wv[TN] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
             for (int i = 0; i < TM; ++i) {
-                const bool skip = av[i] == 0.f;
+                if (SKIP) {
+                    const bool skip = av[i] == 0.f;
 #pragma unroll
-                for (int j = 0; j < TN; ++j) {
-                    float s = __fadd_rn(acc[i][j], __fmul_rn(av[i], wv[j]));
-                    acc[i][j] = skip ? acc[i][j] : s;
+                    for (int j = 0; j < TN; ++j) {
+                        const float s = __fadd_rn(acc[i][j], __fmul_rn(av[i], wv[j]));
+                        acc[i][j] = skip ? acc[i][j] : s;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < TN; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(av[i], wv[j]));
                 }
             }
         }
-        __syncthreads();
-    }
-#pragma unroll
-    for (int i = 0; i < TM; ++i) {
-        uint64_t gm = m0 + ty * TM + i;
-        if (gm >= m) continue;
-#pragma unroll
-        for (int j = 0; j < TN; ++j) {
-            uint64_t gn = n0 + tx * TN + j;
-            if (gn >= n) continue;
-            float v = acc[i][j];
-            if (bias) v = __fadd_rn(v, bias[gn]);
-            if (relu) v = (v < 0.f) ? 0.f : v;
-            h[gm * ldh + gn] = v;
+        if (more) {
+            store_tiles(buf ^ 1);
+            __syncthreads();
+            buf ^= 1;
         }
     }
+
+    // epilogue: bias, ReLU, store (to every replica when broadcasting)
+    const uint64_t gn0 = n0 + tx * TN;
+    const bool vec = (gn0 + TN <= n) && (ldh % 4 == 0);
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+        const uint64_t gm = m0 + ty * TM + i;
+        if (gm >= m) continue;
+        float v[TN];
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+            float x = acc[i][j];
+            if (bias && gn0 + j < n) x = __fadd_rn(x, bias[gn0 + j]);
+            if (relu) x = (x < 0.f) ? 0.f : x;
+            v[j] = x;
+        }
+        const int nd = BCAST ? bc.n : 1;
+        for (int d = 0; d < nd; ++d) {
+            float* row = BCAST ? bc.dst[d] + (bc.row_off + gm) * ldh : h + gm * ldh;
+            if (vec) {
+                reinterpret_cast<float4*>(row + gn0)[0] = make_float4(v[0], v[1], v[2], v[3]);
+                reinterpret_cast<float4*>(row + gn0)[1] = make_float4(v[4], v[5], v[6], v[7]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < TN; ++j)
+                    if (gn0 + j < n) row[gn0 + j] = v[j];
+            }
+        }
+    }
+    if (BCAST) {
+        // publish this CTA's tile to every destination: the barrier orders the
+        // CTA's stores before thread 0's system-scope fence (cumulativity),
+        // then one release-add per destination counter.
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence_system();
+            for (int d = 0; d < bc.n; ++d)
+                asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(bc.ctr[d]) : "memory");
+        }
+    }
+}
+
+__global__ void wait_counter_kernel(const unsigned long long* ctr, unsigned long long target) {
+    unsigned long long v;
+    do {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+    } while (v < target);
+}
+
+// One thread: make this rank's prior work visible system-wide, then bump
+// every rank's counter (a device-side cross-rank barrier arrival).
+__global__ void signal_all_kernel(unsigned long long* const* ctrs, int n) {
+    __threadfence_system();
+    for (int d = 0; d < n; ++d) asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(ctrs[d]) : "memory");
+}
+
+struct CtrArray {
+    unsigned long long* p[kMaxDst];
+};
+__global__ void signal_all_arr_kernel(CtrArray a, int n) {
+    __threadfence_system();
+    for (int d = 0; d < n; ++d) asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(a.p[d]) : "memory");
+}
+
+__global__ void all_finite_kernel(const float* __restrict__ x, uint64_t count, unsigned int* __restrict__ bad) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x)
+        if (!isfinite(x[i])) atomicOr(bad, 1u);
+}
+
+template <bool SKIP, bool BCAST>
+int launch(const float* a, uint64_t m, uint64_t k, uint64_t lda, const float* w, uint64_t n, uint64_t ldw,
+           const float* bias, int relu, float* h, uint64_t ldh, const Bcast& bc, cudaStream_t st) {
+    const unsigned gx = (unsigned)((n + BN - 1) / BN);
+    const uint64_t rows_per = (uint64_t)65535 * BM;  // grid.y limit
+    for (uint64_t r0 = 0; r0 < m; r0 += rows_per) {
+        const uint64_t mm = m - r0 < rows_per ? m - r0 : rows_per;
+        Bcast b2 = bc;
+        b2.row_off += r0;
+        dim3 grid(gx, (unsigned)((mm + BM - 1) / BM));
+        gemm_ordered_kernel<SKIP, BCAST><<<grid, kThreads, 0, st>>>(a + r0 * lda, mm, k, lda, w, n, ldw, bias, relu,
+                                                                     h ? h + r0 * ldh : nullptr, ldh, b2);
+    }
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
 }
 
 }  // namespace
 }  // namespace aes
 
-extern "C" int aes_dev_gemm_bias_act(const float* a, uint64_t m, uint64_t k, uint64_t lda, const float* w,
-                                     uint64_t n, uint64_t ldw, const float* bias, int relu, float* h,
-                                     uint64_t ldh, void* stream) {
+extern "C" {
+
+int aes_dev_gemm_bias_act(const float* a, uint64_t m, uint64_t k, uint64_t lda, const float* w, uint64_t n,
+                          uint64_t ldw, const float* bias, int relu, float* h, uint64_t ldh, void* stream) {
     using namespace aes;
     if (m == 0 || n == 0) return AES_OK;
     if (lda < k || ldw < n || ldh < n) return fail(AES_ERR_INVALID_ARG, "leading dimension too small");
-    dim3 grid((unsigned)((n + BN - 1) / BN), (unsigned)((m + BM - 1) / BM));
-    if (grid.y > 65535u) {
-        // tile rows in chunks the grid can address
-        const uint64_t rows_per = (uint64_t)65535 * BM;
-        for (uint64_t r0 = 0; r0 < m; r0 += rows_per) {
-            uint64_t mm = m - r0 < rows_per ? m - r0 : rows_per;
-            dim3 g2(grid.x, (unsigned)((mm + BM - 1) / BM));
-            gemm_ordered_kernel<<<g2, kThreads, 0, as_stream(stream)>>>(a + r0 * lda, mm, k, lda, w, n, ldw,
-                                                                        bias, relu, h + r0 * ldh, ldh);
-        }
-    } else {
-        gemm_ordered_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(a, m, k, lda, w, n, ldw, bias, relu, h,
-                                                                      ldh);
+    Bcast bc{};
+    return launch<true, false>(a, m, k, lda, w, n, ldw, bias, relu, h, ldh, bc, as_stream(stream));
+}
+
+int aes_dev_gemm_bias_act_ex(const float* a, uint64_t m, uint64_t k, uint64_t lda, const float* w, uint64_t n,
+                             uint64_t ldw, const float* bias, int relu, int finite_w, float* const* dsts,
+                             unsigned long long* const* counters, int n_dst, uint64_t row_offset, uint64_t ldh,
+                             void* stream) {
+    using namespace aes;
+    if (n_dst < 1 || n_dst > kMaxDst) return fail(AES_ERR_INVALID_ARG, "1..16 destinations");
+    if (lda < k || ldw < n || ldh < n) return fail(AES_ERR_INVALID_ARG, "leading dimension too small");
+    if (n == 0) return AES_OK;
+    Bcast bc{};
+    bc.n = n_dst;
+    bc.row_off = row_offset;
+    for (int d = 0; d < n_dst; ++d) {
+        bc.dst[d] = dsts[d];
+        bc.ctr[d] = counters ? counters[d] : nullptr;
     }
+    cudaStream_t st = as_stream(stream);
+    const bool bcast = counters != nullptr;
+    if (!bcast) {
+        if (n_dst != 1) return fail(AES_ERR_INVALID_ARG, "several destinations need arrival counters");
+        float* h = dsts[0] + row_offset * ldh;
+        if (m == 0) return AES_OK;
+        return finite_w ? launch<false, false>(a, m, k, lda, w, n, ldw, bias, relu, h, ldh, bc, st)
+                        : launch<true, false>(a, m, k, lda, w, n, ldw, bias, relu, h, ldh, bc, st);
+    }
+    if (m == 0) return AES_OK;  // nothing to publish: arrival targets count launched CTAs only
+    return finite_w ? launch<false, true>(a, m, k, lda, w, n, ldw, bias, relu, nullptr, ldh, bc, st)
+                    : launch<true, true>(a, m, k, lda, w, n, ldw, bias, relu, nullptr, ldh, bc, st);
+}
+
+uint64_t aes_gemm_ctas(uint64_t m, uint64_t n) {
+    if (m == 0 || n == 0) return 0;
+    return ((n + aes::BN - 1) / aes::BN) * ((m + aes::BM - 1) / aes::BM);
+}
+
+int aes_dev_wait_counter(const unsigned long long* counter, unsigned long long target, void* stream) {
+    aes::wait_counter_kernel<<<1, 1, 0, aes::as_stream(stream)>>>(counter, target);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
 }
+
+int aes_dev_signal_all(unsigned long long* const* counters, int n, void* stream) {
+    using namespace aes;
+    if (n < 1 || n > kMaxDst) return fail(AES_ERR_INVALID_ARG, "1..16 counters");
+    CtrArray a{};
+    for (int d = 0; d < n; ++d) a.p[d] = counters[d];
+    signal_all_arr_kernel<<<1, 1, 0, as_stream(stream)>>>(a, n);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
+int aes_dev_all_finite(const float* x, uint64_t count, unsigned int* bad_flag, void* stream) {
+    using namespace aes;
+    cudaStream_t st = as_stream(stream);
+    AES_CUDA_TRY(cudaMemsetAsync(bad_flag, 0, sizeof(unsigned int), st));
+    if (count) all_finite_kernel<<<grid_for(count, 256, 148 * 8), 256, 0, st>>>(x, count, bad_flag);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
+}  // extern "C"

@@ -22,6 +22,11 @@ proj/src/gnn.cpp:66-78).
 The per-shard compute is injected (`ops`): the product path uses the CUDA C
 ABI (`CudaOps`); tests may inject a CPU checker to exercise the exchange logic
 with a gloo group.
+
+`exchange="p2p"` replaces the all-gather with the fused GEMM + exchange kernel
+(`p2p.PeerReplicas`): each rank's GEMM epilogue stores its output rows
+straight into every rank's next-layer replica over NVLink peer memory and
+signals per-CTA arrivals; the next layer starts once all arrivals landed.
 """
 from __future__ import annotations
 
@@ -75,7 +80,7 @@ class ShardedGCN:
 
     def __init__(self, srow_ptr: torch.Tensor, scol: torch.Tensor, sval: torch.Tensor, n_rows: int,
                  weights: Sequence[torch.Tensor], biases: Sequence[torch.Tensor | None], ops: Ops | None = None,
-                 group=None, balance: str = "rows"):
+                 group=None, balance: str = "rows", exchange: str = "nccl"):
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -94,6 +99,25 @@ class ShardedGCN:
         # shard plan = rows [lo, hi) of the global sampled CSR (absolute offsets)
         self.srow = srow_ptr[lo:hi + 1]
         self.scol, self.sval = scol, sval
+        self.exchange = exchange
+        self.replicas = None
+        if exchange == "p2p":
+            from . import device, p2p
+
+            if balance != "rows":
+                raise ValueError("p2p exchange uses equal-row shards")
+            dims = [weights[0].shape[0]] + [w.shape[1] for w in weights]
+            ld = (max(dims) + 3) & ~3
+            self.replicas = p2p.PeerReplicas(self.per * self.world, ld, group)
+            # finite W makes the reference's zero-skip result-neutral (gemm.cu)
+            flag = torch.zeros(1, dtype=torch.int32, device=weights[0].device)
+            self.finite = []
+            for w in weights:
+                device.check(device.lib().aes_dev_all_finite(w.data_ptr(), w.numel(), flag.data_ptr(),
+                                                             device.stream_of(None)))
+                self.finite.append(int(flag.item()) == 0)
+            self.arrivals = [sum(p2p.gemm_ctas(c1 - c0, w.shape[1]) for c0, c1 in zip(self.cuts, self.cuts[1:]))
+                             for w in weights]
 
     def _gather(self, out_rows: torch.Tensor, f: int, like: torch.Tensor) -> torch.Tensor:
         rows = self.hi - self.lo
@@ -110,9 +134,29 @@ class ShardedGCN:
             return torch.cat(parts)
         return gathered[: self.n]
 
+    def _forward_p2p(self, x: torch.Tensor, return_shard: bool) -> torch.Tensor:
+        rep = self.replicas
+        rows = self.hi - self.lo
+        f0 = x.shape[1]
+        rep.barrier()  # every peer is done with the previous step's replicas
+        rep.bufs[0][: self.n, :f0].copy_(x)
+        h = rep.bufs[0][: self.n, :f0]
+        n_layers = len(self.weights)
+        for l, (w, b) in enumerate(zip(self.weights, self.biases)):
+            agg = self.ops.spmm(self.srow, self.scol, self.sval, h, out=self.ops.alloc(max(rows, 1), h.shape[1], h))
+            out_buf = (l + 1) % 2
+            rep.gemm_publish(out_buf, agg[:rows], w, b, l + 1 < n_layers, self.finite[l], self.lo)
+            rep.wait(self.arrivals[l])
+            h = rep.bufs[out_buf][: self.n, : w.shape[1]]
+        if return_shard:
+            return h[self.lo:self.hi].clone()
+        return h.clone()
+
     def forward(self, x: torch.Tensor, return_shard: bool = False) -> torch.Tensor:
         """x: full [n, F0] replica on this rank.  Returns the full logits
         replica (or only this rank's rows when return_shard)."""
+        if self.exchange == "p2p":
+            return self._forward_p2p(x, return_shard)
         h = x
         rows = self.hi - self.lo
         n_layers = len(self.weights)

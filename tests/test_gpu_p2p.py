@@ -1,0 +1,84 @@
+"""Fused GEMM + exchange over CUDA-IPC peer memory (gcn.ShardedGCN with
+exchange="p2p").  This run has one GPU, so two ranks share cuda:0 as two
+processes: the IPC mapping, P2P epilogue stores, per-CTA system-scope
+arrivals and the device-side step barrier are exercised exactly as across
+NVLink peers.  The result must equal the single-process oracle bit for bit."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from oracle import port
+from tests import graphs
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _problem(n=3001, f=40):
+    rng = np.random.default_rng(21)
+    rp, col, _ = graphs.power_law(n, alpha=1.7, max_deg=500, seed=21)
+    nrp, ncol, nval = port.gcn_normalize(rp, col, True)
+    x = rng.uniform(-1, 1, (n, f)).astype(np.float32)
+    ws = [rng.uniform(-0.5, 0.5, (f, 64)).astype(np.float32), rng.uniform(-0.5, 0.5, (64, 64)).astype(np.float32),
+          rng.uniform(-0.5, 0.5, (64, 7)).astype(np.float32)]
+    bs = [np.full(64, 0.01, np.float32), np.full(64, -0.02, np.float32), np.zeros(7, np.float32)]
+    return nrp, ncol, nval, x, ws, bs
+
+
+def _run(rank, world, port_no, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
+    torch.cuda.set_device(0)
+    if world > 1:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2503_18427_b200 import device
+        from paper_2503_18427_b200.gcn import ShardedGCN
+        nrp, ncol, nval, x, ws, bs = _problem()
+        g = device.Graph.from_numpy(nrp, ncol, nval)
+        plan = device.SampledPlan(g, 16)
+        model = ShardedGCN(plan.srow_ptr, plan.scol, plan.sval, g.n_rows,
+                           [torch.from_numpy(w).cuda() for w in ws], [torch.from_numpy(b).cuda() for b in bs],
+                           exchange="p2p")
+        xt = torch.from_numpy(x).cuda()
+        outs = [model.forward(xt).cpu().numpy() for _ in range(3)]  # repeated steps exercise the barrier
+        torch.cuda.synchronize()
+        q.put((rank, outs))
+    except Exception as e:  # surface the failure to the parent
+        import traceback
+        q.put((rank, traceback.format_exc()))
+        raise
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_p2p_fused_exchange_matches_oracle(world):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = _free_port()
+    procs = [ctx.Process(target=_run, args=(r, world, p, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted([q.get(timeout=300) for _ in procs], key=lambda t: t[0])
+    for pr in procs:
+        pr.join(timeout=120)
+    for _, outs in res:
+        assert not isinstance(outs, str), outs
+    nrp, ncol, nval, x, ws, bs = _problem()
+    want = port.gcn_forward(nrp, ncol, nval, x, ws, bs, 16)
+    for _, outs in res:
+        for o in outs:
+            assert np.array_equal(np.ascontiguousarray(o).view(np.uint32), want.view(np.uint32))
