@@ -151,6 +151,15 @@ AES_API int aes_spmm_sampled(aes_csr_t a, const float* b, uint64_t b_rows, uint6
                              aes_plan_t p, float* c, uint64_t* fma_count, uint64_t* loads_a,
                              uint64_t* loads_b);
 
+/* Stream-ordered form of aes_spmm_sampled for pipelined callers: enqueues
+ * H2D(b) -> SpMM -> D2H(c) on `stream` (NULL = library stream) and returns.
+ * b and c should be pinned; they must stay valid until the stream reaches
+ * this point.  Successive calls on two streams overlap one call's H2D with
+ * the previous call's D2H (both copy engines busy).  The plan must have been
+ * built on `a`. */
+AES_API int aes_spmm_sampled_async(aes_csr_t a, const float* b, uint64_t b_rows, uint64_t f,
+                                   aes_plan_t p, float* c, void* stream);
+
 /* quantize(x, bits) = quantize(x, fit_params(x, bits)) — module.cpp:133-139,
  * quantize.cpp:11-51.  x: host rows x cols f32. */
 AES_API int aes_quantize(const float* x, uint64_t rows, uint64_t cols, uint32_t bits,

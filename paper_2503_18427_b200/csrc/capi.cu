@@ -57,7 +57,17 @@ namespace {
 cudaStream_t lib_stream() {
     static std::once_flag once;
     static cudaStream_t s = nullptr;
-    std::call_once(once, [] { cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking); });
+    std::call_once(once, [] {
+        cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+        // keep freed stream-ordered blocks cached: per-call feature/result
+        // buffers (GBs at the BASELINE shapes) are then recycled, not re-mapped
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
     return s;
 }
 
@@ -773,6 +783,29 @@ int aes_spmm_sampled(aes_csr_t a, const float* b, uint64_t b_rows, uint64_t f, a
     if (fma_count) *fma_count = p->total_slots * f;
     if (loads_a) *loads_a = p->total_slots;
     if (loads_b) *loads_b = p->total_slots * f;
+    return AES_OK;
+}
+
+int aes_spmm_sampled_async(aes_csr_t a, const float* b, uint64_t b_rows, uint64_t f, aes_plan_t p, float* c,
+                           void* stream) {
+    if (!a || !p) return fail(AES_ERR_INVALID_ARG, "null argument");
+    if (a->n_cols != b_rows) return fail(AES_ERR_SHAPE, "ShapeMismatch");
+    if (p->n_rows != a->n_rows) return fail(AES_ERR_PLAN_MISMATCH, "PlanMatrixMismatch");
+    if (a != p->src) return fail(AES_ERR_UNSUPPORTED, "async spmm needs the plan's own matrix");
+    const uint64_t n = a->n_rows;
+    if (n == 0 || f == 0) return AES_OK;
+    lib_stream();  // pool setup
+    cudaStream_t st = stream ? as_stream(stream) : lib_stream();
+    const uint64_t ld = round4(f);
+    float *db = nullptr, *dc = nullptr;
+    AES_CUDA_TRY(cudaMallocAsync((void**)&db, b_rows * ld * 4 + 16, st));
+    AES_CUDA_TRY(cudaMallocAsync((void**)&dc, n * ld * 4 + 16, st));
+    if (ld != f) AES_CUDA_TRY(cudaMemsetAsync(db, 0, b_rows * ld * 4, st));
+    AES_CUDA_TRY(cudaMemcpy2DAsync(db, ld * 4, b, f * 4, f * 4, b_rows, cudaMemcpyHostToDevice, st));
+    AES_TRY(aes_dev_spmm_f32(p->srow_ptr, p->scol, p->sval, n, db, ld, f, dc, ld, st));
+    AES_CUDA_TRY(cudaMemcpy2DAsync(c, f * 4, dc, ld * 4, f * 4, n, cudaMemcpyDeviceToHost, st));
+    AES_CUDA_TRY(cudaFreeAsync(db, st));
+    AES_CUDA_TRY(cudaFreeAsync(dc, st));
     return AES_OK;
 }
 

@@ -17,6 +17,7 @@ ap.add_argument("--width", type=int, default=32)
 ap.add_argument("--variants", default="1,2,3,4,5,6,7,8")
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--dtypes", default="f32,int8")
+ap.add_argument("--strategy", default="adaptive")
 args = ap.parse_args()
 
 n, alpha, maxdeg, f = synth.SHAPES[args.config]
@@ -40,8 +41,8 @@ def timeit(fn, iters):
 
 
 res = {"config": args.config, "width": args.width, "n": n, "nnz": int(rp[-1])}
-t_plan = timeit(lambda: device.SampledPlan(g, args.width), 5)
-plan = device.SampledPlan(g, args.width)
+t_plan = timeit(lambda: device.SampledPlan(g, args.width, args.strategy), 5)
+plan = device.SampledPlan(g, args.width, args.strategy)
 res["plan_ms"] = round(t_plan, 4)
 res["slots"] = plan.total_slots
 q = device.quantize(b)
@@ -71,4 +72,8 @@ for dt in args.dtypes.split(","):
 w = torch.rand(f, f, device="cuda")
 h = device.empty_padded(n, f)
 res["gemm_ms"] = round(timeit(lambda: device.gemm_bias_act(b, w, None, True, out=h), 5), 4)
+ptrs = (__import__("ctypes").c_void_p * 1)(h.data_ptr())
+res["gemm_finite_ms"] = round(timeit(lambda: capi.check(L.aes_dev_gemm_bias_act_ex(
+    b.data_ptr(), n, f, b.stride(0), w.data_ptr(), f, f, None, 1, 1, __import__("ctypes").cast(ptrs, __import__("ctypes").c_void_p),
+    None, 1, 0, h.stride(0), capi.stream_of())), 5), 4)
 print(json.dumps(res))

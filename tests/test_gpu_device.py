@@ -128,3 +128,37 @@ def test_products_shape_row_sample_parity(dev):
     # slot-count invariant (sum of per-row slots) and S <= sum(min(nnz, W))
     deg = np.diff(rp_np).astype(np.int64)
     assert plan.total_slots <= int(np.minimum(deg, 32).sum())
+
+
+def test_async_host_call_matches_sync():
+    """aes_spmm_sampled_async (stream-ordered H2D -> SpMM -> D2H) == the
+    synchronous handle call, on two overlapping streams."""
+    import ctypes
+
+    import torch
+
+    from paper_2503_18427_b200 import capi
+    L = capi.lib()
+    vp, u64 = ctypes.c_void_p, ctypes.c_uint64
+    L.aes_csr_create.argtypes = [u64, u64, vp, u64, vp, vp, u64, vp]
+    L.aes_build_plan_set.argtypes = [vp, ctypes.c_uint32, ctypes.c_int, vp]
+    L.aes_spmm_sampled_async.argtypes = [vp, vp, u64, u64, vp, vp, vp]
+    rp, col, val = graphs.power_law(5000, alpha=1.5, max_deg=2000, seed=8)
+    h, p = ctypes.c_void_p(), ctypes.c_void_p()
+    capi.check(L.aes_csr_create(5000, 5000, rp.ctypes.data, rp.size, col.ctypes.data, val.ctypes.data, col.size,
+                                ctypes.byref(h)))
+    capi.check(L.aes_build_plan_set(h, 32, 0, ctypes.byref(p)))
+    want = port.spmm_sampled(rp, col, val, np.ones((5000, 1), np.float32), 32)  # noqa: F841 (warm oracle)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = []
+    for i, f in enumerate([128, 602, 7, 128]):
+        b = torch.from_numpy(np.random.default_rng(i).standard_normal((5000, f)).astype(np.float32)).pin_memory()
+        c = torch.empty((5000, f), dtype=torch.float32).pin_memory()
+        capi.check(L.aes_spmm_sampled_async(h, b.data_ptr(), 5000, f, p, c.data_ptr(), streams[i % 2].cuda_stream))
+        outs.append((b, c))
+    torch.cuda.synchronize()
+    for b, c in outs:
+        want = port.spmm_sampled(rp, col, val, b.numpy(), 32)
+        assert np.array_equal(bits(c.numpy()), bits(want))
+    L.aes_plan_destroy(p)
+    L.aes_csr_destroy(h)
