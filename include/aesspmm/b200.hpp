@@ -13,8 +13,8 @@
 //    HBM by build_plan_set (the `plans` vector is still filled, eagerly).
 //  * n_threads parameters are accepted and ignored (results never depend on
 //    them, in the reference or here).
-//  * Out of scope for the B200 hot path (not declared): csr_from_triplets,
-//    row_mean_normalize, sage_forward, argmax_rows, evaluate.
+//  * Out of scope for the B200 hot path (not declared): csr_from_triplets
+//    (host-side input construction).
 #pragma once
 
 #include <cstddef>
@@ -77,6 +77,8 @@ AES_CXX_API ValidationResult validate_csr(const CsrMatrix& m);
 AES_CXX_API RowStats row_stats(const CsrMatrix& m);
 /// D^-1/2 (A [+ I]) D^-1/2 (matrix.cpp:130-144), on the GPU.
 AES_CXX_API CsrMatrix gcn_normalize(const CsrMatrix& a, bool add_self_loops);
+/// Row values 1/row_nnz (matrix.cpp:146-158), on the GPU.
+AES_CXX_API CsrMatrix row_mean_normalize(const CsrMatrix& a);
 
 // -------------------------------------------------------------- sampling.hpp
 inline constexpr std::uint64_t kHashPrime = 1429;
@@ -172,11 +174,22 @@ struct GnnModel {
     std::vector<GnnLayer> layers;
 };
 
+struct EvalResult {
+    double accuracy = 0.0;
+    double agreement = 0.0;
+    std::vector<std::uint64_t> per_class;
+};
+
 AES_CXX_API DenseMatrix gcn_forward(const CsrMatrix& adj, const DenseMatrix& features, const GnnModel& model,
                                     const SamplePlanSet* plans = nullptr, unsigned n_threads = 0);
-/// Dispatches on model.kind; SageMean is outside the B200 hot path and throws.
+AES_CXX_API DenseMatrix sage_forward(const CsrMatrix& adj_mean, const DenseMatrix& features, const GnnModel& model,
+                                     const SamplePlanSet* plans = nullptr, unsigned n_threads = 0);
 AES_CXX_API DenseMatrix gnn_forward(const CsrMatrix& adj, const DenseMatrix& features, const GnnModel& model,
                                     const SamplePlanSet* plans = nullptr, unsigned n_threads = 0);
+AES_CXX_API std::vector<std::uint32_t> argmax_rows(const DenseMatrix& logits);
+AES_CXX_API EvalResult evaluate(const DenseMatrix& logits, const std::vector<std::uint32_t>& labels,
+                                const DenseMatrix* reference_logits = nullptr,
+                                const std::vector<std::uint8_t>& mask = {});
 AES_CXX_API DenseMatrix dense_matmul(const DenseMatrix& a, const DenseMatrix& b, unsigned n_threads = 0);
 
 }  // namespace aes

@@ -194,6 +194,24 @@ AES_API int aes_gcn_forward(aes_csr_t adj, const float* x, const uint64_t* dims,
                             const float* weights, const float* biases, const uint64_t* bias_len,
                             aes_plan_t p, float* out);
 
+/* sage_forward(adj_mean, features, model, plans) — gnn.hpp:43-46,
+ * gnn.cpp:80-95: H <- act(concat(H, spmm(adj_mean, H)) @ W + b); layer l's
+ * weight is (2*dims[l]) x dims[l+1]. */
+AES_API int aes_sage_forward(aes_csr_t adj_mean, const float* x, const uint64_t* dims, int n_layers,
+                             const float* weights, const float* biases, const uint64_t* bias_len,
+                             aes_plan_t p, float* out);
+/* row_mean_normalize(a) — matrix.hpp:80-82, matrix.cpp:146-158 */
+AES_API int aes_row_mean_normalize(aes_csr_t a, aes_csr_t* out);
+/* argmax_rows(logits) — gnn.hpp:52, gnn.cpp:105-116 (ties -> lowest index) */
+AES_API int aes_argmax_rows(const float* x, uint64_t rows, uint64_t cols, uint32_t* out);
+/* evaluate(logits, labels, reference_logits, mask) — gnn.hpp:56-60,
+ * gnn.cpp:118-155.  reference_logits / mask may be NULL (mask_len 0 = all
+ * rows); per_class (cols entries) may be NULL.  Errors: "labels length !=
+ * n_nodes", "mask length != n_nodes", "LabelOutOfRange". */
+AES_API int aes_evaluate(const float* logits, uint64_t rows, uint64_t cols, const uint32_t* labels,
+                         uint64_t labels_len, const float* reference_logits, const uint8_t* mask,
+                         uint64_t mask_len, double* accuracy, double* agreement, uint64_t* per_class);
+
 /* ======================================================================
  * Tier 2: device API (device pointers, caller's stream, no sync)
  * ====================================================================== */

@@ -281,6 +281,19 @@ void or_gcn_normalize(uint64_t n, const uint64_t *row_ptr, const uint32_t *col,
             out_val[k] = inv_sqrt_deg[i] * inv_sqrt_deg[out_col[k]];
 }
 
+/* row_mean_normalize (proj/src/matrix.cpp:146-158): val = 1/row_nnz in float. */
+void or_row_mean_normalize(uint64_t n, const uint64_t *row_ptr, float *val) {
+    uint64_t i, k;
+    for (i = 0; i < n; ++i) {
+        uint64_t nnz = row_ptr[i + 1] - row_ptr[i];
+        if (nnz == 0) continue;
+        {
+            float w = 1.0f / (float)nnz;
+            for (k = row_ptr[i]; k < row_ptr[i + 1]; ++k) val[k] = w;
+        }
+    }
+}
+
 /* sampling_rate (proj/src/sampling.cpp:120-152): aggregate slot rate and
  * unique coverage of sampled offsets.  `seen` is scratch of max_row_nnz bytes. */
 int or_sampling_rate(uint64_t n, const uint64_t *row_ptr, uint32_t w, int strategy,

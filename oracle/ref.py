@@ -70,6 +70,10 @@ def shim():
         L.ref_dequantize.argtypes = [vp, u64, u64, f32, f32, u32, vp]
         L.ref_dense_matmul.argtypes = [vp, u64, u64, vp, u64, vp]
         L.ref_gcn_forward.argtypes = [vp, vp, vp, i32, vp, vp, u32, i32, vp]
+        L.ref_gnn_forward.argtypes = [i32, vp, vp, vp, i32, vp, vp, u32, i32, vp]
+        L.ref_row_mean_normalize.argtypes = [vp]
+        L.ref_row_mean_normalize.restype = vp
+        L.ref_evaluate.argtypes = [vp, u64, u64, vp, vp, vp, vp, vp, vp]
         _shim = L
     return _shim
 
@@ -189,6 +193,35 @@ def dense_matmul(a, b):
     c = np.zeros((a.shape[0], b.shape[1]), np.float32)
     _chk(shim().ref_dense_matmul(_p(a), a.shape[0], a.shape[1], _p(b), b.shape[1], _p(c)))
     return c
+
+
+def row_mean_normalize(csr: RefCsr) -> RefCsr:
+    return RefCsr(shim().ref_row_mean_normalize(csr.h))
+
+
+def sage_forward(csr: RefCsr, x, weights, biases, width, strategy=0):
+    """Reference sage_forward (gnn.cpp:80-95); width=None -> exact."""
+    x = np.ascontiguousarray(x, np.float32)
+    dims = np.array([x.shape[1]] + [w.shape[1] for w in weights], np.uint64)
+    wcat = np.concatenate([np.ascontiguousarray(w, np.float32).ravel() for w in weights])
+    bcat = np.concatenate([np.ascontiguousarray(b, np.float32).ravel() for b in biases])
+    out = np.zeros((x.shape[0], int(dims[-1])), np.float32)
+    _chk(shim().ref_gnn_forward(1, csr.h, _p(x), _p(dims), len(weights), _p(wcat), _p(bcat),
+                                0 if width is None else width, strategy, _p(out)))
+    return out
+
+
+def evaluate(logits, labels, ref_logits=None, mask=None):
+    logits = np.ascontiguousarray(logits, np.float32)
+    labels = np.ascontiguousarray(labels, np.uint32)
+    r, c = logits.shape
+    acc, agree = np.zeros(1), np.zeros(1)
+    pc = np.zeros(c, np.uint64)
+    rl = None if ref_logits is None else np.ascontiguousarray(ref_logits, np.float32)
+    mk = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+    _chk(shim().ref_evaluate(_p(logits), r, c, _p(labels), None if rl is None else _p(rl),
+                             None if mk is None else _p(mk), _p(acc), _p(agree), _p(pc)))
+    return float(acc[0]), float(agree[0]), pc
 
 
 def gcn_forward(csr: RefCsr, x, weights, biases, width, strategy=0):

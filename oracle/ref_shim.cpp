@@ -103,6 +103,31 @@ void* ref_gcn_normalize(void* h, int add_self_loops) {
     return out;
 }
 
+// reference row_mean_normalize (proj/src/matrix.cpp:146-158)
+void* ref_row_mean_normalize(void* h) {
+    void* out = nullptr;
+    guard([&] { out = new CsrMatrix(row_mean_normalize(*static_cast<CsrMatrix*>(h))); });
+    return out;
+}
+
+// reference evaluate (proj/src/gnn.cpp:118-155); ref_logits / mask may be null
+int ref_evaluate(const float* logits, std::uint64_t rows, std::uint64_t cols, const std::uint32_t* labels,
+                 const float* ref_logits, const std::uint8_t* mask, double* acc, double* agree,
+                 std::uint64_t* per_class) {
+    return guard([&] {
+        DenseMatrix l = make_dense(rows, cols, logits);
+        std::vector<std::uint32_t> lab(labels, labels + rows);
+        std::vector<std::uint8_t> m;
+        if (mask) m.assign(mask, mask + rows);
+        DenseMatrix r;
+        if (ref_logits) r = make_dense(rows, cols, ref_logits);
+        EvalResult e = evaluate(l, lab, ref_logits ? &r : nullptr, m);
+        *acc = e.accuracy;
+        *agree = e.agreement;
+        std::copy(e.per_class.begin(), e.per_class.end(), per_class);
+    });
+}
+
 // ---- sampling (proj/src/sampling.cpp) ---------------------------------------
 // Flattened plan set: per-row (chunk, cnt), starts_ptr (n+1), starts.
 int ref_build_plans(void* h, std::uint32_t width, int strategy,
@@ -223,32 +248,38 @@ int ref_dense_matmul(const float* a, std::uint64_t m, std::uint64_t k, const flo
 
 // GCN forward: dims[0..n_layers] feature widths; weights/biases concatenated
 // row-major per layer.  width==0 -> exact (plans=nullptr) path.
-int ref_gcn_forward(void* h, const float* x, const std::uint64_t* dims, int n_layers,
+int ref_gnn_forward(int kind, void* h, const float* x, const std::uint64_t* dims, int n_layers,
                     const float* weights, const float* biases, std::uint32_t width,
                     int strategy, float* out) {
     return guard([&] {
         const CsrMatrix& adj = *static_cast<CsrMatrix*>(h);
         GnnModel model;
-        model.kind = ModelKind::Gcn;
+        model.kind = kind ? ModelKind::SageMean : ModelKind::Gcn;
+        const std::uint64_t mult = kind ? 2 : 1;
         std::uint64_t woff = 0, boff = 0;
         for (int l = 0; l < n_layers; ++l) {
             GnnLayer layer;
-            layer.weight = make_dense(dims[l], dims[l + 1], weights + woff);
+            layer.weight = make_dense(mult * dims[l], dims[l + 1], weights + woff);
             layer.bias.assign(biases + boff, biases + boff + dims[l + 1]);
-            woff += dims[l] * dims[l + 1];
+            woff += mult * dims[l] * dims[l + 1];
             boff += dims[l + 1];
             model.layers.push_back(std::move(layer));
         }
         DenseMatrix feats = make_dense(adj.n_rows, dims[0], x);
         DenseMatrix res;
         if (width == 0) {
-            res = gcn_forward(adj, feats, model, nullptr);
+            res = gnn_forward(adj, feats, model, nullptr);
         } else {
             SamplePlanSet ps = build_plan_set(adj, width, static_cast<Strategy>(strategy));
-            res = gcn_forward(adj, feats, model, &ps);
+            res = gnn_forward(adj, feats, model, &ps);
         }
         std::copy(res.data.begin(), res.data.end(), out);
     });
+}
+
+int ref_gcn_forward(void* h, const float* x, const std::uint64_t* dims, int n_layers, const float* weights,
+                    const float* biases, std::uint32_t width, int strategy, float* out) {
+    return ref_gnn_forward(0, h, x, dims, n_layers, weights, biases, width, strategy, out);
 }
 
 }  // extern "C"

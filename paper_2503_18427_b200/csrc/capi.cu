@@ -44,6 +44,10 @@ int launch_validate_rows(const uint64_t*, const uint32_t*, uint64_t, uint64_t, u
                          cudaStream_t);
 int launch_gcn_normalize(const uint64_t*, const uint32_t*, uint64_t, int, const uint64_t*, float*, uint32_t*,
                          float*, cudaStream_t);
+int launch_row_mean(const uint64_t*, uint64_t, float*, cudaStream_t);
+int launch_argmax(const float*, uint64_t, uint64_t, uint64_t, uint32_t*, cudaStream_t);
+int launch_evaluate(const uint32_t*, const uint32_t*, const uint32_t*, const uint8_t*, uint64_t, uint64_t,
+                    unsigned long long*, unsigned long long*, cudaStream_t);
 int launch_explicit_fill(const uint64_t*, const uint32_t*, const uint64_t*, const uint32_t*, const uint32_t*,
                          const float*, uint64_t, const uint64_t*, uint32_t*, float*, cudaStream_t);
 int launch_explicit_rate(const uint64_t*, const uint32_t*, const uint64_t*, const uint32_t*, uint64_t, uint64_t,
@@ -1026,8 +1030,9 @@ int aes_dense_matmul(const float* a, uint64_t m, uint64_t k, const float* b, uin
     return sync();
 }
 
-int aes_gcn_forward(aes_csr_t adj, const float* x, const uint64_t* dims, int n_layers, const float* weights,
-                    const float* biases, const uint64_t* bias_len, aes_plan_t p, float* out) {
+static int gnn_forward_impl(int kind, aes_csr_t adj, const float* x, const uint64_t* dims, int n_layers,
+                            const float* weights, const float* biases, const uint64_t* bias_len, aes_plan_t p,
+                            float* out) {
     if (!adj || !dims) return fail(AES_ERR_INVALID_ARG, "null argument");
     if (adj->n_cols != adj->n_rows) return fail(AES_ERR_SHAPE, "ShapeMismatch");
     if (p && p->n_rows != adj->n_rows) return fail(AES_ERR_PLAN_MISMATCH, "PlanMatrixMismatch");
@@ -1042,18 +1047,35 @@ int aes_gcn_forward(aes_csr_t adj, const float* x, const uint64_t* dims, int n_l
         rp = p->srow_ptr;
         AES_TRY(sampled_for(p, adj, tc, tv, &scol, &sval));
     }
+    const bool sage = kind == 1;  // ModelKind::SageMean: z = concat(h, agg) (gnn.cpp:80-95)
     DBuf<float> h, agg, nxt, dw, db;
     uint64_t ldh;
     AES_TRY(upload_dense(x, n, dims[0], h, ldh));
     uint64_t woff = 0, boff = 0;
     for (int l = 0; l < n_layers; ++l) {
         const uint64_t fin = dims[l], fout = dims[l + 1];
+        const uint64_t kin = sage ? 2 * fin : fin;
         if (bias_len && bias_len[l] != 0 && bias_len[l] != fout) return fail(AES_ERR_SHAPE, "ShapeMismatch");
-        const uint64_t lda = round4(fin ? fin : 1);
+        // agg (or [h | agg] for SAGE) with ld = round4(kin)
+        const uint64_t lda = round4(kin ? kin : 1);
         AES_TRY(agg.alloc(n * lda));
-        AES_TRY(aes_dev_spmm_f32(rp, scol, sval, n, h.p, ldh, fin, agg.p, lda, st));
+        if (sage) {
+            if (lda != kin) AES_CUDA_TRY(cudaMemsetAsync(agg.p, 0, n * lda * 4, st));
+            if (fin)
+                AES_CUDA_TRY(cudaMemcpy2DAsync(agg.p, lda * 4, h.p, ldh * 4, fin * 4, n, cudaMemcpyDeviceToDevice, st));
+            // SpMM writes round4(fin) columns; aggregate into a scratch then place after h
+            DBuf<float> a2;
+            const uint64_t ld2 = round4(fin ? fin : 1);
+            AES_TRY(a2.alloc(n * ld2));
+            AES_TRY(aes_dev_spmm_f32(rp, scol, sval, n, h.p, ldh, fin, a2.p, ld2, st));
+            if (fin)
+                AES_CUDA_TRY(cudaMemcpy2DAsync(agg.p + fin, lda * 4, a2.p, ld2 * 4, fin * 4, n,
+                                               cudaMemcpyDeviceToDevice, st));
+        } else {
+            AES_TRY(aes_dev_spmm_f32(rp, scol, sval, n, h.p, ldh, fin, agg.p, lda, st));
+        }
         uint64_t ldw;
-        AES_TRY(upload_dense(weights + woff, fin, fout, dw, ldw));
+        AES_TRY(upload_dense(weights + woff, kin, fout, dw, ldw));
         const bool has_bias = bias_len ? bias_len[l] != 0 : true;
         if (has_bias) {
             AES_TRY(db.alloc(fout ? fout : 1));
@@ -1062,16 +1084,112 @@ int aes_gcn_forward(aes_csr_t adj, const float* x, const uint64_t* dims, int n_l
         const uint64_t ldo = round4(fout ? fout : 1);
         AES_TRY(nxt.alloc(n * ldo));
         if (ldo != fout) AES_CUDA_TRY(cudaMemsetAsync(nxt.p, 0, n * ldo * 4, st));
-        AES_TRY(aes_dev_gemm_bias_act(agg.p, n, fin, lda, dw.p, fout, ldw, has_bias ? db.p : nullptr,
+        AES_TRY(aes_dev_gemm_bias_act(agg.p, n, kin, lda, dw.p, fout, ldw, has_bias ? db.p : nullptr,
                                       l + 1 < n_layers, nxt.p, ldo, st));
         std::swap(h.p, nxt.p);
         std::swap(h.n, nxt.n);
         ldh = ldo;
-        woff += fin * fout;
+        woff += kin * fout;
         boff += has_bias ? fout : 0;
     }
     AES_TRY(download_dense(h.p, ldh, n, dims[n_layers], out));
     return sync();
+}
+
+int aes_gcn_forward(aes_csr_t adj, const float* x, const uint64_t* dims, int n_layers, const float* weights,
+                    const float* biases, const uint64_t* bias_len, aes_plan_t p, float* out) {
+    return gnn_forward_impl(0, adj, x, dims, n_layers, weights, biases, bias_len, p, out);
+}
+
+int aes_sage_forward(aes_csr_t adj_mean, const float* x, const uint64_t* dims, int n_layers, const float* weights,
+                     const float* biases, const uint64_t* bias_len, aes_plan_t p, float* out) {
+    return gnn_forward_impl(1, adj_mean, x, dims, n_layers, weights, biases, bias_len, p, out);
+}
+
+int aes_row_mean_normalize(aes_csr_t a, aes_csr_t* out) {
+    if (!a || !out) return fail(AES_ERR_INVALID_ARG, "null argument");
+    if (a->n_rows != a->n_cols) return fail(AES_ERR_NOT_SQUARE, "NotSquare");
+    cudaStream_t st = lib_stream();
+    DBuf<uint64_t> rp;
+    DBuf<uint32_t> ci;
+    DBuf<float> vv;
+    AES_TRY(rp.alloc(a->n_rows + 1));
+    AES_TRY(ci.alloc(a->nnz ? a->nnz : 1));
+    AES_TRY(vv.alloc(a->nnz ? a->nnz : 1));
+    AES_CUDA_TRY(cudaMemcpyAsync(rp.p, a->row_ptr, (a->n_rows + 1) * 8, cudaMemcpyDeviceToDevice, st));
+    if (a->nnz) {
+        AES_CUDA_TRY(cudaMemcpyAsync(ci.p, a->col, a->nnz * 4, cudaMemcpyDeviceToDevice, st));
+        AES_CUDA_TRY(cudaMemcpyAsync(vv.p, a->val, a->nnz * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    AES_TRY(launch_row_mean(rp.p, a->n_rows, vv.p, st));
+    AES_TRY(sync());
+    auto* o = new aes_csr_s;
+    o->n_rows = a->n_rows;
+    o->n_cols = a->n_cols;
+    o->nnz = a->nnz;
+    o->row_ptr = rp.release();
+    o->col = ci.release();
+    o->val = vv.release();
+    *out = o;
+    return AES_OK;
+}
+
+int aes_argmax_rows(const float* x, uint64_t rows, uint64_t cols, uint32_t* out) {
+    if (rows == 0) return AES_OK;
+    if (cols == 0) return fail(AES_ERR_INVALID_ARG, "argmax of an empty row");
+    DBuf<float> dx;
+    DBuf<uint32_t> dout;
+    uint64_t ld;
+    AES_TRY(upload_dense(x, rows, cols, dx, ld));
+    AES_TRY(dout.alloc(rows));
+    AES_TRY(launch_argmax(dx.p, rows, cols, ld, dout.p, lib_stream()));
+    AES_CUDA_TRY(cudaMemcpyAsync(out, dout.p, rows * 4, cudaMemcpyDeviceToHost, lib_stream()));
+    return sync();
+}
+
+int aes_evaluate(const float* logits, uint64_t rows, uint64_t cols, const uint32_t* labels, uint64_t labels_len,
+                 const float* reference_logits, const uint8_t* mask, uint64_t mask_len, double* accuracy,
+                 double* agreement, uint64_t* per_class) {
+    if (labels_len != rows) return fail(AES_ERR_INVALID_ARG, "labels length != n_nodes");
+    if (mask && mask_len != 0 && mask_len != rows) return fail(AES_ERR_INVALID_ARG, "mask length != n_nodes");
+    if (mask_len == 0) mask = nullptr;
+    cudaStream_t st = lib_stream();
+    DBuf<float> dl, dr;
+    DBuf<uint32_t> pred, ref, lab;
+    DBuf<uint8_t> dm;
+    DBuf<unsigned long long> counts, pc;
+    uint64_t ld;
+    AES_TRY(counts.alloc(4));
+    AES_TRY(pc.alloc(cols ? cols : 1));
+    AES_CUDA_TRY(cudaMemsetAsync(counts.p, 0, 32, st));
+    AES_CUDA_TRY(cudaMemsetAsync(pc.p, 0, (cols ? cols : 1) * 8, st));
+    if (rows) {
+        if (cols == 0) return fail(AES_ERR_INVALID_ARG, "LabelOutOfRange");
+        AES_TRY(upload_dense(logits, rows, cols, dl, ld));
+        AES_TRY(pred.alloc(rows));
+        AES_TRY(lab.alloc(rows));
+        AES_TRY(launch_argmax(dl.p, rows, cols, ld, pred.p, st));
+        AES_CUDA_TRY(cudaMemcpyAsync(lab.p, labels, rows * 4, cudaMemcpyHostToDevice, st));
+        if (reference_logits) {
+            AES_TRY(upload_dense(reference_logits, rows, cols, dr, ld));
+            AES_TRY(ref.alloc(rows));
+            AES_TRY(launch_argmax(dr.p, rows, cols, ld, ref.p, st));
+        }
+        if (mask) {
+            AES_TRY(dm.alloc(rows));
+            AES_CUDA_TRY(cudaMemcpyAsync(dm.p, mask, rows, cudaMemcpyHostToDevice, st));
+        }
+        AES_TRY(launch_evaluate(pred.p, lab.p, ref.p, dm.p, rows, cols, counts.p, pc.p, st));
+    }
+    unsigned long long c[4];
+    AES_CUDA_TRY(cudaMemcpyAsync(c, counts.p, sizeof(c), cudaMemcpyDeviceToHost, st));
+    if (per_class && cols)
+        AES_CUDA_TRY(cudaMemcpyAsync(per_class, pc.p, cols * 8, cudaMemcpyDeviceToHost, st));
+    AES_TRY(sync());
+    if (c[3]) return fail(AES_ERR_INVALID_ARG, "LabelOutOfRange");
+    if (accuracy) *accuracy = c[0] == 0 ? 0.0 : double(c[1]) / double(c[0]);
+    if (agreement) *agreement = !reference_logits ? 0.0 : (c[0] == 0 ? 0.0 : double(c[2]) / double(c[0]));
+    return AES_OK;
 }
 
 }  // extern "C"

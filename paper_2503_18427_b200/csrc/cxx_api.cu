@@ -318,15 +318,15 @@ DenseMatrix dense_matmul(const DenseMatrix& a, const DenseMatrix& b, unsigned) {
     return c;
 }
 
-DenseMatrix gcn_forward(const CsrMatrix& adj, const DenseMatrix& features, const GnnModel& model,
-                        const SamplePlanSet* plans, unsigned) {
-    if (model.kind != ModelKind::Gcn) throw std::invalid_argument("not a GCN model");
+namespace {
+DenseMatrix forward_impl(bool sage, const CsrMatrix& adj, const DenseMatrix& features, const GnnModel& model,
+                         const SamplePlanSet* plans) {
     if (adj.n_cols != features.n_rows) throw std::invalid_argument("ShapeMismatch");
     if (plans && plans->plans.size() != adj.n_rows) throw std::invalid_argument("PlanMatrixMismatch");
     std::vector<std::uint64_t> dims{features.n_cols}, blen;
     std::vector<float> w, bias;
     for (const GnnLayer& l : model.layers) {
-        if (l.weight.n_rows != dims.back()) throw std::invalid_argument("ShapeMismatch");
+        if (l.weight.n_rows != (sage ? 2 : 1) * dims.back()) throw std::invalid_argument("ShapeMismatch");
         if (!l.bias.empty() && l.bias.size() != l.weight.n_cols) throw std::invalid_argument("ShapeMismatch");
         dims.push_back(l.weight.n_cols);
         w.insert(w.end(), l.weight.data.begin(), l.weight.data.end());
@@ -338,15 +338,65 @@ DenseMatrix gcn_forward(const CsrMatrix& adj, const DenseMatrix& features, const
     Plan scratch;
     aes_plan_t p = plans ? plan_for(*plans, *da, scratch) : nullptr;
     DenseMatrix out(adj.n_rows, dims.back());
-    check(aes_gcn_forward(da->h, features.data.data(), dims.data(), static_cast<int>(model.layers.size()), w.data(),
-                          bias.empty() ? nullptr : bias.data(), blen.data(), p, out.data.data()));
+    auto fn = sage ? aes_sage_forward : aes_gcn_forward;
+    check(fn(da->h, features.data.data(), dims.data(), static_cast<int>(model.layers.size()), w.data(),
+             bias.empty() ? nullptr : bias.data(), blen.data(), p, out.data.data()));
     return out;
+}
+}  // namespace
+
+DenseMatrix gcn_forward(const CsrMatrix& adj, const DenseMatrix& features, const GnnModel& model,
+                        const SamplePlanSet* plans, unsigned) {
+    if (model.kind != ModelKind::Gcn) throw std::invalid_argument("not a GCN model");
+    return forward_impl(false, adj, features, model, plans);
+}
+
+DenseMatrix sage_forward(const CsrMatrix& adj_mean, const DenseMatrix& features, const GnnModel& model,
+                         const SamplePlanSet* plans, unsigned) {
+    if (model.kind != ModelKind::SageMean) throw std::invalid_argument("not a SAGE model");
+    return forward_impl(true, adj_mean, features, model, plans);
 }
 
 DenseMatrix gnn_forward(const CsrMatrix& adj, const DenseMatrix& features, const GnnModel& model,
                         const SamplePlanSet* plans, unsigned n_threads) {
-    if (model.kind == ModelKind::Gcn) return gcn_forward(adj, features, model, plans, n_threads);
-    throw std::invalid_argument("SageMean is outside the B200 AES-SpMM path");
+    return model.kind == ModelKind::Gcn ? gcn_forward(adj, features, model, plans, n_threads)
+                                        : sage_forward(adj, features, model, plans, n_threads);
+}
+
+std::vector<std::uint32_t> argmax_rows(const DenseMatrix& logits) {
+    std::vector<std::uint32_t> out(logits.n_rows);
+    check(aes_argmax_rows(logits.data.data(), logits.n_rows, logits.n_cols, out.data()));
+    return out;
+}
+
+EvalResult evaluate(const DenseMatrix& logits, const std::vector<std::uint32_t>& labels,
+                    const DenseMatrix* reference_logits, const std::vector<std::uint8_t>& mask) {
+    if (labels.size() != logits.n_rows) throw std::invalid_argument("labels length != n_nodes");
+    if (reference_logits && reference_logits->n_rows != logits.n_rows)
+        throw std::invalid_argument("reference shape mismatch");
+    EvalResult r;
+    r.per_class.assign(logits.n_cols, 0);
+    int s = aes_evaluate(logits.data.data(), logits.n_rows, logits.n_cols, labels.data(), labels.size(),
+                         reference_logits ? reference_logits->data.data() : nullptr,
+                         mask.empty() ? nullptr : mask.data(), mask.size(), &r.accuracy, &r.agreement,
+                         reinterpret_cast<std::uint64_t*>(r.per_class.data()));
+    if (s != AES_OK) {
+        if (std::string(aes_last_error()) == "LabelOutOfRange") throw std::out_of_range("LabelOutOfRange");
+        throw_status(s);
+    }
+    return r;
+}
+
+CsrMatrix row_mean_normalize(const CsrMatrix& a) {
+    if (a.n_rows != a.n_cols) throw std::invalid_argument("NotSquare");
+    auto da = upload(a);
+    Csr out;
+    check(aes_row_mean_normalize(da->h, &out.h));
+    CsrMatrix m(a.n_rows, a.n_cols);
+    m.col_ind.resize(a.nnz());
+    m.val.resize(a.nnz());
+    check(aes_csr_download(out.h, m.row_ptr.data(), m.col_ind.data(), m.val.data()));
+    return m;
 }
 
 }  // namespace aes

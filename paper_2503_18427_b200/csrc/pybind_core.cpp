@@ -429,36 +429,99 @@ PYBIND11_MODULE(_core, mod) {
             return py::make_tuple(rn, mx, avg);
         },
         py::arg("matrix"));
+    // GCN / SAGE-mean forward: weights are in_dim x out_dim (in_dim doubles for SAGE)
+    auto forward = [](bool sage, const Csr& adj, F32In x, std::vector<F32In> weights, std::vector<F32In> biases,
+                      std::optional<PlanP> plans) {
+        x = as_2d(x);
+        if (biases.size() != weights.size()) throw py::value_error("one bias per layer (may be empty)");
+        if (adj.n_cols != uint64_t(x.shape(0))) throw py::value_error("ShapeMismatch");
+        std::vector<uint64_t> dims{uint64_t(x.shape(1))}, blen;
+        std::vector<float> wcat, bcat;
+        for (size_t l = 0; l < weights.size(); ++l) {
+            F32In w = as_2d(weights[l]);
+            if (uint64_t(w.shape(0)) != (sage ? 2 : 1) * dims.back()) throw py::value_error("ShapeMismatch");
+            dims.push_back(w.shape(1));
+            wcat.insert(wcat.end(), w.data(), w.data() + w.size());
+            F32In b = biases[l];
+            if (b.size() != 0 && uint64_t(b.size()) != dims.back()) throw py::value_error("ShapeMismatch");
+            blen.push_back(b.size());
+            bcat.insert(bcat.end(), b.data(), b.data() + b.size());
+        }
+        auto out = new_2d(adj.n_rows, dims.back());
+        float* po = out.mutable_data();
+        const float* px = x.data();
+        aes_plan_t ph = plans && *plans ? (*plans)->h : nullptr;
+        check(nogil([&] {
+            auto fn = sage ? aes_sage_forward : aes_gcn_forward;
+            return fn(adj.h, px, dims.data(), int(weights.size()), wcat.data(), bcat.empty() ? nullptr : bcat.data(),
+                      blen.data(), ph, po);
+        }));
+        return out;
+    };
     mod.def(
         "gcn_forward",
-        [](const Csr& adj, F32In x, std::vector<F32In> weights, std::vector<F32In> biases,
-           std::optional<PlanP> plans, unsigned /*n_threads*/) {
-            x = as_2d(x);
-            if (biases.size() != weights.size()) throw py::value_error("one bias per layer (may be empty)");
-            if (adj.n_cols != uint64_t(x.shape(0))) throw py::value_error("ShapeMismatch");
-            std::vector<uint64_t> dims{uint64_t(x.shape(1))}, blen;
-            std::vector<float> wcat, bcat;
-            for (size_t l = 0; l < weights.size(); ++l) {
-                F32In w = as_2d(weights[l]);
-                if (uint64_t(w.shape(0)) != dims.back()) throw py::value_error("ShapeMismatch");
-                dims.push_back(w.shape(1));
-                wcat.insert(wcat.end(), w.data(), w.data() + w.size());
-                F32In b = biases[l];
-                if (b.size() != 0 && uint64_t(b.size()) != dims.back()) throw py::value_error("ShapeMismatch");
-                blen.push_back(b.size());
-                bcat.insert(bcat.end(), b.data(), b.data() + b.size());
-            }
-            auto out = new_2d(adj.n_rows, dims.back());
-            float* po = out.mutable_data();
-            const float* px = x.data();
-            aes_plan_t ph = plans && *plans ? (*plans)->h : nullptr;
-            check(nogil([&] {
-                return aes_gcn_forward(adj.h, px, dims.data(), int(weights.size()), wcat.data(),
-                                       bcat.empty() ? nullptr : bcat.data(), blen.data(), ph, po);
-            }));
-            return out;
-        },
+        [forward](const Csr& adj, F32In x, std::vector<F32In> w, std::vector<F32In> b, std::optional<PlanP> plans,
+                  unsigned) { return forward(false, adj, x, w, b, plans); },
         py::arg("adj"), py::arg("features"), py::arg("weights"), py::arg("biases"),
         py::arg("plans") = py::none(), py::arg("n_threads") = 0,
         "gcn_forward (gnn.cpp:66-78): relu(spmm(adj, H) @ W + b) per layer, no ReLU after the last");
+    mod.def(
+        "sage_forward",
+        [forward](const Csr& adj_mean, F32In x, std::vector<F32In> w, std::vector<F32In> b,
+                  std::optional<PlanP> plans, unsigned) { return forward(true, adj_mean, x, w, b, plans); },
+        py::arg("adj_mean"), py::arg("features"), py::arg("weights"), py::arg("biases"),
+        py::arg("plans") = py::none(), py::arg("n_threads") = 0,
+        "sage_forward (gnn.cpp:80-95): relu(concat(H, spmm(adj_mean, H)) @ W + b) per layer");
+    mod.def(
+        "row_mean_normalize",
+        [](const Csr& a) {
+            aes_csr_t h = nullptr;
+            check(nogil([&] { return aes_row_mean_normalize(a.h, &h); }));
+            return std::make_shared<Csr>(h);
+        },
+        py::arg("a"));
+    mod.def(
+        "argmax_rows",
+        [](F32In logits) {
+            logits = as_2d(logits);
+            uint64_t r = logits.shape(0), c = logits.shape(1);
+            py::array_t<uint32_t> out(r);
+            uint32_t* po = out.mutable_data();
+            const float* px = logits.data();
+            check(nogil([&] { return aes_argmax_rows(px, r, c, po); }));
+            return out;
+        },
+        py::arg("logits"));
+    mod.def(
+        "evaluate",
+        [](F32In logits, py::array_t<uint32_t, py::array::c_style | py::array::forcecast> labels,
+           std::optional<F32In> reference_logits, std::optional<py::array_t<uint8_t, py::array::c_style |
+                                                                             py::array::forcecast>> mask) {
+            logits = as_2d(logits);
+            uint64_t r = logits.shape(0), c = logits.shape(1);
+            const float* ref = nullptr;
+            F32In refa;
+            if (reference_logits) {
+                refa = as_2d(*reference_logits);
+                if (uint64_t(refa.shape(0)) != r) throw py::value_error("reference shape mismatch");
+                ref = refa.data();
+            }
+            const uint8_t* pm = mask ? mask->data() : nullptr;
+            uint64_t ml = mask ? mask->size() : 0;
+            double acc = 0, agree = 0;
+            std::vector<uint64_t> per_class(c);
+            const float* pl = logits.data();
+            const uint32_t* lab = labels.data();
+            uint64_t nl = labels.size();
+            check(nogil([&] {
+                return aes_evaluate(pl, r, c, lab, nl, ref, pm, ml, &acc, &agree, per_class.data());
+            }));
+            py::dict d;
+            d["accuracy"] = acc;
+            d["agreement"] = agree;
+            d["per_class"] = per_class;
+            return d;
+        },
+        py::arg("logits"), py::arg("labels"), py::arg("reference_logits") = py::none(), py::arg("mask") = py::none(),
+        "evaluate (gnn.cpp:118-155): accuracy vs labels, argmax agreement vs reference logits");
 }

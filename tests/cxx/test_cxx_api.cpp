@@ -236,6 +236,29 @@ int main() {
         CHECK(h.n_rows == 300 && h.n_cols == 8);
         model.kind = ModelKind::SageMean;
         CHECK_THROWS(gcn_forward(adj, x, model));
+        // SAGE-mean, one layer, no bias: concat(x, spmm(adj_mean, x)) @ W
+        CsrMatrix am = row_mean_normalize(g);
+        CHECK(am.nnz() == g.nnz() && validate_csr(am).ok());
+        GnnModel sage;
+        sage.kind = ModelKind::SageMean;
+        sage.layers.push_back({random_dense(24, 5, rng), {}});
+        DenseMatrix agg = spmm_exact(am, x);
+        DenseMatrix z(300, 24);
+        for (std::size_t i = 0; i < 300; ++i)
+            for (std::size_t j = 0; j < 12; ++j) z.at(i, j) = x.at(i, j), z.at(i, 12 + j) = agg.at(i, j);
+        CHECK(same_bits(gnn_forward(am, x, sage), dense_matmul(z, sage.layers[0].weight)));
+        std::vector<std::uint32_t> pred = argmax_rows(exact);
+        std::vector<std::uint32_t> labels(pred);
+        EvalResult er = evaluate(exact, labels, &exact);
+        CHECK(er.accuracy == 1.0 && er.agreement == 1.0 && er.per_class.size() == 3);
+        labels[0] = 9;
+        bool oor = false;
+        try {
+            evaluate(exact, labels);
+        } catch (const std::out_of_range&) {
+            oor = true;
+        }
+        CHECK(oor);
     }
     std::printf("%d/%d checks passed\n", g_checks - g_fail, g_checks);
     return g_fail;

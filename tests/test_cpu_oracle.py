@@ -207,6 +207,29 @@ def test_port_matches_reference_live(seed):
 
 
 @needs_ref
+def test_port_sage_eval_match_reference_live():
+    g = oref.gen_synthetic(1500, 1.5, 300, 3)
+    rp, col, _ = g.arrays()
+    val = np.ones(col.size, np.float32)
+    gm = oref.row_mean_normalize(oref.RefCsr.from_arrays(1500, 1500, rp, col, val))
+    mine = port.row_mean_normalize(rp, col, val)
+    assert all(np.array_equal(x, y) for x, y in zip(gm.arrays(), mine))
+    rng = np.random.default_rng(0)
+    x = rng.uniform(-1, 1, (1500, 12)).astype(np.float32)
+    ws = [rng.uniform(-.5, .5, (24, 16)).astype(np.float32), rng.uniform(-.5, .5, (32, 5)).astype(np.float32)]
+    bs = [np.full(16, 0.01, np.float32), np.zeros(5, np.float32)]
+    for w in (None, 8, 32):
+        assert np.array_equal(bits(port.sage_forward(*mine, x, ws, bs, w)), bits(oref.sage_forward(gm, x, ws, bs, w)))
+    logits = port.sage_forward(*mine, x, ws, bs, 8)
+    ref_logits = port.sage_forward(*mine, x, ws, bs, None)
+    labels = rng.integers(0, 5, 1500).astype(np.uint32)
+    acc, agree, pc = oref.evaluate(logits, labels, ref_logits)
+    pred = port.argmax_rows(logits)
+    assert acc == float(np.sum(pred == labels)) / 1500
+    assert agree == float(np.sum(pred == port.argmax_rows(ref_logits))) / 1500
+
+
+@needs_ref
 def test_reference_python_core_loads():
     core = oref.core()
     assert core.select_strategy(100, 32).sample_cnt == 8

@@ -302,3 +302,44 @@ def test_dense_matmul_bit_exact(m):
     assert_bit_equal(m.dense_matmul(a, b), port.dense_matmul(a, b))
     with pytest.raises(ValueError, match="ShapeMismatch"):
         m.dense_matmul(a, b[:5])
+
+
+# --------------------------------------------------------------------------- SAGE / eval (§8f rank 4)
+def test_row_mean_normalize_and_sage_forward(m):
+    rng = np.random.default_rng(12)
+    rp, col, _ = graphs.power_law(2000, alpha=1.6, max_deg=400, seed=12)
+    val = np.ones(col.size, np.float32)
+    a = make(m, rp, col, val)
+    am = m.row_mean_normalize(a)
+    mrp, mcol, mval = port.row_mean_normalize(rp, col, val)
+    got = am.to_arrays()
+    assert np.array_equal(got[0], mrp) and np.array_equal(bits(got[2]), bits(mval))
+    x = rng.uniform(-1, 1, (2000, 24)).astype(np.float32)
+    ws = [rng.uniform(-0.5, 0.5, (48, 32)).astype(np.float32), rng.uniform(-0.5, 0.5, (64, 6)).astype(np.float32)]
+    bs = [np.full(32, 0.01, np.float32), np.zeros(6, np.float32)]
+    for w in (None, 16, 32):
+        plans = None if w is None else m.build_plan_set(am, w)
+        assert_bit_equal(m.sage_forward(am, x, ws, bs, plans), port.sage_forward(mrp, mcol, mval, x, ws, bs, w))
+    with pytest.raises(ValueError, match="ShapeMismatch"):
+        m.sage_forward(am, x, [ws[1]], [bs[1]])
+
+
+def test_argmax_and_evaluate(m):
+    rng = np.random.default_rng(3)
+    logits = rng.standard_normal((5000, 7)).astype(np.float32)
+    logits[10, 2] = logits[10, 5] = 9.0  # tie -> lowest index
+    assert np.array_equal(m.argmax_rows(logits), port.argmax_rows(logits))
+    assert m.argmax_rows(logits)[10] == 2
+    labels = rng.integers(0, 7, 5000).astype(np.uint32)
+    ref = logits + rng.standard_normal(logits.shape).astype(np.float32) * 0.5
+    mask = (rng.random(5000) < 0.3).astype(np.uint8)
+    d = m.evaluate(logits, labels, ref, mask)
+    pred, refp = port.argmax_rows(logits), port.argmax_rows(ref)
+    sel = mask == 1
+    assert d["accuracy"] == float(np.sum(pred[sel] == labels[sel])) / float(sel.sum())
+    assert d["agreement"] == float(np.sum(pred[sel] == refp[sel])) / float(sel.sum())
+    assert list(d["per_class"]) == list(np.bincount(pred[sel], minlength=7))
+    with pytest.raises(ValueError, match="LabelOutOfRange"):
+        m.evaluate(logits, np.full(5000, 7, np.uint32))
+    with pytest.raises(ValueError, match="labels length"):
+        m.evaluate(logits, labels[:10])
