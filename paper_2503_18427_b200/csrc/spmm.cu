@@ -277,7 +277,8 @@ template <class R, int NV, int C, int WARPS, bool FULL>
 __global__ void __launch_bounds__(WARPS * 32)
 spmm_ring_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
                  const float* __restrict__ sval, uint64_t n_rows, const typename R::raw_t* __restrict__ gsrc,
-                 uint32_t ld, uint32_t f4, float4* __restrict__ c, uint64_t ldc4, const float* __restrict__ lut_g) {
+                 uint32_t ld, uint32_t f4, float4* __restrict__ c, uint64_t ldc4, const float* __restrict__ lut_g,
+                 uint32_t group_rows) {
     typedef typename R::raw_t raw_t;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t lane = threadIdx.x & 31;
@@ -291,9 +292,11 @@ spmm_ring_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__
     // ring entry (p, n) of this lane: ring0 + (p * NV + n) * 32 * kBytes
     const uint32_t ring0 = smem0 + R::kLutBytes + (threadIdx.x >> 5) * (C * NV * 32 * R::kBytes) + lane * R::kBytes;
 
-    const uint64_t r0 = ((uint64_t)blockIdx.x * WARPS + (threadIdx.x >> 5)) * 32;
+    // a warp owns `group_rows` (<= 32) consecutive rows; fewer rows per warp
+    // on small graphs keeps every SM busy
+    const uint64_t r0 = ((uint64_t)blockIdx.x * WARPS + (threadIdx.x >> 5)) * group_rows;
     if (r0 >= n_rows) return;
-    const uint32_t nr = (uint32_t)min((uint64_t)32, n_rows - r0);
+    const uint32_t nr = (uint32_t)min((uint64_t)group_rows, n_rows - r0);
     const uint64_t g0 = srow[r0];
     const uint64_t my_end = srow[r0 + 1 + min(lane, nr - 1)];
     // slot offsets inside a 32-row group fit in 32 bits
@@ -491,10 +494,14 @@ int launch_ring_t(const uint64_t* srow, const uint32_t* scol, const float* sval,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set = true;
     }
-    const uint64_t groups = (n + 31) / 32;
+    // rows per warp: 32 when the graph fills >= 8 warps per SM slot at that
+    // size, otherwise shrink (power of 2, >= 2) so the grid still covers the GPU
+    uint32_t gr = 32;
+    while (gr > 2 && (n + gr - 1) / gr < (uint64_t)kNumSMs * 64) gr >>= 1;
+    const uint64_t groups = (n + gr - 1) / gr;
     const unsigned grid = (unsigned)((groups + W - 1) / W);
     spmm_ring_kernel<R, NV, C, W, FULL><<<grid, W * 32, smem, st>>>(srow, scol, sval, n, g.base(), (uint32_t)g.ld4,
-                                                                    f4, c, ldc4, lut);
+                                                                    f4, c, ldc4, lut, gr);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
 }
