@@ -1084,8 +1084,15 @@ static int gnn_forward_impl(int kind, aes_csr_t adj, const float* x, const uint6
         const uint64_t ldo = round4(fout ? fout : 1);
         AES_TRY(nxt.alloc(n * ldo));
         if (ldo != fout) AES_CUDA_TRY(cudaMemsetAsync(nxt.p, 0, n * ldo * 4, st));
-        AES_TRY(aes_dev_gemm_bias_act(agg.p, n, kin, lda, dw.p, fout, ldw, has_bias ? db.p : nullptr,
-                                      l + 1 < n_layers, nxt.p, ldo, st));
+        // finite W makes the reference's zero-skip result-neutral (gemm.cu)
+        DBuf<unsigned int> bad;
+        AES_TRY(bad.alloc(1));
+        AES_TRY(aes_dev_all_finite(dw.p, kin * ldw, bad.p, st));
+        unsigned int w_bad = 0;
+        AES_TRY(d2h_scalar(bad.p, &w_bad));
+        float* dsts[1] = {nxt.p};
+        AES_TRY(aes_dev_gemm_bias_act_ex(agg.p, n, kin, lda, dw.p, fout, ldw, has_bias ? db.p : nullptr,
+                                         l + 1 < n_layers, w_bad == 0, dsts, nullptr, 1, 0, ldo, st));
         std::swap(h.p, nxt.p);
         std::swap(h.n, nxt.n);
         ldh = ldo;

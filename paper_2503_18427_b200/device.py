@@ -193,21 +193,36 @@ def spmm_q8(srow_ptr, scol, sval, q: QuantizedDevice, out=None, stream=None) -> 
     return out
 
 
+def weights_finite(w: torch.Tensor, stream=None) -> bool:
+    """True when w has no inf/NaN (device reduction, one sync)."""
+    flag = torch.zeros(1, dtype=torch.int32, device=w.device)
+    check(lib().aes_dev_all_finite(ptr(w), w.numel(), ptr(flag), stream_of(stream)))
+    return int(flag.item()) == 0
+
+
 def gemm_bias_act(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None, relu: bool, out=None,
-                  stream=None) -> torch.Tensor:
-    """act(a @ w + bias) with the reference's ordered fp32 arithmetic (gnn.cpp:11-52)."""
+                  stream=None, finite_w: bool | None = False) -> torch.Tensor:
+    """act(a @ w + bias) with the reference's ordered fp32 arithmetic
+    (gnn.cpp:11-52).  finite_w=True (or None: check on the device) lets the
+    kernel drop the reference's zero-skip, which is result-neutral then."""
+    import ctypes
+
     m, k = a.shape
     k2, n = w.shape
     if k != k2:
         raise ValueError("ShapeMismatch")
     w = w.contiguous()
+    if finite_w is None:
+        finite_w = weights_finite(w, stream)
     if out is None:
         out = empty_padded(m, n, device=a.device)
         if out.stride(0) != n:
             out.as_strided((m, out.stride(0)), (out.stride(0), 1))[:, n:].zero_()
-    check(lib().aes_dev_gemm_bias_act(ptr(a), m, k, a.stride(0), ptr(w), n, w.stride(0),
-                                      ptr(bias) if bias is not None and bias.numel() else None, int(relu),
-                                      ptr(out), out.stride(0), stream_of(stream)))
+    dsts = (ctypes.c_void_p * 1)(ptr(out))
+    check(lib().aes_dev_gemm_bias_act_ex(ptr(a), m, k, a.stride(0), ptr(w), n, w.stride(0),
+                                         ptr(bias) if bias is not None and bias.numel() else None, int(relu),
+                                         int(bool(finite_w)), ctypes.cast(dsts, ctypes.c_void_p), None, 1, 0,
+                                         out.stride(0), stream_of(stream)))
     return out
 
 
@@ -219,5 +234,5 @@ def gcn_forward(graph: Graph, x: torch.Tensor, weights, biases, plan: SampledPla
         graph.row_ptr, graph.col, graph.val)
     for l, (w, b) in enumerate(zip(weights, biases)):
         agg = spmm(srow, scol, sval, h, stream=stream)
-        h = gemm_bias_act(agg, w, b, relu=l + 1 < len(weights), stream=stream)
+        h = gemm_bias_act(agg, w, b, relu=l + 1 < len(weights), stream=stream, finite_w=None)
     return h
