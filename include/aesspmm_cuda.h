@@ -298,6 +298,15 @@ AES_API int aes_dev_gemm_bias_act_ex(const float* a, uint64_t m, uint64_t k, uin
                                      int relu, int finite_w, float* const* dsts,
                                      unsigned long long* const* counters, int n_dst,
                                      uint64_t row_offset, uint64_t ldh, void* stream);
+/* FAST MODE (opt-in, not bit-exact): the same layer GEMM on the tcgen05
+ * tensor cores (kind::tf32, TMA-fed, TMEM accumulators).  Error bound
+ * |H - H_exact| <= 2^-8 * sum_k |a_ik||w_kj| per element (TF32 operands, fp32
+ * accumulation).  1 <= K <= 128, N <= 128, lda % 4 == 0, A 16-B aligned;
+ * wt_scratch: device buffer of aes_gemm_tf32_scratch_floats(K, N) floats. */
+AES_API int aes_dev_gemm_tf32(const float* a, uint64_t m, uint64_t k, uint64_t lda, const float* w,
+                              uint64_t n, uint64_t ldw, const float* bias, int relu, float* h,
+                              uint64_t ldh, float* wt_scratch, void* stream);
+AES_API uint64_t aes_gemm_tf32_scratch_floats(uint64_t k, uint64_t n);
 /* Number of CTAs (= arrivals per destination) the GEMM above launches. */
 AES_API uint64_t aes_gemm_ctas(uint64_t m, uint64_t n);
 /* Spin (one thread, ld.acquire.sys) until *counter >= target. */

@@ -226,13 +226,35 @@ def gemm_bias_act(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None, r
     return out
 
 
+def gemm_tf32(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None, relu: bool, out=None,
+              stream=None) -> torch.Tensor:
+    """FAST MODE act(a @ w + bias) on the tcgen05 tensor cores (TF32
+    operands, fp32 accumulation; NOT bit-exact: |err| <= 2^-8 sum|a||w|)."""
+    m, k = a.shape
+    k2, n = w.shape
+    if k != k2:
+        raise ValueError("ShapeMismatch")
+    if out is None:
+        out = empty_padded(m, n, device=a.device)
+    scratch = torch.empty(int(lib().aes_gemm_tf32_scratch_floats(k, n)), dtype=torch.float32, device=a.device)
+    check(lib().aes_dev_gemm_tf32(ptr(a), m, k, a.stride(0), ptr(w), n, w.stride(0),
+                                  ptr(bias) if bias is not None and bias.numel() else None, int(relu), ptr(out),
+                                  out.stride(0), ptr(scratch), stream_of(stream)))
+    return out
+
+
 def gcn_forward(graph: Graph, x: torch.Tensor, weights, biases, plan: SampledPlan | None = None,
-                stream=None) -> torch.Tensor:
-    """gcn_forward (proj/src/gnn.cpp:66-78) on one GPU, all tensors in HBM."""
+                stream=None, fast_gemm: bool = False) -> torch.Tensor:
+    """gcn_forward (proj/src/gnn.cpp:66-78) on one GPU, all tensors in HBM.
+    fast_gemm=True runs the layer transform on the tcgen05 tensor cores (TF32,
+    not bit-exact); the aggregation stays the exact sampled SpMM."""
     h = padded(x)
     srow, scol, sval = (plan.srow_ptr, plan.scol, plan.sval) if plan is not None else (
         graph.row_ptr, graph.col, graph.val)
     for l, (w, b) in enumerate(zip(weights, biases)):
         agg = spmm(srow, scol, sval, h, stream=stream)
-        h = gemm_bias_act(agg, w, b, relu=l + 1 < len(weights), stream=stream, finite_w=None)
+        if fast_gemm and agg.shape[1] <= 128 and w.shape[1] <= 128:
+            h = gemm_tf32(agg, w, b, relu=l + 1 < len(weights), stream=stream)
+        else:
+            h = gemm_bias_act(agg, w, b, relu=l + 1 < len(weights), stream=stream, finite_w=None)
     return h
