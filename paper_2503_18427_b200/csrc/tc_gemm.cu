@@ -30,7 +30,7 @@ namespace {
 constexpr int kTileM = 128;
 constexpr int kSlabK = 32;                     // fp32 elements per 128-B swizzle row
 constexpr int kSlabBytes = kTileM * kSlabK * 4;  // 16 KB
-constexpr int kStages = 6;
+constexpr int kStages = 4;
 constexpr int kMaxK = 128, kMaxN = 128;
 constexpr int kThreads = 6 * 32;
 
@@ -104,22 +104,36 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                  : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                 : "r"(taddr));
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+                 "r"(smem_u32(src)), "r"(x), "r"(y)
+                 : "memory");
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_w, uint64_t m,
-               uint32_t k_slabs, uint32_t n, uint32_t n_pad, uint32_t tmem_cols, const float* __restrict__ bias,
-               int relu, float* __restrict__ h, uint64_t ldh) {
+tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_w,
+               const __grid_constant__ CUtensorMap map_h, uint64_t m, uint32_t k_slabs, uint32_t n, uint32_t n_pad,
+               uint32_t tmem_cols, const float* __restrict__ bias, int relu) {
     extern __shared__ __align__(1024) unsigned char smem[];
-    // layout: [A ring: kStages x 16 KB][W^T: k_slabs x (n_pad x 128 B)][barriers]
+    // layout: [A ring: kStages x 16 KB][W^T: k_slabs x (n_pad x 128 B)]
+    //         [output staging: n_slabs x (128 rows x 128 B), 128-B swizzled][barriers]
     unsigned char* a_ring = smem;
     unsigned char* w_smem = smem + kStages * kSlabBytes;
     const uint32_t w_slab_bytes = n_pad * 128;
-    Barriers* bars = reinterpret_cast<Barriers*>(w_smem + k_slabs * w_slab_bytes);
+    const uint32_t n_slabs = (n + 31) / 32;
+    unsigned char* out_smem = w_smem + k_slabs * w_slab_bytes;
+    Barriers* bars = reinterpret_cast<Barriers*>(out_smem + n_slabs * kSlabBytes);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t tiles = (m + kTileM - 1) / kTileM;
@@ -193,36 +207,54 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             if (acc == 0) acc_phase ^= 1;
         }
     } else {
-        // epilogue warps 2..5 -> TMEM lane quadrant (warp % 4)
+        // epilogue warps 2..5 -> TMEM lane quadrant (warp % 4) = tile rows
+        // 32*quad .. +31.  TMEM -> registers -> bias/ReLU -> 128-B-swizzled
+        // staging (conflict-free 16-B stores) -> TMA tensor store.
         const uint32_t quad = warp & 3;
+        const bool issuer = (warp == 2 && lane == 0);
+        const uint32_t r_local = quad * 32 + lane;
         uint32_t acc = 0, acc_phase = 0;
         for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
             mbar_wait(&bars->tmem_full[acc], acc_phase);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint64_t row = t * kTileM + quad * 32 + lane;
-            float* hrow = h + row * ldh;
-            for (uint32_t c0 = 0; c0 < n; c0 += 8) {
-                uint32_t r[8];
-                tmem_ld8(tmem_base + ((quad * 32) << 16) + acc * n_pad + c0, r);
+            // the previous tile's TMA store must have finished reading staging
+            if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            for (uint32_t s = 0; s < n_slabs; ++s) {
+                uint32_t r[32];
+                tmem_ld32(tmem_base + ((quad * 32) << 16) + acc * n_pad + s * 32, r);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (row < m) {
+                unsigned char* slab = out_smem + s * kSlabBytes + r_local * 128;
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        if (c0 + j < n) {
-                            float v = __uint_as_float(r[j]);
-                            if (bias) v = __fadd_rn(v, bias[c0 + j]);
-                            if (relu) v = (v < 0.f) ? 0.f : v;
-                            hrow[c0 + j] = v;
-                        }
+                for (int c = 0; c < 8; ++c) {  // 16-B chunk c of this row, swizzled by row % 8
+                    float v[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint32_t col = s * 32 + c * 4 + j;
+                        float x = __uint_as_float(r[c * 4 + j]);
+                        if (bias && col < n) x = __fadd_rn(x, bias[col]);
+                        if (relu) x = (x < 0.f) ? 0.f : x;
+                        v[j] = x;
                     }
+                    *reinterpret_cast<float4*>(slab + ((c ^ (r_local & 7)) * 16)) = make_float4(v[0], v[1], v[2], v[3]);
                 }
             }
+            // TMEM accumulator can be reused as soon as it is in registers/smem
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars->tmem_empty[acc]);
+            // make the generic-proxy smem writes visible to the TMA (async proxy)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (issuer) {
+                for (uint32_t s = 0; s < n_slabs; ++s)
+                    tma_store_2d(&map_h, out_smem + s * kSlabBytes, (int)(s * 32), (int)(t * kTileM));
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
+        if (issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     __syncthreads();
     if (warp == 1) {
@@ -286,20 +318,25 @@ extern "C" int aes_dev_gemm_tf32(const float* a, uint64_t m, uint64_t k, uint64_
     while (tmem_cols < 2 * n_pad) tmem_cols <<= 1;
     if (!wt_scratch) return fail(AES_ERR_INVALID_ARG, "W^T scratch (n_pad * k_pad floats) required");
     transpose_pad_kernel<<<64, 256, 0, st>>>(w, (uint32_t)k, (uint32_t)n, ldw, wt_scratch, n_pad, k_pad);
-    CUtensorMap map_a, map_w;
+    if (ldh % 4 || (uintptr_t)h % 16) return fail(AES_ERR_UNSUPPORTED, "H rows must be 16-B aligned");
+    CUtensorMap map_a, map_w, map_h;
     AES_TRY(make_map(&map_a, a, k, m, lda, kSlabK, kTileM));
     AES_TRY(make_map(&map_w, wt_scratch, k_pad, n_pad, k_pad, kSlabK, n_pad));
-    const size_t smem = (size_t)kStages * kSlabBytes + (size_t)k_slabs * n_pad * 128 + sizeof(Barriers) + 1024;
+    AES_TRY(make_map(&map_h, h, n, m, ldh, kSlabK, kTileM));
+    const uint32_t n_slabs = (uint32_t)((n + 31) / 32);
+    const size_t smem = (size_t)kStages * kSlabBytes + (size_t)k_slabs * n_pad * 128 + (size_t)n_slabs * kSlabBytes +
+                        sizeof(Barriers) + 1024;
     static bool attr = false;
     if (!attr) {
-        AES_CUDA_TRY(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)(kStages * kSlabBytes + 4 * kMaxN * 128 + sizeof(Barriers) + 1024)));
+        AES_CUDA_TRY(cudaFuncSetAttribute(
+            tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            (int)(kStages * kSlabBytes + 4 * kMaxN * 128 + 4 * kSlabBytes + sizeof(Barriers) + 1024)));
         attr = true;
     }
     const uint64_t tiles = (m + kTileM - 1) / kTileM;
     const unsigned grid = (unsigned)(tiles < (uint64_t)kNumSMs ? tiles : (uint64_t)kNumSMs);
-    tc_gemm_kernel<<<grid, kThreads, smem, st>>>(map_a, map_w, m, k_slabs, (uint32_t)n, n_pad, tmem_cols, bias, relu,
-                                                 h, ldh);
+    tc_gemm_kernel<<<grid, kThreads, smem, st>>>(map_a, map_w, map_h, m, k_slabs, (uint32_t)n, n_pad, tmem_cols, bias,
+                                                 relu);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
 }
