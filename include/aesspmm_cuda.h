@@ -200,6 +200,13 @@ AES_API int aes_gcn_forward(aes_csr_t adj, const float* x, const uint64_t* dims,
 AES_API int aes_sage_forward(aes_csr_t adj_mean, const float* x, const uint64_t* dims, int n_layers,
                              const float* weights, const float* biases, const uint64_t* bias_len,
                              aes_plan_t p, float* out);
+/* GCN (kind 0) / SAGE-mean (kind 1) forward with an opt-in fast layer
+ * transform: fast_gemm != 0 runs each GEMM with K, N <= 128 on the tcgen05
+ * tensor cores (TF32; NOT bit-exact, see aes_dev_gemm_tf32).  fast_gemm == 0
+ * is aes_gcn_forward / aes_sage_forward. */
+AES_API int aes_gnn_forward_ex(int kind, aes_csr_t adj, const float* x, const uint64_t* dims,
+                               int n_layers, const float* weights, const float* biases,
+                               const uint64_t* bias_len, aes_plan_t p, int fast_gemm, float* out);
 /* row_mean_normalize(a) — matrix.hpp:80-82, matrix.cpp:146-158 */
 AES_API int aes_row_mean_normalize(aes_csr_t a, aes_csr_t* out);
 /* argmax_rows(logits) — gnn.hpp:52, gnn.cpp:105-116 (ties -> lowest index) */

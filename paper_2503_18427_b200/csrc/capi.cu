@@ -1032,7 +1032,7 @@ int aes_dense_matmul(const float* a, uint64_t m, uint64_t k, const float* b, uin
 
 static int gnn_forward_impl(int kind, aes_csr_t adj, const float* x, const uint64_t* dims, int n_layers,
                             const float* weights, const float* biases, const uint64_t* bias_len, aes_plan_t p,
-                            float* out) {
+                            float* out, int fast_gemm = 0) {
     if (!adj || !dims) return fail(AES_ERR_INVALID_ARG, "null argument");
     if (adj->n_cols != adj->n_rows) return fail(AES_ERR_SHAPE, "ShapeMismatch");
     if (p && p->n_rows != adj->n_rows) return fail(AES_ERR_PLAN_MISMATCH, "PlanMatrixMismatch");
@@ -1084,15 +1084,23 @@ static int gnn_forward_impl(int kind, aes_csr_t adj, const float* x, const uint6
         const uint64_t ldo = round4(fout ? fout : 1);
         AES_TRY(nxt.alloc(n * ldo));
         if (ldo != fout) AES_CUDA_TRY(cudaMemsetAsync(nxt.p, 0, n * ldo * 4, st));
-        // finite W makes the reference's zero-skip result-neutral (gemm.cu)
-        DBuf<unsigned int> bad;
-        AES_TRY(bad.alloc(1));
-        AES_TRY(aes_dev_all_finite(dw.p, kin * ldw, bad.p, st));
-        unsigned int w_bad = 0;
-        AES_TRY(d2h_scalar(bad.p, &w_bad));
-        float* dsts[1] = {nxt.p};
-        AES_TRY(aes_dev_gemm_bias_act_ex(agg.p, n, kin, lda, dw.p, fout, ldw, has_bias ? db.p : nullptr,
-                                         l + 1 < n_layers, w_bad == 0, dsts, nullptr, 1, 0, ldo, st));
+        if (fast_gemm && kin <= 128 && fout <= 128 && kin > 0) {
+            // opt-in tcgen05 TF32 layer transform (not bit-exact; tc_gemm.cu)
+            DBuf<float> wt;
+            AES_TRY(wt.alloc(aes_gemm_tf32_scratch_floats(kin, fout)));
+            AES_TRY(aes_dev_gemm_tf32(agg.p, n, kin, lda, dw.p, fout, ldw, has_bias ? db.p : nullptr,
+                                      l + 1 < n_layers, nxt.p, ldo, wt.p, st));
+        } else {
+            // finite W makes the reference's zero-skip result-neutral (gemm.cu)
+            DBuf<unsigned int> bad;
+            AES_TRY(bad.alloc(1));
+            AES_TRY(aes_dev_all_finite(dw.p, kin * ldw, bad.p, st));
+            unsigned int w_bad = 0;
+            AES_TRY(d2h_scalar(bad.p, &w_bad));
+            float* dsts[1] = {nxt.p};
+            AES_TRY(aes_dev_gemm_bias_act_ex(agg.p, n, kin, lda, dw.p, fout, ldw, has_bias ? db.p : nullptr,
+                                             l + 1 < n_layers, w_bad == 0, dsts, nullptr, 1, 0, ldo, st));
+        }
         std::swap(h.p, nxt.p);
         std::swap(h.n, nxt.n);
         ldh = ldo;
@@ -1111,6 +1119,12 @@ int aes_gcn_forward(aes_csr_t adj, const float* x, const uint64_t* dims, int n_l
 int aes_sage_forward(aes_csr_t adj_mean, const float* x, const uint64_t* dims, int n_layers, const float* weights,
                      const float* biases, const uint64_t* bias_len, aes_plan_t p, float* out) {
     return gnn_forward_impl(1, adj_mean, x, dims, n_layers, weights, biases, bias_len, p, out);
+}
+
+int aes_gnn_forward_ex(int kind, aes_csr_t adj, const float* x, const uint64_t* dims, int n_layers,
+                       const float* weights, const float* biases, const uint64_t* bias_len, aes_plan_t p, int fast_gemm,
+                       float* out) {
+    return gnn_forward_impl(kind, adj, x, dims, n_layers, weights, biases, bias_len, p, out, fast_gemm);
 }
 
 int aes_row_mean_normalize(aes_csr_t a, aes_csr_t* out) {

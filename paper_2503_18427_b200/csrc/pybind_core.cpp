@@ -431,7 +431,7 @@ PYBIND11_MODULE(_core, mod) {
         py::arg("matrix"));
     // GCN / SAGE-mean forward: weights are in_dim x out_dim (in_dim doubles for SAGE)
     auto forward = [](bool sage, const Csr& adj, F32In x, std::vector<F32In> weights, std::vector<F32In> biases,
-                      std::optional<PlanP> plans) {
+                      std::optional<PlanP> plans, bool fast_gemm) {
         x = as_2d(x);
         if (biases.size() != weights.size()) throw py::value_error("one bias per layer (may be empty)");
         if (adj.n_cols != uint64_t(x.shape(0))) throw py::value_error("ShapeMismatch");
@@ -452,25 +452,27 @@ PYBIND11_MODULE(_core, mod) {
         const float* px = x.data();
         aes_plan_t ph = plans && *plans ? (*plans)->h : nullptr;
         check(nogil([&] {
-            auto fn = sage ? aes_sage_forward : aes_gcn_forward;
-            return fn(adj.h, px, dims.data(), int(weights.size()), wcat.data(), bcat.empty() ? nullptr : bcat.data(),
-                      blen.data(), ph, po);
+            return aes_gnn_forward_ex(sage ? 1 : 0, adj.h, px, dims.data(), int(weights.size()), wcat.data(),
+                                      bcat.empty() ? nullptr : bcat.data(), blen.data(), ph, fast_gemm ? 1 : 0, po);
         }));
         return out;
     };
     mod.def(
         "gcn_forward",
         [forward](const Csr& adj, F32In x, std::vector<F32In> w, std::vector<F32In> b, std::optional<PlanP> plans,
-                  unsigned) { return forward(false, adj, x, w, b, plans); },
+                  unsigned, bool fast_gemm) { return forward(false, adj, x, w, b, plans, fast_gemm); },
         py::arg("adj"), py::arg("features"), py::arg("weights"), py::arg("biases"),
-        py::arg("plans") = py::none(), py::arg("n_threads") = 0,
-        "gcn_forward (gnn.cpp:66-78): relu(spmm(adj, H) @ W + b) per layer, no ReLU after the last");
+        py::arg("plans") = py::none(), py::arg("n_threads") = 0, py::arg("fast_gemm") = false,
+        "gcn_forward (gnn.cpp:66-78): relu(spmm(adj, H) @ W + b) per layer, no ReLU after the last. "
+        "fast_gemm=True: layer transforms on the tcgen05 tensor cores (TF32, not bit-exact)");
     mod.def(
         "sage_forward",
         [forward](const Csr& adj_mean, F32In x, std::vector<F32In> w, std::vector<F32In> b,
-                  std::optional<PlanP> plans, unsigned) { return forward(true, adj_mean, x, w, b, plans); },
+                  std::optional<PlanP> plans, unsigned, bool fast_gemm) {
+            return forward(true, adj_mean, x, w, b, plans, fast_gemm);
+        },
         py::arg("adj_mean"), py::arg("features"), py::arg("weights"), py::arg("biases"),
-        py::arg("plans") = py::none(), py::arg("n_threads") = 0,
+        py::arg("plans") = py::none(), py::arg("n_threads") = 0, py::arg("fast_gemm") = false,
         "sage_forward (gnn.cpp:80-95): relu(concat(H, spmm(adj_mean, H)) @ W + b) per layer");
     mod.def(
         "row_mean_normalize",

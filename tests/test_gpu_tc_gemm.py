@@ -29,6 +29,31 @@ def test_tf32_gemm_within_bound(m, k, n):
         assert bool((err <= bound + 2.0 ** -20).all()), float((err - bound).max())
 
 
+def test_core_fast_gemm_option():
+    """_core.gcn_forward / sage_forward(fast_gemm=True): close to the exact
+    (bit-exact-with-reference) result, same argmax on almost every row."""
+    import paper_2503_18427_b200 as m
+    from oracle import port
+    from tests import graphs
+    rng = np.random.default_rng(9)
+    rp, col, _ = graphs.power_law(2500, alpha=1.8, max_deg=300, seed=9)
+    nrp, ncol, nval = port.gcn_normalize(rp, col, True)
+    adj = m.CsrMatrix(2500, 2500, nrp, ncol, nval)
+    x = rng.uniform(-1, 1, (2500, 64)).astype(np.float32)
+    ws = [rng.uniform(-0.5, 0.5, (64, 64)).astype(np.float32), rng.uniform(-0.5, 0.5, (64, 16)).astype(np.float32)]
+    bs = [np.full(64, 0.01, np.float32), np.zeros(16, np.float32)]
+    plans = m.build_plan_set(adj, 32)
+    exact = m.gcn_forward(adj, x, ws, bs, plans)
+    fast = m.gcn_forward(adj, x, ws, bs, plans, fast_gemm=True)
+    assert np.abs(fast - exact).max() / np.abs(exact).max() < 2e-2
+    assert (fast.argmax(1) == exact.argmax(1)).mean() > 0.98
+    am = m.row_mean_normalize(m.CsrMatrix(2500, 2500, rp, col, np.ones(col.size, np.float32)))
+    ws2 = [rng.uniform(-0.5, 0.5, (128, 32)).astype(np.float32)]
+    e2 = m.sage_forward(am, x, ws2, [np.zeros(32, np.float32)])
+    f2 = m.sage_forward(am, x, ws2, [np.zeros(32, np.float32)], fast_gemm=True)
+    assert np.abs(f2 - e2).max() / np.abs(e2).max() < 2e-2
+
+
 def test_fast_gcn_forward_close_to_exact():
     import torch
 
