@@ -314,6 +314,17 @@ AES_API int aes_dev_gemm_tf32(const float* a, uint64_t m, uint64_t k, uint64_t l
                               uint64_t n, uint64_t ldw, const float* bias, int relu, float* h,
                               uint64_t ldh, float* wt_scratch, void* stream);
 AES_API uint64_t aes_gemm_tf32_scratch_floats(uint64_t k, uint64_t n);
+/* Fast-mode GEMM fused with the layer exchange: the TMA-store epilogue writes
+ * every 128-row tile to rows [row_offset, ...) of each replica dsts[0..n_dst)
+ * (own + CUDA-IPC peer pointers, <= 8), then each CTA adds the number of
+ * tiles it stored to every counters[d] (system-scope release).  A rank waits
+ * for aes_gemm_tf32_ctas(m_p) summed over all producers p. */
+AES_API int aes_dev_gemm_tf32_bcast(const float* a, uint64_t m, uint64_t k, uint64_t lda,
+                                    const float* w, uint64_t n, uint64_t ldw, const float* bias,
+                                    int relu, float* const* dsts, unsigned long long* const* counters,
+                                    int n_dst, uint64_t row_offset, uint64_t ldh, float* wt_scratch,
+                                    void* stream);
+AES_API uint64_t aes_gemm_tf32_ctas(uint64_t m);
 /* Number of CTAs (= arrivals per destination) the GEMM above launches. */
 AES_API uint64_t aes_gemm_ctas(uint64_t m, uint64_t n);
 /* Spin (one thread, ld.acquire.sys) until *counter >= target. */

@@ -54,6 +54,10 @@ def lib():
         L.aes_dev_gemm_tf32.argtypes = [vp, u64, u64, u64, vp, u64, u64, vp, i32, vp, u64, vp, vp]
         L.aes_gemm_tf32_scratch_floats.argtypes = [u64, u64]
         L.aes_gemm_tf32_scratch_floats.restype = u64
+        L.aes_dev_gemm_tf32_bcast.argtypes = [vp, u64, u64, u64, vp, u64, u64, vp, i32, vp, vp, i32, u64, u64, vp,
+                                              vp]
+        L.aes_gemm_tf32_ctas.argtypes = [u64]
+        L.aes_gemm_tf32_ctas.restype = u64
         L.aes_gemm_ctas.argtypes = [u64, u64]
         L.aes_gemm_ctas.restype = u64
         L.aes_dev_wait_counter.argtypes = [vp, u64, vp]

@@ -34,6 +34,15 @@ constexpr int kStages = 4;
 constexpr int kMaxK = 128, kMaxN = 128;
 constexpr int kThreads = 6 * 32;
 
+// Output tensor maps: one per destination replica (own + peers for the fused
+// exchange) and, when fused, each destination's arrival counter.
+constexpr int kMaxOut = 8;
+struct OutMaps {
+    CUtensorMap map[kMaxOut];
+    unsigned long long* ctr[kMaxOut];
+    int n;
+};
+
 struct __align__(8) Barriers {
     uint64_t full[kStages];
     uint64_t empty[kStages];
@@ -123,7 +132,7 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
 
 __global__ void __launch_bounds__(kThreads, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_w,
-               const __grid_constant__ CUtensorMap map_h, uint64_t m, uint32_t k_slabs, uint32_t n, uint32_t n_pad,
+               const __grid_constant__ OutMaps outs, uint64_t m, uint32_t k_slabs, uint32_t n, uint32_t n_pad,
                uint32_t tmem_cols, const float* __restrict__ bias, int relu) {
     extern __shared__ __align__(1024) unsigned char smem[];
     // layout: [A ring: kStages x 16 KB][W^T: k_slabs x (n_pad x 128 B)]
@@ -248,13 +257,26 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             asm volatile("bar.sync 1, 128;" ::: "memory");
             if (issuer) {
                 for (uint32_t s = 0; s < n_slabs; ++s)
-                    tma_store_2d(&map_h, out_smem + s * kSlabBytes, (int)(s * 32), (int)(t * kTileM));
+                    for (int d = 0; d < outs.n; ++d)  // own replica and every peer's, over NVLink
+                        tma_store_2d(&outs.map[d], out_smem + s * kSlabBytes, (int)(s * 32), (int)(t * kTileM));
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
-        if (issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        if (issuer) {
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // all tile writes complete
+            if (outs.ctr[0]) {
+                // publish this CTA's tiles to every destination (fused exchange):
+                // async-proxy writes -> generic proxy -> system-scope release
+                uint64_t mine = 0;
+                for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) ++mine;
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                __threadfence_system();
+                for (int d = 0; d < outs.n; ++d)
+                    asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(outs.ctr[d]), "l"(mine) : "memory");
+            }
+        }
     }
     __syncthreads();
     if (warp == 1) {
@@ -299,17 +321,13 @@ int make_map(CUtensorMap* map, const float* base, uint64_t inner, uint64_t outer
     return AES_OK;
 }
 
-}  // namespace
-}  // namespace aes
-
-extern "C" int aes_dev_gemm_tf32(const float* a, uint64_t m, uint64_t k, uint64_t lda, const float* w, uint64_t n,
-                                 uint64_t ldw, const float* bias, int relu, float* h, uint64_t ldh, float* wt_scratch,
-                                 void* stream) {
-    using namespace aes;
-    cudaStream_t st = as_stream(stream);
+int launch_tc_gemm(const float* a, uint64_t m, uint64_t k, uint64_t lda, const float* w, uint64_t n, uint64_t ldw,
+                   const float* bias, int relu, float* const* dsts, unsigned long long* const* counters, int n_dst,
+                   uint64_t row_offset, uint64_t ldh, float* wt_scratch, cudaStream_t st) {
     if (m == 0 || n == 0) return AES_OK;
     if (k == 0 || k > (uint64_t)kMaxK || n > (uint64_t)kMaxN)
         return fail(AES_ERR_UNSUPPORTED, "tcgen05 GEMM takes 1 <= K <= 128 and N <= 128");
+    if (n_dst < 1 || n_dst > kMaxOut) return fail(AES_ERR_INVALID_ARG, "1..8 output replicas");
     if (lda % 4 || (uintptr_t)a % 16) return fail(AES_ERR_UNSUPPORTED, "A rows must be 16-B aligned");
     const uint32_t k_slabs = (uint32_t)((k + kSlabK - 1) / kSlabK);
     const uint32_t k_pad = k_slabs * kSlabK;
@@ -318,11 +336,17 @@ extern "C" int aes_dev_gemm_tf32(const float* a, uint64_t m, uint64_t k, uint64_
     while (tmem_cols < 2 * n_pad) tmem_cols <<= 1;
     if (!wt_scratch) return fail(AES_ERR_INVALID_ARG, "W^T scratch (n_pad * k_pad floats) required");
     transpose_pad_kernel<<<64, 256, 0, st>>>(w, (uint32_t)k, (uint32_t)n, ldw, wt_scratch, n_pad, k_pad);
-    if (ldh % 4 || (uintptr_t)h % 16) return fail(AES_ERR_UNSUPPORTED, "H rows must be 16-B aligned");
-    CUtensorMap map_a, map_w, map_h;
+    CUtensorMap map_a, map_w;
     AES_TRY(make_map(&map_a, a, k, m, lda, kSlabK, kTileM));
     AES_TRY(make_map(&map_w, wt_scratch, k_pad, n_pad, k_pad, kSlabK, n_pad));
-    AES_TRY(make_map(&map_h, h, n, m, ldh, kSlabK, kTileM));
+    OutMaps outs{};
+    outs.n = n_dst;
+    for (int d = 0; d < n_dst; ++d) {
+        float* h = dsts[d] + row_offset * ldh;
+        if (ldh % 4 || (uintptr_t)h % 16) return fail(AES_ERR_UNSUPPORTED, "H rows must be 16-B aligned");
+        AES_TRY(make_map(&outs.map[d], h, n, m, ldh, kSlabK, kTileM));
+        outs.ctr[d] = counters ? counters[d] : nullptr;
+    }
     const uint32_t n_slabs = (uint32_t)((n + 31) / 32);
     const size_t smem = (size_t)kStages * kSlabBytes + (size_t)k_slabs * n_pad * 128 + (size_t)n_slabs * kSlabBytes +
                         sizeof(Barriers) + 1024;
@@ -335,10 +359,34 @@ extern "C" int aes_dev_gemm_tf32(const float* a, uint64_t m, uint64_t k, uint64_
     }
     const uint64_t tiles = (m + kTileM - 1) / kTileM;
     const unsigned grid = (unsigned)(tiles < (uint64_t)kNumSMs ? tiles : (uint64_t)kNumSMs);
-    tc_gemm_kernel<<<grid, kThreads, smem, st>>>(map_a, map_w, map_h, m, k_slabs, (uint32_t)n, n_pad, tmem_cols, bias,
+    tc_gemm_kernel<<<grid, kThreads, smem, st>>>(map_a, map_w, outs, m, k_slabs, (uint32_t)n, n_pad, tmem_cols, bias,
                                                  relu);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
+}
+
+}  // namespace
+}  // namespace aes
+
+extern "C" int aes_dev_gemm_tf32(const float* a, uint64_t m, uint64_t k, uint64_t lda, const float* w, uint64_t n,
+                                 uint64_t ldw, const float* bias, int relu, float* h, uint64_t ldh, float* wt_scratch,
+                                 void* stream) {
+    float* dsts[1] = {h};
+    return aes::launch_tc_gemm(a, m, k, lda, w, n, ldw, bias, relu, dsts, nullptr, 1, 0, ldh, wt_scratch,
+                               aes::as_stream(stream));
+}
+
+extern "C" int aes_dev_gemm_tf32_bcast(const float* a, uint64_t m, uint64_t k, uint64_t lda, const float* w,
+                                       uint64_t n, uint64_t ldw, const float* bias, int relu, float* const* dsts,
+                                       unsigned long long* const* counters, int n_dst, uint64_t row_offset,
+                                       uint64_t ldh, float* wt_scratch, void* stream) {
+    return aes::launch_tc_gemm(a, m, k, lda, w, n, ldw, bias, relu, dsts, counters, n_dst, row_offset, ldh,
+                               wt_scratch, aes::as_stream(stream));
+}
+
+extern "C" uint64_t aes_gemm_tf32_ctas(uint64_t m) {
+    // arrivals per destination = 128-row tiles this launch stores
+    return (m + aes::kTileM - 1) / aes::kTileM;
 }
 
 extern "C" uint64_t aes_gemm_tf32_scratch_floats(uint64_t k, uint64_t n) {

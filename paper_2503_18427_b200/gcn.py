@@ -80,7 +80,7 @@ class ShardedGCN:
 
     def __init__(self, srow_ptr: torch.Tensor, scol: torch.Tensor, sval: torch.Tensor, n_rows: int,
                  weights: Sequence[torch.Tensor], biases: Sequence[torch.Tensor | None], ops: Ops | None = None,
-                 group=None, balance: str = "rows", exchange: str = "nccl"):
+                 group=None, balance: str = "rows", exchange: str = "nccl", fast_gemm: bool = False):
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -116,8 +116,10 @@ class ShardedGCN:
                 device.check(device.lib().aes_dev_all_finite(w.data_ptr(), w.numel(), flag.data_ptr(),
                                                              device.stream_of(None)))
                 self.finite.append(int(flag.item()) == 0)
-            self.arrivals = [sum(p2p.gemm_ctas(c1 - c0, w.shape[1]) for c0, c1 in zip(self.cuts, self.cuts[1:]))
-                             for w in weights]
+            # fast mode (tcgen05 TF32, not bit-exact) where the layer shape allows
+            self.fast = [fast_gemm and w.shape[0] <= 128 and w.shape[1] <= 128 for w in weights]
+            self.arrivals = [sum(p2p.gemm_ctas(c1 - c0, w.shape[1], fast) for c0, c1 in zip(self.cuts, self.cuts[1:]))
+                             for w, fast in zip(weights, self.fast)]
 
     def _gather(self, out_rows: torch.Tensor, f: int, like: torch.Tensor) -> torch.Tensor:
         rows = self.hi - self.lo
@@ -145,7 +147,7 @@ class ShardedGCN:
         for l, (w, b) in enumerate(zip(self.weights, self.biases)):
             agg = self.ops.spmm(self.srow, self.scol, self.sval, h, out=self.ops.alloc(max(rows, 1), h.shape[1], h))
             out_buf = (l + 1) % 2
-            rep.gemm_publish(out_buf, agg[:rows], w, b, l + 1 < n_layers, self.finite[l], self.lo)
+            rep.gemm_publish(out_buf, agg[:rows], w, b, l + 1 < n_layers, self.finite[l], self.lo, fast=self.fast[l])
             rep.wait(self.arrivals[l])
             h = rep.bufs[out_buf][: self.n, : w.shape[1]]
         if return_shard:

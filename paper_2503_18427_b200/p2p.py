@@ -62,12 +62,24 @@ class PeerReplicas:
             dist.barrier(group)
 
     def gemm_publish(self, out_buf: int, a: torch.Tensor, w: torch.Tensor, bias, relu: bool, finite_w: bool,
-                     row_offset: int, stream=None):
+                     row_offset: int, stream=None, fast: bool = False):
         """act(a @ w + bias) for this rank's rows, stored into every rank's
-        replica `out_buf` at rows [row_offset, row_offset + m)."""
+        replica `out_buf` at rows [row_offset, row_offset + m).  fast=True
+        uses the tcgen05 TF32 kernel whose TMA-store epilogue writes the
+        peers' replicas (not bit-exact)."""
         m, k = a.shape
         n = w.shape[1]
         w = w.contiguous()
+        if fast:
+            scratch = torch.empty(int(lib().aes_gemm_tf32_scratch_floats(k, n)), dtype=torch.float32,
+                                  device=a.device)
+            check(lib().aes_dev_gemm_tf32_bcast(
+                a.data_ptr(), m, k, a.stride(0), w.data_ptr(), n, w.stride(0),
+                None if bias is None or bias.numel() == 0 else bias.data_ptr(), int(relu),
+                ctypes.cast(self.dst[out_buf], ctypes.c_void_p), ctypes.cast(self.ctr, ctypes.c_void_p), self.world,
+                row_offset, self.ld, scratch.data_ptr(), stream_of(stream)))
+            self._keep = scratch  # alive until the stream passes the next wait
+            return
         check(lib().aes_dev_gemm_bias_act_ex(
             a.data_ptr(), m, k, a.stride(0), w.data_ptr(), n, w.stride(0),
             None if bias is None or bias.numel() == 0 else bias.data_ptr(), int(relu), int(finite_w),
@@ -90,7 +102,10 @@ class PeerReplicas:
         check(lib().aes_dev_wait_counter(self.counter.data_ptr(), self.expected, stream_of(stream)))
 
 
-def gemm_ctas(m: int, n: int) -> int:
+def gemm_ctas(m: int, n: int, fast: bool = False) -> int:
+    """Arrivals one producer's publishing GEMM adds to each counter."""
+    if fast:
+        return int(lib().aes_gemm_tf32_ctas(m)) if m and n else 0
     return int(lib().aes_gemm_ctas(m, n))
 
 
