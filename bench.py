@@ -330,6 +330,13 @@ def run_ours(args):
     if not args.no_e2e and args.dtype == "f32":
         e2e = run_e2e(args, rp, col, val, b, lo, hi, f, n, total_bytes, dist, world)
 
+    # ---- one GCN layer through the row-sharded driver (SpMM -> GEMM -> exchange
+    # fused into the GEMM epilogue over peer memory): exact ordered-fp32 GEMM
+    # (bit-exact with the reference) and the tcgen05 TF32 fast mode
+    gcn_layer = None
+    if not args.no_layer and args.dtype == "f32" and args.mode == "spmm":
+        gcn_layer = run_gcn_layer(args, full_plan, n, f, b, dist)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         b_np = np.ascontiguousarray(b.cpu().numpy())
@@ -350,7 +357,7 @@ def run_ours(args):
                              % (n * f * elem / 1e9, n * f * 4 / 1e9),
                        "parallelism": f"row-sharded x{world}" if world > 1 else "single GPU"},
             "roofline": roofline, "clocks": clocks,
-            "e2e": e2e, "cpu_baseline": cpu,
+            "e2e": e2e, "cpu_baseline": cpu, "gcn_layer": gcn_layer,
             "gpu_launches": args.steps * (1 + (1 if args.mode == "layer" else 0)),
         }
         print(json.dumps(line), flush=True)
@@ -358,6 +365,41 @@ def run_ours(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def run_gcn_layer(args, plan, n, f, b, dist):
+    """Time one GCN layer (F -> F, ReLU) with gcn.ShardedGCN(exchange="p2p"):
+    sampled SpMM of this rank's rows, then the layer GEMM whose epilogue writes
+    every rank's next-layer replica (peer memory) and signals arrivals."""
+    import torch
+
+    from paper_2503_18427_b200.gcn import ShardedGCN
+    w = (torch.rand(f, f, device="cuda", generator=torch.Generator("cuda").manual_seed(3)) - 0.5)
+    bias = torch.full((f,), 0.01, device="cuda")
+    x = b[:, :f]
+    out = {}
+    for name, fast in (("exact_ordered_fp32", False), ("fast_tcgen05_tf32", True)):
+        model = ShardedGCN(plan.srow_ptr, plan.scol, plan.sval, n, [w], [bias], exchange="p2p", fast_gemm=fast)
+        for _ in range(2):
+            model.forward(x)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        steps = max(3, min(args.steps, 10))
+        s.record()
+        for _ in range(steps):
+            model.forward(x)
+        e.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([s.elapsed_time(e) / steps], dtype=torch.float64, device="cuda")
+        if dist:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        out[name + "_ms"] = round(float(t.item()), 4)
+        del model
+    out["exchange"] = "fused into the GEMM epilogue (P2P stores to every rank's replica + sys-scope arrivals)"
+    out["note"] = "exact mode is bit-exact with the reference; fast mode |err| <= 2^-8 sum|a||w| (TF32)"
+    return out
 
 
 def run_e2e(args, rp, col, val, b, lo, hi, f, n, total_bytes, dist, world):
@@ -448,6 +490,7 @@ def main():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-layer", action="store_true", help="skip the GCN layer (SpMM+GEMM+exchange) timing")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = max(args.warmup, 1)

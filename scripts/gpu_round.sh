@@ -10,12 +10,12 @@ timeout 300 python bench.py --dtype int8 --no-e2e --no-cpu-baseline > gpurun_out
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2>&1; cat gpurun_out/bench_ref.json
 # launch list of the timed region only (NVTX range "timed")
 timeout 300 ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum --clock-control none --csv \
-    --log-file gpurun_out/launches_timed.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+    --log-file gpurun_out/launches_timed.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-layer > /dev/null 2>&1
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_all.csv \
-    python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+    python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-layer > /dev/null 2>&1
 for dt in f32 int8; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:spmm_ring -s 2 -c 1 -o gpurun_out/prof_spmm_$dt -f \
-      python bench.py --steps 2 --warmup 2 --dtype $dt --no-e2e --no-cpu-baseline > gpurun_out/ncu_$dt.log 2>&1; tail -1 gpurun_out/ncu_$dt.log
+      python bench.py --steps 2 --warmup 2 --dtype $dt --no-e2e --no-cpu-baseline --no-layer > gpurun_out/ncu_$dt.log 2>&1; tail -1 gpurun_out/ncu_$dt.log
 done
 python scripts/ncu_summary.py gpurun_out/prof_spmm_f32.ncu-rep gpurun_out/prof_spmm_int8.ncu-rep > gpurun_out/ncu_full_summary.json
 python scripts/launch_summary.py gpurun_out/launches_timed.csv > gpurun_out/launches_timed_summary.json
