@@ -136,12 +136,20 @@ class ShardedGCN:
             return torch.cat(parts)
         return gathered[: self.n]
 
-    def _forward_p2p(self, x: torch.Tensor, return_shard: bool) -> torch.Tensor:
+    def input_view(self) -> torch.Tensor:
+        """The layer-0 replica buffer [n, F0] (p2p exchange): fill it once and
+        call forward(None) to skip the per-step feature copy."""
+        return self.replicas.bufs[0][: self.n, : self.weights[0].shape[0]]
+
+    def _forward_p2p(self, x: torch.Tensor | None, return_shard: bool, copy_out: bool = True) -> torch.Tensor:
         rep = self.replicas
         rows = self.hi - self.lo
-        f0 = x.shape[1]
+        f0 = self.weights[0].shape[0]
         rep.barrier()  # every peer is done with the previous step's replicas
-        rep.bufs[0][: self.n, :f0].copy_(x)
+        if x is not None:
+            rep.bufs[0][: self.n, :f0].copy_(x)
+        elif len(self.weights) > 1:
+            raise ValueError("forward(None) reuses the input replica: single-layer models only")
         h = rep.bufs[0][: self.n, :f0]
         n_layers = len(self.weights)
         for l, (w, b) in enumerate(zip(self.weights, self.biases)):
@@ -151,14 +159,15 @@ class ShardedGCN:
             rep.wait(self.arrivals[l])
             h = rep.bufs[out_buf][: self.n, : w.shape[1]]
         if return_shard:
-            return h[self.lo:self.hi].clone()
-        return h.clone()
+            return h[self.lo:self.hi].clone() if copy_out else h[self.lo:self.hi]
+        return h.clone() if copy_out else h
 
-    def forward(self, x: torch.Tensor, return_shard: bool = False) -> torch.Tensor:
+    def forward(self, x: torch.Tensor | None, return_shard: bool = False, copy_out: bool = True) -> torch.Tensor:
         """x: full [n, F0] replica on this rank.  Returns the full logits
         replica (or only this rank's rows when return_shard)."""
         if self.exchange == "p2p":
-            return self._forward_p2p(x, return_shard)
+            # copy_out=False returns a view of the replica (valid until the next step)
+            return self._forward_p2p(x, return_shard, copy_out)
         h = x
         rows = self.hi - self.lo
         n_layers = len(self.weights)
