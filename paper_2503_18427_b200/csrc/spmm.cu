@@ -471,6 +471,165 @@ spmm_scalar_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict
 }
 
 // ---------------------------------------------------------------------------
+// int8 dual-stream kernel (F <= 128 codes, ldq % 8 == 0).  The int8 SpMM is
+// instruction-bound, not HBM-bound: a 128-B code row feeds 128 LUT decodes
+// and 256 FP ops, so per-slot bookkeeping (wait, shuffles, issue, row-end
+// test) matters.  Here each half-warp runs its own row-group stream with 8
+// codes per lane (LDGSTS.64), so one warp instruction advances two slots and
+// the bookkeeping is paid once per pair; the LUT is laid out with a 256-B row
+// stride so PRMT(code, lane*4) yields the byte offset of lut[code][lane]
+// directly (one PRMT + one LDS per code).  Same slot order and roundings as
+// the fp32 kernel: bit-identical to spmm over dequantize(Q).
+// ---------------------------------------------------------------------------
+template <int C, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+spmm_q8_dual_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
+                    const float* __restrict__ sval, uint64_t n_rows, const uint2* __restrict__ q, uint32_t ld8,
+                    uint32_t f8, float4* __restrict__ c, uint64_t ldc4, const float* __restrict__ lut_g,
+                    uint32_t group_rows) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr uint32_t kLutBytes = 256 * 256;  // lut[q] at q*256, lane j at +4j (upper half unused)
+    for (int i = threadIdx.x; i < 256 * 32; i += WARPS * 32)
+        reinterpret_cast<float*>(smem_raw)[(i >> 5) * 64 + (i & 31)] = lut_g[i >> 5];
+    __syncthreads();
+
+    const uint32_t lane = threadIdx.x & 31, h = lane >> 4, hl = lane & 15;
+    const uint32_t hbase = h << 4;
+    const uint32_t hmask = 0xFFFFu << hbase;
+    const uint32_t lane4 = lane * 4;  // byte 0 of the decode PRMT
+    const uint32_t ring0 = smem_addr(smem_raw) + kLutBytes + (threadIdx.x >> 5) * (2 * C * 128) + h * (C * 128) + hl * 8;
+
+    // this half-warp's row group
+    const uint64_t gidx = ((uint64_t)blockIdx.x * WARPS + (threadIdx.x >> 5)) * 2 + h;
+    const uint64_t r0 = gidx * group_rows;
+    const bool active = r0 < n_rows;
+    const uint32_t nr = active ? (uint32_t)min((uint64_t)group_rows, n_rows - r0) : 1;
+    const uint64_t g0 = active ? srow[r0] : 0;
+    const uint64_t my_end = active ? srow[r0 + 1 + min(hl, nr - 1)] : 0;
+    const uint64_t end_all = __shfl_sync(0xffffffffu, my_end, hbase + nr - 1);
+    const uint32_t total = active ? (uint32_t)(end_all - g0) : 0u;
+    const uint32_t rel = (uint32_t)(my_end - g0);
+    const uint32_t total_max = max(total, __shfl_xor_sync(0xffffffffu, total, 16));
+    const uint32_t* gcol = scol + g0;
+    const float* gval = sval + g0;
+    const char* glb = reinterpret_cast<const char*>(q + hl);
+    const uint32_t ld_bytes = ld8 * 8;
+    const bool colok = hl < f8;
+
+    auto ld_col = [&](uint32_t chunk) -> uint32_t {
+        const uint32_t s = chunk * C + hl;
+        return (hl < (uint32_t)C && s < total) ? ld_meta_u32(gcol + s) : 0u;
+    };
+    auto ld_val = [&](uint32_t chunk) -> float {
+        const uint32_t s = chunk * C + hl;
+        return (hl < (uint32_t)C && s < total) ? ld_meta_f32(gval + s) : 0.f;
+    };
+    auto issue = [&](int p, uint32_t col) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(ring0 + p * 128),
+                     "l"(glb + (uint64_t)col * ld_bytes)
+                     : "memory");
+    };
+    {
+        const uint32_t mc0 = ld_col(0);
+#pragma unroll
+        for (int p = 0; p < C; ++p) {
+            const uint32_t col = __shfl_sync(0xffffffffu, mc0, hbase + p);
+            if ((uint32_t)p < total && colok) issue(p, col);
+            cp_commit();
+        }
+    }
+    uint32_t mc_is = ld_col(1), mc_nx = ld_col(2);
+    float mv_cur = ld_val(0), mv_nx = ld_val(1);
+
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+    float4* crow = c + r0 * ldc4 + hl * 2;
+    uint32_t row = 0;
+    uint32_t row_end = __shfl_sync(0xffffffffu, rel, hbase);
+    auto store_row = [&](uint32_t r) {
+        if (colok) {  // F % 8 == 0 here: both float4 halves are in the row
+            float4* dst = crow + (uint64_t)r * ldc4;
+            __stcs(dst, make_float4(acc[0], acc[1], acc[2], acc[3]));
+            __stcs(dst + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+    };
+    // half-uniform (divergent between halves): uses the half's lane mask
+    auto advance_rows = [&](uint32_t pos) {
+        do {
+            store_row(row);
+            ++row;
+            row_end = __shfl_sync(hmask, rel, hbase + min(row, nr - 1));
+        } while (row < nr && row_end == pos);
+    };
+    if (active && row_end == 0) advance_rows(0);
+
+    auto decode_acc = [&](uint32_t r, int base, float v) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t off = __byte_perm(r, lane4, 0x6504u | (k << 4));  // (code << 8) | lane*4
+            const float d = *reinterpret_cast<const float*>(smem_raw + off);
+            acc[base + k] = __fadd_rn(acc[base + k], __fmul_rn(v, d));
+        }
+    };
+
+    uint32_t kc = 0;
+    for (uint32_t t0 = 0; t0 < total_max; t0 += C, ++kc) {
+#pragma unroll
+        for (int p = 0; p < C; ++p) {
+            const uint32_t t = t0 + p;
+            cp_wait<C - 1>();
+            const float v = __shfl_sync(0xffffffffu, mv_cur, hbase + p);
+            const bool live = t < total;
+            if (live && colok) {
+                uint2 r;
+                asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(ring0 + p * 128));
+                decode_acc(r.x, 0, v);
+                decode_acc(r.y, 4, v);
+            }
+            const uint32_t col = __shfl_sync(0xffffffffu, mc_is, hbase + p);
+            if (t + C < total && colok) issue(p, col);
+            cp_commit();
+            if (live && t + 1 == row_end) advance_rows(t + 1);
+        }
+        mv_cur = mv_nx;
+        mc_is = mc_nx;
+        mv_nx = ld_val(kc + 2);
+        mc_nx = ld_col(kc + 3);
+    }
+    cp_wait<0>();
+    if (active)
+        while (row < nr) {
+            store_row(row);
+            ++row;
+        }
+}
+
+template <int C, int WARPS>
+int launch_q8_dual(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, const uint8_t* q,
+                   uint64_t ldq, uint32_t f8, float4* c, uint64_t ldc4, const float* lut, cudaStream_t st) {
+    const size_t smem = 256 * 256 + (size_t)WARPS * 2 * C * 128;
+    static bool attr_set = false;
+    if (!attr_set) {
+        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_q8_dual_kernel<C, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+        attr_set = true;
+    }
+    uint32_t gr = 16;  // row ends live in the 16 lanes of a half-warp
+    while (gr > 2 && (n + gr - 1) / gr < (uint64_t)kNumSMs * 128) gr >>= 1;
+    const uint64_t groups = (n + gr - 1) / gr;
+    const uint64_t warps = (groups + 1) / 2;
+    const unsigned grid = (unsigned)((warps + WARPS - 1) / WARPS);
+    spmm_q8_dual_kernel<C, WARPS><<<grid, WARPS * 32, smem, st>>>(srow, scol, sval, n,
+                                                                   reinterpret_cast<const uint2*>(q),
+                                                                   (uint32_t)(ldq / 8), f8, c, ldc4, lut, gr);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
+// ---------------------------------------------------------------------------
 // dispatch
 // ---------------------------------------------------------------------------
 int g_spmm_variant = 0;          // 0 = auto; see aes_dev_spmm_set_variant
@@ -633,6 +792,22 @@ int aes_dev_spmm_q8(const uint64_t* srow_ptr, const uint32_t* scol, const float*
         (uintptr_t)c % 16 != 0 || ldc < f4 * 4 || lut == nullptr)
         return fail(AES_ERR_UNSUPPORTED,
                     "spmm_q8 needs ldq % 4 == 0, ldc % 4 == 0 and ld >= round_up(f, 4)");
+    // dual-stream kernel (variants 20-24): F % 8 == 0, F <= 128, 8-B aligned
+    // code rows.  Measured slower than the single-stream ring on B200
+    // (1.02 vs 0.89 ms, products): the half-warp row-end divergence costs what
+    // the shared bookkeeping saves, so it is opt-in only.
+    const int v = g_spmm_variant;
+    if (v >= 20 && f % 8 == 0 && f <= 128 && ldq % 8 == 0 && (uintptr_t)q % 8 == 0) {
+        float4* c4 = reinterpret_cast<float4*>(c);
+        const uint32_t f8 = (uint32_t)(f / 8);
+        switch (v) {
+            case 21: return launch_q8_dual<8, 8>(srow_ptr, scol, sval, n_rows, q, ldq, f8, c4, ldc / 4, lut, st);
+            case 22: return launch_q8_dual<16, 8>(srow_ptr, scol, sval, n_rows, q, ldq, f8, c4, ldc / 4, lut, st);
+            case 23: return launch_q8_dual<16, 4>(srow_ptr, scol, sval, n_rows, q, ldq, f8, c4, ldc / 4, lut, st);
+            case 24: return launch_q8_dual<8, 16>(srow_ptr, scol, sval, n_rows, q, ldq, f8, c4, ldc / 4, lut, st);
+            default: return launch_q8_dual<8, 8>(srow_ptr, scol, sval, n_rows, q, ldq, f8, c4, ldc / 4, lut, st);
+        }
+    }
     GatherQ8 g{reinterpret_cast<const uint32_t*>(q), ldq / 4};
     return launch_vector(srow_ptr, scol, sval, n_rows, g, (uint32_t)f4,
                          reinterpret_cast<float4*>(c), ldc / 4, lut, st);

@@ -18,6 +18,7 @@ ap.add_argument("--variants", default="1,2,3,4,5,6,7,8")
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--dtypes", default="f32,int8")
 ap.add_argument("--strategy", default="adaptive")
+ap.add_argument("--q8-variants", default=None, help="int8 schedules (default: --variants)")
 args = ap.parse_args()
 
 n, alpha, maxdeg, f = synth.SHAPES[args.config]
@@ -50,7 +51,8 @@ res["quantize_ms"] = round(timeit(lambda: device.quantize(b, params=(q.x_min, q.
 for dt in args.dtypes.split(","):
     out = device.empty_padded(n, f)
     ref = None
-    for v in [int(x) for x in args.variants.split(",")]:
+    vlist = args.q8_variants if (dt == "int8" and args.q8_variants) else args.variants
+    for v in [int(x) for x in vlist.split(",")]:
         L.aes_dev_spmm_set_variant(v)
         if dt == "f32":
             fn = lambda: device.spmm_plan(plan, b, out=out)  # noqa: E731
