@@ -47,7 +47,8 @@ typedef enum {
     AES_ERR_INVALID_ARG = 9,     /* null handle / bad argument */
     AES_ERR_CUDA = 10,           /* CUDA runtime error (message has details) */
     AES_ERR_UNSUPPORTED = 11,    /* layout the kernels do not take */
-    AES_ERR_NOT_SQUARE = 12      /* "NotSquare"              matrix.cpp:131 */
+    AES_ERR_NOT_SQUARE = 12,     /* "NotSquare"              matrix.cpp:131 */
+    AES_ERR_IO = 13              /* std::runtime_error of io.cpp ("BadMagic: path", ...) */
 } aes_status;
 
 typedef enum { AES_ADAPTIVE = 0, AES_AFS = 1, AES_SFS = 2, AES_FULL = 3 } aes_strategy;
@@ -218,6 +219,24 @@ AES_API int aes_argmax_rows(const float* x, uint64_t rows, uint64_t cols, uint32
 AES_API int aes_evaluate(const float* logits, uint64_t rows, uint64_t cols, const uint32_t* labels,
                          uint64_t labels_len, const float* reference_logits, const uint8_t* mask,
                          uint64_t mask_len, double* accuracy, double* agreement, uint64_t* per_class);
+
+/* Binary files straight to HBM (formats of proj/src/io.cpp:117-220).  The
+ * payload streams through pinned double buffers overlapped with the H2D
+ * copies; load_ms (may be NULL) receives the wall time, like
+ * load_features(path, &load_ms) (io.hpp:36-38).
+ *   aes_fmat_info        header: dtype 0 = f32, 1 = u8 codes (+ x_min, x_max)
+ *   aes_fmat_load_device payload into a device buffer with row pitch ld_elems
+ *   aes_fmat_load_qfeat  dtype-1 file -> HBM QuantizedFeatures (codes + LUT)
+ *   aes_csr_load         CSRB -> HBM CsrMatrix, validated on the GPU
+ *                        ("invalid CSR payload: ..." as io.cpp:142-143) */
+AES_API int aes_fmat_info(const char* path, int* dtype, uint64_t* rows, uint64_t* cols, float* x_min,
+                          float* x_max);
+AES_API int aes_fmat_load_device(const char* path, void* d_dst, uint64_t ld_elems, double* load_ms);
+AES_API int aes_fmat_load_qfeat(const char* path, aes_qfeat_t* out, double* load_ms);
+AES_API int aes_fmat_save_f32(const float* x, uint64_t rows, uint64_t cols, const char* path);
+AES_API int aes_fmat_save_qfeat(aes_qfeat_t q, const char* path);
+AES_API int aes_csr_load(const char* path, aes_csr_t* out, double* load_ms);
+AES_API int aes_csr_save(aes_csr_t a, const char* path);
 
 /* ======================================================================
  * Tier 2: device API (device pointers, caller's stream, no sync)

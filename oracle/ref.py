@@ -71,6 +71,13 @@ def shim():
         L.ref_dense_matmul.argtypes = [vp, u64, u64, vp, u64, vp]
         L.ref_gcn_forward.argtypes = [vp, vp, vp, i32, vp, vp, u32, i32, vp]
         L.ref_gnn_forward.argtypes = [i32, vp, vp, vp, i32, vp, vp, u32, i32, vp]
+        cp = C.c_char_p
+        L.ref_save_csr_binary.argtypes = [vp, cp]
+        L.ref_load_csr_binary.argtypes = [cp]
+        L.ref_load_csr_binary.restype = vp
+        L.ref_save_fmat_f32.argtypes = [vp, u64, u64, cp]
+        L.ref_save_fmat_q8.argtypes = [vp, u64, u64, f32, f32, cp]
+        L.ref_load_fmat.argtypes = [cp, vp, vp, vp, vp, vp, vp, vp]
         L.ref_row_mean_normalize.argtypes = [vp]
         L.ref_row_mean_normalize.restype = vp
         L.ref_evaluate.argtypes = [vp, u64, u64, vp, vp, vp, vp, vp, vp]
@@ -193,6 +200,44 @@ def dense_matmul(a, b):
     c = np.zeros((a.shape[0], b.shape[1]), np.float32)
     _chk(shim().ref_dense_matmul(_p(a), a.shape[0], a.shape[1], _p(b), b.shape[1], _p(c)))
     return c
+
+
+def save_csr_binary(csr: RefCsr, path: str):
+    _chk(shim().ref_save_csr_binary(csr.h, path.encode()))
+
+
+def load_csr_binary(path: str) -> RefCsr:
+    h = shim().ref_load_csr_binary(path.encode())
+    if not h:
+        raise ValueError(shim().ref_last_error().decode())
+    return RefCsr(h)
+
+
+def save_fmat_f32(x, path: str):
+    x = np.ascontiguousarray(x, np.float32)
+    _chk(shim().ref_save_fmat_f32(_p(x), x.shape[0], x.shape[1], path.encode()))
+
+
+def save_fmat_q8(codes, lo, hi, path: str):
+    codes = np.ascontiguousarray(codes, np.uint16)
+    _chk(shim().ref_save_fmat_q8(_p(codes), codes.shape[0], codes.shape[1], lo, hi, path.encode()))
+
+
+def load_fmat(path: str):
+    """(dtype, array) where array is f32 features (dtype 0) or
+    (codes u16, lo, hi) (dtype 1) — reference load_features (io.cpp:183-220)."""
+    dt = np.zeros(1, np.int32)
+    r, c = np.zeros(1, np.uint64), np.zeros(1, np.uint64)
+    lo, hi = np.zeros(1, np.float32), np.zeros(1, np.float32)
+    _chk(shim().ref_load_fmat(path.encode(), _p(dt), _p(r), _p(c), _p(lo), _p(hi), None, None))
+    rows, cols = int(r[0]), int(c[0])
+    if dt[0] == 0:
+        x = np.zeros((rows, cols), np.float32)
+        _chk(shim().ref_load_fmat(path.encode(), _p(dt), _p(r), _p(c), _p(lo), _p(hi), _p(x), None))
+        return 0, x
+    codes = np.zeros((rows, cols), np.uint16)
+    _chk(shim().ref_load_fmat(path.encode(), _p(dt), _p(r), _p(c), _p(lo), _p(hi), None, _p(codes)))
+    return 1, (codes, float(lo[0]), float(hi[0]))
 
 
 def row_mean_normalize(csr: RefCsr) -> RefCsr:

@@ -20,6 +20,7 @@
 
 #include "aesspmm/bench.hpp"
 #include "aesspmm/gnn.hpp"
+#include "aesspmm/io.hpp"
 #include "aesspmm/matrix.hpp"
 #include "aesspmm/quantize.hpp"
 #include "aesspmm/sampling.hpp"
@@ -125,6 +126,52 @@ int ref_evaluate(const float* logits, std::uint64_t rows, std::uint64_t cols, co
         *acc = e.accuracy;
         *agree = e.agreement;
         std::copy(e.per_class.begin(), e.per_class.end(), per_class);
+    });
+}
+
+// ---- binary I/O (proj/src/io.cpp) -------------------------------------------
+int ref_save_csr_binary(void* h, const char* path) {
+    return guard([&] { save_csr_binary(*static_cast<CsrMatrix*>(h), path); });
+}
+void* ref_load_csr_binary(const char* path) {
+    void* out = nullptr;
+    guard([&] { out = new CsrMatrix(load_csr_binary(path)); });
+    return out;
+}
+int ref_save_fmat_f32(const float* x, std::uint64_t r, std::uint64_t c, const char* path) {
+    return guard([&] { save_fmat(make_dense(r, c, x), path); });
+}
+int ref_save_fmat_q8(const std::uint16_t* codes, std::uint64_t r, std::uint64_t c, float lo, float hi,
+                     const char* path) {
+    return guard([&] {
+        QuantizedFeatures q;
+        q.n_rows = r;
+        q.n_cols = c;
+        q.codes.assign(codes, codes + r * c);
+        q.params = QuantParams{lo, hi, 8};
+        save_fmat(q, path);
+    });
+}
+// dtype 0 -> x (r*c floats), dtype 1 -> codes + lo/hi
+int ref_load_fmat(const char* path, int* dtype, std::uint64_t* r, std::uint64_t* c, float* lo, float* hi, float* x,
+                  std::uint16_t* codes) {
+    return guard([&] {
+        Features f = load_features(path);
+        if (std::holds_alternative<DenseMatrix>(f)) {
+            const DenseMatrix& m = std::get<DenseMatrix>(f);
+            *dtype = 0;
+            *r = m.n_rows;
+            *c = m.n_cols;
+            if (x) std::copy(m.data.begin(), m.data.end(), x);
+        } else {
+            const QuantizedFeatures& q = std::get<QuantizedFeatures>(f);
+            *dtype = 1;
+            *r = q.n_rows;
+            *c = q.n_cols;
+            *lo = q.params.x_min;
+            *hi = q.params.x_max;
+            if (codes) std::copy(q.codes.begin(), q.codes.end(), codes);
+        }
     });
 }
 

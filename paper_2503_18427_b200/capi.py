@@ -63,6 +63,10 @@ def lib():
         L.aes_dev_wait_counter.argtypes = [vp, u64, vp]
         L.aes_dev_all_finite.argtypes = [vp, u64, vp, vp]
         L.aes_dev_signal_all.argtypes = [vp, i32, vp]
+        cp = C.c_char_p
+        L.aes_fmat_info.argtypes = [cp, vp, vp, vp, vp, vp]
+        L.aes_fmat_load_device.argtypes = [cp, vp, u64, vp]
+        L.aes_fmat_save_f32.argtypes = [vp, u64, u64, cp]
         L.aes_select_strategy.argtypes = [u64, u32, vp, vp]
         L.aes_hash_start.argtypes = [u32, u64, u32]
         L.aes_hash_start.restype = u32

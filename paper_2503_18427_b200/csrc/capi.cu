@@ -321,6 +321,7 @@ const char* aes_status_name(int s) {
         case AES_ERR_CUDA: return "CudaError";
         case AES_ERR_UNSUPPORTED: return "Unsupported";
         case AES_ERR_NOT_SQUARE: return "NotSquare";
+        case AES_ERR_IO: return "IoError";
         default: return "Unknown";
     }
 }
@@ -1214,3 +1215,92 @@ int aes_evaluate(const float* logits, uint64_t rows, uint64_t cols, const uint32
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// helpers for io.cu (same translation-unit-private allocator and stream)
+// ---------------------------------------------------------------------------
+namespace aes {
+
+void* capi_alloc(size_t bytes) {
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, bytes ? bytes : 16, lib_stream()) != cudaSuccess) return nullptr;
+    if (cudaStreamSynchronize(lib_stream()) != cudaSuccess) return nullptr;
+    return p;
+}
+
+void capi_free(void* p) {
+    if (p) cudaFreeAsync(p, lib_stream());
+}
+
+// QuantizedFeatures over device u8 codes (ownership of d_codes moves in).
+int capi_make_qfeat_u8(const uint8_t* d_codes, uint64_t rows, uint64_t cols, uint64_t ld, float lo, float hi,
+                       aes_qfeat_t* out) {
+    auto* q = new aes_qfeat_s;
+    q->rows = rows;
+    q->cols = cols;
+    q->ld = ld;
+    q->x_min = lo;
+    q->x_max = hi;
+    q->bits = 8;
+    q->u8 = true;
+    q->codes = const_cast<uint8_t*>(d_codes);
+    cudaStream_t st = lib_stream();
+    int s = cudaMallocAsync((void**)&q->lut, 256 * sizeof(float), st) == cudaSuccess ? AES_OK
+                                                                                    : fail(AES_ERR_CUDA, "alloc");
+    if (!s) s = aes_dev_dequant_lut(lo, hi, 8, q->lut, st);
+    if (!s) s = sync();
+    if (s) {
+        q->codes = nullptr;  // caller keeps ownership on failure
+        aes_qfeat_destroy(q);
+        return s;
+    }
+    *out = q;
+    return AES_OK;
+}
+
+// CsrMatrix over device arrays (ownership moves in on success), validated.
+int capi_csr_from_device(uint64_t n_rows, uint64_t n_cols, uint64_t nnz, uint64_t* rp, uint32_t* col, float* val,
+                         aes_csr_t* out) {
+    auto* a = new aes_csr_s;
+    a->n_rows = n_rows;
+    a->n_cols = n_cols;
+    a->nnz = nnz;
+    a->row_ptr = rp;
+    a->col = col;
+    a->val = val;
+    uint64_t first = 0;
+    int s = d2h_scalar(rp, &first);
+    if (!s) s = validate_device(a, n_rows + 1, nnz, first);
+    if (s) {
+        a->row_ptr = nullptr;
+        a->col = nullptr;
+        a->val = nullptr;
+        delete a;
+        return s;
+    }
+    *out = a;
+    return AES_OK;
+}
+
+int capi_qfeat_device(aes_qfeat_t q, const void** codes, uint64_t* ld, int* u8) {
+    if (!q) return fail(AES_ERR_INVALID_ARG, "null qfeat");
+    *codes = q->codes;
+    *ld = q->ld;
+    *u8 = q->u8 ? 1 : 0;
+    return AES_OK;
+}
+
+int capi_csr_device(aes_csr_t a, const uint64_t** rp, const uint32_t** col, const float** val, uint64_t* n_rows,
+                    uint64_t* n_cols, uint64_t* nnz) {
+    if (!a) return fail(AES_ERR_INVALID_ARG, "null csr");
+    AES_TRY(sync());
+    *rp = a->row_ptr;
+    *col = a->col;
+    *val = a->val;
+    *n_rows = a->n_rows;
+    *n_cols = a->n_cols;
+    *nnz = a->nnz;
+    return AES_OK;
+}
+
+}  // namespace aes

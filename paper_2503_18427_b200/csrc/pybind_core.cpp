@@ -25,6 +25,7 @@ namespace {
     switch (status) {
         case AES_ERR_CUDA:
         case AES_ERR_UNSUPPORTED:
+        case AES_ERR_IO:  // std::runtime_error in the reference's io.cpp
             throw std::runtime_error(msg);
         default:
             throw py::value_error(msg);  // std::invalid_argument -> ValueError
@@ -474,6 +475,59 @@ PYBIND11_MODULE(_core, mod) {
         py::arg("adj_mean"), py::arg("features"), py::arg("weights"), py::arg("biases"),
         py::arg("plans") = py::none(), py::arg("n_threads") = 0, py::arg("fast_gemm") = false,
         "sage_forward (gnn.cpp:80-95): relu(concat(H, spmm(adj_mean, H)) @ W + b) per layer");
+    // ---- binary files straight to HBM (io.cpp:117-220 formats)
+    mod.def(
+        "load_csr_binary",
+        [](const std::string& path) {
+            aes_csr_t h = nullptr;
+            double ms = 0;
+            check(nogil([&] { return aes_csr_load(path.c_str(), &h, &ms); }));
+            return std::make_shared<Csr>(h);
+        },
+        py::arg("path"), "CSRB file -> HBM CsrMatrix (validated on the GPU)");
+    mod.def(
+        "save_csr_binary",
+        [](const Csr& m, const std::string& path) { check(nogil([&] { return aes_csr_save(m.h, path.c_str()); })); },
+        py::arg("matrix"), py::arg("path"));
+    mod.def(
+        "load_features",
+        [](const std::string& path) -> py::tuple {
+            int dtype = 0;
+            uint64_t r = 0, c = 0;
+            float lo = 0, hi = 0;
+            check(aes_fmat_info(path.c_str(), &dtype, &r, &c, &lo, &hi));
+            double ms = 0;
+            if (dtype == 1) {
+                aes_qfeat_t h = nullptr;
+                check(nogil([&] { return aes_fmat_load_qfeat(path.c_str(), &h, &ms); }));
+                return py::make_tuple(std::make_shared<QFeat>(h), ms);
+            }
+            // dtype 0: f32 features as numpy (the reference returns a host DenseMatrix)
+            auto out = new_2d(r, c);
+            float* po = out.mutable_data();
+            FILE* f = fopen(path.c_str(), "rb");
+            if (!f) throw std::runtime_error("Io: cannot open for reading: " + path);
+            fseek(f, 22, SEEK_SET);
+            size_t got = fread(po, 4, r * c, f);
+            fclose(f);
+            if (got != r * c) throw std::runtime_error("TruncatedFile: " + path);
+            return py::make_tuple(out, ms);
+        },
+        py::arg("path"), "FMAT file -> (QuantizedFeatures in HBM | float32 array, load_ms)");
+    mod.def(
+        "save_fmat",
+        [](py::object obj, const std::string& path) {
+            if (py::isinstance<QFeat>(obj)) {
+                const QFeat& q = obj.cast<const QFeat&>();
+                check(nogil([&] { return aes_fmat_save_qfeat(q.h, path.c_str()); }));
+                return;
+            }
+            F32In x = as_2d(obj.cast<F32In>());
+            const float* px = x.data();
+            uint64_t r = x.shape(0), c = x.shape(1);
+            check(nogil([&] { return aes_fmat_save_f32(px, r, c, path.c_str()); }));
+        },
+        py::arg("features"), py::arg("path"), "save_fmat (io.cpp:160-181): f32 array or 8-bit QuantizedFeatures");
     mod.def(
         "row_mean_normalize",
         [](const Csr& a) {

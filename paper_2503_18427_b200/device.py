@@ -174,6 +174,34 @@ def quantize(x: torch.Tensor, bits: int = 8, params=None, stream=None) -> Quanti
     return QuantizedDevice(codes, lo, hi, bits, lut)
 
 
+def load_fmat(path: str, device="cuda"):
+    """FMAT file (proj/src/io.cpp:149-220 format) straight into HBM, streamed
+    through pinned double buffers.  Returns (features, load_ms): a float32
+    tensor (row stride padded to 4) for dtype 0, a QuantizedDevice (u8 codes +
+    exact LUT, no host dequantization) for dtype 1."""
+    import ctypes
+
+    import numpy as np
+
+    L = lib()
+    dt = np.zeros(1, np.int32)
+    r, c = np.zeros(1, np.uint64), np.zeros(1, np.uint64)
+    lo, hi = np.zeros(1, np.float32), np.zeros(1, np.float32)
+    check(L.aes_fmat_info(path.encode(), dt.ctypes.data, r.ctypes.data, c.ctypes.data, lo.ctypes.data,
+                          hi.ctypes.data))
+    rows, cols = int(r[0]), int(c[0])
+    ms = ctypes.c_double()
+    if dt[0] == 0:
+        out = empty_padded(rows, cols, device=device)
+        check(L.aes_fmat_load_device(path.encode(), ptr(out), out.stride(0), ctypes.addressof(ms)))
+        return out, ms.value
+    codes = empty_padded(rows, cols, dtype=torch.uint8, device=device)
+    check(L.aes_fmat_load_device(path.encode(), ptr(codes), codes.stride(0), ctypes.addressof(ms)))
+    lut = torch.zeros(256, dtype=torch.float32, device=device)
+    check(L.aes_dev_dequant_lut(float(lo[0]), float(hi[0]), 8, ptr(lut), stream_of(None)))
+    return QuantizedDevice(codes, float(lo[0]), float(hi[0]), 8, lut), ms.value
+
+
 def dequantize(q: QuantizedDevice, stream=None) -> torch.Tensor:
     rows, cols = q.codes.shape
     out = empty_padded(rows, cols, device=q.codes.device)

@@ -119,6 +119,30 @@ def test_compute_without_gpu_fails_loudly():
         m.CsrMatrix(2, 2, np.array([0, 1, 2], np.uint64), np.array([0, 1], np.uint32), np.ones(2, np.float32))
 
 
+def test_fmat_header_parse_matches_reference_writer(tmp_path):
+    """aes_fmat_info is host-only file parsing: check it on files written by
+    the reference's own save_fmat (io.cpp:160-181)."""
+    from oracle import ref as oref
+    if not oref.available():
+        pytest.skip("oracle/_ref not built")
+    from paper_2503_18427_b200 import capi
+    L = capi.lib()
+    x = np.random.default_rng(0).standard_normal((10, 7)).astype(np.float32)
+    p0, p1 = str(tmp_path / "a.fmat"), str(tmp_path / "b.fmat")
+    oref.save_fmat_f32(x, p0)
+    oref.save_fmat_q8(np.arange(70, dtype=np.uint16).reshape(10, 7), -1.5, 2.5, p1)
+    for p, want in ((p0, (0, 10, 7, 0.0, 0.0)), (p1, (1, 10, 7, -1.5, 2.5))):
+        dt, r, c = np.zeros(1, np.int32), np.zeros(1, np.uint64), np.zeros(1, np.uint64)
+        lo, hi = np.zeros(1, np.float32), np.zeros(1, np.float32)
+        capi.check(L.aes_fmat_info(p.encode(), dt.ctypes.data, r.ctypes.data, c.ctypes.data, lo.ctypes.data,
+                                   hi.ctypes.data))
+        assert (int(dt[0]), int(r[0]), int(c[0]), float(lo[0]), float(hi[0])) == want
+    bad = str(tmp_path / "bad.fmat")
+    open(bad, "wb").write(b"FMAX" + bytes(30))
+    with pytest.raises(capi.AesError, match="BadMagic"):
+        capi.check(L.aes_fmat_info(bad.encode(), None, None, None, None, None))
+
+
 def test_bench_helpers():
     import bench
     assert bench.alg_bytes(2_450_000, 13_963_464, 128) == 8_535_001_288 + 0 * 1  # SURVEY §8d arithmetic

@@ -162,3 +162,30 @@ def test_async_host_call_matches_sync():
         assert np.array_equal(bits(c.numpy()), bits(want))
     L.aes_plan_destroy(p)
     L.aes_csr_destroy(h)
+
+
+@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5, 6, 7, 8, 21, 22, 23, 24])
+def test_every_spmm_schedule_is_bit_exact(dev, variant):
+    """All schedule variants (aes_dev_spmm_set_variant) give the oracle's bits,
+    fp32 and int8 (the int8 dual-stream kernel is variants 21-24)."""
+    import torch
+
+    from paper_2503_18427_b200 import capi
+    L = capi.lib()
+    rp, col, val = graphs.power_law(6000, alpha=1.4, max_deg=3000, seed=variant)
+    g = dev.Graph.from_numpy(rp, col, val)
+    x_np = np.random.default_rng(variant).uniform(-1, 1, (6000, 128)).astype(np.float32)
+    x = torch.from_numpy(x_np).cuda()
+    plan = dev.SampledPlan(g, 32)
+    q = dev.quantize(x)
+    lo, hi = port.fit_params(x_np)
+    deq = port.dequantize(port.quantize(x_np, lo, hi), lo, hi)
+    try:
+        L.aes_dev_spmm_set_variant(variant)
+        out = dev.spmm_plan(plan, x)
+        outq = dev.spmm_q8(plan.srow_ptr, plan.scol, plan.sval, q)
+        torch.cuda.synchronize()
+    finally:
+        L.aes_dev_spmm_set_variant(0)
+    assert np.array_equal(bits(to_np(out)), bits(port.spmm_sampled(rp, col, val, x_np, 32)))
+    assert np.array_equal(bits(to_np(outq)), bits(port.spmm_sampled(rp, col, val, deq, 32)))
