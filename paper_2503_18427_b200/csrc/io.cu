@@ -15,9 +15,14 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <unistd.h>
+
+#include <atomic>
 #include <chrono>
 #include <mutex>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "common.cuh"
 
@@ -85,6 +90,35 @@ int open_magic(File& fh, const char* path, const char magic[4]) {
     return AES_OK;
 }
 
+// Read `bytes` at file offset `pos` with several threads (page-cache copies
+// are memcpy-bound on one core; the pinned buffer then goes out by DMA).
+bool parallel_pread(int fd, char* dst, uint64_t bytes, int64_t pos) {
+    const unsigned hw = std::thread::hardware_concurrency();
+    const unsigned nt = bytes < (8u << 20) ? 1u : (hw > 16 ? 16u : (hw ? hw : 1u));
+    const uint64_t per = (bytes + nt - 1) / nt;
+    std::atomic<bool> ok{true};
+    auto work = [&](unsigned t) {
+        uint64_t off = t * per, end = off + per < bytes ? off + per : bytes;
+        while (off < end) {
+            ssize_t r = pread(fd, dst + off, end - off, pos + (int64_t)off);
+            if (r <= 0) {
+                ok = false;
+                return;
+            }
+            off += (uint64_t)r;
+        }
+    };
+    if (nt == 1) {
+        work(0);
+    } else {
+        std::vector<std::thread> th;
+        for (unsigned t = 1; t < nt; ++t) th.emplace_back(work, t);
+        work(0);
+        for (auto& x : th) x.join();
+    }
+    return ok;
+}
+
 // Stream `rows` rows of `row_bytes` from the file into dst (row pitch
 // dst_pitch bytes), double-buffered through pinned memory.
 int stream_rows(File& fh, void* dst, uint64_t rows, uint64_t row_bytes, uint64_t dst_pitch) {
@@ -95,15 +129,20 @@ int stream_rows(File& fh, void* dst, uint64_t rows, uint64_t row_bytes, uint64_t
     const uint64_t rows_per = row_bytes >= kChunk ? 1 : kChunk / row_bytes;
     if (row_bytes > kChunk) return io_fail("row larger than the staging chunk", fh.path);
     int b = 0;
+    const int fd = fileno(fh.f);
+    int64_t pos = ftell(fh.f);
     for (uint64_t r0 = 0; r0 < rows; r0 += rows_per, b ^= 1) {
         const uint64_t nr = rows - r0 < rows_per ? rows - r0 : rows_per;
         AES_CUDA_TRY(cudaEventSynchronize(s.done[b]));  // this buffer's previous copy has drained
-        if (fread(s.buf[b], 1, nr * row_bytes, fh.f) != nr * row_bytes) return io_fail("TruncatedFile", fh.path);
+        if (!parallel_pread(fd, static_cast<char*>(s.buf[b]), nr * row_bytes, pos))
+            return io_fail("TruncatedFile", fh.path);
+        pos += (int64_t)(nr * row_bytes);
         AES_CUDA_TRY(cudaMemcpy2DAsync(static_cast<char*>(dst) + r0 * dst_pitch, dst_pitch, s.buf[b], row_bytes,
                                        row_bytes, nr, cudaMemcpyHostToDevice, s.st));
         AES_CUDA_TRY(cudaEventRecord(s.done[b], s.st));
     }
     AES_CUDA_TRY(cudaStreamSynchronize(s.st));
+    fseek(fh.f, pos, SEEK_SET);  // keep the FILE position in step for the next array
     return AES_OK;
 }
 
