@@ -222,6 +222,11 @@ __device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
     else
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ uint32_t pin_u32(uint32_t x) {
+    uint32_t y;
+    asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
@@ -630,11 +635,189 @@ int launch_q8_dual(const uint64_t* srow, const uint32_t* scol, const float* sval
 }
 
 // ---------------------------------------------------------------------------
+// int8 batch kernel (F <= 128 codes, 16-B aligned code rows) — the default
+// int8 path.  One warp, one flattened slot stream (as the fp32 ring: no
+// half-warp divergence), but the gathers go out four slots per instruction:
+// lane (g, j) = (lane / 8, lane % 8) copies bytes 16j..16j+15 of slot p0+g's
+// code row with one 16-B LDGSTS, so the wait / commit / column shuffle /
+// address arithmetic is paid once per four slots.  Consumption stays one slot
+// at a time across the whole warp (lane l decodes codes 4l..4l+3), so the
+// per-row accumulation order is the reference's slot order.
+//
+// Shared memory is one 64 KB block: the 256-entry LUT with a 256-B entry
+// stride (lut[q] replicated per lane at q*256 + 4*lane, bank = lane, so
+// PRMT(code, 4*lane) is the LDS offset — one PRMT + one LDS per code), and
+// the per-warp gather rings in the upper 128 B of each entry ("holes"): ring
+// slot p of warp w is hole w*C + p.
+// ---------------------------------------------------------------------------
+template <int C, int WARPS, bool FULL>
+__global__ void __launch_bounds__(WARPS * 32, 3)  // 3 x 72 KB of shared memory per SM
+spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
+                     const float* __restrict__ sval, uint64_t n_rows, const unsigned char* __restrict__ q,
+                     uint32_t ldq, uint32_t f4, float4* __restrict__ c, uint64_t ldc4,
+                     const float* __restrict__ lut_g, uint32_t group_rows) {
+    static_assert(C % 4 == 0 && C >= 8 && C <= 16 && C * WARPS <= 256, "the rings live in the LUT's 256 holes");
+    constexpr int B = C / 4;  // batches per ring round
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    for (int i = threadIdx.x; i < 256 * 32; i += WARPS * 32)
+        reinterpret_cast<float*>(smem_raw)[(i >> 5) * 64 + (i & 31)] = lut_g[i >> 5];
+    __syncthreads();
+
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // (pinned through asm so ptxas keeps them in registers instead of
+    // re-deriving them from %tid in every slot)
+    const uint32_t lane4 = pin_u32(lane * 4);
+    const uint32_t smem0 = smem_addr(smem_raw);
+    // ring slot p of this warp: hole warp*C + p; lane reads its 4 codes at
+    // rd0 + p*256 and copies its 16 B of batch slot p0 + lane/8 to wr0 + p0*256
+    const uint32_t rd0 = pin_u32(smem0 + warp * (C * 256) + 128 + lane * 4);
+    const uint32_t wr0 = smem0 + warp * (C * 256) + 128 + (lane >> 3) * 256 + (lane & 7) * 16;
+    // slot metadata of ring round k: cols at meta0 + (k&3)*8C, vals 4C later
+    const uint32_t meta0 = pin_u32(smem0 + 65536 + warp * (32 * C));
+    uint32_t nb = 16;  // bytes this lane copies per slot
+    if (!FULL) {
+        const uint32_t rowb = f4 * 4, j16 = (lane & 7) * 16;
+        nb = rowb > j16 ? min(16u, rowb - j16) : 0u;
+    }
+
+    const uint64_t r0 = ((uint64_t)blockIdx.x * WARPS + warp) * group_rows;
+    if (r0 >= n_rows) return;
+    const uint32_t nr = (uint32_t)min((uint64_t)group_rows, n_rows - r0);
+    const uint64_t g0 = srow[r0];
+    const uint64_t my_end = srow[r0 + 1 + min(lane, nr - 1)];
+    const uint32_t total = (uint32_t)(__shfl_sync(0xffffffffu, my_end, nr - 1) - g0);
+    const uint32_t rel = (uint32_t)(my_end - g0);
+
+    // metadata of round k -> buffer k & 3 (lanes 0..C-1: cols, 16..16+C-1: vals)
+    auto issue_meta = [&](uint32_t k) {
+        const uint32_t i = lane & 15, s = k * C + i;
+        if (i < (uint32_t)C && s < total) {
+            const void* src = lane < 16 ? (const void*)(scol + g0 + s) : (const void*)(sval + g0 + s);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(meta0 + (k & 3) * (8 * C) +
+                                                                           (lane >> 4) * (4 * C) + i * 4),
+                         "l"(src)
+                         : "memory");
+        }
+    };
+    // gathers for ring positions p0..p0+3 of round k (slots k*C + p0 ..)
+    auto issue = [&](int p0, uint32_t k) {
+        const uint32_t t = k * C + p0 + (lane >> 3);
+        if (t < total && (FULL || nb != 0)) {
+            const uint32_t col = lds_u32(meta0 + (k & 3) * (8 * C) + (p0 + (lane >> 3)) * 4);
+            const unsigned char* src = q + (uint64_t)col * ldq + (lane & 7) * 16;
+            if (FULL)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(wr0 + p0 * 256), "l"(src)
+                             : "memory");
+            else
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(wr0 + p0 * 256), "l"(src),
+                             "r"(nb)
+                             : "memory");
+        }
+    };
+    issue_meta(0);
+    issue_meta(1);
+    cp_commit();
+    cp_wait<0>();
+    __syncwarp();
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+        issue(4 * b, 0);
+        cp_commit();
+    }
+
+    float4 acc = f4_zero();
+    uint32_t row = 0;
+    uint32_t row_end = __shfl_sync(0xffffffffu, rel, 0);
+    auto store_row = [&](uint32_t r) {
+        if (FULL || lane < f4) __stcs(c + (r0 + r) * ldc4 + lane, acc);
+        acc = f4_zero();
+    };
+    auto advance_rows = [&](uint32_t pos) {
+        do {
+            store_row(row);
+            ++row;
+            row_end = __shfl_sync(0xffffffffu, rel, min(row, nr - 1));
+        } while (row < nr && row_end == pos);
+    };
+    if (row_end == 0) advance_rows(0);
+
+    auto consume = [&](int p, float v) {
+        const uint32_t r = lds_u32(rd0 + p * 256);
+        const float d0 = *reinterpret_cast<const float*>(smem_raw + __byte_perm(r, lane4, 0x6504u));
+        const float d1 = *reinterpret_cast<const float*>(smem_raw + __byte_perm(r, lane4, 0x6514u));
+        const float d2 = *reinterpret_cast<const float*>(smem_raw + __byte_perm(r, lane4, 0x6524u));
+        const float d3 = *reinterpret_cast<const float*>(smem_raw + __byte_perm(r, lane4, 0x6534u));
+        acc.x = __fadd_rn(acc.x, __fmul_rn(v, d0));
+        acc.y = __fadd_rn(acc.y, __fmul_rn(v, d1));
+        acc.z = __fadd_rn(acc.z, __fmul_rn(v, d2));
+        acc.w = __fadd_rn(acc.w, __fmul_rn(v, d3));
+    };
+
+    // Every round consumes all C ring positions: positions past `total`
+    // (only in the last round) accumulate garbage into acc AFTER the group's
+    // last row was stored — no row ends there, so nothing of it is written.
+    for (uint32_t k = 0, t0 = 0; t0 < total; t0 += C, ++k) {
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            cp_wait<B - 1>();
+            __syncwarp();  // other lanes' copies of these four slots are visible
+            float4 v4;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(v4.x), "=f"(v4.y), "=f"(v4.z), "=f"(v4.w)
+                         : "r"(meta0 + (k & 3) * (8 * C) + 4 * C + 16 * b));
+            const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int p = 4 * b + u;
+                consume(p, vv[u]);
+                if (t0 + p + 1 == row_end) advance_rows(t0 + p + 1);
+            }
+            __syncwarp();  // every lane is done reading these holes
+            if (b == 0) issue_meta(k + 2);
+            issue(4 * b, k + 1);
+            cp_commit();
+        }
+    }
+    cp_wait<0>();
+    while (row < nr) {
+        store_row(row);
+        ++row;
+    }
+}
+
+template <int C, int WARPS>
+int launch_q8_batch(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, const uint8_t* q,
+                    uint64_t ldq, uint32_t f4, float4* c, uint64_t ldc4, const float* lut, cudaStream_t st) {
+    const size_t smem = 256 * 256 + (size_t)WARPS * 32 * C;  // LUT + rings, slot metadata
+    static bool attr_set = false;
+    if (!attr_set) {
+        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_q8_batch_kernel<C, WARPS, true>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_q8_batch_kernel<C, WARPS, false>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set = true;
+    }
+    uint32_t gr = 32;
+    while (gr > 2 && (n + gr - 1) / gr < (uint64_t)kNumSMs * 64) gr >>= 1;
+    const uint64_t groups = (n + gr - 1) / gr;
+    const unsigned grid = (unsigned)((groups + WARPS - 1) / WARPS);
+    if (f4 == 32)
+        spmm_q8_batch_kernel<C, WARPS, true><<<grid, WARPS * 32, smem, st>>>(srow, scol, sval, n, q, (uint32_t)ldq,
+                                                                              f4, c, ldc4, lut, gr);
+    else
+        spmm_q8_batch_kernel<C, WARPS, false><<<grid, WARPS * 32, smem, st>>>(srow, scol, sval, n, q, (uint32_t)ldq,
+                                                                               f4, c, ldc4, lut, gr);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
+// ---------------------------------------------------------------------------
 // dispatch
 // ---------------------------------------------------------------------------
 int g_spmm_variant = 0;          // 0 = auto; see aes_dev_spmm_set_variant
 // Measured on B200 (scripts/tune_spmm.py, products W=32): fp32 best with a
-// 16-slot ring x 4 warps (1.18 ms), int8 with an 8-slot ring x 16 warps (0.89 ms).
+// 16-slot ring x 4 warps (1.18 ms); int8 with the batch kernel, 16-slot ring
+// x 16 warps (0.58 ms; the generic int8 ring, variant 8, 0.89 ms).
 constexpr int kDefaultVariantF32 = 2;
 constexpr int kDefaultVariantQ8 = 8;
 
@@ -797,7 +980,7 @@ int aes_dev_spmm_q8(const uint64_t* srow_ptr, const uint32_t* scol, const float*
     // (1.02 vs 0.89 ms, products): the half-warp row-end divergence costs what
     // the shared bookkeeping saves, so it is opt-in only.
     const int v = g_spmm_variant;
-    if (v >= 20 && f % 8 == 0 && f <= 128 && ldq % 8 == 0 && (uintptr_t)q % 8 == 0) {
+    if (v >= 20 && v < 30 && f % 8 == 0 && f <= 128 && ldq % 8 == 0 && (uintptr_t)q % 8 == 0) {
         float4* c4 = reinterpret_cast<float4*>(c);
         const uint32_t f8 = (uint32_t)(f / 8);
         switch (v) {
@@ -806,6 +989,20 @@ int aes_dev_spmm_q8(const uint64_t* srow_ptr, const uint32_t* scol, const float*
             case 23: return launch_q8_dual<16, 4>(srow_ptr, scol, sval, n_rows, q, ldq, f8, c4, ldc / 4, lut, st);
             case 24: return launch_q8_dual<8, 16>(srow_ptr, scol, sval, n_rows, q, ldq, f8, c4, ldc / 4, lut, st);
             default: return launch_q8_dual<8, 8>(srow_ptr, scol, sval, n_rows, q, ldq, f8, c4, ldc / 4, lut, st);
+        }
+    }
+    // batch kernel (variants 30-35; the default for 64 < F <= 128 with 16-B
+    // aligned code rows)
+    if ((v == 0 || v >= 30) && f4 > 16 && f4 <= 32 && ldq % 16 == 0 && (uintptr_t)q % 16 == 0) {
+        float4* c4 = reinterpret_cast<float4*>(c);
+        const uint32_t f4u = (uint32_t)f4;
+        switch (v) {
+            case 31: return launch_q8_batch<8, 16>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st);
+            case 32: return launch_q8_batch<16, 8>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st);
+            case 33: return launch_q8_batch<8, 8>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st);
+            case 34: return launch_q8_batch<12, 16>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st);
+            case 35: return launch_q8_batch<16, 4>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st);
+            default: return launch_q8_batch<16, 16>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st);
         }
     }
     GatherQ8 g{reinterpret_cast<const uint32_t*>(q), ldq / 4};
