@@ -650,7 +650,7 @@ int launch_q8_dual(const uint64_t* srow, const uint32_t* scol, const float* sval
 // the per-warp gather rings in the upper 128 B of each entry ("holes"): ring
 // slot p of warp w is hole w*C + p.
 // ---------------------------------------------------------------------------
-template <int C, int WARPS, bool FULL>
+template <int C, int WARPS, bool FULL, bool FASTB>
 __global__ void __launch_bounds__(WARPS * 32, 3)  // 3 x 72 KB of shared memory per SM
 spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
                      const float* __restrict__ sval, uint64_t n_rows, const unsigned char* __restrict__ q,
@@ -658,6 +658,7 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
                      const float* __restrict__ lut_g, uint32_t group_rows) {
     static_assert(C % 4 == 0 && C >= 8 && C <= 16 && C * WARPS <= 256, "the rings live in the LUT's 256 holes");
     constexpr int B = C / 4;  // batches per ring round
+    constexpr uint32_t kEndsBytes = 144;  // 33 row ends per warp
     extern __shared__ __align__(16) unsigned char smem_raw[];
     for (int i = threadIdx.x; i < 256 * 32; i += WARPS * 32)
         reinterpret_cast<float*>(smem_raw)[(i >> 5) * 64 + (i & 31)] = lut_g[i >> 5];
@@ -686,7 +687,12 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
     const uint64_t g0 = srow[r0];
     const uint64_t my_end = srow[r0 + 1 + min(lane, nr - 1)];
     const uint32_t total = (uint32_t)(__shfl_sync(0xffffffffu, my_end, nr - 1) - g0);
-    const uint32_t rel = (uint32_t)(my_end - g0);
+    // row ends (relative to g0) in shared memory: ends[r] for r < nr, and
+    // ends[r] = total for r >= nr, so advance_rows needs no shuffle
+    const uint32_t ends0 = smem0 + 65536 + WARPS * 32 * C + warp * kEndsBytes;
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(ends0 + lane * 4), "r"((uint32_t)(my_end - g0)) : "memory");
+    if (lane == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(ends0 + 128), "r"(total) : "memory");
+    __syncwarp();
 
     // metadata of round k -> buffer k & 3 (lanes 0..C-1: cols, 16..16+C-1: vals)
     auto issue_meta = [&](uint32_t k) {
@@ -727,16 +733,17 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
 
     float4 acc = f4_zero();
     uint32_t row = 0;
-    uint32_t row_end = __shfl_sync(0xffffffffu, rel, 0);
+    uint32_t row_end = lds_u32(ends0);
     auto store_row = [&](uint32_t r) {
-        if (FULL || lane < f4) __stcs(c + (r0 + r) * ldc4 + lane, acc);
+        // row index and stride fit 32 bits (u32 column indices bound n_rows)
+        if (FULL || lane < f4) __stcs(c + (uint64_t)((uint32_t)r0 + r) * (uint32_t)ldc4 + lane, acc);
         acc = f4_zero();
     };
     auto advance_rows = [&](uint32_t pos) {
         do {
             store_row(row);
             ++row;
-            row_end = __shfl_sync(0xffffffffu, rel, min(row, nr - 1));
+            row_end = lds_u32(ends0 + row * 4);
         } while (row < nr && row_end == pos);
     };
     if (row_end == 0) advance_rows(0);
@@ -766,11 +773,16 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
                          : "=f"(v4.x), "=f"(v4.y), "=f"(v4.z), "=f"(v4.w)
                          : "r"(meta0 + (k & 3) * (8 * C) + 4 * C + 16 * b));
             const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+            if (FASTB && row_end > t0 + 4 * b + 4) {  // no row ends in this batch
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int p = 4 * b + u;
-                consume(p, vv[u]);
-                if (t0 + p + 1 == row_end) advance_rows(t0 + p + 1);
+                for (int u = 0; u < 4; ++u) consume(4 * b + u, vv[u]);
+            } else {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int p = 4 * b + u;
+                    consume(p, vv[u]);
+                    if (t0 + p + 1 == row_end) advance_rows(t0 + p + 1);
+                }
             }
             __syncwarp();  // every lane is done reading these holes
             if (b == 0) issue_meta(k + 2);
@@ -785,15 +797,15 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
     }
 }
 
-template <int C, int WARPS>
+template <int C, int WARPS, bool FASTB = true>
 int launch_q8_batch(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, const uint8_t* q,
                     uint64_t ldq, uint32_t f4, float4* c, uint64_t ldc4, const float* lut, cudaStream_t st) {
-    const size_t smem = 256 * 256 + (size_t)WARPS * 32 * C;  // LUT + rings, slot metadata
+    const size_t smem = 256 * 256 + (size_t)WARPS * (32 * C + 144);  // LUT + rings, slot metadata, row ends
     static bool attr_set = false;
     if (!attr_set) {
-        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_q8_batch_kernel<C, WARPS, true>,
+        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_q8_batch_kernel<C, WARPS, true, FASTB>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_q8_batch_kernel<C, WARPS, false>,
+        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_q8_batch_kernel<C, WARPS, false, FASTB>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set = true;
     }
@@ -802,10 +814,10 @@ int launch_q8_batch(const uint64_t* srow, const uint32_t* scol, const float* sva
     const uint64_t groups = (n + gr - 1) / gr;
     const unsigned grid = (unsigned)((groups + WARPS - 1) / WARPS);
     if (f4 == 32)
-        spmm_q8_batch_kernel<C, WARPS, true><<<grid, WARPS * 32, smem, st>>>(srow, scol, sval, n, q, (uint32_t)ldq,
+        spmm_q8_batch_kernel<C, WARPS, true, FASTB><<<grid, WARPS * 32, smem, st>>>(srow, scol, sval, n, q, (uint32_t)ldq,
                                                                               f4, c, ldc4, lut, gr);
     else
-        spmm_q8_batch_kernel<C, WARPS, false><<<grid, WARPS * 32, smem, st>>>(srow, scol, sval, n, q, (uint32_t)ldq,
+        spmm_q8_batch_kernel<C, WARPS, false, FASTB><<<grid, WARPS * 32, smem, st>>>(srow, scol, sval, n, q, (uint32_t)ldq,
                                                                                f4, c, ldc4, lut, gr);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
@@ -1002,6 +1014,8 @@ int aes_dev_spmm_q8(const uint64_t* srow_ptr, const uint32_t* scol, const float*
             case 33: return launch_q8_batch<8, 8>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st);
             case 34: return launch_q8_batch<12, 16>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st);
             case 35: return launch_q8_batch<16, 4>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st);
+            case 36: return launch_q8_batch<16, 16, false>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st);
+            case 37: return launch_q8_batch<12, 16, false>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st);
             default: return launch_q8_batch<16, 16>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st);
         }
     }
