@@ -110,6 +110,9 @@ int sync() {
 }
 
 uint64_t round4(uint64_t x) { return (x + 3) & ~3ull; }
+// u8 code rows are padded to 16 B so the int8 SpMM can gather them with
+// 16-B cp.async (spmm.cu, batch kernel)
+uint64_t round16(uint64_t x) { return (x + 15) & ~15ull; }
 
 // Upload a host row-major rows x cols f32 matrix into a device buffer with
 // ld = round4(cols), pad columns zeroed (the vector kernels read them).
@@ -825,7 +828,7 @@ static int make_qfeat(const float* x, uint64_t rows, uint64_t cols, float lo, fl
     q->x_max = hi;
     q->bits = bits;
     q->u8 = bits <= 8;
-    q->ld = q->u8 ? round4(cols ? cols : 1) : cols;
+    q->ld = q->u8 ? round16(cols ? cols : 1) : cols;
     const size_t esz = q->u8 ? 1 : 2;
     int s = AES_OK;
     if (cudaMallocAsync(&q->codes, rows * q->ld * esz + 16, st) != cudaSuccess) s = fail(AES_ERR_CUDA, "alloc");
@@ -899,7 +902,7 @@ int aes_qfeat_from_codes(const uint16_t* codes, uint64_t rows, uint64_t cols, fl
     int s = AES_OK;
     if (bits <= 8) {
         DBuf<unsigned int> ovf;
-        uint64_t ld = round4(cols ? cols : 1);
+        uint64_t ld = round16(cols ? cols : 1);
         void* c8 = nullptr;
         s = ovf.alloc(1);
         if (!s && cudaMallocAsync(&c8, rows * ld + 16, st) != cudaSuccess) s = fail(AES_ERR_CUDA, "alloc");

@@ -223,7 +223,7 @@ int aes_fmat_load_qfeat(const char* path, aes_qfeat_t* out, double* load_ms) {
     FmatHeader h;
     AES_TRY(read_fmat_header(fh, path, h));
     if (h.dtype != 1) return io_fail("FMAT dtype 1 (u8 codes) expected", path);
-    const uint64_t ld = (h.cols + 3) & ~3ull;
+    const uint64_t ld = (h.cols + 15) & ~15ull;  // 16-B code rows (int8 SpMM batch kernel)
     auto* codes = static_cast<uint8_t*>(capi_alloc(h.rows * ld + 16));
     if (!codes) return fail(AES_ERR_CUDA, "alloc");
     if (ld != h.cols) cudaMemset(codes, 0, h.rows * ld);

@@ -227,6 +227,15 @@ __device__ __forceinline__ uint32_t pin_u32(uint32_t x) {
     asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
     return y;
 }
+// Offset of the dynamic shared-memory window inside the CTA's shared window
+// on sm_100a (1 KB reserved; the SASS of cvta.shared is (CgaCtaId<<24)+0x400).
+constexpr uint32_t kDynSmemOffset = 0x400;
+// LDS at (addr + kDynSmemOffset); not volatile so ptxas may schedule it
+__device__ __forceinline__ float lds_lut(uint32_t addr) {
+    float v;
+    asm("ld.shared.f32 %0, [%1+1024];" : "=f"(v) : "r"(addr));
+    return v;
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
@@ -665,16 +674,26 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
     __syncthreads();
 
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t smem0 = smem_addr(smem_raw);
+    // LUT address of (code, lane) = smem0 + code*256 + lane*4.  The dynamic
+    // window starts at a fixed offset (kDynSmemOffset) above the CTA's
+    // window base (the high byte), so one PRMT builds base_hi | code<<8 |
+    // lane*4 and the offset rides in the LDS immediate: no add per code.
+    // A different layout would silently read wrong entries, so trap on it.
+    if ((smem0 & 0xFFFFFFu) != kDynSmemOffset) __trap();
     // (pinned through asm so ptxas keeps them in registers instead of
     // re-deriving them from %tid in every slot)
-    const uint32_t lane4 = pin_u32(lane * 4);
-    const uint32_t smem0 = smem_addr(smem_raw);
+    const uint32_t lane4 = pin_u32((smem0 & 0xFF000000u) | (lane * 4));
     // ring slot p of this warp: hole warp*C + p; lane reads its 4 codes at
     // rd0 + p*256 and copies its 16 B of batch slot p0 + lane/8 to wr0 + p0*256
     const uint32_t rd0 = pin_u32(smem0 + warp * (C * 256) + 128 + lane * 4);
     const uint32_t wr0 = smem0 + warp * (C * 256) + 128 + (lane >> 3) * 256 + (lane & 7) * 16;
     // slot metadata of ring round k: cols at meta0 + (k&3)*8C, vals 4C later
     const uint32_t meta0 = pin_u32(smem0 + 65536 + warp * (32 * C));
+    // column tile blockIdx.y: codes 128y.., output float4 columns 32y..
+    q += (size_t)blockIdx.y * 128;
+    c += (size_t)blockIdx.y * 32;
+    f4 = min(32u, f4 - blockIdx.y * 32);
     uint32_t nb = 16;  // bytes this lane copies per slot
     if (!FULL) {
         const uint32_t rowb = f4 * 4, j16 = (lane & 7) * 16;
@@ -750,10 +769,10 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
 
     auto consume = [&](int p, float v) {
         const uint32_t r = lds_u32(rd0 + p * 256);
-        const float d0 = *reinterpret_cast<const float*>(smem_raw + __byte_perm(r, lane4, 0x6504u));
-        const float d1 = *reinterpret_cast<const float*>(smem_raw + __byte_perm(r, lane4, 0x6514u));
-        const float d2 = *reinterpret_cast<const float*>(smem_raw + __byte_perm(r, lane4, 0x6524u));
-        const float d3 = *reinterpret_cast<const float*>(smem_raw + __byte_perm(r, lane4, 0x6534u));
+        const float d0 = lds_lut(__byte_perm(r, lane4, 0x7604u));
+        const float d1 = lds_lut(__byte_perm(r, lane4, 0x7614u));
+        const float d2 = lds_lut(__byte_perm(r, lane4, 0x7624u));
+        const float d3 = lds_lut(__byte_perm(r, lane4, 0x7634u));
         acc.x = __fadd_rn(acc.x, __fmul_rn(v, d0));
         acc.y = __fadd_rn(acc.y, __fmul_rn(v, d1));
         acc.z = __fadd_rn(acc.z, __fmul_rn(v, d2));
@@ -809,16 +828,21 @@ int launch_q8_batch(const uint64_t* srow, const uint32_t* scol, const float* sva
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set = true;
     }
+    // 128-code column tiles run side by side as blockIdx.y; rows per warp
+    // shrink until (row groups x tiles) fills >= 64 warps per SM
+    const uint32_t tiles = (f4 + 31) / 32;
     uint32_t gr = 32;
-    while (gr > 2 && (n + gr - 1) / gr < (uint64_t)kNumSMs * 64) gr >>= 1;
+    while (gr > 2 && (n + gr - 1) / gr * tiles < (uint64_t)kNumSMs * 64) gr >>= 1;
     const uint64_t groups = (n + gr - 1) / gr;
-    const unsigned grid = (unsigned)((groups + WARPS - 1) / WARPS);
-    if (f4 == 32)
-        spmm_q8_batch_kernel<C, WARPS, true, FASTB><<<grid, WARPS * 32, smem, st>>>(srow, scol, sval, n, q, (uint32_t)ldq,
-                                                                              f4, c, ldc4, lut, gr);
+    const dim3 grid((unsigned)((groups + WARPS - 1) / WARPS), tiles);
+    if (f4 % 32 == 0)
+        spmm_q8_batch_kernel<C, WARPS, true, FASTB><<<grid, WARPS * 32, smem, st>>>(srow, scol, sval, n, q,
+                                                                                     (uint32_t)ldq, f4, c, ldc4,
+                                                                                     lut, gr);
     else
-        spmm_q8_batch_kernel<C, WARPS, false, FASTB><<<grid, WARPS * 32, smem, st>>>(srow, scol, sval, n, q, (uint32_t)ldq,
-                                                                               f4, c, ldc4, lut, gr);
+        spmm_q8_batch_kernel<C, WARPS, false, FASTB><<<grid, WARPS * 32, smem, st>>>(srow, scol, sval, n, q,
+                                                                                      (uint32_t)ldq, f4, c, ldc4,
+                                                                                      lut, gr);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
 }
@@ -1003,9 +1027,10 @@ int aes_dev_spmm_q8(const uint64_t* srow_ptr, const uint32_t* scol, const float*
             default: return launch_q8_dual<8, 8>(srow_ptr, scol, sval, n_rows, q, ldq, f8, c4, ldc / 4, lut, st);
         }
     }
-    // batch kernel (variants 30-35; the default for 64 < F <= 128 with 16-B
-    // aligned code rows)
-    if ((v == 0 || v >= 30) && f4 > 16 && f4 <= 32 && ldq % 16 == 0 && (uintptr_t)q % 16 == 0) {
+    // batch kernel (variants 30-37; the default for F > 64 with 16-B aligned
+    // code rows).  Wider rows run as 128-code column tiles (grid.y): every
+    // tile re-reads only the 8-B slot metadata next to its 128-B gathers.
+    if ((v == 0 || v >= 30) && f4 > 16 && ldq % 16 == 0 && (uintptr_t)q % 16 == 0 && f4 / 32 < 65535) {
         float4* c4 = reinterpret_cast<float4*>(c);
         const uint32_t f4u = (uint32_t)f4;
         switch (v) {

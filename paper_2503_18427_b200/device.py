@@ -40,7 +40,9 @@ def padded(x: torch.Tensor) -> torch.Tensor:
 
 
 def empty_padded(rows: int, cols: int, dtype=torch.float32, device="cuda") -> torch.Tensor:
-    buf = torch.empty((rows, _round4(max(cols, 1))), dtype=dtype, device=device)
+    """[rows, cols] view of a buffer whose rows are padded to 16 bytes."""
+    per16 = max(1, 16 // torch.empty((), dtype=dtype).element_size())
+    buf = torch.empty((rows, -(-max(cols, 1) // per16) * per16), dtype=dtype, device=device)
     return buf[:, :cols]
 
 

@@ -56,11 +56,14 @@ def test_row_shards_equal_global(dev):
     assert torch.equal(torch.cat(parts), full)
 
 
-def test_device_q8(dev):
+@pytest.mark.parametrize("f", [72, 100, 128, 130, 256, 602])
+def test_device_q8(dev, f):
+    """Device int8 path; F > 64 with 16-B aligned code rows runs the batch
+    kernel (128-code column tiles when F > 128)."""
     import torch
     rp, col, val = graphs.power_law(3000, alpha=1.5, max_deg=2000, seed=2)
     g = dev.Graph.from_numpy(rp, col, val)
-    x_np = np.random.default_rng(2).uniform(-1, 1, (3000, 128)).astype(np.float32)
+    x_np = np.random.default_rng(f).uniform(-1, 1, (3000, f)).astype(np.float32)
     x = torch.from_numpy(x_np).cuda()
     q = dev.quantize(x)
     lo, hi = port.fit_params(x_np)
@@ -72,6 +75,11 @@ def test_device_q8(dev):
     want = port.spmm_sampled(rp, col, val, port.dequantize(codes, lo, hi), 32)
     assert np.array_equal(bits(to_np(out)), bits(want))
     assert np.array_equal(bits(to_np(dev.dequantize(q))), bits(port.dequantize(codes, lo, hi)))
+    # unaligned code rows (ld = f) take the generic ring kernel: same bits
+    qc = dev.QuantizedDevice(q.codes.contiguous(), q.x_min, q.x_max, q.bits, q.lut)
+    if f % 4 == 0:
+        out2 = dev.spmm_q8(plan.srow_ptr, plan.scol, plan.sval, qc)
+        assert np.array_equal(bits(to_np(out2)), bits(want))
 
 
 def test_device_gcn_forward(dev):
