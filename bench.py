@@ -277,9 +277,9 @@ def run_ours(args):
 
     def step():
         if quant is not None:
-            device.spmm_q8(srow, full_plan.scol, full_plan.sval, quant, out=out)
+            device.spmm_q8(srow, full_plan.scol, full_plan.sval, quant, out=out, max_row_slots=full_plan.row_bound)
         else:
-            device.spmm(srow, full_plan.scol, full_plan.sval, b, out=out)
+            device.spmm(srow, full_plan.scol, full_plan.sval, b, out=out, max_row_slots=full_plan.row_bound)
         if layer is not None:
             w, bias, h_next, gathered = layer
             device.gemm_bias_act(out, w, bias, True, out=h_next)
@@ -379,7 +379,8 @@ def run_gcn_layer(args, plan, n, f, b, dist):
     x = b[:, :f]
     out = {}
     for name, fast in (("exact_ordered_fp32", False), ("fast_tcgen05_tf32", True)):
-        model = ShardedGCN(plan.srow_ptr, plan.scol, plan.sval, n, [w], [bias], exchange="p2p", fast_gemm=fast)
+        model = ShardedGCN(plan.srow_ptr, plan.scol, plan.sval, n, [w], [bias], exchange="p2p", fast_gemm=fast,
+                           max_row_slots=plan.row_bound)
         model.input_view().copy_(x)  # features resident in the replica; steps run in place
         x_step = None
         for _ in range(2):

@@ -42,8 +42,11 @@ def lib():
         L.aes_dev_scan_workspace_bytes.argtypes = [u64]
         L.aes_dev_sample_plan.argtypes = [vp, u64, u32, i32, vp, vp, vp, sz, vp]
         L.aes_dev_sample_fill.argtypes = [vp, vp, vp, vp, u64, u32, i32, vp, vp, vp, vp]
+        L.aes_dev_spmm_set_schedule.argtypes = [C.c_int]
         L.aes_dev_spmm_f32.argtypes = [vp, vp, vp, u64, vp, u64, u64, vp, u64, vp]
         L.aes_dev_spmm_q8.argtypes = [vp, vp, vp, u64, vp, u64, u64, vp, vp, u64, vp]
+        L.aes_dev_spmm_f32_ex.argtypes = [vp, vp, vp, u64, vp, u64, u64, vp, u64, u64, vp]
+        L.aes_dev_spmm_q8_ex.argtypes = [vp, vp, vp, u64, vp, u64, u64, vp, vp, u64, u64, vp]
         L.aes_dev_fit_params.argtypes = [vp, u64, vp, vp, sz, vp]
         L.aes_dev_quantize.argtypes = [vp, u64, u64, u64, f32, f32, u32, vp, u64, vp]
         L.aes_dev_dequantize.argtypes = [vp, u64, u64, u64, f32, f32, u32, vp, u64, vp]

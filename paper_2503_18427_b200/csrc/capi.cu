@@ -263,16 +263,23 @@ int validate_device(const aes_csr_s* a, uint64_t row_ptr_len, uint64_t nnz_len, 
     return AES_OK;
 }
 
+// Most slots any row of a plan's sampled CSR can have (0 = unbounded: no
+// plan (exact), FULL plans, host-supplied plans) — picks the ring schedule.
+uint64_t plan_row_bound(const aes_plan_s* p) {
+    if (!p || p->explicit_plan || p->strategy == AES_FULL) return 0;
+    return p->width;
+}
+
 // spmm over a device CSR (original or sampled) with host dense operands.
 int spmm_host(const uint64_t* rp, const uint32_t* col, const float* val, uint64_t n_rows, const float* b,
-              uint64_t b_rows, uint64_t f, float* c) {
+              uint64_t b_rows, uint64_t f, float* c, uint64_t row_bound) {
     if (n_rows == 0 || f == 0) return AES_OK;
     DBuf<float> db, dc;
     uint64_t ldb = 0;
     AES_TRY(upload_dense(b, b_rows, f, db, ldb));
     const uint64_t ldc = ldb;
     AES_TRY(dc.alloc(n_rows * ldc));
-    AES_TRY(aes_dev_spmm_f32(rp, col, val, n_rows, db.p, ldb, f, dc.p, ldc, lib_stream()));
+    AES_TRY(aes_dev_spmm_f32_ex(rp, col, val, n_rows, db.p, ldb, f, dc.p, ldc, row_bound, lib_stream()));
     AES_TRY(download_dense(dc.p, ldc, n_rows, f, c));
     return sync();
 }
@@ -773,7 +780,7 @@ int aes_sampling_rate(aes_plan_t p, aes_csr_t a, double* aggregate, double* uniq
 int aes_spmm_exact(aes_csr_t a, const float* b, uint64_t b_rows, uint64_t f, float* c) {
     if (!a) return fail(AES_ERR_INVALID_ARG, "null csr");
     if (a->n_cols != b_rows) return fail(AES_ERR_SHAPE, "ShapeMismatch");
-    return spmm_host(a->row_ptr, a->col, a->val, a->n_rows, b, b_rows, f, c);
+    return spmm_host(a->row_ptr, a->col, a->val, a->n_rows, b, b_rows, f, c, 0);
 }
 
 int aes_spmm_sampled(aes_csr_t a, const float* b, uint64_t b_rows, uint64_t f, aes_plan_t p, float* c,
@@ -786,7 +793,7 @@ int aes_spmm_sampled(aes_csr_t a, const float* b, uint64_t b_rows, uint64_t f, a
     const uint32_t* scol;
     const float* sval;
     AES_TRY(sampled_for(p, a, tc, tv, &scol, &sval));
-    AES_TRY(spmm_host(p->srow_ptr, scol, sval, a->n_rows, b, b_rows, f, c));
+    AES_TRY(spmm_host(p->srow_ptr, scol, sval, a->n_rows, b, b_rows, f, c, plan_row_bound(p)));
     // WorkCounter semantics (spmm.cpp:95-97): fma = slots*F, loads_a = slots
     if (fma_count) *fma_count = p->total_slots * f;
     if (loads_a) *loads_a = p->total_slots;
@@ -810,7 +817,7 @@ int aes_spmm_sampled_async(aes_csr_t a, const float* b, uint64_t b_rows, uint64_
     AES_CUDA_TRY(cudaMallocAsync((void**)&dc, n * ld * 4 + 16, st));
     if (ld != f) AES_CUDA_TRY(cudaMemsetAsync(db, 0, b_rows * ld * 4, st));
     AES_CUDA_TRY(cudaMemcpy2DAsync(db, ld * 4, b, f * 4, f * 4, b_rows, cudaMemcpyHostToDevice, st));
-    AES_TRY(aes_dev_spmm_f32(p->srow_ptr, p->scol, p->sval, n, db, ld, f, dc, ld, st));
+    AES_TRY(aes_dev_spmm_f32_ex(p->srow_ptr, p->scol, p->sval, n, db, ld, f, dc, ld, plan_row_bound(p), st));
     AES_CUDA_TRY(cudaMemcpy2DAsync(c, f * 4, dc, ld * 4, f * 4, n, cudaMemcpyDeviceToHost, st));
     AES_CUDA_TRY(cudaFreeAsync(db, st));
     AES_CUDA_TRY(cudaFreeAsync(dc, st));
@@ -1010,12 +1017,13 @@ int aes_spmm_sampled_q8(aes_csr_t a, aes_qfeat_t q, aes_plan_t p, float* c) {
     DBuf<float> dc;
     AES_TRY(dc.alloc(n * ldc));
     if (q->u8) {
-        AES_TRY(aes_dev_spmm_q8(rp, scol, sval, n, (const uint8_t*)q->codes, q->ld, f, q->lut, dc.p, ldc, st));
+        AES_TRY(aes_dev_spmm_q8_ex(rp, scol, sval, n, (const uint8_t*)q->codes, q->ld, f, q->lut, dc.p, ldc,
+                                   plan_row_bound(p), st));
     } else {  // 9..16-bit codes: dequantize on the GPU, then the fp32 kernel
         DBuf<float> dx;
         uint64_t ld;
         AES_TRY(dequant_device(q, dx, ld));
-        AES_TRY(aes_dev_spmm_f32(rp, scol, sval, n, dx.p, ld, f, dc.p, ldc, st));
+        AES_TRY(aes_dev_spmm_f32_ex(rp, scol, sval, n, dx.p, ld, f, dc.p, ldc, plan_row_bound(p), st));
     }
     AES_TRY(download_dense(dc.p, ldc, n, f, c));
     return sync();
@@ -1071,12 +1079,12 @@ static int gnn_forward_impl(int kind, aes_csr_t adj, const float* x, const uint6
             DBuf<float> a2;
             const uint64_t ld2 = round4(fin ? fin : 1);
             AES_TRY(a2.alloc(n * ld2));
-            AES_TRY(aes_dev_spmm_f32(rp, scol, sval, n, h.p, ldh, fin, a2.p, ld2, st));
+            AES_TRY(aes_dev_spmm_f32_ex(rp, scol, sval, n, h.p, ldh, fin, a2.p, ld2, plan_row_bound(p), st));
             if (fin)
                 AES_CUDA_TRY(cudaMemcpy2DAsync(agg.p + fin, lda * 4, a2.p, ld2 * 4, fin * 4, n,
                                                cudaMemcpyDeviceToDevice, st));
         } else {
-            AES_TRY(aes_dev_spmm_f32(rp, scol, sval, n, h.p, ldh, fin, agg.p, lda, st));
+            AES_TRY(aes_dev_spmm_f32_ex(rp, scol, sval, n, h.p, ldh, fin, agg.p, lda, plan_row_bound(p), st));
         }
         uint64_t ldw;
         AES_TRY(upload_dense(weights + woff, kin, fout, dw, ldw));

@@ -106,6 +106,11 @@ class SampledPlan:
                                     ptr(self.sval), st))
         del ws
 
+    @property
+    def row_bound(self) -> int:
+        """Most slots any row can have: W for Adaptive/Afs/Sfs, unbounded (0) for FULL."""
+        return 0 if self.strategy == capi.strategy_code("full") else self.width
+
     def algorithmic_bytes(self, f: int, elem_bytes: int = 4) -> int:
         """Bytes one SpMM over this plan must move:
         8(N+1) row offsets + 8S (col, val) + e*F*S gathered + 4*F*N written."""
@@ -113,19 +118,22 @@ class SampledPlan:
         return 8 * (n + 1) + 8 * s + elem_bytes * f * s + 4 * f * n
 
 
-def spmm(srow_ptr, scol, sval, b: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-    """C = A_sampled @ B (bit-exact with the reference spmm_sampled)."""
+def spmm(srow_ptr, scol, sval, b: torch.Tensor, out: torch.Tensor | None = None, stream=None,
+         max_row_slots: int = 0) -> torch.Tensor:
+    """C = A_sampled @ B (bit-exact with the reference spmm_sampled).
+    max_row_slots bounds the slots of any row (0 = unbounded; picks the
+    row-group schedule, see aes_dev_spmm_f32_ex)."""
     n = srow_ptr.numel() - 1
     f = b.shape[1]
     if out is None:
         out = empty_padded(n, f, device=b.device)
-    check(lib().aes_dev_spmm_f32(ptr(srow_ptr), ptr(scol), ptr(sval), n, ptr(b), b.stride(0), f, ptr(out),
-                                 out.stride(0), stream_of(stream)))
+    check(lib().aes_dev_spmm_f32_ex(ptr(srow_ptr), ptr(scol), ptr(sval), n, ptr(b), b.stride(0), f, ptr(out),
+                                    out.stride(0), max_row_slots, stream_of(stream)))
     return out
 
 
 def spmm_plan(plan: SampledPlan, b: torch.Tensor, out=None, stream=None) -> torch.Tensor:
-    return spmm(plan.srow_ptr, plan.scol, plan.sval, b, out, stream)
+    return spmm(plan.srow_ptr, plan.scol, plan.sval, b, out, stream, plan.row_bound)
 
 
 def spmm_exact(g: Graph, b: torch.Tensor, out=None, stream=None) -> torch.Tensor:
@@ -212,14 +220,14 @@ def dequantize(q: QuantizedDevice, stream=None) -> torch.Tensor:
     return out
 
 
-def spmm_q8(srow_ptr, scol, sval, q: QuantizedDevice, out=None, stream=None) -> torch.Tensor:
+def spmm_q8(srow_ptr, scol, sval, q: QuantizedDevice, out=None, stream=None, max_row_slots: int = 0) -> torch.Tensor:
     """spmm(A, dequantize(Q)) with dequantization fused into the u8 gather."""
     n = srow_ptr.numel() - 1
     f = q.codes.shape[1]
     if out is None:
         out = empty_padded(n, f, device=q.codes.device)
-    check(lib().aes_dev_spmm_q8(ptr(srow_ptr), ptr(scol), ptr(sval), n, ptr(q.codes), q.codes.stride(0), f,
-                                ptr(q.lut), ptr(out), out.stride(0), stream_of(stream)))
+    check(lib().aes_dev_spmm_q8_ex(ptr(srow_ptr), ptr(scol), ptr(sval), n, ptr(q.codes), q.codes.stride(0), f,
+                                   ptr(q.lut), ptr(out), out.stride(0), max_row_slots, stream_of(stream)))
     return out
 
 

@@ -65,11 +65,14 @@ class Ops:
     alloc: Callable  # alloc(rows, cols, like) -> tensor (row stride padded as needed)
 
 
-def cuda_ops() -> Ops:
+def cuda_ops(max_row_slots: int = 0) -> Ops:
+    """The CUDA path; max_row_slots bounds the slots per row of the sampled
+    CSR (plan width, 0 = unbounded) and picks the SpMM row-group schedule."""
     from . import device
 
     return Ops(
-        spmm=lambda srow, scol, sval, h, out=None: device.spmm(srow, scol, sval, h, out=out),
+        spmm=lambda srow, scol, sval, h, out=None: device.spmm(srow, scol, sval, h, out=out,
+                                                              max_row_slots=max_row_slots),
         gemm_bias_act=lambda a, w, b, relu, out=None: device.gemm_bias_act(a, w, b, relu, out=out),
         alloc=lambda rows, cols, like: device.empty_padded(rows, cols, device=like.device),
     )
@@ -80,11 +83,12 @@ class ShardedGCN:
 
     def __init__(self, srow_ptr: torch.Tensor, scol: torch.Tensor, sval: torch.Tensor, n_rows: int,
                  weights: Sequence[torch.Tensor], biases: Sequence[torch.Tensor | None], ops: Ops | None = None,
-                 group=None, balance: str = "rows", exchange: str = "nccl", fast_gemm: bool = False):
+                 group=None, balance: str = "rows", exchange: str = "nccl", fast_gemm: bool = False,
+                 max_row_slots: int = 0):
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
-        self.ops = ops or cuda_ops()
+        self.ops = ops or cuda_ops(max_row_slots)
         self.n = n_rows
         self.weights = list(weights)
         self.biases = list(biases)

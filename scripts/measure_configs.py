@@ -75,7 +75,7 @@ def spmm_config(name, widths, dtypes=("f32", "int8"), cpu=True):
                 ms = gpu_ms(lambda: device.spmm_plan(plan, b, out=c))
                 by = plan.algorithmic_bytes(f, 4)
             else:
-                ms = gpu_ms(lambda: device.spmm_q8(plan.srow_ptr, plan.scol, plan.sval, q, out=c))
+                ms = gpu_ms(lambda: device.spmm_q8(plan.srow_ptr, plan.scol, plan.sval, q, out=c, max_row_slots=plan.row_bound))
                 by = plan.algorithmic_bytes(f, 1)
             out["runs"].append({"W": w, "dtype": dt, "slots": plan.total_slots, "spmm_ms": round(ms, 4),
                                 "alg_GBps": round(by / ms / 1e6, 1), "plan_ms": round(plan_ms, 4)})

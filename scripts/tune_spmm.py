@@ -19,6 +19,7 @@ ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--dtypes", default="f32,int8")
 ap.add_argument("--strategy", default="adaptive")
 ap.add_argument("--q8-variants", default=None, help="int8 schedules (default: --variants)")
+ap.add_argument("--sched", type=int, default=0, help="ring row-group schedule (aes_dev_spmm_set_schedule)")
 args = ap.parse_args()
 
 n, alpha, maxdeg, f = synth.SHAPES[args.config]
@@ -26,6 +27,7 @@ rp, col, val = synth.power_law_csr(n, alpha, maxdeg, seed=1, device="cuda")
 g = device.Graph(rp, col, val, n)
 b = synth.features(n, f, seed=5)
 L = capi.lib()
+capi.check(L.aes_dev_spmm_set_schedule(args.sched))
 
 
 def timeit(fn, iters):
@@ -58,7 +60,7 @@ for dt in args.dtypes.split(","):
             fn = lambda: device.spmm_plan(plan, b, out=out)  # noqa: E731
             by = plan.algorithmic_bytes(f, 4)
         else:
-            fn = lambda: device.spmm_q8(plan.srow_ptr, plan.scol, plan.sval, q, out=out)  # noqa: E731
+            fn = lambda: device.spmm_q8(plan.srow_ptr, plan.scol, plan.sval, q, out=out, max_row_slots=plan.row_bound)  # noqa: E731
             by = plan.algorithmic_bytes(f, 1)
         ms = timeit(fn, args.iters)
         fn()

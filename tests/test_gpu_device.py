@@ -198,3 +198,54 @@ def test_every_spmm_schedule_is_bit_exact(dev, variant):
         L.aes_dev_spmm_set_variant(0)
     assert np.array_equal(bits(to_np(out)), bits(port.spmm_sampled(rp, col, val, x_np, 32)))
     assert np.array_equal(bits(to_np(outq)), bits(port.spmm_sampled(rp, col, val, deq, 32)))
+
+
+@pytest.mark.parametrize("sched", [1, 2])
+def test_ring_schedules_bit_exact(dev, sched):
+    """Static and heavy-first dynamic row-group schedules give the oracle's
+    bits, on a graph whose hub rows exceed the heavy threshold (4096 slots)."""
+    import torch
+
+    from paper_2503_18427_b200 import capi
+    L = capi.lib()
+    rp, col, val = graphs.power_law(12000, alpha=1.2, max_deg=9000, seed=3)
+    assert np.diff(rp).max() > 4096
+    g = dev.Graph.from_numpy(rp, col, val)
+    x_np = np.random.default_rng(3).uniform(-1, 1, (12000, 128)).astype(np.float32)
+    x = torch.from_numpy(x_np).cuda()
+    try:
+        capi.check(L.aes_dev_spmm_set_schedule(sched))
+        exact = dev.spmm_exact(g, x)
+        sampled = dev.spmm_plan(dev.SampledPlan(g, 32), x)
+        torch.cuda.synchronize()
+    finally:
+        L.aes_dev_spmm_set_schedule(0)
+    assert np.array_equal(bits(to_np(exact)), bits(port.spmm_csr(rp, col, val, x_np)))
+    assert np.array_equal(bits(to_np(sampled)), bits(port.spmm_sampled(rp, col, val, x_np, 32)))
+
+
+@pytest.mark.parametrize("sched", [1, 2])
+@pytest.mark.parametrize("f", [128, 300])
+def test_q8_schedules_bit_exact(dev, sched, f):
+    """int8 batch kernel under both schedules, exact (unbounded rows) and
+    sampled, single and multi column tile."""
+    import torch
+
+    from paper_2503_18427_b200 import capi
+    L = capi.lib()
+    rp, col, val = graphs.power_law(12000, alpha=1.2, max_deg=9000, seed=4)
+    g = dev.Graph.from_numpy(rp, col, val)
+    x_np = np.random.default_rng(4).uniform(-1, 1, (12000, f)).astype(np.float32)
+    q = dev.quantize(torch.from_numpy(x_np).cuda())
+    lo, hi = port.fit_params(x_np)
+    deq = port.dequantize(port.quantize(x_np, lo, hi), lo, hi)
+    plan = dev.SampledPlan(g, 32)
+    try:
+        capi.check(L.aes_dev_spmm_set_schedule(sched))
+        exact = dev.spmm_q8(g.row_ptr, g.col, g.val, q)
+        sampled = dev.spmm_q8(plan.srow_ptr, plan.scol, plan.sval, q, max_row_slots=plan.row_bound)
+        torch.cuda.synchronize()
+    finally:
+        L.aes_dev_spmm_set_schedule(0)
+    assert np.array_equal(bits(to_np(exact)), bits(port.spmm_csr(rp, col, val, deq)))
+    assert np.array_equal(bits(to_np(sampled)), bits(port.spmm_sampled(rp, col, val, deq, 32)))
