@@ -186,6 +186,30 @@ def gcn_forward(row_ptr, col, val, x, weights, biases, w: int | None, strategy: 
     return h
 
 
+def gcn_forward_int8_exchange(row_ptr, col, val, x, weights, biases, w: int | None,
+                              strategy: int = ADAPTIVE):
+    """The int8-exchange variant of gcn_forward, composed
+    only of reference functions: every hidden layer output H_l (l >= 1) is
+    replaced by dequantize(quantize(H_l, fit_params(H_l, 8))) before the next
+    aggregation (quantize.cpp:11-64, gnn.cpp:66-78); the input x and the
+    final logits stay fp32."""
+    if w is None:
+        srow, scol, sval = (np.ascontiguousarray(row_ptr, np.uint64),
+                            np.ascontiguousarray(col, np.uint32),
+                            np.ascontiguousarray(val, np.float32))
+    else:
+        srow, scol, sval = sample_csr(row_ptr, col, val, w, strategy)
+    h = np.ascontiguousarray(x, np.float32)
+    for l, (wt, bs) in enumerate(zip(weights, biases)):
+        if l > 0:
+            lo, hi = fit_params(h)
+            h = dequantize(quantize(h, lo, hi), lo, hi)
+        agg = spmm_csr(srow, scol, sval, h)
+        h = dense_matmul(agg, wt)
+        h = bias_act(h, bs if (bs is not None and len(bs)) else None, relu=(l + 1 < len(weights)))
+    return h
+
+
 def row_mean_normalize(row_ptr, col, val):
     """proj/src/matrix.cpp:146-158."""
     row_ptr = np.ascontiguousarray(row_ptr, np.uint64)

@@ -169,6 +169,28 @@ def fit_params(x: torch.Tensor, stream=None):
     return float(r[0]), float(r[1])
 
 
+def fit_params_raw(x: torch.Tensor, stream=None) -> torch.Tensor:
+    """fit_params without the host sync: float32 [x_min, x_max, flag, -] on the
+    device, flag (int32 bits) = 1 when a non-finite element was seen."""
+    L = lib()
+    x = x.contiguous()
+    n = x.numel()
+    if n == 0:
+        raise ValueError("EmptyMatrix")
+    ws_bytes = L.aes_dev_scan_workspace_bytes(1)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=x.device)
+    res = torch.empty(4, dtype=torch.float32, device=x.device)
+    check(L.aes_dev_fit_params(ptr(x), n, ptr(res), ptr(ws), ws_bytes, stream_of(stream)))
+    return res
+
+
+def dequant_lut(lo: float, hi: float, bits: int = 8, dev="cuda", stream=None) -> torch.Tensor:
+    """The 256-entry exact dequantization table (quantize.cpp:53-64)."""
+    lut = torch.zeros(256, dtype=torch.float32, device=dev)
+    check(lib().aes_dev_dequant_lut(lo, hi, bits, ptr(lut), stream_of(stream)))
+    return lut
+
+
 def quantize(x: torch.Tensor, bits: int = 8, params=None, stream=None) -> QuantizedDevice:
     """quantize(x, fit_params(x, bits)) — quantize.cpp:23-51, codes kept as u8."""
     if not 1 <= bits <= 8:

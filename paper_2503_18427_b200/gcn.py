@@ -63,6 +63,13 @@ class Ops:
     spmm: Callable
     gemm_bias_act: Callable
     alloc: Callable  # alloc(rows, cols, like) -> tensor (row stride padded as needed)
+    # int8 exchange (exchange_dtype="int8"):
+    #   fit_params(A) -> float32 tensor [lo, hi, flag] (flag: int32 bits, 1 = non-finite)
+    #   quantize(A, lo, hi) -> uint8 codes [rows, cols] (8-bit, quantize.cpp:23-51)
+    #   spmm_q8(srow, scol, sval, codes, lo, hi, out) -> spmm over dequantize(codes)
+    fit_params: Callable | None = None
+    quantize: Callable | None = None
+    spmm_q8: Callable | None = None
 
 
 def cuda_ops(max_row_slots: int = 0) -> Ops:
@@ -75,6 +82,11 @@ def cuda_ops(max_row_slots: int = 0) -> Ops:
                                                               max_row_slots=max_row_slots),
         gemm_bias_act=lambda a, w, b, relu, out=None: device.gemm_bias_act(a, w, b, relu, out=out),
         alloc=lambda rows, cols, like: device.empty_padded(rows, cols, device=like.device),
+        fit_params=device.fit_params_raw,
+        quantize=lambda a, lo, hi: device.quantize(a, 8, params=(lo, hi)).codes,
+        spmm_q8=lambda srow, scol, sval, codes, lo, hi, out=None: device.spmm_q8(
+            srow, scol, sval, device.QuantizedDevice(codes, lo, hi, 8, device.dequant_lut(lo, hi, 8, codes.device)),
+            out=out, max_row_slots=max_row_slots),
     )
 
 
@@ -84,7 +96,7 @@ class ShardedGCN:
     def __init__(self, srow_ptr: torch.Tensor, scol: torch.Tensor, sval: torch.Tensor, n_rows: int,
                  weights: Sequence[torch.Tensor], biases: Sequence[torch.Tensor | None], ops: Ops | None = None,
                  group=None, balance: str = "rows", exchange: str = "nccl", fast_gemm: bool = False,
-                 max_row_slots: int = 0):
+                 max_row_slots: int = 0, exchange_dtype: str = "f32"):
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -98,6 +110,15 @@ class ShardedGCN:
         else:
             self.cuts, self.per = equal_row_cuts(n_rows, self.world)
         self.balance = balance
+        if exchange_dtype not in ("f32", "int8"):
+            raise ValueError("exchange_dtype must be 'f32' or 'int8'")
+        # int8 exchange: hidden layer outputs travel as global-params 8-bit codes
+        # (4x fewer bytes) and the next layer aggregates them
+        # with the fused-dequant SpMM.  Equals the reference composition
+        # dequantize(quantize(H, fit_params(H))) per hidden layer, bit for bit.
+        self.qx = exchange_dtype == "int8"
+        if self.qx and exchange != "nccl":
+            raise ValueError("exchange_dtype='int8' runs over the NCCL exchange")
         lo, hi = self.cuts[self.rank], self.cuts[self.rank + 1]
         self.lo, self.hi = lo, hi
         # shard plan = rows [lo, hi) of the global sampled CSR (absolute offsets)
@@ -125,20 +146,57 @@ class ShardedGCN:
             self.arrivals = [sum(p2p.gemm_ctas(c1 - c0, w.shape[1], fast) for c0, c1 in zip(self.cuts, self.cuts[1:]))
                              for w, fast in zip(weights, self.fast)]
 
+    def _global_params(self, out_rows: torch.Tensor):
+        """fit_params over the whole (row-sharded) H: each rank's first-occurrence
+        (min, max), folded in rank order with the reference's serial rule
+        (quantize.cpp:14-19: replace only on a strict < / >), which equals the
+        serial scan of the concatenated rows."""
+        import numpy as np
+
+        rows = self.hi - self.lo
+        if rows:
+            st = self.ops.fit_params(out_rows[:rows])[:3].reshape(1, 3).to(torch.float32)
+        else:  # empty shard: flag 2
+            st = torch.tensor([[0.0, 0.0, float(np.array([2], np.int32).view(np.float32)[0])]],
+                              device=out_rows.device)
+        if self.world > 1:
+            allt = torch.empty((self.world, 3), dtype=torch.float32, device=st.device)
+            dist.all_gather_into_tensor(allt, st.contiguous(), group=self.group)
+        else:
+            allt = st
+        v = allt.cpu().numpy()
+        flags = v.view(np.int32)[:, 2]
+        lo = hi = None
+        for r in range(v.shape[0]):
+            if flags[r] == 1:
+                raise ValueError("NonFinite")
+            if flags[r] == 2:
+                continue
+            if lo is None:
+                lo, hi = v[r, 0], v[r, 1]
+            else:
+                lo = v[r, 0] if v[r, 0] < lo else lo
+                hi = v[r, 1] if v[r, 1] > hi else hi
+        if lo is None:
+            raise ValueError("EmptyMatrix")
+        return float(lo), float(hi)
+
     def _gather(self, out_rows: torch.Tensor, f: int, like: torch.Tensor) -> torch.Tensor:
         rows = self.hi - self.lo
         if self.world == 1:
             return out_rows[:rows]
         # the send buffer must be exactly `per` rows; padded rows hold zeros
-        send = torch.zeros((self.per, f), dtype=out_rows.dtype, device=out_rows.device)
+        # (u8 code rows are padded to 16 B for the int8 SpMM's 16-B gathers)
+        fw = -(-f // 16) * 16 if out_rows.dtype == torch.uint8 else f
+        send = torch.zeros((self.per, fw), dtype=out_rows.dtype, device=out_rows.device)
         send[:rows].copy_(out_rows[:rows, :f])
-        gathered = torch.empty((self.world * self.per, f), dtype=out_rows.dtype, device=out_rows.device)
+        gathered = torch.empty((self.world * self.per, fw), dtype=out_rows.dtype, device=out_rows.device)
         dist.all_gather_into_tensor(gathered, send, group=self.group)
         if self.balance == "slots":
             parts = [gathered[r * self.per: r * self.per + (c1 - c0)]
                      for r, (c0, c1) in enumerate(zip(self.cuts, self.cuts[1:]))]
-            return torch.cat(parts)
-        return gathered[: self.n]
+            return torch.cat(parts)[:, :f]
+        return gathered[: self.n, :f]
 
     def input_view(self) -> torch.Tensor:
         """The layer-0 replica buffer [n, F0] (p2p exchange): fill it once and
@@ -173,13 +231,26 @@ class ShardedGCN:
             # copy_out=False returns a view of the replica (valid until the next step)
             return self._forward_p2p(x, return_shard, copy_out)
         h = x
+        hq = None  # (codes replica, lo, hi) when the layer input arrived as int8
         rows = self.hi - self.lo
         n_layers = len(self.weights)
         for l, (w, b) in enumerate(zip(self.weights, self.biases)):
-            agg = self.ops.spmm(self.srow, self.scol, self.sval, h, out=self.ops.alloc(max(rows, 1), h.shape[1], h))
+            if hq is None:
+                agg = self.ops.spmm(self.srow, self.scol, self.sval, h,
+                                    out=self.ops.alloc(max(rows, 1), h.shape[1], h))
+            else:
+                codes, lo, hi = hq
+                agg = self.ops.spmm_q8(self.srow, self.scol, self.sval, codes, lo, hi,
+                                       out=self.ops.alloc(max(rows, 1), codes.shape[1], x))
             out = self.ops.gemm_bias_act(agg[:rows] if rows else agg[:0], w, b, relu=l + 1 < n_layers,
-                                         out=self.ops.alloc(max(rows, 1), w.shape[1], h))
+                                         out=self.ops.alloc(max(rows, 1), w.shape[1], x))
             if return_shard and l + 1 == n_layers:
                 return out[:rows]
-            h = self._gather(out, w.shape[1], h)
+            if self.qx and l + 1 < n_layers:
+                lo, hi = self._global_params(out)
+                codes = self.ops.quantize(out[:rows], lo, hi) if rows else \
+                    torch.zeros((0, w.shape[1]), dtype=torch.uint8, device=out.device)
+                hq = (self._gather(codes, w.shape[1], codes), lo, hi)
+            else:
+                h = self._gather(out, w.shape[1], h)
         return h

@@ -249,3 +249,29 @@ def test_q8_schedules_bit_exact(dev, sched, f):
         L.aes_dev_spmm_set_schedule(0)
     assert np.array_equal(bits(to_np(exact)), bits(port.spmm_csr(rp, col, val, deq)))
     assert np.array_equal(bits(to_np(sampled)), bits(port.spmm_sampled(rp, col, val, deq, 32)))
+
+
+@pytest.mark.parametrize("f", [40, 128])
+def test_sharded_gcn_int8_exchange_cuda_ops(dev, f):
+    """ShardedGCN(exchange_dtype="int8") on the CUDA ops (device fit_params,
+    u8 quantize, fused-dequant SpMM over the code replica) equals the
+    reference composition, bit for bit.  (world 2 of the same driver logic:
+    tests/test_cpu_dist.py over gloo.)"""
+    import torch
+
+    from paper_2503_18427_b200.gcn import ShardedGCN
+    rng = np.random.default_rng(f)
+    rp, col, _ = graphs.power_law(5000, alpha=1.7, max_deg=800, seed=f)
+    nrp, ncol, nval = port.gcn_normalize(rp, col, True)
+    x = rng.uniform(-1, 1, (5000, f)).astype(np.float32)
+    ws = [rng.uniform(-0.5, 0.5, s).astype(np.float32) for s in [(f, 128), (128, 128), (128, 10)]]
+    bs = [np.full(128, 0.01, np.float32), np.full(128, -0.01, np.float32), np.zeros(10, np.float32)]
+    g = dev.Graph.from_numpy(nrp, ncol, nval)
+    plan = dev.SampledPlan(g, 32)
+    model = ShardedGCN(plan.srow_ptr, plan.scol, plan.sval, g.n_rows, [torch.from_numpy(w).cuda() for w in ws],
+                       [torch.from_numpy(b).cuda() for b in bs], max_row_slots=plan.row_bound,
+                       exchange_dtype="int8")
+    out = model.forward(torch.from_numpy(x).cuda())
+    torch.cuda.synchronize()
+    want = port.gcn_forward_int8_exchange(nrp, ncol, nval, x, ws, bs, 32)
+    assert np.array_equal(bits(to_np(out)), bits(want))
