@@ -230,16 +230,34 @@ def cpu_baseline(args, rp_np, col_np, val_np, b_np, f):
             "ms": round(t, 3)}
 
 
+def max_over_ranks(x: float, dist) -> float:
+    """MAX over ranks (a device tensor under NCCL, a host one under gloo)."""
+    import torch
+    if not dist:
+        return float(x)
+    on_gpu = dist.get_backend() == "nccl"
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if on_gpu else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ours(args):
     import numpy as np
     import torch
 
     rank, world, local = dist_env()
+    # one GPU per rank; AES_BENCH_BACKEND=gloo (with ranks sharing a device)
+    # is a functional check of the multi-rank path on a one-GPU box only
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("AES_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     from paper_2503_18427_b200 import capi, device, synth
 
@@ -310,10 +328,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     clocks = sampler.stop()
     ms_total = start.elapsed_time(end)
-    t_rank = torch.tensor([ms_total], device="cuda", dtype=torch.float64)
-    if dist:
-        dist.all_reduce(t_rank, op=dist.ReduceOp.MAX)
-    ms_step = float(t_rank.item()) / args.steps
+    ms_step = max_over_ranks(ms_total, dist) / args.steps
     total_bytes = alg_bytes(n, int(srow_host[-1]), f, elem)
     my_bytes = alg_bytes(shard_rows, shard_slots, f, elem)
     value = total_bytes / (ms_step * 1e-3) / 1e9
@@ -395,10 +410,7 @@ def run_gcn_layer(args, plan, n, f, b, dist):
             model.forward(x_step, copy_out=False)
         e.record()
         torch.cuda.synchronize()
-        t = torch.tensor([s.elapsed_time(e) / steps], dtype=torch.float64, device="cuda")
-        if dist:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        out[name + "_ms"] = round(float(t.item()), 4)
+        out[name + "_ms"] = round(max_over_ranks(s.elapsed_time(e) / steps, dist), 4)
         del model
     out["exchange"] = "fused into the GEMM epilogue (P2P stores to every rank's replica + sys-scope arrivals)"
     out["note"] = "exact mode is bit-exact with the reference; fast mode |err| <= 2^-8 sum|a||w| (TF32)"
@@ -456,11 +468,7 @@ def run_e2e(args, rp, col, val, b, lo, hi, f, n, total_bytes, dist, world):
         for i in range(steps):
             fn(i)
         sync()
-        t = (time.perf_counter() - t0) / steps
-        tt = torch.tensor([t], dtype=torch.float64, device="cuda")
-        if dist:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        return float(tt.item())
+        return max_over_ranks((time.perf_counter() - t0) / steps, dist)
 
     steps = max(1, min(args.steps, 10))
     for _ in range(max(1, min(args.warmup, 3))):
