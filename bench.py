@@ -480,7 +480,25 @@ def run_e2e(args, rp, col, val, b, lo, hi, f, n, total_bytes, dist, world):
     t = timed(call_async, steps, torch.cuda.synchronize)
     L.aes_plan_destroy(p)
     L.aes_csr_destroy(h)
+    # the e2e ceiling: the same H2D + D2H bytes as plain pinned copies, both
+    # directions at once (no SpMM) — what PCIe allows per step on this box
+    d_in = torch.empty((n, f), dtype=torch.float32, device="cuda")
+    d_out = torch.empty_like(c_host, device="cuda")
+
+    def copies(i):
+        with torch.cuda.stream(streams[0]):
+            d_in.copy_(b_host, non_blocking=True)
+        with torch.cuda.stream(streams[1]):
+            c_host.copy_(d_out, non_blocking=True)
+
+    copies(0)
+    torch.cuda.synchronize()
+    t_copy = timed(copies, 3, torch.cuda.synchronize)
+    del d_in, d_out
     return {"value": round(total_bytes / t / 1e9, 3), "unit": "GB/s", "ms_per_step": round(t * 1e3, 3),
+            "pcie_ceiling": {"ms_per_step": round(t_copy * 1e3, 3), "frac": round(t_copy / t, 4),
+                             "what": "pinned H2D of the features + D2H of the result, both directions at once, "
+                                     "no compute: the e2e step cannot beat this"},
             "h2d_bytes_per_step": n * f * 4, "d2h_bytes_per_step": (hi - lo) * f * 4,
             "path": "C-ABI aes_spmm_sampled_async on 2 streams, pinned host buffers, steps=%d" % steps,
             "sync_call": {"value": round(total_bytes / t_sync / 1e9, 3), "ms_per_step": round(t_sync * 1e3, 3),

@@ -70,6 +70,12 @@ cudaStream_t lib_stream() {
         if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
             uint64_t thr = ~0ull;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            // and never hand a block still pending on another stream to a new
+            // allocation: that inserts a cross-stream wait, which serialises
+            // callers pipelining aes_spmm_sampled_async over several streams
+            int no = 0;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowOpportunistic, &no);
+            cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
         }
     });
     return s;

@@ -150,11 +150,23 @@ gemm_ordered_kernel(const float* __restrict__ a, uint64_t m, uint64_t k, uint64_
     }
 }
 
+// Spins with a 60 s deadline: a peer that never arrives (a crashed rank, a
+// miscounted arrival) turns into a launch error instead of a hung GPU.
+constexpr unsigned long long kWaitDeadlineNs = 60ull * 1000 * 1000 * 1000;
+
 __global__ void wait_counter_kernel(const unsigned long long* ctr, unsigned long long target) {
-    unsigned long long v;
-    do {
+    unsigned long long v, t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
         asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
-    } while (v < target);
+        if (v >= target) return;
+        __nanosleep(64);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > kWaitDeadlineNs) {
+            printf("aes_dev_wait_counter: %llu of %llu arrivals after 60 s\n", v, target);
+            __trap();
+        }
+    }
 }
 
 // One thread: make this rank's prior work visible system-wide, then bump
