@@ -260,6 +260,7 @@ def run_ours(args):
             dist.init_process_group(backend)
 
     from paper_2503_18427_b200 import capi, device, synth
+    capi.check(capi.lib().aes_dev_spmm_set_schedule(args.sched))
 
     n, alpha, maxdeg, f = SHAPES[args.config]
     rp, col, val = synth.power_law_csr(n, alpha, maxdeg, seed=args.seed, device="cuda")
@@ -517,6 +518,8 @@ def main():
     ap.add_argument("--dtype", default="f32", choices=["f32", "int8"])
     ap.add_argument("--mode", default="spmm", choices=["spmm", "layer"])
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--sched", type=int, default=0,
+                    help="SpMM row schedule (aes_dev_spmm_set_schedule; 0 = library default)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-layer", action="store_true", help="skip the GCN layer (SpMM+GEMM+exchange) timing")

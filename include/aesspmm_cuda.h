@@ -274,9 +274,8 @@ AES_API int aes_dev_spmm_f32(const uint64_t* srow_ptr, const uint32_t* scol, con
                              uint64_t ldc, void* stream);
 /* Same, with a bound on the slots of any one row (0 = unknown).  Sampled
  * plans bound it by their width (Adaptive/Sfs/Afs); exact SpMM and FULL plans
- * do not.  Unbounded rows select the heavy-first dynamic schedule
- * (aes_dev_spmm_set_schedule), which keeps hub rows off the tail
- * (products exact 7.0 -> 5.3 ms). */
+ * do not.  (Kept for callers that know the bound; the default balanced
+ * schedule handles hub rows without it, see aes_dev_spmm_set_schedule.) */
 AES_API int aes_dev_spmm_f32_ex(const uint64_t* srow_ptr, const uint32_t* scol, const float* sval,
                                 uint64_t n_rows, const float* b, uint64_t ldb, uint64_t f, float* c,
                                 uint64_t ldc, uint64_t max_row_slots, void* stream);
@@ -285,12 +284,12 @@ AES_API int aes_dev_spmm_f32_ex(const uint64_t* srow_ptr, const uint32_t* scol, 
  * 1 register-staged batches, 2..8 shared-memory cp.async rings of different
  * depth x warps-per-CTA.  Results are bit-identical for every variant. */
 AES_API int aes_dev_spmm_set_variant(int variant);
-/* Row-group schedule of the ring kernels: 1 = static (warp w takes row
+/* Row-group schedule of the SpMM kernels: 1 = static (warp w takes row
  * group w), 2 = heavy-first dynamic (groups with > 4096 slots first, then
- * the rest, by ticket from one counter), 0 = auto (dynamic unless the caller
- * bounds the slots per row, see aes_dev_spmm_f32_ex).  Results are
- * bit-identical under every schedule (each group is one warp's ordered
- * stream). */
+ * the rest, by ticket from one counter), 3 = balanced persistent (one wave of
+ * resident warps, each owning a contiguous row range with an equal share of
+ * slots + rows), 0 = auto (balanced).  Results are bit-identical under every
+ * schedule (each row group is one warp's ordered stream). */
 AES_API int aes_dev_spmm_set_schedule(int schedule);
 
 /* Int8 variant: Q is u8 codes (ldq bytes per row), lut[256] the exact

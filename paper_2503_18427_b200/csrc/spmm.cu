@@ -21,6 +21,7 @@
 //    bit-identical to the fp32 kernel over dequantize(Q).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -287,21 +288,27 @@ struct RingQ8 {
     }
 };
 
-// One warp, one row group [r0, r0 + group_rows): the ring schedule below.
+// One warp, rows [rb, re) as ONE slot stream: the ring never drains at a
+// row-group boundary.  Row ends (relative to the range's first slot) live in
+// a 32-row window held one per lane; the next window's ends are loaded when
+// the current one is entered, so crossing into it costs a register move.
+// Caller guarantees srow[re] - srow[rb] < 2^31.
 template <class R, int NV, int C, bool FULL>
-__device__ __forceinline__ void ring_group(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
-                                           const float* __restrict__ sval, uint64_t n_rows,
+__device__ __forceinline__ void ring_range(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
+                                           const float* __restrict__ sval,
                                            const typename R::raw_t* __restrict__ gsrc, uint32_t ld, uint32_t f4,
                                            float4* __restrict__ c, uint64_t ldc4, uint32_t ring0,
-                                           uint32_t lut_lane, uint64_t r0, uint32_t group_rows) {
+                                           uint32_t lut_lane, uint64_t rb, uint64_t re) {
     typedef typename R::raw_t raw_t;
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t nr = (uint32_t)min((uint64_t)group_rows, n_rows - r0);
-    const uint64_t g0 = srow[r0];
-    const uint64_t my_end = srow[r0 + 1 + min(lane, nr - 1)];
-    // slot offsets inside a 32-row group fit in 32 bits
-    const uint32_t total = (uint32_t)(__shfl_sync(0xffffffffu, my_end, nr - 1) - g0);
-    const uint32_t rel = (uint32_t)(my_end - g0);
+    const uint64_t g0 = srow[rb];
+    const uint32_t total = (uint32_t)(srow[re] - g0);
+    // end of row w + lane (relative to g0); rows past re read as `total`
+    auto window = [&](uint64_t w) -> uint32_t {
+        return (uint32_t)(srow[min(w + 1 + lane, re)] - g0);
+    };
+    uint32_t rel = window(rb);
+    uint32_t rel_nx = window(rb + 32);
     const uint32_t* gcol = scol + g0;
     const float* gval = sval + g0;
     const char* glb = reinterpret_cast<const char*>(gsrc + lane);
@@ -341,22 +348,28 @@ __device__ __forceinline__ void ring_group(const uint64_t* __restrict__ srow, co
     float4 acc[NV];
 #pragma unroll
     for (int n = 0; n < NV; ++n) acc[n] = f4_zero();
-    float4* crow = c + r0 * ldc4 + lane;
-    uint32_t row = 0;
+    float4* crow = c + lane;
+    uint64_t ra = rb;  // next row to store
+    uint32_t wi = 0;   // its index in the window
     uint32_t row_end = __shfl_sync(0xffffffffu, rel, 0);
-    auto store_row = [&](uint32_t r) {
+    auto store_row = [&]() {
 #pragma unroll
         for (int n = 0; n < NV; ++n) {
-            if (colok[n]) __stcs(crow + (uint64_t)r * ldc4 + 32u * n, acc[n]);
+            if (colok[n]) __stcs(crow + ra * ldc4 + 32u * n, acc[n]);
             acc[n] = f4_zero();
         }
     };
     auto advance_rows = [&](uint32_t pos) {  // rows ending at slot position pos
         do {
-            store_row(row);
-            ++row;
-            row_end = __shfl_sync(0xffffffffu, rel, min(row, nr - 1));
-        } while (row < nr && row_end == pos);
+            store_row();
+            ++ra;
+            if (++wi == 32) {
+                wi = 0;
+                rel = rel_nx;
+                rel_nx = window(ra + 32);
+            }
+            row_end = __shfl_sync(0xffffffffu, rel, wi);
+        } while (ra < re && row_end == pos);
     };
     if (row_end == 0) advance_rows(0);
 
@@ -390,9 +403,21 @@ __device__ __forceinline__ void ring_group(const uint64_t* __restrict__ srow, co
         mc_nx = ld_col(k + 3);
     }
     cp_wait<0>();
-    while (row < nr) {
-        store_row(row);
-        ++row;
+    for (; ra < re; ++ra) store_row();  // trailing empty rows
+}
+
+// Rows [rb, re) in slices whose slot counts fit the stream's 32-bit offsets.
+template <class R, int NV, int C, bool FULL>
+__device__ __forceinline__ void ring_rows(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
+                                          const float* __restrict__ sval,
+                                          const typename R::raw_t* __restrict__ gsrc, uint32_t ld, uint32_t f4,
+                                          float4* __restrict__ c, uint64_t ldc4, uint32_t ring0, uint32_t lut_lane,
+                                          uint64_t rb, uint64_t re) {
+    while (rb < re) {
+        uint64_t e = re;
+        if (srow[re] - srow[rb] >= (1ull << 31)) e = min(rb + 1, re);  // (never at the BASELINE shapes)
+        ring_range<R, NV, C, FULL>(srow, scol, sval, gsrc, ld, f4, c, ldc4, ring0, lut_lane, rb, e);
+        rb = e;
     }
 }
 
@@ -424,7 +449,8 @@ spmm_ring_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__
     // on small graphs keeps every SM busy
     const uint64_t r0 = ((uint64_t)blockIdx.x * WARPS + (threadIdx.x >> 5)) * group_rows;
     if (r0 >= n_rows) return;
-    ring_group<R, NV, C, FULL>(srow, scol, sval, n_rows, gsrc, ld, f4, c, ldc4, ring0, lut_lane, r0, group_rows);
+    ring_rows<R, NV, C, FULL>(srow, scol, sval, gsrc, ld, f4, c, ldc4, ring0, lut_lane, r0,
+                              min(r0 + group_rows, n_rows));
 }
 
 // Heavy-first dynamic schedule for unbounded rows (exact SpMM, FULL plans):
@@ -437,6 +463,9 @@ spmm_ring_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__
 // long groups start early and short ones fill in behind them.  Each group is
 // still one warp's ordered stream: results are unchanged.
 constexpr uint32_t kHeavySlots = 4096;
+constexpr int kSchedStatic = 1, kSchedDyn = 2, kSchedBal = 3;
+constexpr int kSchedBalOne = 4;  // balanced, one wave (rows of unknown length: hub rows stay spread)
+constexpr int kSchedAuto = 5;    // bounded rows, per-kernel choice (see the launchers)
 struct DynSched {
     unsigned int next;     // ticket counter
     unsigned int n_heavy;  // heavy groups listed
@@ -479,10 +508,74 @@ spmm_ring_dyn_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
         nw = __shfl_sync(0xffffffffu, nw, 0);
         const uint64_t g = w < n_heavy ? (uint64_t)ws->heavy[w] : w - n_heavy;
         if (w < n_heavy || !group_is_heavy(srow, n_rows, group_rows, g))
-            ring_group<R, NV, C, FULL>(srow, scol, sval, n_rows, gsrc, ld, f4, c, ldc4, ring0, lut_lane,
-                                       g * group_rows, group_rows);
+            ring_rows<R, NV, C, FULL>(srow, scol, sval, gsrc, ld, f4, c, ldc4, ring0, lut_lane, g * group_rows,
+                                      min(g * group_rows + group_rows, n_rows));
         w = nw;
     }
+}
+
+// ---------------------------------------------------------------------------
+// Balanced persistent schedule (the default): one wave of resident warps,
+// warp w of W owns the contiguous rows whose work key
+//     key(r) = (srow[r] - srow[0]) + kRowCost * r      (slots + per-row cost)
+// falls in [w*K/W, (w+1)*K/W), K = key(n), and walks them in groups of <= 32
+// rows.  Every warp gets the same work whatever the shard size, so there is
+// no partial last wave (a row-sharded products shard at P = 8 is 2.7 waves of
+// 32-row groups under the static schedule) and hub rows are balanced by
+// construction (a warp holding a 17 k-slot row gets few others).  The range
+// ends come from two 16-ary searches over srow, one per half-warp, 5-6
+// dependent loads at kernel start.  Each group is still one warp's ordered
+// stream, so results are unchanged.
+// ---------------------------------------------------------------------------
+constexpr uint64_t kRowCost = 1;  // a row's store + bookkeeping ~ one gathered slot
+
+// First row r in [0, n] with key(r) >= target (key(n) >= target required),
+// searched by the 16 lanes of this half-warp; every lane of the half gets it.
+__device__ __forceinline__ uint64_t bal_lower_bound(const uint64_t* __restrict__ srow, uint64_t n, uint64_t s0,
+                                                    uint64_t target) {
+    const uint32_t lane = threadIdx.x & 31, i = lane & 15;
+    const uint32_t hmask = 0xFFFFu << (lane & 16);
+    uint64_t lo = 0, hi = n;  // answer in [lo, hi]
+    // warp-uniform trip count (the halves may need different numbers of
+    // rounds; a finished half re-probes lo == hi and stays put)
+    while (__any_sync(0xffffffffu, lo < hi)) {
+        const uint64_t step = (hi - lo + 16) / 16;  // ceil((hi - lo + 1) / 16)
+        const uint64_t p = min(lo + (i + 1) * step - 1, hi);
+        const bool ge = (srow[p] - s0) + kRowCost * p >= target;
+        const uint32_t bal = (__ballot_sync(0xffffffffu, ge) & hmask) >> (lane & 16);
+        const uint32_t j = __ffs(bal) - 1;  // bal != 0: probe 15 is hi
+        const uint64_t pj = __shfl_sync(0xffffffffu, p, (lane & 16) + j);
+        const uint64_t pm = __shfl_sync(0xffffffffu, p, (lane & 16) + (j ? j - 1 : 0));
+        lo = j ? pm + 1 : lo;
+        hi = pj;
+    }
+    return lo;
+}
+
+// Rows [rb, re) of global warp gw out of nw.
+__device__ __forceinline__ void bal_range(const uint64_t* __restrict__ srow, uint64_t n_rows, uint64_t gw,
+                                          uint64_t nw, uint64_t& rb, uint64_t& re) {
+    const uint64_t s0 = srow[0];
+    const uint64_t total = (srow[n_rows] - s0) + kRowCost * n_rows;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t k = gw + (lane >> 4);  // lower half: begin, upper half: end
+    // k * total / nw without 64-bit overflow (total < 2^63 / nw in practice)
+    const uint64_t target = k >= nw ? total : (uint64_t)(((unsigned __int128)total * k) / nw);
+    const uint64_t r = bal_lower_bound(srow, n_rows, s0, target);
+    rb = __shfl_sync(0xffffffffu, r, 0);
+    re = __shfl_sync(0xffffffffu, r, 16);
+}
+
+template <class R, int NV, int C, int WARPS, bool FULL>
+__global__ void __launch_bounds__(WARPS * 32)
+spmm_ring_bal_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
+                     const float* __restrict__ sval, uint64_t n_rows, const typename R::raw_t* __restrict__ gsrc,
+                     uint32_t ld, uint32_t f4, float4* __restrict__ c, uint64_t ldc4, const float* __restrict__ lut_g) {
+    uint32_t ring0, lut_lane;
+    ring_setup<R, C, NV, WARPS>(lut_g, ring0, lut_lane);
+    uint64_t rb, re;
+    bal_range(srow, n_rows, (uint64_t)blockIdx.x * WARPS + (threadIdx.x >> 5), (uint64_t)gridDim.x * WARPS, rb, re);
+    ring_rows<R, NV, C, FULL>(srow, scol, sval, gsrc, ld, f4, c, ldc4, ring0, lut_lane, rb, re);
 }
 
 // ---------------------------------------------------------------------------
@@ -734,7 +827,7 @@ int launch_q8_dual(const uint64_t* srow, const uint32_t* scol, const float* sval
 // the per-warp gather rings in the upper 128 B of each entry ("holes"): ring
 // slot p of warp w is hole w*C + p.
 // ---------------------------------------------------------------------------
-template <int C, int WARPS, bool FULL, bool FASTB, bool DYN>
+template <int C, int WARPS, bool FULL, bool FASTB, int SCHED>  // SCHED: 0 static, 1 dynamic, 2 balanced
 __global__ void __launch_bounds__(WARPS * 32, 3)  // 3 x 72 KB of shared memory per SM
 spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
                      const float* __restrict__ sval, uint64_t n_rows, const unsigned char* __restrict__ q,
@@ -777,7 +870,8 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
 
     const uint32_t ends0 = smem0 + 65536 + WARPS * 32 * C + warp * kEndsBytes;
 
-  auto run_group = [&](const uint64_t r0) {
+  // 32-row groups (static / dynamic schedules): one ring fill and drain per group
+  auto run_group32 = [&](const uint64_t r0) {
     const uint32_t nr = (uint32_t)min((uint64_t)group_rows, n_rows - r0);
     const uint64_t g0 = srow[r0];
     const uint64_t my_end = srow[r0 + 1 + min(lane, nr - 1)];
@@ -892,9 +986,139 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
     __syncwarp();  // the next group reuses this warp's ring, metadata and row ends
   };
 
-    if (!DYN) {
+  // rows [rb, re) as one slot stream (srow[re] - srow[rb] < 2^31); row ends
+  // relative to the first slot in a 32-row shared-memory window
+  auto run_range = [&](const uint64_t rb, const uint64_t re) {
+    const uint64_t g0 = srow[rb];
+    const uint32_t total = (uint32_t)(srow[re] - g0);
+    const uint32_t nrows = (uint32_t)(re - rb);  // >= 1
+    const uint64_t* rend = srow + rb + 1;         // end of row rb + i at rend[i]
+    float4* const crow = c + rb * ldc4 + lane;
+    auto window = [&](uint32_t w) -> uint32_t { return (uint32_t)(rend[min(w + lane, nrows - 1)] - g0); };
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(ends0 + lane * 4), "r"(window(0)) : "memory");
+    __syncwarp();
+
+    // metadata of round k -> buffer k & 3 (lanes 0..C-1: cols, 16..16+C-1: vals)
+    auto issue_meta = [&](uint32_t k) {
+        const uint32_t i = lane & 15, s = k * C + i;
+        if (i < (uint32_t)C && s < total) {
+            const void* src = lane < 16 ? (const void*)(scol + g0 + s) : (const void*)(sval + g0 + s);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(meta0 + (k & 3) * (8 * C) +
+                                                                           (lane >> 4) * (4 * C) + i * 4),
+                         "l"(src)
+                         : "memory");
+        }
+    };
+    // gathers for ring positions p0..p0+3 of round k (slots k*C + p0 ..)
+    auto issue = [&](int p0, uint32_t k) {
+        const uint32_t t = k * C + p0 + (lane >> 3);
+        if (t < total && (FULL || nb != 0)) {
+            const uint32_t col = lds_u32(meta0 + (k & 3) * (8 * C) + (p0 + (lane >> 3)) * 4);
+            const unsigned char* src = q + (uint64_t)col * ldq + (lane & 7) * 16;
+            if (FULL)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(wr0 + p0 * 256), "l"(src)
+                             : "memory");
+            else
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(wr0 + p0 * 256), "l"(src),
+                             "r"(nb)
+                             : "memory");
+        }
+    };
+    issue_meta(0);
+    issue_meta(1);
+    cp_commit();
+    cp_wait<0>();
+    __syncwarp();
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+        issue(4 * b, 0);
+        cp_commit();
+    }
+
+    float4 acc = f4_zero();
+    uint32_t ri = 0;  // next row to store (relative to rb)
+    uint32_t wi = 0;  // its index in the window
+    uint32_t row_end = lds_u32(ends0);
+    auto store_row = [&]() {
+        if (FULL || lane < f4) __stcs(crow + (uint64_t)ri * (uint32_t)ldc4, acc);
+        acc = f4_zero();
+    };
+    auto advance_rows = [&](uint32_t pos) {
+        do {
+            store_row();
+            ++ri;
+            if (++wi == 32) {  // enter the next window (its load latency is
+                wi = 0;            // covered by the SM's other warps: issue-bound)
+                const uint32_t e = window(ri);
+                __syncwarp();
+                asm volatile("st.shared.u32 [%0], %1;" ::"r"(ends0 + lane * 4), "r"(e) : "memory");
+                __syncwarp();
+            }
+            row_end = lds_u32(ends0 + wi * 4);
+        } while (ri < nrows && row_end == pos);
+    };
+    if (row_end == 0) advance_rows(0);
+
+    auto consume = [&](int p, float v) {
+        const uint32_t r = lds_u32(rd0 + p * 256);
+        const float d0 = lds_lut(__byte_perm(r, lane4, 0x7604u));
+        const float d1 = lds_lut(__byte_perm(r, lane4, 0x7614u));
+        const float d2 = lds_lut(__byte_perm(r, lane4, 0x7624u));
+        const float d3 = lds_lut(__byte_perm(r, lane4, 0x7634u));
+        acc.x = __fadd_rn(acc.x, __fmul_rn(v, d0));
+        acc.y = __fadd_rn(acc.y, __fmul_rn(v, d1));
+        acc.z = __fadd_rn(acc.z, __fmul_rn(v, d2));
+        acc.w = __fadd_rn(acc.w, __fmul_rn(v, d3));
+    };
+
+    // Every round consumes all C ring positions: positions past `total`
+    // (only in the last round) accumulate garbage into acc AFTER the group's
+    // last row was stored — no row ends there, so nothing of it is written.
+    for (uint32_t k = 0, t0 = 0; t0 < total; t0 += C, ++k) {
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            cp_wait<B - 1>();
+            __syncwarp();  // other lanes' copies of these four slots are visible
+            float4 v4;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(v4.x), "=f"(v4.y), "=f"(v4.z), "=f"(v4.w)
+                         : "r"(meta0 + (k & 3) * (8 * C) + 4 * C + 16 * b));
+            const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+            if (FASTB && row_end > t0 + 4 * b + 4) {  // no row ends in this batch
+#pragma unroll
+                for (int u = 0; u < 4; ++u) consume(4 * b + u, vv[u]);
+            } else {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int p = 4 * b + u;
+                    consume(p, vv[u]);
+                    if (t0 + p + 1 == row_end) advance_rows(t0 + p + 1);
+                }
+            }
+            __syncwarp();  // every lane is done reading these holes
+            if (b == 0) issue_meta(k + 2);
+            issue(4 * b, k + 1);
+            cp_commit();
+        }
+    }
+    cp_wait<0>();
+    for (; ri < nrows; ++ri) store_row();  // (only when the range has no slots)
+    __syncwarp();  // the next range reuses this warp's ring, metadata and row ends
+  };
+
+    if (SCHED == 0) {
         const uint64_t r0 = ((uint64_t)blockIdx.x * WARPS + warp) * group_rows;
-        if (r0 < n_rows) run_group(r0);
+        if (r0 < n_rows) run_group32(r0);
+        return;
+    }
+    if (SCHED == 2) {  // balanced persistent: this warp's slot-balanced row range
+        uint64_t rb, re;
+        bal_range(srow, n_rows, (uint64_t)blockIdx.x * WARPS + warp, (uint64_t)gridDim.x * WARPS, rb, re);
+        while (rb < re) {  // slices with 32-bit slot offsets (one slice at the BASELINE shapes)
+            const uint64_t e = srow[re] - srow[rb] >= (1ull << 31) ? rb + 1 : re;
+            run_range(rb, e);
+            rb = e;
+        }
         return;
     }
     // heavy-first tickets (see spmm_ring_dyn_kernel), one counter per column tile
@@ -909,24 +1133,48 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
         if (lane == 0) nw = atomicAdd(next, 1u);
         nw = __shfl_sync(0xffffffffu, nw, 0);
         const uint64_t g = w < n_heavy ? (uint64_t)ws->heavy[w] : w - n_heavy;
-        if (w < n_heavy || !group_is_heavy(srow, n_rows, group_rows, g)) run_group(g * group_rows);
+        if (w < n_heavy || !group_is_heavy(srow, n_rows, group_rows, g)) run_group32(g * group_rows);
         w = nw;
     }
+}
+
+// Balanced schedule: `waves` x resident CTAs, every warp one equal-work row
+// range.  Measured on B200 (scripts/shard_scaling.py, products W=32):
+//  * fp32 ring: one wave is 8 % slower than the static grid on the full graph
+//    (1.28 vs 1.18 ms: with every warp far apart the C-row writes and the
+//    metadata streams lose their locality); ~20-row ranges in successive
+//    waves keep the active rows contiguous and match it (1.18 ms), while at
+//    P = 8 the shards still end in whole waves (0.169 vs 0.177 ms);
+//  * int8 batch kernel: one wave is best (each extra wave re-fills the 64 KB
+//    LUT per CTA): 0.59 ms full graph, 0.095 vs 0.107 ms at P = 8.
+// AES_SPMM_BAL_WAVES overrides the count (tuning only).
+uint32_t bal_waves(uint64_t n_rows, uint64_t resident_warps, uint64_t rows_per_range) {
+    static int env = -1;
+    if (env < 0) {
+        const char* e = getenv("AES_SPMM_BAL_WAVES");
+        env = e ? atoi(e) : 0;
+    }
+    if (env > 0) return (uint32_t)env;
+    if (rows_per_range == 0 || resident_warps == 0) return 1;
+    const uint64_t w = n_rows / (resident_warps * rows_per_range);
+    return (uint32_t)(w < 1 ? 1 : w > 64 ? 64 : w);
 }
 
 template <int C, int WARPS, bool FULL, bool FASTB>
 int launch_q8_batch_t(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, const uint8_t* q,
                       uint64_t ldq, uint32_t f4, float4* c, uint64_t ldc4, const float* lut, cudaStream_t st,
-                      bool dyn) {
+                      int dyn) {
     const size_t smem = 256 * 256 + (size_t)WARPS * (32 * C + 144);  // LUT + rings, slot metadata, row ends
     static int occ = 0;
     if (occ == 0) {
-        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, false>,
+        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 0>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, true>,
+        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 1>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         AES_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &occ, spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, true>, WARPS * 32, smem));
+            &occ, spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 1>, WARPS * 32, smem));
+        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 2>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         if (occ < 1) occ = 1;
     }
     // 128-code column tiles run side by side as blockIdx.y; rows per warp
@@ -936,7 +1184,21 @@ int launch_q8_batch_t(const uint64_t* srow, const uint32_t* scol, const float* s
     while (gr > 2 && (n + gr - 1) / gr * tiles < (uint64_t)kNumSMs * 64) gr >>= 1;
     const uint64_t groups = (n + gr - 1) / gr;
     const unsigned gx = (unsigned)((groups + WARPS - 1) / WARPS);
-    if (dyn && groups < (1ull << 31)) {
+    // auto: the 32-row-group grid when it runs >= 4 waves (0.56 ms on the
+    // full products graph, vs 0.59-0.60 balanced), the balanced wave when it
+    // would end in a partial wave (row shards: P = 8 0.107 -> 0.095 ms)
+    if (dyn == kSchedAuto) dyn = gx * tiles >= 4ull * kNumSMs * occ ? kSchedStatic : kSchedBal;
+    if (dyn == kSchedBal || dyn == kSchedBalOne) {  // one wave of resident CTAs per column tile
+        // whole waves: the tiles share the resident CTA slots (rounding up
+        // would leave one CTA for a second, nearly empty wave)
+        const uint64_t per_wave = (uint64_t)kNumSMs * occ / tiles;
+        const uint64_t per_tile = (per_wave ? per_wave : 1) * bal_waves(n, per_wave * WARPS, 0);
+        spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 2><<<dim3((unsigned)per_tile, tiles), WARPS * 32, smem, st>>>(
+            srow, scol, sval, n, q, (uint32_t)ldq, f4, c, ldc4, lut, 32, 0, nullptr);
+        AES_CUDA_TRY(cudaGetLastError());
+        return AES_OK;
+    }
+    if (dyn == kSchedDyn && groups < (1ull << 31)) {
         DynSched* ws = nullptr;
         const size_t ws_bytes = sizeof(DynSched) + (groups + tiles) * sizeof(unsigned int);
         AES_CUDA_TRY(cudaMallocAsync((void**)&ws, ws_bytes, st));
@@ -945,13 +1207,13 @@ int launch_q8_batch_t(const uint64_t* srow, const uint32_t* scol, const float* s
         heavy_scan_kernel<<<grid_for(groups, 256, kNumSMs * 8), 256, 0, st>>>(srow, n, gr, groups, ws);
         const uint64_t per_tile = ((uint64_t)kNumSMs * occ + tiles - 1) / tiles;
         const dim3 grid((unsigned)(gx < per_tile ? gx : per_tile), tiles);
-        spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, true><<<grid, WARPS * 32, smem, st>>>(
+        spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 1><<<grid, WARPS * 32, smem, st>>>(
             srow, scol, sval, n, q, (uint32_t)ldq, f4, c, ldc4, lut, gr, groups, ws);
         AES_CUDA_TRY(cudaGetLastError());
         AES_CUDA_TRY(cudaFreeAsync(ws, st));
         return AES_OK;
     }
-    spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, false><<<dim3(gx, tiles), WARPS * 32, smem, st>>>(
+    spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 0><<<dim3(gx, tiles), WARPS * 32, smem, st>>>(
         srow, scol, sval, n, q, (uint32_t)ldq, f4, c, ldc4, lut, gr, groups, nullptr);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
@@ -960,7 +1222,7 @@ int launch_q8_batch_t(const uint64_t* srow, const uint32_t* scol, const float* s
 template <int C, int WARPS, bool FASTB = true>
 int launch_q8_batch(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, const uint8_t* q,
                     uint64_t ldq, uint32_t f4, float4* c, uint64_t ldc4, const float* lut, cudaStream_t st,
-                    bool dyn) {
+                    int dyn) {
     if (f4 % 32 == 0)
         return launch_q8_batch_t<C, WARPS, true, FASTB>(srow, scol, sval, n, q, ldq, f4, c, ldc4, lut, st, dyn);
     return launch_q8_batch_t<C, WARPS, false, FASTB>(srow, scol, sval, n, q, ldq, f4, c, ldc4, lut, st, dyn);
@@ -970,14 +1232,17 @@ int launch_q8_batch(const uint64_t* srow, const uint32_t* scol, const float* sva
 // dispatch
 // ---------------------------------------------------------------------------
 int g_spmm_variant = 0;          // 0 = auto; see aes_dev_spmm_set_variant
-int g_spmm_sched = 0;            // ring schedule: 0 auto, 1 static, 2 heavy-first dynamic
-// auto: the dynamic schedule when a 32-row group may exceed kHeavySlots
-// (max_row_slots unknown (0) or > kHeavySlots / 32: exact SpMM, FULL plans,
-// wide windows); the static one for bounded sampled plans, where it is 2.5 %
-// faster (no pre-pass, no tickets; products W=32 1.18 vs 1.21 ms)
-bool use_dynamic(uint64_t max_row_slots) {
-    if (g_spmm_sched != 0) return g_spmm_sched == 2;
-    return max_row_slots == 0 || max_row_slots * 32 > kHeavySlots;
+int g_spmm_sched = 0;            // row schedule: 0 auto, kSched* otherwise
+// auto: the balanced persistent schedule for every plan.  Measured on B200
+// (scripts/shard_scaling.py): it matches the static one on the full products
+// graph and removes the partial last wave on row shards; on unbounded rows
+// (exact SpMM, FULL plans) it also replaces the heavy-first dynamic schedule
+// (no pre-pass, no workspace allocation, no tickets).
+int pick_schedule(uint64_t max_row_slots) {
+    if (g_spmm_sched != 0) return g_spmm_sched;
+    // bounded rows: per-kernel choice; unknown row lengths: one balanced wave
+    // (a hub row lands in a range of its own weight, no heavy-first pre-pass)
+    return max_row_slots != 0 && max_row_slots <= 256 ? kSchedAuto : kSchedBalOne;
 }
 // Measured on B200 (scripts/tune_spmm.py, products W=32): fp32 best with a
 // 16-slot ring x 4 warps (1.18 ms); int8 with the batch kernel, 16-slot ring
@@ -991,18 +1256,28 @@ template <> struct RingOf<GatherQ8> { typedef RingQ8 type; };
 
 template <class G, int NV, int C, int W, bool FULL>
 int launch_ring_t(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, G g, uint32_t f4,
-                  float4* c, uint64_t ldc4, const float* lut, cudaStream_t st, bool dyn) {
+                  float4* c, uint64_t ldc4, const float* lut, cudaStream_t st, int dyn) {
     typedef typename RingOf<G>::type R;
     const size_t smem = (size_t)R::kLutBytes + (size_t)W * C * NV * 32 * R::kBytes;
-    static int occ = 0;  // per template instance: resident blocks per SM of the dynamic kernel
+    static int occ = 0;  // per template instance: resident blocks per SM (balanced / dynamic kernels)
     if (occ == 0) {
         AES_CUDA_TRY(cudaFuncSetAttribute(spmm_ring_kernel<R, NV, C, W, FULL>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         AES_CUDA_TRY(cudaFuncSetAttribute(spmm_ring_dyn_kernel<R, NV, C, W, FULL>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        AES_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmm_ring_dyn_kernel<R, NV, C, W, FULL>,
+        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_ring_bal_kernel<R, NV, C, W, FULL>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        AES_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmm_ring_bal_kernel<R, NV, C, W, FULL>,
                                                                    W * 32, smem));
         if (occ < 1) occ = 1;
+    }
+    if (dyn == kSchedAuto) dyn = kSchedBal;  // fp32 ring: balanced waves at every size (1.17 vs 1.18 ms full graph)
+    if (dyn == kSchedBal || dyn == kSchedBalOne) {  // waves of resident CTAs, slot-balanced row ranges
+        const uint64_t waves = dyn == kSchedBalOne ? 1 : bal_waves(n, (uint64_t)kNumSMs * occ * W, 20);
+        spmm_ring_bal_kernel<R, NV, C, W, FULL><<<(unsigned)(waves * kNumSMs * occ), W * 32, smem, st>>>(
+            srow, scol, sval, n, g.base(), (uint32_t)g.ld4, f4, c, ldc4, lut);
+        AES_CUDA_TRY(cudaGetLastError());
+        return AES_OK;
     }
     // rows per warp: 32 when the graph fills >= 8 warps per SM slot at that
     // size, otherwise shrink (power of 2, >= 2) so the grid still covers the GPU
@@ -1010,7 +1285,7 @@ int launch_ring_t(const uint64_t* srow, const uint32_t* scol, const float* sval,
     while (gr > 2 && (n + gr - 1) / gr < (uint64_t)kNumSMs * 64) gr >>= 1;
     const uint64_t groups = (n + gr - 1) / gr;
     const unsigned grid = (unsigned)((groups + W - 1) / W);
-    if (dyn && groups < (1ull << 31)) {
+    if (dyn == kSchedDyn && groups < (1ull << 31)) {
         DynSched* ws = nullptr;
         AES_CUDA_TRY(cudaMallocAsync((void**)&ws, sizeof(DynSched) + groups * sizeof(unsigned int), st));
         AES_CUDA_TRY(cudaMemsetAsync(ws, 0, 16, st));
@@ -1030,14 +1305,14 @@ int launch_ring_t(const uint64_t* srow, const uint32_t* scol, const float* sval,
 
 template <class G, int NV, int C, int W>
 int launch_ring(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, G g, uint32_t f4,
-                float4* c, uint64_t ldc4, const float* lut, cudaStream_t st, bool dyn) {
+                float4* c, uint64_t ldc4, const float* lut, cudaStream_t st, int dyn) {
     if (f4 == 32u * NV) return launch_ring_t<G, NV, C, W, true>(srow, scol, sval, n, g, f4, c, ldc4, lut, st, dyn);
     return launch_ring_t<G, NV, C, W, false>(srow, scol, sval, n, g, f4, c, ldc4, lut, st, dyn);
 }
 
 template <class G>
 int launch_vector(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n,
-                  G g, uint32_t f4, float4* c, uint64_t ldc4, const float* lut, cudaStream_t st, bool dyn) {
+                  G g, uint32_t f4, float4* c, uint64_t ldc4, const float* lut, cudaStream_t st, int dyn) {
     const size_t smem = lut ? 256 * 32 * sizeof(float) : 0;
     if (f4 <= 16) {
         uint32_t lpr = f4 <= 1 ? 1 : f4 <= 2 ? 2 : f4 <= 4 ? 4 : f4 <= 8 ? 8 : 16;
@@ -1124,7 +1399,7 @@ int aes_dev_spmm_set_variant(int variant) {
 }
 
 int aes_dev_spmm_set_schedule(int schedule) {
-    if (schedule < 0 || schedule > 2) return aes::fail(AES_ERR_INVALID_ARG, "schedule must be 0, 1 or 2");
+    if (schedule < 0 || schedule > 3) return aes::fail(AES_ERR_INVALID_ARG, "schedule must be 0, 1, 2 or 3");
     aes::g_spmm_sched = schedule;
     return AES_OK;
 }
@@ -1139,7 +1414,7 @@ int aes_dev_spmm_f32_ex(const uint64_t* srow_ptr, const uint32_t* scol, const fl
                         uint64_t n_rows, const float* b, uint64_t ldb, uint64_t f, float* c,
                         uint64_t ldc, uint64_t max_row_slots, void* stream) {
     using namespace aes;
-    const bool dyn = use_dynamic(max_row_slots);
+    const int dyn = pick_schedule(max_row_slots);
     cudaStream_t st = as_stream(stream);
     if (n_rows == 0 || f == 0) return AES_OK;
     if (ldb < f || ldc < f) return fail(AES_ERR_INVALID_ARG, "leading dimension smaller than f");
@@ -1167,7 +1442,7 @@ int aes_dev_spmm_q8_ex(const uint64_t* srow_ptr, const uint32_t* scol, const flo
                        uint64_t n_rows, const uint8_t* q, uint64_t ldq, uint64_t f, const float* lut,
                        float* c, uint64_t ldc, uint64_t max_row_slots, void* stream) {
     using namespace aes;
-    const bool dyn = use_dynamic(max_row_slots);
+    const int dyn = pick_schedule(max_row_slots);
     cudaStream_t st = as_stream(stream);
     if (n_rows == 0 || f == 0) return AES_OK;
     const uint64_t f4 = (f + 3) / 4;

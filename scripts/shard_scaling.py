@@ -38,7 +38,15 @@ def time_ms(fn, reps=20):
 
 
 def main():
-    config = sys.argv[1] if len(sys.argv) > 1 else "products"
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("config", nargs="?", default="products")
+    ap.add_argument("--sched", type=int, default=0, help="aes_dev_spmm_set_schedule: 0 auto, 1 static, 2 dynamic")
+    args = ap.parse_args()
+    config = args.config
+    from paper_2503_18427_b200 import capi
+    capi.check(capi.lib().aes_dev_spmm_set_schedule(args.sched))
     n, alpha, maxdeg, f = SHAPES[config]
     rp, col, val = synth.power_law_csr(n, alpha, maxdeg, seed=1, device="cuda")
     g = device.Graph(rp, col, val, n)
@@ -72,7 +80,7 @@ def main():
         for r in rows:
             r["efficiency"] = round(r["value_gbs"] / (base * r["P"]), 4)
         res[dtype] = rows
-    print(json.dumps({"config": config, "slots": total_slots, "scaling": res}))
+    print(json.dumps({"config": config, "sched": args.sched, "slots": total_slots, "scaling": res}))
 
 
 if __name__ == "__main__":
