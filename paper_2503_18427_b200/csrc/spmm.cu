@@ -32,15 +32,24 @@ constexpr int kThreads = 256;
 
 __device__ __forceinline__ float4 f4_zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
 
-// acc += v * b with separate IEEE roundings (FMUL then FADD).  Note: ptxas
-// 12.9 fuses packed mul.rn.f32x2 + add.rn.f32x2 (even via inline PTX or
-// -fmad=false) into FFMA2, which would change the result bits, so the packed
-// FP32x2 pipe is not used here; tests/test_sass.py guards the SASS.
+// acc += v * b with separate IEEE roundings (FMUL then FADD).  ptxas 12.9
+// fuses a packed mul.rn.f32x2 feeding add.rn.f32x2 into FFMA2 (even via
+// inline PTX, in one asm block, or with -fmad=false), which would change the
+// result bits; it leaves scalar FMULs feeding one FADD2 alone.  So the adds
+// go out in pairs, (a0, a1) = (RN(a0 + p0), RN(a1 + p1)) as one FADD2
+// (add.rn.f32x2 is two independent IEEE adds), and the products stay scalar:
+// 3 instructions per 2 elements instead of 4.  tests/test_cpu_boundary.py
+// greps the SASS of every SpMM / GEMM kernel for FFMA/FFMA2.
+__device__ __forceinline__ void add2_rn(float& a0, float& a1, float p0, float p1) {
+    unsigned long long a, p;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(a0), "f"(a1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(p) : "f"(p0), "f"(p1));
+    asm("add.rn.f32x2 %0, %0, %1;" : "+l"(a) : "l"(p));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(a));
+}
 __device__ __forceinline__ void f4_axpy(float4& acc, float v, const float4& b) {
-    acc.x = __fadd_rn(acc.x, __fmul_rn(v, b.x));
-    acc.y = __fadd_rn(acc.y, __fmul_rn(v, b.y));
-    acc.z = __fadd_rn(acc.z, __fmul_rn(v, b.z));
-    acc.w = __fadd_rn(acc.w, __fmul_rn(v, b.w));
+    add2_rn(acc.x, acc.y, __fmul_rn(v, b.x), __fmul_rn(v, b.y));
+    add2_rn(acc.z, acc.w, __fmul_rn(v, b.z), __fmul_rn(v, b.w));
 }
 
 __device__ __forceinline__ uint32_t ld_meta_u32(const uint32_t* p) { return __ldcs(p); }
@@ -942,10 +951,8 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
         const float d1 = lds_lut(__byte_perm(r, lane4, 0x7614u));
         const float d2 = lds_lut(__byte_perm(r, lane4, 0x7624u));
         const float d3 = lds_lut(__byte_perm(r, lane4, 0x7634u));
-        acc.x = __fadd_rn(acc.x, __fmul_rn(v, d0));
-        acc.y = __fadd_rn(acc.y, __fmul_rn(v, d1));
-        acc.z = __fadd_rn(acc.z, __fmul_rn(v, d2));
-        acc.w = __fadd_rn(acc.w, __fmul_rn(v, d3));
+        add2_rn(acc.x, acc.y, __fmul_rn(v, d0), __fmul_rn(v, d1));
+        add2_rn(acc.z, acc.w, __fmul_rn(v, d2), __fmul_rn(v, d3));
     };
 
     // Every round consumes all C ring positions: positions past `total`
@@ -1065,10 +1072,8 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
         const float d1 = lds_lut(__byte_perm(r, lane4, 0x7614u));
         const float d2 = lds_lut(__byte_perm(r, lane4, 0x7624u));
         const float d3 = lds_lut(__byte_perm(r, lane4, 0x7634u));
-        acc.x = __fadd_rn(acc.x, __fmul_rn(v, d0));
-        acc.y = __fadd_rn(acc.y, __fmul_rn(v, d1));
-        acc.z = __fadd_rn(acc.z, __fmul_rn(v, d2));
-        acc.w = __fadd_rn(acc.w, __fmul_rn(v, d3));
+        add2_rn(acc.x, acc.y, __fmul_rn(v, d0), __fmul_rn(v, d1));
+        add2_rn(acc.z, acc.w, __fmul_rn(v, d2), __fmul_rn(v, d3));
     };
 
     // Every round consumes all C ring positions: positions past `total`
