@@ -14,10 +14,13 @@ timeout 300 ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum 
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_all.csv \
     python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-layer > /dev/null 2>&1
 for dt in f32 int8; do
-  timeout 600 ncu --set full --clock-control none --import-source on -k "regex:spmm_ring|spmm_q8_batch" -s 2 -c 1 -o gpurun_out/prof_spmm_$dt -f \
+  timeout 600 ncu --set full --clock-control none --import-source on -k "regex:spmm_ring|spmm_q8_batch" -s 2 -c 1 -o /tmp/prof_spmm_$dt -f \
       python bench.py --steps 2 --warmup 2 --dtype $dt --no-e2e --no-cpu-baseline --no-layer > gpurun_out/ncu_$dt.log 2>&1; tail -1 gpurun_out/ncu_$dt.log
 done
-python scripts/ncu_summary.py gpurun_out/prof_spmm_f32.ncu-rep gpurun_out/prof_spmm_int8.ncu-rep > gpurun_out/ncu_full_summary.json
+python scripts/shard_scaling.py products > gpurun_out/shard_scaling_products.json
+python scripts/shard_scaling.py reddit > gpurun_out/shard_scaling_reddit.json
+python scripts/measure_pcie.py > gpurun_out/pcie.json
+python scripts/ncu_summary.py /tmp/prof_spmm_f32.ncu-rep /tmp/prof_spmm_int8.ncu-rep > gpurun_out/ncu_full_summary.json
 python scripts/launch_summary.py gpurun_out/launches_timed.csv > gpurun_out/launches_timed_summary.json
 python scripts/launch_summary.py gpurun_out/launches_all.csv > gpurun_out/launches_all_summary.json
-ls gpurun_out
+ls -la gpurun_out
