@@ -97,6 +97,20 @@ __host__ __device__ __forceinline__ uint32_t row_start(uint64_t nnz, uint32_t w,
 }
 
 // ---------------------------------------------------------------------------
+// (a0, a1) = (RN(a0 + p0), RN(a1 + p1)) as one FADD2: add.rn.f32x2 is two
+// independent IEEE round-to-nearest adds.  Feed it scalar FMULs only — ptxas
+// 12.9 contracts a packed mul.rn.f32x2 feeding add.rn.f32x2 into FFMA2 (one
+// rounding), which would change the result bits (see spmm.cu).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void add2_rn(float& a0, float& a1, float p0, float p1) {
+    unsigned long long a, p;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(a0), "f"(a1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(p) : "f"(p0), "f"(p1));
+    asm("add.rn.f32x2 %0, %0, %1;" : "+l"(a) : "l"(p));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(a));
+}
+
+// ---------------------------------------------------------------------------
 // Launch geometry
 // ---------------------------------------------------------------------------
 constexpr int kNumSMs = 148;

@@ -40,13 +40,6 @@ __device__ __forceinline__ float4 f4_zero() { return make_float4(0.f, 0.f, 0.f, 
 // (add.rn.f32x2 is two independent IEEE adds), and the products stay scalar:
 // 3 instructions per 2 elements instead of 4.  tests/test_cpu_boundary.py
 // greps the SASS of every SpMM / GEMM kernel for FFMA/FFMA2.
-__device__ __forceinline__ void add2_rn(float& a0, float& a1, float p0, float p1) {
-    unsigned long long a, p;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(a0), "f"(a1));
-    asm("mov.b64 %0, {%1, %2};" : "=l"(p) : "f"(p0), "f"(p1));
-    asm("add.rn.f32x2 %0, %0, %1;" : "+l"(a) : "l"(p));
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(a));
-}
 __device__ __forceinline__ void f4_axpy(float4& acc, float v, const float4& b) {
     add2_rn(acc.x, acc.y, __fmul_rn(v, b.x), __fmul_rn(v, b.y));
     add2_rn(acc.z, acc.w, __fmul_rn(v, b.z), __fmul_rn(v, b.w));
