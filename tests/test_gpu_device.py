@@ -200,10 +200,11 @@ def test_every_spmm_schedule_is_bit_exact(dev, variant):
     assert np.array_equal(bits(to_np(outq)), bits(port.spmm_sampled(rp, col, val, deq, 32)))
 
 
-@pytest.mark.parametrize("sched", [1, 2])
+@pytest.mark.parametrize("sched", [0, 1, 2, 3])
 def test_ring_schedules_bit_exact(dev, sched):
-    """Static and heavy-first dynamic row-group schedules give the oracle's
-    bits, on a graph whose hub rows exceed the heavy threshold (4096 slots)."""
+    """Auto, static, heavy-first dynamic and balanced row schedules give the
+    oracle's bits, on a graph whose hub rows exceed the heavy threshold (4096
+    slots)."""
     import torch
 
     from paper_2503_18427_b200 import capi
@@ -224,10 +225,10 @@ def test_ring_schedules_bit_exact(dev, sched):
     assert np.array_equal(bits(to_np(sampled)), bits(port.spmm_sampled(rp, col, val, x_np, 32)))
 
 
-@pytest.mark.parametrize("sched", [1, 2])
+@pytest.mark.parametrize("sched", [0, 1, 2, 3])
 @pytest.mark.parametrize("f", [128, 300])
 def test_q8_schedules_bit_exact(dev, sched, f):
-    """int8 batch kernel under both schedules, exact (unbounded rows) and
+    """int8 batch kernel under every schedule, exact (unbounded rows) and
     sampled, single and multi column tile."""
     import torch
 
@@ -275,3 +276,73 @@ def test_sharded_gcn_int8_exchange_cuda_ops(dev, f):
     torch.cuda.synchronize()
     want = port.gcn_forward_int8_exchange(nrp, ncol, nval, x, ws, bs, 32)
     assert np.array_equal(bits(to_np(out)), bits(want))
+
+
+def _edge_graphs():
+    """(name, row_ptr, col, val): shapes that stress the balanced schedule's
+    row ranges and 32-row end windows."""
+    rng = np.random.default_rng(11)
+    out = []
+    # fewer rows than warps in a wave: most warps get empty ranges
+    rp, col, val = graphs.power_law(5, alpha=1.5, max_deg=5, seed=1)
+    out.append(("tiny", rp, col, val))
+    # long runs of empty rows (crossing several 32-row windows) around a hub row
+    n = 3000
+    deg = rng.integers(1, 40, n)
+    deg[100:400] = 0
+    deg[1000:1041] = 0
+    deg[2999] = 0
+    deg[1500] = 2900
+    rows = [np.sort(rng.choice(n, size=int(d), replace=False)) for d in deg]
+    rp = np.zeros(n + 1, np.uint64)
+    rp[1:] = np.cumsum([r.size for r in rows])
+    col = np.concatenate(rows).astype(np.uint32)
+    out.append(("empty_runs", rp, col, rng.uniform(-1, 1, col.size).astype(np.float32)))
+    # every row empty but the last
+    n = 700
+    rp = np.zeros(n + 1, np.uint64)
+    rp[-1] = 50
+    col = np.sort(rng.choice(n, 50, replace=False)).astype(np.uint32)
+    out.append(("last_only", rp, col, rng.uniform(-1, 1, 50).astype(np.float32)))
+    return out
+
+
+@pytest.mark.parametrize("sched", [0, 3])
+@pytest.mark.parametrize("f", [128, 602])
+def test_balanced_schedule_edge_cases(dev, sched, f):
+    """Balanced ranges with empty ranges, runs of empty rows across window
+    boundaries, hub rows and row shards (srow offset != 0): fp32 and int8,
+    exact and sampled, bit-exact vs the oracle."""
+    import torch
+
+    from paper_2503_18427_b200 import capi
+    L = capi.lib()
+    for name, rp, col, val in _edge_graphs():
+        n = rp.size - 1
+        g = dev.Graph.from_numpy(rp, col, val, n_cols=n)
+        x_np = np.random.default_rng(f).uniform(-1, 1, (n, f)).astype(np.float32)
+        x = dev.padded(torch.from_numpy(x_np).cuda())
+        q = dev.quantize(x)
+        lo, hi = port.fit_params(x_np)
+        deq = port.dequantize(port.quantize(x_np, lo, hi), lo, hi)
+        plan = dev.SampledPlan(g, 32)
+        cut = n // 3
+        try:
+            capi.check(L.aes_dev_spmm_set_schedule(sched))
+            exact = dev.spmm_exact(g, x)
+            sampled = dev.spmm_plan(plan, x)
+            shard = dev.spmm(plan.srow_ptr[cut:], plan.scol, plan.sval, x, max_row_slots=plan.row_bound)
+            exact_q = dev.spmm_q8(g.row_ptr, g.col, g.val, q)
+            sampled_q = dev.spmm_q8(plan.srow_ptr, plan.scol, plan.sval, q, max_row_slots=plan.row_bound)
+            shard_q = dev.spmm_q8(plan.srow_ptr[cut:], plan.scol, plan.sval, q, max_row_slots=plan.row_bound)
+            torch.cuda.synchronize()
+        finally:
+            L.aes_dev_spmm_set_schedule(0)
+        want = port.spmm_sampled(rp, col, val, x_np, 32)
+        want_q = port.spmm_sampled(rp, col, val, deq, 32)
+        assert np.array_equal(bits(to_np(exact)), bits(port.spmm_csr(rp, col, val, x_np))), name
+        assert np.array_equal(bits(to_np(sampled)), bits(want)), name
+        assert np.array_equal(bits(to_np(shard)), bits(want[cut:])), name
+        assert np.array_equal(bits(to_np(exact_q)), bits(port.spmm_csr(rp, col, val, deq))), name
+        assert np.array_equal(bits(to_np(sampled_q)), bits(want_q)), name
+        assert np.array_equal(bits(to_np(shard_q)), bits(want_q[cut:])), name
