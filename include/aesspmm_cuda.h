@@ -373,6 +373,34 @@ AES_API int aes_dev_signal_all(unsigned long long* const* counters, int n, void*
 /* *bad_flag = 1 if any of x[0..count) is inf/NaN (stream-ordered). */
 AES_API int aes_dev_all_finite(const float* x, uint64_t count, unsigned int* bad_flag, void* stream);
 
+/* ---- int8 layer exchange over peer memory (exchange.cu) ------------------
+ * Replaces, per hidden GCN layer, the reference composition
+ * dequantize(quantize(H, fit_params(H))) (proj/src/quantize.cpp:11-64) +
+ * the all-gather of H, with no host round trip:
+ *   aes_dev_fit_params(own rows) -> aes_dev_publish_params -> wait (world
+ *   arrivals) -> aes_dev_fold_params_lut -> aes_dev_quantize_bcast -> wait
+ *   (sum over ranks of aes_quantize_bcast_ctas(rows_r) arrivals) ->
+ *   aes_dev_spmm_q8_ex over the code replica with the folded LUT.
+ * Stores (min, max, flag) of this rank's fit_params result (or, when
+ * empty != 0, the empty-shard marker) into slot `rank` of every rank's
+ * float[4*world] parameter array, then +1 on every rank's counter. */
+AES_API int aes_dev_publish_params(const float* fit_result, int empty, int rank, float* const* peer_params,
+                                   unsigned long long* const* peer_counters, int world, void* stream);
+/* Folds the world triples in rank order with the reference's strict < / >
+ * rule into out[0..1] = (x_min, x_max), out[2] = status bits (0 ok,
+ * 1 NonFinite, 2 EmptyMatrix), and writes the exact dequantization table of
+ * those params to lut[256] (as aes_dev_dequant_lut). */
+AES_API int aes_dev_fold_params_lut(const float* params, int world, uint32_t bits, float* out, float* lut,
+                                    void* stream);
+/* Arrivals (per destination) aes_dev_quantize_bcast adds for `rows` rows. */
+AES_API uint64_t aes_quantize_bcast_ctas(uint64_t rows);
+/* quantize(x, (lohi[0], lohi[1]), bits) of this shard's rows, codes stored
+ * at rows row_off.. of every dst_codes[d] (ldq % 16 == 0), then one
+ * system-scope release-add per CTA on every peer_counters[d]. */
+AES_API int aes_dev_quantize_bcast(const float* x, uint64_t rows, uint64_t cols, uint64_t ldx, const float* lohi,
+                                   uint32_t bits, uint8_t* const* dst_codes, uint64_t row_off, uint64_t ldq,
+                                   unsigned long long* const* peer_counters, int world, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,6 +27,15 @@ with a gloo group.
 (`p2p.PeerReplicas`): each rank's GEMM epilogue stores its output rows
 straight into every rank's next-layer replica over NVLink peer memory and
 signals per-CTA arrivals; the next layer starts once all arrivals landed.
+
+`exchange_dtype="int8"` sends hidden layer outputs as 8-bit codes with one
+set of global params (the reference composition dequantize(quantize(H,
+fit_params(H)))).  Over NCCL the per-rank (min, max) are all-gathered and
+folded on the host; with `exchange="p2p"` everything stays on the device
+(exchange.cu): each rank publishes its fit_params triple into every rank's
+parameter array, folds all of them in rank order on the device into the
+params and the exact dequantization LUT, and quantizes its rows straight into
+every rank's code replica — no host sync, no collective on the data path.
 """
 from __future__ import annotations
 
@@ -101,6 +110,7 @@ class ShardedGCN:
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.ops = ops or cuda_ops(max_row_slots)
+        self.max_row_slots = max_row_slots
         self.n = n_rows
         self.weights = list(weights)
         self.biases = list(biases)
@@ -117,8 +127,6 @@ class ShardedGCN:
         # with the fused-dequant SpMM.  Equals the reference composition
         # dequantize(quantize(H, fit_params(H))) per hidden layer, bit for bit.
         self.qx = exchange_dtype == "int8"
-        if self.qx and exchange != "nccl":
-            raise ValueError("exchange_dtype='int8' runs over the NCCL exchange")
         lo, hi = self.cuts[self.rank], self.cuts[self.rank + 1]
         self.lo, self.hi = lo, hi
         # shard plan = rows [lo, hi) of the global sampled CSR (absolute offsets)
@@ -133,7 +141,15 @@ class ShardedGCN:
                 raise ValueError("p2p exchange uses equal-row shards")
             dims = [weights[0].shape[0]] + [w.shape[1] for w in weights]
             ld = (max(dims) + 3) & ~3
-            self.replicas = p2p.PeerReplicas(self.per * self.world, ld, group)
+            # int8 exchange: code replicas for the hidden layer outputs (rows
+            # padded to 16 B for the int8 SpMM's 16-B gathers)
+            code_ld = -(-max(w.shape[1] for w in weights[:-1]) // 16) * 16 if self.qx and len(weights) > 1 else 0
+            self.replicas = p2p.PeerReplicas(self.per * self.world, ld, group, code_ld=code_ld)
+            self.code_arrivals = sum(p2p.quantize_ctas(c1 - c0) for c0, c1 in zip(self.cuts, self.cuts[1:]))
+            # per layer parity: folded [x_min, x_max, status, 0] and the exact LUT (local)
+            dev = weights[0].device
+            self.q_params = [torch.zeros(4, dtype=torch.float32, device=dev) for _ in range(2)]
+            self.q_luts = [torch.zeros(256, dtype=torch.float32, device=dev) for _ in range(2)]
             # finite W makes the reference's zero-skip result-neutral (gemm.cu)
             flag = torch.zeros(1, dtype=torch.int32, device=weights[0].device)
             self.finite = []
@@ -213,16 +229,61 @@ class ShardedGCN:
         elif len(self.weights) > 1:
             raise ValueError("forward(None) reuses the input replica: single-layer models only")
         h = rep.bufs[0][: self.n, :f0]
+        hq = None  # (code replica [n, F], lut) when the layer input arrived as int8
+        statuses = []
         n_layers = len(self.weights)
         for l, (w, b) in enumerate(zip(self.weights, self.biases)):
-            agg = self.ops.spmm(self.srow, self.scol, self.sval, h, out=self.ops.alloc(max(rows, 1), h.shape[1], h))
+            if hq is None:
+                agg = self.ops.spmm(self.srow, self.scol, self.sval, h,
+                                    out=self.ops.alloc(max(rows, 1), h.shape[1], h))
+            else:
+                agg = self._spmm_codes(*hq)
+            if self.qx and l + 1 < n_layers:
+                hq = self._int8_publish(l, agg, w, b, rows)
+                statuses.append(self.q_params[l % 2][2:3])
+                continue
             out_buf = (l + 1) % 2
             rep.gemm_publish(out_buf, agg[:rows], w, b, l + 1 < n_layers, self.finite[l], self.lo, fast=self.fast[l])
             rep.wait(self.arrivals[l])
             h = rep.bufs[out_buf][: self.n, : w.shape[1]]
+            hq = None
+        if statuses:  # one read-back per step: the device folds' NonFinite / EmptyMatrix
+            st = torch.cat(statuses).view(torch.int32).cpu().tolist()
+            if 1 in st:
+                raise ValueError("NonFinite")
+            if 2 in st:
+                raise ValueError("EmptyMatrix")
         if return_shard:
             return h[self.lo:self.hi].clone() if copy_out else h[self.lo:self.hi]
         return h.clone() if copy_out else h
+
+    def _int8_publish(self, l: int, agg: torch.Tensor, w: torch.Tensor, b, rows: int):
+        """Hidden layer l with the int8 exchange over peer memory: local GEMM,
+        device fit_params of this rank's rows, params to every rank, device
+        fold + LUT, codes quantized straight into every rank's replica."""
+        from . import device
+
+        rep = self.replicas
+        x = self.ops.alloc(max(rows, 1), w.shape[1], agg)
+        if self.fast[l]:
+            device.gemm_tf32(agg[:rows], w, b, True, out=x[:rows])
+        else:
+            self.ops.gemm_bias_act(agg[:rows], w, b, relu=True, out=x)
+        buf = l % 2
+        fit = self.ops.fit_params(x[:rows]) if rows else None
+        rep.exchange_params(buf, fit, self.q_params[buf], self.q_luts[buf])
+        if rows:
+            rep.quantize_publish(buf, x[:rows], self.q_params[buf], self.lo)
+        rep.wait_codes(self.code_arrivals)
+        return rep.codes[buf][: self.n, : w.shape[1]], self.q_luts[buf]
+
+    def _spmm_codes(self, codes: torch.Tensor, lut: torch.Tensor) -> torch.Tensor:
+        from . import device
+
+        rows = self.hi - self.lo
+        out = self.ops.alloc(max(rows, 1), codes.shape[1], codes.new_empty(0, dtype=torch.float32))
+        q = device.QuantizedDevice(codes, 0.0, 0.0, 8, lut)  # params live in the LUT (device fold)
+        return device.spmm_q8(self.srow, self.scol, self.sval, q, out=out, max_row_slots=self.max_row_slots)
 
     def forward(self, x: torch.Tensor | None, return_shard: bool = False, copy_out: bool = True) -> torch.Tensor:
         """x: full [n, F0] replica on this rank.  Returns the full logits

@@ -36,27 +36,45 @@ class PeerReplicas:
     """Two activation replicas [rows, ld] + one u64 arrival counter per rank,
     mapped on every rank."""
 
-    def __init__(self, rows: int, ld: int, group=None, device=None):
+    def __init__(self, rows: int, ld: int, group=None, device=None, code_ld: int = 0):
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         device = device or torch.device("cuda", torch.cuda.current_device())
         self.ld = ld
         self.bufs = [torch.zeros((rows, ld), dtype=torch.float32, device=device) for _ in range(2)]
-        # [0] layer arrivals (per CTA), [1] step-start barrier arrivals (per rank)
-        self.counter = torch.zeros(2, dtype=torch.int64, device=device)
+        # [0] fp32 layer arrivals (per CTA), [1] step-start barrier arrivals (per
+        # rank), [2] int8-exchange param arrivals (per rank), [3] code arrivals (per CTA)
+        self.counter = torch.zeros(4, dtype=torch.int64, device=device)
+        # int8 exchange (code_ld > 0): two code replicas (layer parity) and two
+        # [world, 4] parameter arrays, also peer-mapped
+        self.code_ld = code_ld
+        self.codes = [torch.zeros((rows, code_ld), dtype=torch.uint8, device=device) for _ in range(2)] \
+            if code_ld else []
+        self.params = [torch.zeros(4 * self.world, dtype=torch.float32, device=device) for _ in range(2)] \
+            if code_ld else []
         if self.world > 1:
             self.peer_bufs = [_exchange(b, group) for b in self.bufs]
             self.peer_ctrs = _exchange(self.counter, group)
+            self.peer_codes = [_exchange(c, group) for c in self.codes]
+            self.peer_params = [_exchange(pr, group) for pr in self.params]
         else:
             self.peer_bufs = [[b] for b in self.bufs]
             self.peer_ctrs = [self.counter]
+            self.peer_codes = [[c] for c in self.codes]
+            self.peer_params = [[pr] for pr in self.params]
         ptrs = ctypes.c_void_p * self.world
         self.dst = [ptrs(*[t.data_ptr() for t in pb]) for pb in self.peer_bufs]
         self.ctr = ptrs(*[t.data_ptr() for t in self.peer_ctrs])
         self.bar = ptrs(*[t.data_ptr() + 8 for t in self.peer_ctrs])
+        self.par_ctr = ptrs(*[t.data_ptr() + 16 for t in self.peer_ctrs])
+        self.code_ctr = ptrs(*[t.data_ptr() + 24 for t in self.peer_ctrs])
+        self.code_dst = [ptrs(*[t.data_ptr() for t in pc]) for pc in self.peer_codes]
+        self.par_dst = [ptrs(*[t.data_ptr() for t in pp]) for pp in self.peer_params]
         self.expected = 0
         self.bar_expected = 0
+        self.par_expected = 0
+        self.code_expected = 0
         torch.cuda.synchronize()
         if dist.is_initialized():
             dist.barrier(group)
@@ -101,6 +119,40 @@ class PeerReplicas:
         self.expected += arrivals
         check(lib().aes_dev_wait_counter(self.counter.data_ptr(), self.expected, stream_of(stream)))
 
+    # ---- int8 exchange (exchange.cu) ---------------------------------------
+    def exchange_params(self, buf: int, fit_result: torch.Tensor | None, out4: torch.Tensor, lut: torch.Tensor,
+                        stream=None):
+        """Publish this rank's fit_params triple (None: empty shard) to every
+        rank, wait for all ranks', fold them in rank order on the device into
+        out4 = [x_min, x_max, status, 0] and the exact 256-entry LUT."""
+        st = stream_of(stream)
+        check(lib().aes_dev_publish_params(None if fit_result is None else fit_result.data_ptr(),
+                                           int(fit_result is None), self.rank,
+                                           ctypes.cast(self.par_dst[buf], ctypes.c_void_p),
+                                           ctypes.cast(self.par_ctr, ctypes.c_void_p), self.world, st))
+        self.par_expected += self.world
+        check(lib().aes_dev_wait_counter(self.counter.data_ptr() + 16, self.par_expected, st))
+        check(lib().aes_dev_fold_params_lut(self.params[buf].data_ptr(), self.world, 8, out4.data_ptr(),
+                                            lut.data_ptr(), st))
+
+    def quantize_publish(self, buf: int, x: torch.Tensor, lohi: torch.Tensor, row_offset: int, stream=None):
+        """Codes of this rank's rows x (params from the device fold) into every
+        rank's code replica `buf` at rows [row_offset, row_offset + len(x))."""
+        rows, cols = x.shape
+        check(lib().aes_dev_quantize_bcast(x.data_ptr(), rows, cols, x.stride(0), lohi.data_ptr(), 8,
+                                           ctypes.cast(self.code_dst[buf], ctypes.c_void_p), row_offset,
+                                           self.code_ld, ctypes.cast(self.code_ctr, ctypes.c_void_p), self.world,
+                                           stream_of(stream)))
+
+    def wait_codes(self, arrivals: int, stream=None):
+        self.code_expected += arrivals
+        check(lib().aes_dev_wait_counter(self.counter.data_ptr() + 24, self.code_expected, stream_of(stream)))
+
+
+def quantize_ctas(rows: int) -> int:
+    """Arrivals one producer's aes_dev_quantize_bcast adds to each counter."""
+    return int(lib().aes_quantize_bcast_ctas(rows))
+
 
 def gemm_ctas(m: int, n: int, fast: bool = False) -> int:
     """Arrivals one producer's publishing GEMM adds to each counter."""
@@ -109,4 +161,4 @@ def gemm_ctas(m: int, n: int, fast: bool = False) -> int:
     return int(lib().aes_gemm_ctas(m, n))
 
 
-__all__ = ["PeerReplicas", "gemm_ctas", "capi"]
+__all__ = ["PeerReplicas", "gemm_ctas", "quantize_ctas", "capi"]

@@ -34,7 +34,7 @@ def _problem(n=3001, f=40):
     return nrp, ncol, nval, x, ws, bs
 
 
-def _run(rank, world, port_no, q, fast=False):
+def _run(rank, world, port_no, q, fast=False, exchange_dtype="f32"):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
@@ -49,7 +49,8 @@ def _run(rank, world, port_no, q, fast=False):
         plan = device.SampledPlan(g, 16)
         model = ShardedGCN(plan.srow_ptr, plan.scol, plan.sval, g.n_rows,
                            [torch.from_numpy(w).cuda() for w in ws], [torch.from_numpy(b).cuda() for b in bs],
-                           exchange="p2p", fast_gemm=fast)
+                           exchange="p2p", fast_gemm=fast, exchange_dtype=exchange_dtype,
+                           max_row_slots=plan.row_bound)
         xt = torch.from_numpy(x).cuda()
         outs = [model.forward(xt).cpu().numpy() for _ in range(3)]  # repeated steps exercise the barrier
         torch.cuda.synchronize()
@@ -106,6 +107,31 @@ def test_p2p_fused_exchange_matches_oracle(world):
         assert not isinstance(outs, str), outs
     nrp, ncol, nval, x, ws, bs = _problem()
     want = port.gcn_forward(nrp, ncol, nval, x, ws, bs, 16)
+    for _, outs in res:
+        for o in outs:
+            assert np.array_equal(np.ascontiguousarray(o).view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_p2p_int8_exchange_matches_reference_composition(world):
+    """int8 layer exchange over peer memory (exchange.cu): device-side param
+    publish + rank-order fold + LUT, codes quantized straight into every
+    rank's replica.  Bit-exact vs the reference composition
+    dequantize(quantize(H, fit_params(H))) per hidden layer."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = _free_port()
+    procs = [ctx.Process(target=_run, args=(r, world, p, q, False, "int8")) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted([q.get(timeout=300) for _ in procs], key=lambda t: t[0])
+    for pr in procs:
+        pr.join(timeout=120)
+    for _, outs in res:
+        assert not isinstance(outs, str), outs
+    nrp, ncol, nval, x, ws, bs = _problem()
+    want = port.gcn_forward_int8_exchange(nrp, ncol, nval, x, ws, bs, 16)
     for _, outs in res:
         for o in outs:
             assert np.array_equal(np.ascontiguousarray(o).view(np.uint32), want.view(np.uint32))
