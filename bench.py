@@ -423,7 +423,30 @@ def run_gcn_layer(args, plan, n, f, b, dist):
         torch.cuda.synchronize()
         out[name + "_ms"] = round(max_over_ranks(s.elapsed_time(e) / steps, dist), 4)
         del model
+    # two layers (F -> F -> F): the hidden output crosses the exchange as fp32
+    # (GEMM epilogue broadcast) or as int8 codes (device param fold + quantize
+    # straight into every replica, exchange.cu); exact GEMMs, input copied in
+    w2 = (torch.rand(f, f, device="cuda", generator=torch.Generator("cuda").manual_seed(4)) - 0.5)
+    for name, xdt in (("f32", "f32"), ("int8", "int8")):
+        model = ShardedGCN(plan.srow_ptr, plan.scol, plan.sval, n, [w, w2], [bias, bias], exchange="p2p",
+                           exchange_dtype=xdt, max_row_slots=plan.row_bound)
+        for _ in range(2):
+            model.forward(x, copy_out=False)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        steps = max(3, min(args.steps, 5))
+        s.record()
+        for _ in range(steps):
+            model.forward(x, copy_out=False)
+        e.record()
+        torch.cuda.synchronize()
+        out[f"two_layer_{name}_exchange_ms"] = round(max_over_ranks(s.elapsed_time(e) / steps, dist), 4)
+        del model
     out["exchange"] = "fused into the GEMM epilogue (P2P stores to every rank's replica + sys-scope arrivals)"
+    out["int8_exchange"] = ("hidden layer output as 8-bit codes: per-rank fit_params published to every rank, "
+                            "rank-order fold + LUT on the device, codes quantized into every replica (4x fewer bytes)")
     out["note"] = "exact mode is bit-exact with the reference; fast mode |err| <= 2^-8 sum|a||w| (TF32)"
     return out
 

@@ -33,7 +33,7 @@ namespace aes {
 namespace {
 
 constexpr int kMaxRanks = 16;
-constexpr int kQuantRows = 32;      // rows per quantize CTA (one arrival each)
+constexpr int kQuantRows = 256;     // rows per quantize CTA (one system-scope arrival each)
 constexpr int kQuantThreads = 256;
 
 struct PtrArr {
@@ -110,38 +110,51 @@ __global__ void fold_params_lut_kernel(const float* __restrict__ params, int wor
 
 // quantize(x, params) for rows [0, rows) of this shard, codes stored into
 // every destination replica at rows row_off.., then one arrival per CTA per
-// destination.  lohi = fold_params_lut's output (device).
+// destination.  lohi = fold_params_lut's output (device).  Warp per row,
+// lane per 4 columns (float4 loads when the rows are 16-B aligned).
+__device__ __forceinline__ uint32_t quantize_code(float x, double lo, double range, double dlev) {
+    if (range == 0.0) return 0u;  // degenerate range: every code 0 (quantize.cpp:35-38)
+    double qd = floor(__dadd_rn(__dmul_rn(__ddiv_rn(__dsub_rn((double)x, lo), range), dlev), 0.0078125));
+    qd = qd < 0.0 ? 0.0 : qd;  // std::clamp(q, 0, levels)
+    qd = dlev < qd ? dlev : qd;
+    return (uint32_t)qd;
+}
+
 __global__ void __launch_bounds__(kQuantThreads)
-quantize_bcast_kernel(const float* __restrict__ x, uint64_t rows, uint64_t cols, uint64_t ldx,
+quantize_bcast_kernel(const float* __restrict__ x, uint64_t rows, uint32_t cols, uint64_t ldx,
                       const float* __restrict__ lohi, uint32_t levels, PtrArr dst, uint64_t row_off, uint64_t ldq,
-                      PtrArr ctrs, int n) {
+                      PtrArr ctrs, int n, bool vec) {
     const uint64_t r0 = (uint64_t)blockIdx.x * kQuantRows;
-    const uint64_t nr = min((uint64_t)kQuantRows, rows - r0);
+    const uint32_t nr = (uint32_t)min((uint64_t)kQuantRows, rows - r0);
     const double lo = (double)lohi[0];
     const double range = __dsub_rn((double)lohi[1], lo);
     const double dlev = (double)levels;
-    const uint64_t c4n = (cols + 3) / 4;
-    for (uint64_t e = threadIdx.x; e < nr * c4n; e += kQuantThreads) {
-        const uint64_t r = r0 + e / c4n, c = (e % c4n) * 4;
-        uint32_t packed = 0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            uint32_t code = 0;
-            if (c + i < cols && range != 0.0) {  // degenerate range: every code 0 (quantize.cpp:35-38)
-                const double v = (double)__ldcs(x + r * ldx + c + i);
-                double qd = floor(__dadd_rn(__dmul_rn(__ddiv_rn(__dsub_rn(v, lo), range), dlev), 0.0078125));
-                qd = qd < 0.0 ? 0.0 : qd;  // std::clamp(q, 0, levels)
-                qd = dlev < qd ? dlev : qd;
-                code = (uint32_t)qd;
-            }
-            packed |= code << (8 * i);
-        }
-        for (int d = 0; d < n; ++d) {
-            uint8_t* row = static_cast<uint8_t*>(dst.p[d]) + (row_off + r) * ldq;
-            if (c + 4 <= cols) {
-                *reinterpret_cast<uint32_t*>(row + c) = packed;  // ldq % 16 == 0, c % 4 == 0
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t c4n = (cols + 3) / 4;
+    for (uint32_t rr = warp; rr < nr; rr += kQuantThreads / 32) {
+        const uint64_t r = r0 + rr;
+        const float* xr = x + r * ldx;
+        for (uint32_t c4 = lane; c4 < c4n; c4 += 32) {
+            const uint32_t c = c4 * 4;
+            float v[4];
+            if (vec) {
+                const float4 t = __ldcs(reinterpret_cast<const float4*>(xr + c));
+                v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
             } else {
-                for (int i = 0; c + i < cols; ++i) row[c + i] = (uint8_t)(packed >> (8 * i));
+#pragma unroll
+                for (int i = 0; i < 4; ++i) v[i] = c + i < cols ? __ldcs(xr + c + i) : 0.f;
+            }
+            uint32_t packed = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (c + i < cols) packed |= quantize_code(v[i], lo, range, dlev) << (8 * i);
+            for (int d = 0; d < n; ++d) {
+                uint8_t* row = static_cast<uint8_t*>(dst.p[d]) + (row_off + r) * ldq;
+                if (c + 4 <= cols) {
+                    *reinterpret_cast<uint32_t*>(row + c) = packed;  // ldq % 16 == 0, c % 4 == 0
+                } else {
+                    for (uint32_t i = 0; c + i < cols; ++i) row[c + i] = (uint8_t)(packed >> (8 * i));
+                }
             }
         }
     }
@@ -201,8 +214,11 @@ int aes_dev_quantize_bcast(const float* x, uint64_t rows, uint64_t cols, uint64_
         dp.p[d] = dst_codes[d];
         cp.p[d] = peer_counters[d];
     }
+    if (cols >= (1ull << 32)) return fail(AES_ERR_INVALID_ARG, "too many columns");
+    // rows 16-B aligned and padded to whole float4s: vector loads
+    const bool vec = ldx % 4 == 0 && (uintptr_t)x % 16 == 0 && ldx >= (cols + 3) / 4 * 4;
     quantize_bcast_kernel<<<(unsigned)ctas, kQuantThreads, 0, as_stream(stream)>>>(
-        x, rows, cols, ldx, lohi, (1u << bits) - 1u, dp, row_off, ldq, cp, world);
+        x, rows, (uint32_t)cols, ldx, lohi, (1u << bits) - 1u, dp, row_off, ldq, cp, world, vec);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
 }

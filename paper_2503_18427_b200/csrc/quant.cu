@@ -19,7 +19,7 @@ namespace aes {
 namespace {
 
 constexpr int kFitThreads = 256;
-constexpr int kFitBlocks = 148 * 4;
+constexpr int kFitBlocks = 148 * 8;
 
 struct MinMax {
     float lo, hi;
@@ -63,16 +63,49 @@ __device__ MinMax block_reduce(MinMax m) {
 }
 
 // Level 1: block b reduces the contiguous chunk [b*chunk, (b+1)*chunk).
+// A thread sees its elements in increasing index order, so the strict
+// compares alone keep the first occurrence (an equal later value never
+// replaces); the index only matters when partial results merge.
+__device__ __forceinline__ void fit_elem(MinMax& m, float v, uint64_t i) {
+    if (!isfinite(v)) { m.bad = 1; return; }
+    if (v < m.lo) { m.lo = v; m.ilo = i; }
+    if (v > m.hi) { m.hi = v; m.ihi = i; }
+}
+
 __global__ void __launch_bounds__(kFitThreads)
 fit_partial_kernel(const float* __restrict__ x, uint64_t n, uint64_t chunk, MinMax* __restrict__ part) {
-    const uint64_t b0 = (uint64_t)blockIdx.x * chunk;
+    const uint64_t b0 = min(n, (uint64_t)blockIdx.x * chunk);  // trailing blocks may be empty
     const uint64_t b1 = min(n, b0 + chunk);
     MinMax m{INFINITY, -INFINITY, ~0ull, ~0ull, 0u};
-    for (uint64_t i = b0 + threadIdx.x; i < b1; i += kFitThreads) {
-        float v = __ldcs(x + i);
-        if (!isfinite(v)) { m.bad = 1; continue; }
-        if (v < m.lo || (v == m.lo && i < m.ilo)) { m.lo = v; m.ilo = i; }
-        if (v > m.hi || (v == m.hi && i < m.ihi)) { m.hi = v; m.ihi = i; }
+    if ((uintptr_t)(x + b0) % 16 == 0) {
+        // float4 loads, 4 in flight per thread (chunk is a multiple of 4 here)
+        const float4* x4 = reinterpret_cast<const float4*>(x + b0);
+        const uint64_t n4 = (b1 - b0) / 4;
+        uint64_t j = threadIdx.x;
+        for (; j + 3 * kFitThreads < n4; j += 4 * kFitThreads) {
+            float4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = __ldcs(x4 + j + u * kFitThreads);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint64_t i = b0 + 4 * (j + u * kFitThreads);
+                fit_elem(m, v[u].x, i);
+                fit_elem(m, v[u].y, i + 1);
+                fit_elem(m, v[u].z, i + 2);
+                fit_elem(m, v[u].w, i + 3);
+            }
+        }
+        for (; j < n4; j += kFitThreads) {
+            const float4 v = __ldcs(x4 + j);
+            const uint64_t i = b0 + 4 * j;
+            fit_elem(m, v.x, i);
+            fit_elem(m, v.y, i + 1);
+            fit_elem(m, v.z, i + 2);
+            fit_elem(m, v.w, i + 3);
+        }
+        for (uint64_t i = b0 + 4 * n4 + threadIdx.x; i < b1; i += kFitThreads) fit_elem(m, __ldcs(x + i), i);
+    } else {
+        for (uint64_t i = b0 + threadIdx.x; i < b1; i += kFitThreads) fit_elem(m, __ldcs(x + i), i);
     }
     m = block_reduce(m);
     if (threadIdx.x == 0) part[blockIdx.x] = m;
@@ -167,7 +200,7 @@ int aes_dev_fit_params(const float* x, uint64_t n, float* result, void* workspac
     uint64_t nbl = (n + kFitThreads - 1) / kFitThreads;
     int nb = (int)(nbl < (uint64_t)kFitBlocks ? nbl : (uint64_t)kFitBlocks);
     if (workspace_bytes < nb * sizeof(MinMax)) return fail(AES_ERR_INVALID_ARG, "fit workspace too small");
-    uint64_t chunk = (n + nb - 1) / nb;
+    uint64_t chunk = ((n + nb - 1) / nb + 3) & ~3ull;  // multiple of 4: float4-aligned chunks
     auto* part = static_cast<MinMax*>(workspace);
     fit_partial_kernel<<<nb, kFitThreads, 0, st>>>(x, n, chunk, part);
     fit_final_kernel<<<1, kFitThreads, 0, st>>>(x, part, nb, result);
