@@ -28,6 +28,7 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include "quantize.cuh"
 
 namespace aes {
 namespace {
@@ -110,25 +111,17 @@ __global__ void fold_params_lut_kernel(const float* __restrict__ params, int wor
 
 // quantize(x, params) for rows [0, rows) of this shard, codes stored into
 // every destination replica at rows row_off.., then one arrival per CTA per
-// destination.  lohi = fold_params_lut's output (device).  Warp per row,
-// lane per 4 columns (float4 loads when the rows are 16-B aligned).
-__device__ __forceinline__ uint32_t quantize_code(float x, double lo, double range, double dlev) {
-    if (range == 0.0) return 0u;  // degenerate range: every code 0 (quantize.cpp:35-38)
-    double qd = floor(__dadd_rn(__dmul_rn(__ddiv_rn(__dsub_rn((double)x, lo), range), dlev), 0.0078125));
-    qd = qd < 0.0 ? 0.0 : qd;  // std::clamp(q, 0, levels)
-    qd = dlev < qd ? dlev : qd;
-    return (uint32_t)qd;
-}
-
+// destination.  lohi = fold_params_lut's params
+// (device); codes through quantize.cuh's fp32 fast path with the exact fp64
+// fallback.  Warp per row, lane per 4 columns (float4 loads when the rows are
+// 16-B aligned).
 __global__ void __launch_bounds__(kQuantThreads)
 quantize_bcast_kernel(const float* __restrict__ x, uint64_t rows, uint32_t cols, uint64_t ldx,
                       const float* __restrict__ lohi, uint32_t levels, PtrArr dst, uint64_t row_off, uint64_t ldq,
                       PtrArr ctrs, int n, bool vec) {
     const uint64_t r0 = (uint64_t)blockIdx.x * kQuantRows;
     const uint32_t nr = (uint32_t)min((uint64_t)kQuantRows, rows - r0);
-    const double lo = (double)lohi[0];
-    const double range = __dsub_rn((double)lohi[1], lo);
-    const double dlev = (double)levels;
+    const QuantParamsDev p = quant_params(lohi[0], lohi[1], levels);
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t c4n = (cols + 3) / 4;
     for (uint32_t rr = warp; rr < nr; rr += kQuantThreads / 32) {
@@ -147,7 +140,7 @@ quantize_bcast_kernel(const float* __restrict__ x, uint64_t rows, uint32_t cols,
             uint32_t packed = 0;
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-                if (c + i < cols) packed |= quantize_code(v[i], lo, range, dlev) << (8 * i);
+                if (c + i < cols) packed |= quant_code(v[i], p) << (8 * i);
             for (int d = 0; d < n; ++d) {
                 uint8_t* row = static_cast<uint8_t*>(dst.p[d]) + (row_off + r) * ldq;
                 if (c + 4 <= cols) {
@@ -192,6 +185,7 @@ int aes_dev_fold_params_lut(const float* params, int world, uint32_t bits, float
     using namespace aes;
     if (world < 1 || world > kMaxRanks) return fail(AES_ERR_INVALID_ARG, "1..16 ranks");
     if (bits < 1 || bits > 8) return fail(AES_ERR_UNSUPPORTED, "LUT needs bits <= 8");
+    if (!out || !lut) return fail(AES_ERR_INVALID_ARG, "null output");
     fold_params_lut_kernel<<<1, 256, 0, as_stream(stream)>>>(params, world, (1u << bits) - 1u, out, lut);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;

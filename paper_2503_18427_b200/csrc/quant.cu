@@ -14,6 +14,7 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include "quantize.cuh"
 
 namespace aes {
 namespace {
@@ -126,48 +127,45 @@ fit_final_kernel(const float* __restrict__ x, const MinMax* __restrict__ part, i
     }
 }
 
-template <typename CodeT>
-__global__ void quantize_kernel(const float* __restrict__ x, uint64_t rows, uint64_t cols, uint64_t ldx,
-                                double lo, double range, double levels, CodeT* __restrict__ q, uint64_t ldq) {
-    const uint64_t total = rows * cols;
-    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
-         e += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t r = e / cols, c = e - r * cols;
-        const double v = (double)__ldcs(x + r * ldx + c);
-        double code;
-        if (range == 0.0) {
-            code = 0.0;
-        } else {
-            const double ratio = __ddiv_rn(__dsub_rn(v, lo), range);
-            code = floor(__dadd_rn(__dmul_rn(ratio, levels), 0.0078125));
-            code = code < 0.0 ? 0.0 : code;            // std::clamp(q, 0, levels)
-            code = levels < code ? levels : code;
-        }
-        q[r * ldq + c] = (CodeT)(uint32_t)code;
-    }
-}
 
 // Vector form for the common contiguous case: 4 floats -> 4 codes per thread.
-__global__ void quantize_u8_vec4_kernel(const float4* __restrict__ x, uint64_t n4, double lo, double range,
-                                        double levels, uchar4* __restrict__ q) {
-    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n4;
-         e += (uint64_t)gridDim.x * blockDim.x) {
-        const float4 v = __ldcs(x + e);
-        float in[4] = {v.x, v.y, v.z, v.w};
-        unsigned char out[4];
+
+// Codes through the fp32 fast path with the exact fp64 fallback
+// (quantize.cuh): bit-identical to the reference, off the fp64 pipe.
+constexpr int kQuantBlocks = 148 * 8;
+template <typename CodeT>
+__global__ void __launch_bounds__(256)
+quantize_fast_kernel(const float* __restrict__ x, uint64_t rows, uint64_t cols, uint64_t ldx, float lo_f,
+                     float hi_f, uint32_t levels, CodeT* __restrict__ q, uint64_t ldq, int flat4) {
+    const QuantParamsDev p = quant_params(lo_f, hi_f, levels);
+    if (flat4) {  // contiguous rows: one float4 -> four codes
+        const uint64_t n4 = rows * cols / 4;
+        const float4* x4 = reinterpret_cast<const float4*>(x);
+        const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+        auto put = [&](uint64_t e, const float4& v) {
+            const uint32_t c0 = quant_code(v.x, p), c1 = quant_code(v.y, p), c2 = quant_code(v.z, p),
+                           c3 = quant_code(v.w, p);
+            if (sizeof(CodeT) == 1)
+                __stcs(reinterpret_cast<uchar4*>(q) + e, make_uchar4(c0, c1, c2, c3));
+            else
+                __stcs(reinterpret_cast<ushort4*>(q) + e, make_ushort4(c0, c1, c2, c3));
+        };
+        uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+        for (; e + 3 * stride < n4; e += 4 * stride) {  // 4 loads in flight per thread
+            float4 v[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            double code = 0.0;
-            if (range != 0.0) {
-                const double ratio = __ddiv_rn(__dsub_rn((double)in[i], lo), range);
-                code = floor(__dadd_rn(__dmul_rn(ratio, levels), 0.0078125));
-                code = code < 0.0 ? 0.0 : code;
-                code = levels < code ? levels : code;
-            }
-            out[i] = (unsigned char)(uint32_t)code;
+            for (int u = 0; u < 4; ++u) v[u] = __ldcs(x4 + e + u * stride);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) put(e + u * stride, v[u]);
         }
-        __stcs(q + e, make_uchar4(out[0], out[1], out[2], out[3]));
+        for (; e < n4; e += stride) put(e, __ldcs(x4 + e));
+        return;
     }
+    // general strides: warp per row, lane per column
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t r = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps)
+        for (uint64_t c = lane; c < cols; c += 32) q[r * ldq + c] = (CodeT)quant_code(__ldcs(x + r * ldx + c), p);
 }
 
 template <typename CodeT>
@@ -215,23 +213,15 @@ int aes_dev_quantize(const float* x, uint64_t rows, uint64_t cols, uint64_t ldx,
     if (bits < 1 || bits > 16 || !(lo <= hi)) return fail(AES_ERR_QPARAMS, "invalid QuantParams");
     const uint64_t total = rows * cols;
     if (total == 0) return AES_OK;
-    const double dlo = (double)lo, range = (double)hi - (double)lo;
-    const double levels = (double)((1u << bits) - 1u);
-    const unsigned grid = grid_for(total, 256, 148 * 32);
-    if (bits <= 8) {
-        if (ldx == cols && ldq == cols && total % 4 == 0 && (uintptr_t)x % 16 == 0 &&
-            (uintptr_t)codes % 4 == 0) {
-            quantize_u8_vec4_kernel<<<grid_for(total / 4, 256, 148 * 32), 256, 0, st>>>(
-                reinterpret_cast<const float4*>(x), total / 4, dlo, range, levels,
-                static_cast<uchar4*>(codes));
-        } else {
-            quantize_kernel<uint8_t><<<grid, 256, 0, st>>>(x, rows, cols, ldx, dlo, range, levels,
-                                                           static_cast<uint8_t*>(codes), ldq);
-        }
-    } else {
-        quantize_kernel<uint16_t><<<grid, 256, 0, st>>>(x, rows, cols, ldx, dlo, range, levels,
-                                                        static_cast<uint16_t*>(codes), ldq);
-    }
+    const int flat4 = ldx == cols && ldq == cols && total % 4 == 0 && (uintptr_t)x % 16 == 0 &&
+                      (uintptr_t)codes % (bits <= 8 ? 4 : 8) == 0;
+    const unsigned blocks = grid_for(flat4 ? total / 4 : rows * 32, 256, kQuantBlocks);
+    if (bits <= 8)
+        quantize_fast_kernel<uint8_t><<<blocks, 256, 0, st>>>(x, rows, cols, ldx, lo, hi, (1u << bits) - 1u,
+                                                              static_cast<uint8_t*>(codes), ldq, flat4);
+    else
+        quantize_fast_kernel<uint16_t><<<blocks, 256, 0, st>>>(x, rows, cols, ldx, lo, hi, (1u << bits) - 1u,
+                                                               static_cast<uint16_t*>(codes), ldq, flat4);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
 }

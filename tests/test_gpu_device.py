@@ -346,3 +346,40 @@ def test_balanced_schedule_edge_cases(dev, sched, f):
         assert np.array_equal(bits(to_np(exact_q)), bits(port.spmm_csr(rp, col, val, deq))), name
         assert np.array_equal(bits(to_np(sampled_q)), bits(want_q)), name
         assert np.array_equal(bits(to_np(shard_q)), bits(want_q[cut:])), name
+
+
+@pytest.mark.parametrize("bits", [1, 4, 8])
+@pytest.mark.parametrize("shape", [(1000, 128), (333, 7)])
+def test_quantize_threshold_table_extremes(dev, bits, shape):
+    """The table-driven u8 quantize (quantize.cuh) equals the reference fp64
+    formula on adversarial params and values: tiny / huge / subnormal ranges,
+    values outside [lo, hi], +-0, +-inf, FLT_MAX, and values packed around
+    every code boundary (contiguous float4 path and strided path)."""
+    import torch
+    rng = np.random.default_rng(bits * 7 + shape[1])
+    params = [(-1.0, 1.0), (0.0, 1e-30), (-1e30, 1e30), (-3.5, np.float32(-3.5) + np.float32(4e-6)),
+              (1e-40, 2e-40), (-5.0, 5.0), (2.0, 2.0), (-3e38, 3e38), (0.1, 0.7)]
+    for lo, hi in params:
+        lo, hi = float(np.float32(lo)), float(np.float32(hi))
+        n = shape[0] * shape[1]
+        span = hi - lo
+        x = rng.uniform(lo - 0.1 * span, hi + 0.1 * span, n).astype(np.float32) if span else \
+            rng.uniform(-1, 1, n).astype(np.float32)
+        # values around the code boundaries: the dequantized grid and its neighbours
+        grid = np.float32(lo) + (np.arange(n // 4) % ((1 << bits) + 1)).astype(np.float64) * \
+            (span / ((1 << bits) - 1) if span else 0.0)
+        g32 = grid.astype(np.float32)
+        x[: n // 4] = np.where(rng.random(n // 4) < 0.5, np.nextafter(g32, np.float32(np.inf)),
+                               np.nextafter(g32, np.float32(-np.inf)))
+        special = np.array([lo, hi, 0.0, -0.0, np.inf, -np.inf, 3.4028235e38, -3.4028235e38, 1e-45, -1e-45],
+                           np.float32)
+        x[n // 4: n // 4 + special.size] = special
+        x = x.reshape(shape)
+        xt = torch.from_numpy(x).cuda()
+        if shape[1] % 4:
+            xt = dev.padded(xt)  # strided rows: the general path
+        q = dev.quantize(xt, bits, params=(lo, hi))
+        torch.cuda.synchronize()
+        want = port.quantize(x, lo, hi, bits)
+        got = to_np(q.codes).astype(np.uint16)
+        assert np.array_equal(got, want), (lo, hi, bits, int((got != want).sum()))
