@@ -414,12 +414,29 @@ __device__ __forceinline__ void ring_rows(const uint64_t* __restrict__ srow, con
                                           const float* __restrict__ sval,
                                           const typename R::raw_t* __restrict__ gsrc, uint32_t ld, uint32_t f4,
                                           float4* __restrict__ c, uint64_t ldc4, uint32_t ring0, uint32_t lut_lane,
-                                          uint64_t rb, uint64_t re) {
+                                          uint64_t rb, uint64_t re, uint64_t hub_thr = ~0ull) {
+    const uint32_t lane = threadIdx.x & 31;
     while (rb < re) {
-        uint64_t e = re;
-        if (srow[re] - srow[rb] >= (1ull << 31)) e = min(rb + 1, re);  // (never at the BASELINE shapes)
-        ring_range<R, NV, C, FULL>(srow, scol, sval, gsrc, ld, f4, c, ldc4, ring0, lut_lane, rb, e);
-        rb = e;
+        // next hub row (> hub_thr slots: spmm_hub_kernel stores it) in [rb, re)
+        uint64_t hub = re;
+        if (hub_thr != ~0ull) {
+            for (uint64_t w = rb; w < re; w += 32) {
+                const uint64_t r = w + lane;
+                const bool big = r < re && srow[r + 1] - srow[r] > hub_thr;
+                const uint32_t m = __ballot_sync(0xffffffffu, big);
+                if (m) {
+                    hub = w + __ffs(m) - 1;
+                    break;
+                }
+            }
+        }
+        while (rb < hub) {
+            uint64_t e = hub;
+            if (srow[hub] - srow[rb] >= (1ull << 31)) e = min(rb + 1, hub);  // (never at the BASELINE shapes)
+            ring_range<R, NV, C, FULL>(srow, scol, sval, gsrc, ld, f4, c, ldc4, ring0, lut_lane, rb, e);
+            rb = e;
+        }
+        rb = hub < re ? hub + 1 : re;
     }
 }
 
@@ -568,16 +585,125 @@ __device__ __forceinline__ void bal_range(const uint64_t* __restrict__ srow, uin
     re = __shfl_sync(0xffffffffu, r, 16);
 }
 
+// Hub rows (rows of unknown length: exact SpMM, FULL plans).  A row holding
+// far more than a balanced warp share keeps its one warp busy long after the
+// rest finish (arxiv exact: a 13 k-slot row takes 0.8 ms on one warp while
+// the whole rest of the graph needs 0.1 ms).  Order forbids splitting a row's
+// slots, but not its columns: spmm_hub_kernel gives each hub row a CTA whose
+// 128 lanes own one output column each and stream the row's slots through
+// 128-deep per-warp cp.async rings (64 KB in flight per row, 8x a warp's),
+// and the balanced kernel skips those rows.  Both kernels derive the same
+// threshold from the same quantities.
+constexpr uint64_t kHubMinSlots = 1024;
+__device__ __forceinline__ uint64_t hub_threshold(const uint64_t* __restrict__ srow, uint64_t n_rows, uint64_t nw) {
+    const uint64_t key = (srow[n_rows] - srow[0]) + kRowCost * n_rows;
+    return max(kHubMinSlots, 2 * key / nw);  // more than two balanced shares
+}
+
+constexpr int kHubWarps = 4, kHubRing = 128, kHubBatch = 16, kHubRows = 256;
+__global__ void __launch_bounds__(kHubWarps * 32)
+spmm_hub_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
+                const float* __restrict__ sval, uint64_t n_rows, const float* __restrict__ b, uint64_t ldb,
+                uint32_t f, float* __restrict__ c, uint64_t ldc, uint64_t bal_warps) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ uint32_t hubs[kHubRows];
+    __shared__ uint32_t n_hubs;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t thr = hub_threshold(srow, n_rows, bal_warps);
+    if (tid == 0) n_hubs = 0;
+    __syncthreads();
+    const uint64_t r0 = (uint64_t)blockIdx.x * kHubRows;
+    for (uint32_t i = tid; i < kHubRows; i += kHubWarps * 32) {
+        const uint64_t r = r0 + i;
+        if (r < n_rows && srow[r + 1] - srow[r] > thr) hubs[atomicAdd(&n_hubs, 1u)] = i;
+    }
+    __syncthreads();
+    const uint32_t nh = n_hubs;
+    const uint32_t ring = smem_addr(smem_raw) + warp * (kHubRing * 128) + lane * 4;
+    for (uint32_t hi = 0; hi < nh; ++hi) {
+        const uint64_t h = r0 + hubs[hi];
+        const uint64_t g0 = srow[h];
+        const uint32_t total = (uint32_t)(srow[h + 1] - g0);  // < 2^32 (u32 plan slots)
+        for (uint32_t cb = warp * 32; cb < f; cb += kHubWarps * 32) {  // column block of this warp
+            const uint32_t col = cb + lane;
+            // lanes past f read column f - 1 (in bounds) and store nothing
+            const float* bc = b + min(col, f - 1);
+            // slots are padded to whole chunks of 32: metadata past `total`
+            // reads as (col 0, val 0) — a harmless in-bounds gather that is
+            // never accumulated (the loop stops at total)
+            auto ld_col = [&](uint32_t k) -> uint32_t {
+                const uint32_t s = k * 32 + lane;
+                return s < total ? ld_meta_u32(scol + g0 + s) : 0u;
+            };
+            auto ld_val = [&](uint32_t k) -> float {
+                const uint32_t s = k * 32 + lane;
+                return s < total ? ld_meta_f32(sval + g0 + s) : 0.f;
+            };
+            // ring entry of slot 32k + j: ring + ((k % kChunks) * 32 + j) * 128
+            constexpr uint32_t kChunks = kHubRing / 32;
+            auto issue_chunk_slot = [&](uint32_t base, uint32_t j, uint32_t cidx) {
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(base + j * 128),
+                             "l"(bc + (uint64_t)cidx * ldb)
+                             : "memory");
+            };
+            // prologue: chunks 0 .. kChunks-1 in flight, kHubBatch slots per commit group
+#pragma unroll
+            for (uint32_t k = 0; k < kChunks; ++k) {
+                const uint32_t mc = ld_col(k);
+                const uint32_t base = ring + k * 32 * 128;
+#pragma unroll
+                for (uint32_t j = 0; j < 32; ++j) {
+                    issue_chunk_slot(base, j, __shfl_sync(0xffffffffu, mc, j));
+                    if (j % kHubBatch == kHubBatch - 1) cp_commit();
+                }
+            }
+            float acc = 0.f;
+            float mv = ld_val(0);
+            uint32_t mc_ahead = ld_col(kChunks);  // columns of the chunk issued while consuming chunk 0
+            const uint32_t chunks = (total + 31) / 32;
+            for (uint32_t k = 0; k < chunks; ++k) {
+                const float mv_nx = ld_val(k + 1);
+                const uint32_t mc_nx = ld_col(k + 1 + kChunks);
+                const uint32_t base = ring + (k % kChunks) * 32 * 128;
+                const uint32_t left = total - k * 32;  // >= 1
+                if (left >= 32) {  // whole chunk: no per-slot bound checks
+#pragma unroll
+                    for (uint32_t j = 0; j < 32; ++j) {
+                        if (j % kHubBatch == 0) cp_wait<kHubRing / kHubBatch - 1>();
+                        acc = __fadd_rn(acc, __fmul_rn(__shfl_sync(0xffffffffu, mv, j), lds_f32(base + j * 128)));
+                        issue_chunk_slot(base, j, __shfl_sync(0xffffffffu, mc_ahead, j));
+                        if (j % kHubBatch == kHubBatch - 1) cp_commit();
+                    }
+                } else {  // last, partial chunk: nothing more is committed, so wait for all
+                    cp_wait<0>();
+#pragma unroll
+                    for (uint32_t j = 0; j < 32; ++j)
+                        if (j < left)
+                            acc = __fadd_rn(acc, __fmul_rn(__shfl_sync(0xffffffffu, mv, j), lds_f32(base + j * 128)));
+                }
+                mv = mv_nx;
+                mc_ahead = mc_nx;
+            }
+            cp_wait<0>();
+            __syncwarp();
+            if (col < f) c[h * ldc + col] = acc;
+        }
+    }
+}
+
 template <class R, int NV, int C, int WARPS, bool FULL>
 __global__ void __launch_bounds__(WARPS * 32)
 spmm_ring_bal_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
                      const float* __restrict__ sval, uint64_t n_rows, const typename R::raw_t* __restrict__ gsrc,
-                     uint32_t ld, uint32_t f4, float4* __restrict__ c, uint64_t ldc4, const float* __restrict__ lut_g) {
+                     uint32_t ld, uint32_t f4, float4* __restrict__ c, uint64_t ldc4, const float* __restrict__ lut_g,
+                     int hubs) {
     uint32_t ring0, lut_lane;
     ring_setup<R, C, NV, WARPS>(lut_g, ring0, lut_lane);
     uint64_t rb, re;
-    bal_range(srow, n_rows, (uint64_t)blockIdx.x * WARPS + (threadIdx.x >> 5), (uint64_t)gridDim.x * WARPS, rb, re);
-    ring_rows<R, NV, C, FULL>(srow, scol, sval, gsrc, ld, f4, c, ldc4, ring0, lut_lane, rb, re);
+    const uint64_t nw = (uint64_t)gridDim.x * WARPS;
+    bal_range(srow, n_rows, (uint64_t)blockIdx.x * WARPS + (threadIdx.x >> 5), nw, rb, re);
+    ring_rows<R, NV, C, FULL>(srow, scol, sval, gsrc, ld, f4, c, ldc4, ring0, lut_lane, rb, re,
+                              hubs ? hub_threshold(srow, n_rows, nw) : ~0ull);
 }
 
 // ---------------------------------------------------------------------------
@@ -1272,8 +1398,25 @@ int launch_ring_t(const uint64_t* srow, const uint32_t* scol, const float* sval,
     if (dyn == kSchedAuto) dyn = kSchedBal;  // fp32 ring: balanced waves at every size (1.17 vs 1.18 ms full graph)
     if (dyn == kSchedBal || dyn == kSchedBalOne) {  // waves of resident CTAs, slot-balanced row ranges
         const uint64_t waves = dyn == kSchedBalOne ? 1 : bal_waves(n, (uint64_t)kNumSMs * occ * W, 20);
-        spmm_ring_bal_kernel<R, NV, C, W, FULL><<<(unsigned)(waves * kNumSMs * occ), W * 32, smem, st>>>(
-            srow, scol, sval, n, g.base(), (uint32_t)g.ld4, f4, c, ldc4, lut);
+        const uint64_t grid = waves * kNumSMs * occ;
+        // rows of unknown length, fp32 rows of <= 128 floats: hub rows go to
+        // spmm_hub_kernel (column-split CTA per row), the balanced kernel skips them
+        const int hubs = dyn == kSchedBalOne && R::kLutBytes == 0 && NV == 1;
+        if (hubs) {
+            static bool hub_attr = false;
+            const size_t hub_smem = (size_t)kHubWarps * kHubRing * 128;
+            if (!hub_attr) {
+                AES_CUDA_TRY(cudaFuncSetAttribute(spmm_hub_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)hub_smem));
+                hub_attr = true;
+            }
+            spmm_hub_kernel<<<(unsigned)((n + kHubRows - 1) / kHubRows), kHubWarps * 32, hub_smem, st>>>(
+                srow, scol, sval, n, reinterpret_cast<const float*>(g.base()), (uint64_t)g.ld4 * 4, f4 * 4,
+                reinterpret_cast<float*>(c), ldc4 * 4, grid * W);
+            AES_CUDA_TRY(cudaGetLastError());
+        }
+        spmm_ring_bal_kernel<R, NV, C, W, FULL><<<(unsigned)grid, W * 32, smem, st>>>(
+            srow, scol, sval, n, g.base(), (uint32_t)g.ld4, f4, c, ldc4, lut, hubs);
         AES_CUDA_TRY(cudaGetLastError());
         return AES_OK;
     }

@@ -260,6 +260,16 @@ def weights_finite(w: torch.Tensor, stream=None) -> bool:
     return int(flag.item()) == 0
 
 
+def all_weights_finite(weights, stream=None) -> list[bool]:
+    """weights_finite for several tensors with a single device read-back."""
+    if not weights:
+        return []
+    flags = torch.zeros(len(weights), dtype=torch.int32, device=weights[0].device)
+    for i, w in enumerate(weights):
+        check(lib().aes_dev_all_finite(ptr(w), w.numel(), flags.data_ptr() + 4 * i, stream_of(stream)))
+    return [v == 0 for v in flags.cpu().tolist()]
+
+
 def gemm_bias_act(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None, relu: bool, out=None,
                   stream=None, finite_w: bool | None = False) -> torch.Tensor:
     """act(a @ w + bias) with the reference's ordered fp32 arithmetic
@@ -311,10 +321,12 @@ def gcn_forward(graph: Graph, x: torch.Tensor, weights, biases, plan: SampledPla
     h = padded(x)
     srow, scol, sval = (plan.srow_ptr, plan.scol, plan.sval) if plan is not None else (
         graph.row_ptr, graph.col, graph.val)
+    bound = plan.row_bound if plan is not None else 0
+    finite = all_weights_finite(weights, stream)  # one read-back for every layer
     for l, (w, b) in enumerate(zip(weights, biases)):
-        agg = spmm(srow, scol, sval, h, stream=stream)
+        agg = spmm(srow, scol, sval, h, stream=stream, max_row_slots=bound)
         if fast_gemm and agg.shape[1] <= 128 and w.shape[1] <= 128:
             h = gemm_tf32(agg, w, b, relu=l + 1 < len(weights), stream=stream)
         else:
-            h = gemm_bias_act(agg, w, b, relu=l + 1 < len(weights), stream=stream, finite_w=None)
+            h = gemm_bias_act(agg, w, b, relu=l + 1 < len(weights), stream=stream, finite_w=finite[l])
     return h
