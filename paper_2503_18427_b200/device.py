@@ -314,15 +314,18 @@ def gemm_tf32(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None, relu:
 
 
 def gcn_forward(graph: Graph, x: torch.Tensor, weights, biases, plan: SampledPlan | None = None,
-                stream=None, fast_gemm: bool = False) -> torch.Tensor:
+                stream=None, fast_gemm: bool = False, finite=None) -> torch.Tensor:
     """gcn_forward (proj/src/gnn.cpp:66-78) on one GPU, all tensors in HBM.
     fast_gemm=True runs the layer transform on the tcgen05 tensor cores (TF32,
-    not bit-exact); the aggregation stays the exact sampled SpMM."""
+    not bit-exact); the aggregation stays the exact sampled SpMM.  finite:
+    per-layer "weights have no inf/NaN" flags (checked on the device with one
+    read-back when None)."""
     h = padded(x)
     srow, scol, sval = (plan.srow_ptr, plan.scol, plan.sval) if plan is not None else (
         graph.row_ptr, graph.col, graph.val)
     bound = plan.row_bound if plan is not None else 0
-    finite = all_weights_finite(weights, stream)  # one read-back for every layer
+    if finite is None:
+        finite = all_weights_finite(weights, stream)  # one read-back for every layer
     for l, (w, b) in enumerate(zip(weights, biases)):
         agg = spmm(srow, scol, sval, h, stream=stream, max_row_slots=bound)
         if fast_gemm and agg.shape[1] <= 128 and w.shape[1] <= 128:
@@ -330,3 +333,38 @@ def gcn_forward(graph: Graph, x: torch.Tensor, weights, biases, plan: SampledPla
         else:
             h = gemm_bias_act(agg, w, b, relu=l + 1 < len(weights), stream=stream, finite_w=finite[l])
     return h
+
+
+class GcnForwardGraph:
+    """gcn_forward captured once into a CUDA graph and replayed per call.
+
+    For the small BASELINE graphs (cora, pubmed, arxiv) a forward is a dozen
+    short kernels whose host-side launch cost (Python + ctypes per call)
+    exceeds their GPU time; replaying one graph launches them all with a
+    single call.  Shapes, weights, plan and output buffers are fixed at
+    capture; run(x) copies x into the captured input and replays.  The
+    kernels and their results are exactly those of gcn_forward."""
+
+    def __init__(self, graph: Graph, x_like: torch.Tensor, weights, biases, plan: SampledPlan | None = None,
+                 fast_gemm: bool = False):
+        self.weights, self.biases = list(weights), list(biases)
+        finite = all_weights_finite(self.weights)
+        self.x = empty_padded(x_like.shape[0], x_like.shape[1], device=x_like.device)
+        self.x.copy_(x_like)
+        self.stream = torch.cuda.Stream()
+        self.stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self.stream):  # warm-up: kernel attributes, allocator pool
+            gcn_forward(graph, self.x, self.weights, self.biases, plan, fast_gemm=fast_gemm, finite=finite)
+        self.stream.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            self.out = gcn_forward(graph, self.x, self.weights, self.biases, plan, fast_gemm=fast_gemm,
+                                   finite=finite)
+
+    def run(self, x: torch.Tensor | None = None) -> torch.Tensor:
+        """Forward of x (None: the input already in self.x); returns the
+        captured output buffer (overwritten by the next run)."""
+        if x is not None:
+            self.x.copy_(x)
+        self.graph.replay()
+        return self.out

@@ -97,6 +97,12 @@ def test_device_gcn_forward(dev):
     out = dev.gcn_forward(g, torch.from_numpy(x).cuda(), tw, tb, plan)
     want = port.gcn_forward(nrp, ncol, nval, x, ws, bs, 32)
     assert np.array_equal(bits(to_np(out)), bits(want))
+    # the same forward captured in a CUDA graph and replayed, on new inputs too
+    cg = dev.GcnForwardGraph(g, torch.from_numpy(x).cuda(), tw, tb, plan)
+    assert np.array_equal(bits(to_np(cg.run())), bits(want))
+    x2 = rng.uniform(-1, 1, (3000, 128)).astype(np.float32)
+    got2 = to_np(cg.run(torch.from_numpy(x2).cuda()))
+    assert np.array_equal(bits(got2), bits(port.gcn_forward(nrp, ncol, nval, x2, ws, bs, 32)))
 
 
 @pytest.mark.slow
