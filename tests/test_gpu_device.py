@@ -374,7 +374,8 @@ def test_quantize_threshold_table_extremes(dev, bits, shape):
         # values around the code boundaries: the dequantized grid and its neighbours
         grid = np.float32(lo) + (np.arange(n // 4) % ((1 << bits) + 1)).astype(np.float64) * \
             (span / ((1 << bits) - 1) if span else 0.0)
-        g32 = grid.astype(np.float32)
+        with np.errstate(over="ignore"):  # grid points past FLT_MAX become inf: fine, also a test value
+            g32 = grid.astype(np.float32)
         x[: n // 4] = np.where(rng.random(n // 4) < 0.5, np.nextafter(g32, np.float32(np.inf)),
                                np.nextafter(g32, np.float32(-np.inf)))
         special = np.array([lo, hi, 0.0, -0.0, np.inf, -np.inf, 3.4028235e38, -3.4028235e38, 1e-45, -1e-45],
