@@ -342,6 +342,16 @@ AES_API int aes_dev_gemm_bias_act_ex(const float* a, uint64_t m, uint64_t k, uin
                                      int relu, int finite_w, float* const* dsts,
                                      unsigned long long* const* counters, int n_dst,
                                      uint64_t row_offset, uint64_t ldh, void* stream);
+/* Same with halo masks (need: one per destination, NULL entries = every
+ * row): output row r (replica index) is stored to destination d only if
+ * need[d][r] != 0 — the rows d's sampled slots reference (SURVEY §8f rank 1:
+ * a shard needs 93 / 74 / 49 % of the remote rows at P = 2 / 4 / 8).  The
+ * arrival count per CTA is unchanged. */
+AES_API int aes_dev_gemm_bias_act_halo(const float* a, uint64_t m, uint64_t k, uint64_t lda,
+                                       const float* w, uint64_t n, uint64_t ldw, const float* bias,
+                                       int relu, int finite_w, float* const* dsts,
+                                       unsigned long long* const* counters, const uint8_t* const* need,
+                                       int n_dst, uint64_t row_offset, uint64_t ldh, void* stream);
 /* FAST MODE (opt-in, not bit-exact): the same layer GEMM on the tcgen05
  * tensor cores (kind::tf32, TMA-fed, TMEM accumulators).  Error bound
  * |H - H_exact| <= 2^-8 * sum_k |a_ik||w_kj| per element (TF32 operands, fp32
@@ -396,10 +406,13 @@ AES_API int aes_dev_fold_params_lut(const float* params, int world, uint32_t bit
 AES_API uint64_t aes_quantize_bcast_ctas(uint64_t rows);
 /* quantize(x, (lohi[0], lohi[1]), bits) of this shard's rows, codes stored
  * at rows row_off.. of every dst_codes[d] (ldq % 16 == 0), then one
- * system-scope release-add per CTA on every peer_counters[d]. */
+ * system-scope release-add per CTA on every peer_counters[d].  need (NULL, or
+ * one per destination, NULL entries = every row): halo masks, row r is sent
+ * to d only if need[d][r] != 0 (the rows d's sampled slots reference). */
 AES_API int aes_dev_quantize_bcast(const float* x, uint64_t rows, uint64_t cols, uint64_t ldx, const float* lohi,
                                    uint32_t bits, uint8_t* const* dst_codes, uint64_t row_off, uint64_t ldq,
-                                   unsigned long long* const* peer_counters, int world, void* stream);
+                                   unsigned long long* const* peer_counters, const uint8_t* const* need,
+                                   int world, void* stream);
 
 #ifdef __cplusplus
 }

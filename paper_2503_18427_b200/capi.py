@@ -54,6 +54,8 @@ def lib():
         L.aes_dev_gemm_bias_act.argtypes = [vp, u64, u64, u64, vp, u64, u64, vp, i32, vp, u64, vp]
         L.aes_dev_gemm_bias_act_ex.argtypes = [vp, u64, u64, u64, vp, u64, u64, vp, i32, i32, vp, vp, i32, u64,
                                                u64, vp]
+        L.aes_dev_gemm_bias_act_halo.argtypes = [vp, u64, u64, u64, vp, u64, u64, vp, i32, i32, vp, vp, vp, i32,
+                                                 u64, u64, vp]
         L.aes_dev_gemm_tf32.argtypes = [vp, u64, u64, u64, vp, u64, u64, vp, i32, vp, u64, vp, vp]
         L.aes_gemm_tf32_scratch_floats.argtypes = [u64, u64]
         L.aes_gemm_tf32_scratch_floats.restype = u64
@@ -70,7 +72,7 @@ def lib():
         L.aes_dev_fold_params_lut.argtypes = [vp, i32, u32, vp, vp, vp]
         L.aes_quantize_bcast_ctas.argtypes = [u64]
         L.aes_quantize_bcast_ctas.restype = u64
-        L.aes_dev_quantize_bcast.argtypes = [vp, u64, u64, u64, vp, u32, vp, u64, u64, vp, i32, vp]
+        L.aes_dev_quantize_bcast.argtypes = [vp, u64, u64, u64, vp, u32, vp, u64, u64, vp, vp, i32, vp]
         cp = C.c_char_p
         L.aes_fmat_info.argtypes = [cp, vp, vp, vp, vp, vp]
         L.aes_fmat_load_device.argtypes = [cp, vp, u64, vp]

@@ -118,7 +118,7 @@ __global__ void fold_params_lut_kernel(const float* __restrict__ params, int wor
 __global__ void __launch_bounds__(kQuantThreads)
 quantize_bcast_kernel(const float* __restrict__ x, uint64_t rows, uint32_t cols, uint64_t ldx,
                       const float* __restrict__ lohi, uint32_t levels, PtrArr dst, uint64_t row_off, uint64_t ldq,
-                      PtrArr ctrs, int n, bool vec) {
+                      PtrArr ctrs, PtrArr need, int n, bool vec) {
     const uint64_t r0 = (uint64_t)blockIdx.x * kQuantRows;
     const uint32_t nr = (uint32_t)min((uint64_t)kQuantRows, rows - r0);
     const QuantParamsDev p = quant_params(lohi[0], lohi[1], levels);
@@ -142,6 +142,8 @@ quantize_bcast_kernel(const float* __restrict__ x, uint64_t rows, uint32_t cols,
             for (int i = 0; i < 4; ++i)
                 if (c + i < cols) packed |= quant_code(v[i], p) << (8 * i);
             for (int d = 0; d < n; ++d) {
+                const uint8_t* nd = static_cast<const uint8_t*>(need.p[d]);
+                if (nd && !nd[row_off + r]) continue;  // halo: d never reads this row
                 uint8_t* row = static_cast<uint8_t*>(dst.p[d]) + (row_off + r) * ldq;
                 if (c + 4 <= cols) {
                     *reinterpret_cast<uint32_t*>(row + c) = packed;  // ldq % 16 == 0, c % 4 == 0
@@ -195,7 +197,8 @@ uint64_t aes_quantize_bcast_ctas(uint64_t rows) { return (rows + aes::kQuantRows
 
 int aes_dev_quantize_bcast(const float* x, uint64_t rows, uint64_t cols, uint64_t ldx, const float* lohi,
                            uint32_t bits, uint8_t* const* dst_codes, uint64_t row_off, uint64_t ldq,
-                           unsigned long long* const* peer_counters, int world, void* stream) {
+                           unsigned long long* const* peer_counters, const uint8_t* const* need, int world,
+                           void* stream) {
     using namespace aes;
     if (world < 1 || world > kMaxRanks) return fail(AES_ERR_INVALID_ARG, "1..16 ranks");
     if (bits < 1 || bits > 8) return fail(AES_ERR_UNSUPPORTED, "int8 exchange needs bits <= 8");
@@ -203,16 +206,17 @@ int aes_dev_quantize_bcast(const float* x, uint64_t rows, uint64_t cols, uint64_
     const uint64_t ctas = aes_quantize_bcast_ctas(rows);
     if (ctas == 0) return AES_OK;
     if (ctas >= (1ull << 31)) return fail(AES_ERR_INVALID_ARG, "too many rows");
-    PtrArr dp{}, cp{};
+    PtrArr dp{}, cp{}, np_{};
     for (int d = 0; d < world; ++d) {
         dp.p[d] = dst_codes[d];
         cp.p[d] = peer_counters[d];
+        np_.p[d] = need ? const_cast<uint8_t*>(need[d]) : nullptr;
     }
     if (cols >= (1ull << 32)) return fail(AES_ERR_INVALID_ARG, "too many columns");
     // rows 16-B aligned and padded to whole float4s: vector loads
     const bool vec = ldx % 4 == 0 && (uintptr_t)x % 16 == 0 && ldx >= (cols + 3) / 4 * 4;
     quantize_bcast_kernel<<<(unsigned)ctas, kQuantThreads, 0, as_stream(stream)>>>(
-        x, rows, (uint32_t)cols, ldx, lohi, (1u << bits) - 1u, dp, row_off, ldq, cp, world, vec);
+        x, rows, (uint32_t)cols, ldx, lohi, (1u << bits) - 1u, dp, row_off, ldq, cp, np_, world, vec);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
 }

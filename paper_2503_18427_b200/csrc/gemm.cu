@@ -28,6 +28,7 @@ constexpr int kMaxDst = 16;
 struct Bcast {
     float* dst[kMaxDst];                   // replica base pointers (own + peers)
     unsigned long long* ctr[kMaxDst];      // arrival counters (one per destination rank)
+    const uint8_t* need[kMaxDst];          // halo masks: row r goes to d only if need[d][r] (null: every row)
     int n;
     uint64_t row_off;                      // this shard's first row in the replica
 };
@@ -126,6 +127,7 @@ gemm_ordered_kernel(const float* __restrict__ a, uint64_t m, uint64_t k, uint64_
         }
         const int nd = BCAST ? bc.n : 1;
         for (int d = 0; d < nd; ++d) {
+            if (BCAST && bc.need[d] && !bc.need[d][bc.row_off + gm]) continue;  // halo: d never reads this row
             float* row = BCAST ? bc.dst[d] + (bc.row_off + gm) * ldh : h + gm * ldh;
             if (vec) {
                 reinterpret_cast<float4*>(row + gn0)[0] = make_float4(v[0], v[1], v[2], v[3]);
@@ -224,6 +226,14 @@ int aes_dev_gemm_bias_act_ex(const float* a, uint64_t m, uint64_t k, uint64_t ld
                              uint64_t ldw, const float* bias, int relu, int finite_w, float* const* dsts,
                              unsigned long long* const* counters, int n_dst, uint64_t row_offset, uint64_t ldh,
                              void* stream) {
+    return aes_dev_gemm_bias_act_halo(a, m, k, lda, w, n, ldw, bias, relu, finite_w, dsts, counters, nullptr, n_dst,
+                                      row_offset, ldh, stream);
+}
+
+int aes_dev_gemm_bias_act_halo(const float* a, uint64_t m, uint64_t k, uint64_t lda, const float* w, uint64_t n,
+                               uint64_t ldw, const float* bias, int relu, int finite_w, float* const* dsts,
+                               unsigned long long* const* counters, const uint8_t* const* need, int n_dst,
+                               uint64_t row_offset, uint64_t ldh, void* stream) {
     using namespace aes;
     if (n_dst < 1 || n_dst > kMaxDst) return fail(AES_ERR_INVALID_ARG, "1..16 destinations");
     if (lda < k || ldw < n || ldh < n) return fail(AES_ERR_INVALID_ARG, "leading dimension too small");
@@ -234,6 +244,7 @@ int aes_dev_gemm_bias_act_ex(const float* a, uint64_t m, uint64_t k, uint64_t ld
     for (int d = 0; d < n_dst; ++d) {
         bc.dst[d] = dsts[d];
         bc.ctr[d] = counters ? counters[d] : nullptr;
+        bc.need[d] = need ? need[d] : nullptr;
     }
     cudaStream_t st = as_stream(stream);
     const bool bcast = counters != nullptr;

@@ -75,12 +75,25 @@ class PeerReplicas:
         self.bar_expected = 0
         self.par_expected = 0
         self.code_expected = 0
+        self.need_ptrs = None
         torch.cuda.synchronize()
         if dist.is_initialized():
             dist.barrier(group)
 
+    def set_halo(self, need: torch.Tensor):
+        """This rank's halo mask (uint8 [rows]: 1 = this rank reads that row of
+        the replicas); every producer then stores a row into this rank's
+        replica only where the mask is set."""
+        self.need = need.contiguous()
+        peers = _exchange(self.need, self.group) if self.world > 1 else [self.need]
+        self._peer_need = peers  # keep the IPC mappings alive
+        self.need_ptrs = (ctypes.c_void_p * self.world)(*[t.data_ptr() for t in peers])
+        torch.cuda.synchronize()
+        if dist.is_initialized():
+            dist.barrier(self.group)
+
     def gemm_publish(self, out_buf: int, a: torch.Tensor, w: torch.Tensor, bias, relu: bool, finite_w: bool,
-                     row_offset: int, stream=None, fast: bool = False):
+                     row_offset: int, stream=None, fast: bool = False, halo: bool = False):
         """act(a @ w + bias) for this rank's rows, stored into every rank's
         replica `out_buf` at rows [row_offset, row_offset + m).  fast=True
         uses the tcgen05 TF32 kernel whose TMA-store epilogue writes the
@@ -98,11 +111,12 @@ class PeerReplicas:
                 row_offset, self.ld, scratch.data_ptr(), stream_of(stream)))
             self._keep = scratch  # alive until the stream passes the next wait
             return
-        check(lib().aes_dev_gemm_bias_act_ex(
+        need = ctypes.cast(self.need_ptrs, ctypes.c_void_p) if halo and self.need_ptrs is not None else None
+        check(lib().aes_dev_gemm_bias_act_halo(
             a.data_ptr(), m, k, a.stride(0), w.data_ptr(), n, w.stride(0),
             None if bias is None or bias.numel() == 0 else bias.data_ptr(), int(relu), int(finite_w),
-            ctypes.cast(self.dst[out_buf], ctypes.c_void_p), ctypes.cast(self.ctr, ctypes.c_void_p), self.world,
-            row_offset, self.ld, stream_of(stream)))
+            ctypes.cast(self.dst[out_buf], ctypes.c_void_p), ctypes.cast(self.ctr, ctypes.c_void_p), need,
+            self.world, row_offset, self.ld, stream_of(stream)))
 
     def barrier(self, stream=None):
         """Device-side barrier across ranks (stream-ordered): no rank starts
@@ -135,14 +149,17 @@ class PeerReplicas:
         check(lib().aes_dev_fold_params_lut(self.params[buf].data_ptr(), self.world, 8, out4.data_ptr(),
                                             lut.data_ptr(), st))
 
-    def quantize_publish(self, buf: int, x: torch.Tensor, lohi: torch.Tensor, row_offset: int, stream=None):
+    def quantize_publish(self, buf: int, x: torch.Tensor, lohi: torch.Tensor, row_offset: int, stream=None,
+                         halo: bool = False):
         """Codes of this rank's rows x (params from the device fold) into every
         rank's code replica `buf` at rows [row_offset, row_offset + len(x))."""
         rows, cols = x.shape
         check(lib().aes_dev_quantize_bcast(x.data_ptr(), rows, cols, x.stride(0), lohi.data_ptr(), 8,
                                            ctypes.cast(self.code_dst[buf], ctypes.c_void_p), row_offset,
-                                           self.code_ld, ctypes.cast(self.code_ctr, ctypes.c_void_p), self.world,
-                                           stream_of(stream)))
+                                           self.code_ld, ctypes.cast(self.code_ctr, ctypes.c_void_p),
+                                           ctypes.cast(self.need_ptrs, ctypes.c_void_p)
+                                           if halo and self.need_ptrs is not None else None,
+                                           self.world, stream_of(stream)))
 
     def wait_codes(self, arrivals: int, stream=None):
         self.code_expected += arrivals

@@ -34,7 +34,7 @@ def _problem(n=3001, f=40):
     return nrp, ncol, nval, x, ws, bs
 
 
-def _run(rank, world, port_no, q, fast=False, exchange_dtype="f32"):
+def _run(rank, world, port_no, q, fast=False, exchange_dtype="f32", halo=False):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
@@ -50,10 +50,19 @@ def _run(rank, world, port_no, q, fast=False, exchange_dtype="f32"):
         model = ShardedGCN(plan.srow_ptr, plan.scol, plan.sval, g.n_rows,
                            [torch.from_numpy(w).cuda() for w in ws], [torch.from_numpy(b).cuda() for b in bs],
                            exchange="p2p", fast_gemm=fast, exchange_dtype=exchange_dtype,
-                           max_row_slots=plan.row_bound)
+                           max_row_slots=plan.row_bound, halo=halo)
         xt = torch.from_numpy(x).cuda()
         outs = [model.forward(xt).cpu().numpy() for _ in range(3)]  # repeated steps exercise the barrier
         torch.cuda.synchronize()
+        if halo and exchange_dtype == "f32":
+            # rows this rank never reads were never sent: in the replica that
+            # held the input (40 columns) and then the second hidden layer
+            # (64 columns), their columns 40..63 are still the initial zeros
+            need = model.replicas.need[: g.n_rows].bool()
+            unsent = ~need
+            tail = model.replicas.bufs[0][: g.n_rows, 40:64]
+            outs.append((int(unsent.sum().item()), bool((tail[unsent] == 0).all().item()),
+                         float((tail[need] != 0).any(1).float().mean().item())))
         q.put((rank, outs))
     except Exception as e:  # surface the failure to the parent
         import traceback
@@ -135,3 +144,33 @@ def test_p2p_int8_exchange_matches_reference_composition(world):
     for _, outs in res:
         for o in outs:
             assert np.array_equal(np.ascontiguousarray(o).view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("exchange_dtype", ["f32", "int8"])
+def test_p2p_halo_exchange_matches_oracle(exchange_dtype):
+    """Halo exchange: producers store a hidden-layer row
+    into a peer's replica only where the peer's sampled slots reference it.
+    Results stay bit-exact, and the rows a rank never reads are never sent."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = _free_port()
+    procs = [ctx.Process(target=_run, args=(r, 2, p, q, False, exchange_dtype, True)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = sorted([q.get(timeout=300) for _ in procs], key=lambda t: t[0])
+    for pr in procs:
+        pr.join(timeout=120)
+    for _, outs in res:
+        assert not isinstance(outs, str), outs
+    nrp, ncol, nval, x, ws, bs = _problem()
+    if exchange_dtype == "f32":
+        want = port.gcn_forward(nrp, ncol, nval, x, ws, bs, 16)
+    else:
+        want = port.gcn_forward_int8_exchange(nrp, ncol, nval, x, ws, bs, 16)
+    for _, outs in res:
+        for o in outs[:3]:
+            assert np.array_equal(np.ascontiguousarray(o).view(np.uint32), want.view(np.uint32))
+        if exchange_dtype == "f32":
+            n_unsent, untouched, sent_filled = outs[3]
+            assert n_unsent > 0 and untouched and sent_filled > 0.9
