@@ -427,9 +427,12 @@ def run_gcn_layer(args, plan, n, f, b, dist):
     # (GEMM epilogue broadcast) or as int8 codes (device param fold + quantize
     # straight into every replica, exchange.cu); exact GEMMs, input copied in
     w2 = (torch.rand(f, f, device="cuda", generator=torch.Generator("cuda").manual_seed(4)) - 0.5)
-    for name, xdt in (("f32", "f32"), ("int8", "int8")):
+    variants = [("f32", "f32", False), ("int8", "int8", False)]
+    if dist:  # halo masks only differ from a full broadcast with peers
+        variants += [("f32_halo", "f32", True), ("int8_halo", "int8", True)]
+    for name, xdt, halo in variants:
         model = ShardedGCN(plan.srow_ptr, plan.scol, plan.sval, n, [w, w2], [bias, bias], exchange="p2p",
-                           exchange_dtype=xdt, max_row_slots=plan.row_bound)
+                           exchange_dtype=xdt, max_row_slots=plan.row_bound, halo=halo)
         for _ in range(2):
             model.forward(x, copy_out=False)
         torch.cuda.synchronize()
@@ -447,6 +450,7 @@ def run_gcn_layer(args, plan, n, f, b, dist):
     out["exchange"] = "fused into the GEMM epilogue (P2P stores to every rank's replica + sys-scope arrivals)"
     out["int8_exchange"] = ("hidden layer output as 8-bit codes: per-rank fit_params published to every rank, "
                             "rank-order fold + LUT on the device, codes quantized into every replica (4x fewer bytes)")
+    out["halo"] = "hidden-layer rows stored only into the replicas whose sampled slots reference them (N > 1)"
     out["note"] = "exact mode is bit-exact with the reference; fast mode |err| <= 2^-8 sum|a||w| (TF32)"
     return out
 
