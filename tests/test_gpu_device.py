@@ -369,8 +369,9 @@ def test_quantize_threshold_table_extremes(dev, bits, shape):
         lo, hi = float(np.float32(lo)), float(np.float32(hi))
         n = shape[0] * shape[1]
         span = hi - lo
-        x = rng.uniform(lo - 0.1 * span, hi + 0.1 * span, n).astype(np.float32) if span else \
-            rng.uniform(-1, 1, n).astype(np.float32)
+        with np.errstate(over="ignore"):  # (-3e38, 3e38) +- 10 %: beyond FLT_MAX -> +-inf, also test values
+            x = rng.uniform(lo - 0.1 * span, hi + 0.1 * span, n).astype(np.float32) if span else \
+                rng.uniform(-1, 1, n).astype(np.float32)
         # values around the code boundaries: the dequantized grid and its neighbours
         grid = np.float32(lo) + (np.arange(n // 4) % ((1 << bits) + 1)).astype(np.float64) * \
             (span / ((1 << bits) - 1) if span else 0.0)
