@@ -393,6 +393,19 @@ def run_ours(args):
     return 0
 
 
+def release(model):
+    """Drop a model's peer mappings on every rank before any rank frees the
+    exported buffers (CUDA IPC: consumers close before producers exit)."""
+    import gc
+
+    import torch
+    model.replicas = None
+    gc.collect()
+    torch.cuda.synchronize()
+    if torch.distributed.is_initialized():
+        torch.distributed.barrier()
+
+
 def run_gcn_layer(args, plan, n, f, b, dist):
     """Time one GCN layer (F -> F, ReLU) with gcn.ShardedGCN(exchange="p2p"):
     sampled SpMM of this rank's rows, then the layer GEMM whose epilogue writes
@@ -422,6 +435,7 @@ def run_gcn_layer(args, plan, n, f, b, dist):
         e.record()
         torch.cuda.synchronize()
         out[name + "_ms"] = round(max_over_ranks(s.elapsed_time(e) / steps, dist), 4)
+        release(model)
         del model
     # two layers (F -> F -> F): the hidden output crosses the exchange as fp32
     # (GEMM epilogue broadcast) or as int8 codes (device param fold + quantize
@@ -446,6 +460,7 @@ def run_gcn_layer(args, plan, n, f, b, dist):
         e.record()
         torch.cuda.synchronize()
         out[f"two_layer_{name}_exchange_ms"] = round(max_over_ranks(s.elapsed_time(e) / steps, dist), 4)
+        release(model)
         del model
     out["exchange"] = "fused into the GEMM epilogue (P2P stores to every rank's replica + sys-scope arrivals)"
     out["int8_exchange"] = ("hidden layer output as 8-bit codes: per-rank fit_params published to every rank, "
