@@ -956,7 +956,11 @@ int launch_q8_dual(const uint64_t* srow, const uint32_t* scol, const float* sval
 // slot p of warp w is hole w*C + p.
 // ---------------------------------------------------------------------------
 template <int C, int WARPS, bool FULL, bool FASTB, int SCHED>  // SCHED: 0 static, 1 dynamic, 2 balanced
-__global__ void __launch_bounds__(WARPS * 32, 3)  // 3 x 72 KB of shared memory per SM
+// 3 x 74 KB CTAs per SM (40 registers) for whole 128-code tiles; the partial-
+// tile form (F % 128 != 0, e.g. reddit's 602) runs faster at 2 CTAs with room
+// for 64 registers (reddit int8 0.64 -> 0.59 ms; products, whole tiles, loses
+// 4-20 % that way)
+__global__ void __launch_bounds__(WARPS * 32, FULL ? 3 : 2)
 spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
                      const float* __restrict__ sval, uint64_t n_rows, const unsigned char* __restrict__ q,
                      uint32_t ldq, uint32_t f4, float4* __restrict__ c, uint64_t ldc4,
