@@ -587,7 +587,7 @@ __device__ __forceinline__ void bal_range(const uint64_t* __restrict__ srow, uin
 
 // Hub rows (rows of unknown length: exact SpMM, FULL plans).  A row holding
 // far more than a balanced warp share keeps its one warp busy long after the
-// rest finish (arxiv exact: a 13 k-slot row takes 0.8 ms on one warp while
+// rest finish (arxiv exact: its 8.8 k-slot row took 0.8 ms on one warp while
 // the whole rest of the graph needs 0.1 ms).  Order forbids splitting a row's
 // slots, but not its columns: spmm_hub_kernel gives each hub row a CTA whose
 // 128 lanes own one output column each and stream the row's slots through
