@@ -383,6 +383,27 @@ AES_API int aes_dev_signal_all(unsigned long long* const* counters, int n, void*
 /* *bad_flag = 1 if any of x[0..count) is inf/NaN (stream-ordered). */
 AES_API int aes_dev_all_finite(const float* x, uint64_t count, unsigned int* bad_flag, void* stream);
 
+/* ---- row-sharded GCN forward over NCCL (sharded.cu) ----------------------
+ * gcn_forward (proj/src/gnn.cpp:66-78) on one rank of an equal-row sharded
+ * graph: per layer the shard's sampled SpMM, the ordered-fp32 GEMM + bias
+ * (+ ReLU but on the last layer) into a [rows_per_rank, ld] block, and an
+ * ncclAllGather of the blocks (rank order) into the other replica.
+ * srow_shard: the shard's shard_rows+1 row offsets into the GLOBAL sampled
+ * CSR (scol, sval); replica_a holds the layer-0 input for every row
+ * ([world * rows_per_rank, ld], ld % 4 == 0, dims[l] <= ld), replica_b is the
+ * ping-pong partner; *out_replica receives the one holding the logits of all
+ * rows.  weights / biases: host arrays of n_layers device pointers (biases
+ * may be NULL or hold NULL entries).  nccl_comm: the caller's ncclComm_t
+ * (NCCL is looked up at run time in the process).  Bit-identical to the
+ * single-GPU forward.  Stream-ordered; no host synchronisation. */
+AES_API uint64_t aes_gcn_sharded_workspace_bytes(uint64_t rows_per_rank, uint64_t ld);
+AES_API int aes_gcn_forward_sharded(const uint64_t* srow_shard, const uint32_t* scol, const float* sval,
+                                    uint64_t shard_rows, uint64_t rows_per_rank, int n_layers, const uint64_t* dims,
+                                    const float* const* weights, const float* const* biases, int finite_w,
+                                    float* replica_a, float* replica_b, uint64_t ld, uint64_t max_row_slots,
+                                    void* workspace, size_t workspace_bytes, void* nccl_comm, float** out_replica,
+                                    void* stream);
+
 /* ---- int8 layer exchange over peer memory (exchange.cu) ------------------
  * Replaces, per hidden GCN layer, the reference composition
  * dequantize(quantize(H, fit_params(H))) (proj/src/quantize.cpp:11-64) +

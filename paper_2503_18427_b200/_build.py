@@ -66,7 +66,7 @@ def build(force: bool = False, verbose: bool = False) -> None:
                     print(r.stdout, r.stderr)
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < _newest(objs):
         _run([NVCC] + GENCODE + ["-shared", "-o", LIB] + objs +
-             ["-Xlinker", "-soname,libaescuda.so", "-cudart=static"])
+             ["-Xlinker", "-soname,libaescuda.so", "-cudart=static", "-ldl"])
     core_src = os.path.join(CSRC, "pybind_core.cpp")
     if force or not os.path.exists(CORE) or os.path.getmtime(CORE) < max(
             os.path.getmtime(core_src), os.path.getmtime(LIB), hdr_time):

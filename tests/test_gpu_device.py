@@ -391,3 +391,52 @@ def test_quantize_threshold_table_extremes(dev, bits, shape):
         want = port.quantize(x, lo, hi, bits)
         got = to_np(q.codes).astype(np.uint16)
         assert np.array_equal(got, want), (lo, hi, bits, int((got != want).sum()))
+
+
+def test_gcn_forward_sharded_c_abi_nccl(dev):
+    """aes_gcn_forward_sharded (the C-ABI row-sharded forward over an
+    ncclComm_t) on a one-rank NCCL communicator: the replica it
+    returns holds the single-GPU forward's logits bit for bit."""
+    import ctypes
+
+    import torch
+
+    from paper_2503_18427_b200 import capi
+    L = capi.lib()
+    nccl = ctypes.CDLL("libnccl.so.2")  # the copy torch already loaded
+    comm = ctypes.c_void_p()
+    dev_list = (ctypes.c_int * 1)(torch.cuda.current_device())
+    assert nccl.ncclCommInitAll(ctypes.byref(comm), 1, dev_list) == 0
+    try:
+        rng = np.random.default_rng(12)
+        n = 2500
+        rp, col, _ = graphs.power_law(n, alpha=1.8, max_deg=400, seed=12)
+        nrp, ncol, nval = port.gcn_normalize(rp, col, True)
+        g = dev.Graph.from_numpy(nrp, ncol, nval)
+        plan = dev.SampledPlan(g, 16)
+        dims = [40, 64, 64, 7]
+        x = rng.uniform(-1, 1, (n, dims[0])).astype(np.float32)
+        ws = [rng.uniform(-0.5, 0.5, (a, b)).astype(np.float32) for a, b in zip(dims, dims[1:])]
+        bs = [np.full(b, 0.01, np.float32) for b in dims[1:]]
+        tw = [torch.from_numpy(w).cuda() for w in ws]
+        tb = [torch.from_numpy(b).cuda() for b in bs]
+        ld = 64
+        ra = torch.zeros((n, ld), device="cuda")
+        rb = torch.zeros((n, ld), device="cuda")
+        ra[:, : dims[0]] = torch.from_numpy(x).cuda()
+        wsb = int(L.aes_gcn_sharded_workspace_bytes(n, ld))
+        work = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+        dims_h = (ctypes.c_uint64 * 4)(*dims)
+        wp = (ctypes.c_void_p * 3)(*[t.data_ptr() for t in tw])
+        bp = (ctypes.c_void_p * 3)(*[t.data_ptr() for t in tb])
+        out = ctypes.c_void_p()
+        capi.check(L.aes_gcn_forward_sharded(plan.srow_ptr.data_ptr(), plan.scol.data_ptr(), plan.sval.data_ptr(),
+                                             n, n, 3, dims_h, wp, bp, 1, ra.data_ptr(), rb.data_ptr(), ld,
+                                             plan.row_bound, work.data_ptr(), wsb, comm, ctypes.byref(out),
+                                             capi.stream_of(None)))
+        torch.cuda.synchronize()
+        got = (ra if out.value == ra.data_ptr() else rb)[:, : dims[-1]].cpu().numpy()
+        want = port.gcn_forward(nrp, ncol, nval, x, ws, bs, 16)
+        assert np.array_equal(bits(got), bits(want))
+    finally:
+        nccl.ncclCommDestroy(comm)
