@@ -207,10 +207,12 @@ def test_every_spmm_schedule_is_bit_exact(dev, variant):
 
 
 @pytest.mark.parametrize("sched", [0, 1, 2, 3])
-def test_ring_schedules_bit_exact(dev, sched):
+@pytest.mark.parametrize("f", [128, 100])
+def test_ring_schedules_bit_exact(dev, sched, f):
     """Auto, static, heavy-first dynamic and balanced row schedules give the
     oracle's bits, on a graph whose hub rows exceed the heavy threshold (4096
-    slots)."""
+    slots) and the hub-row kernel's (auto: column-split CTA per hub row; F=100
+    exercises its partial last column block)."""
     import torch
 
     from paper_2503_18427_b200 import capi
@@ -218,7 +220,7 @@ def test_ring_schedules_bit_exact(dev, sched):
     rp, col, val = graphs.power_law(12000, alpha=1.2, max_deg=9000, seed=3)
     assert np.diff(rp).max() > 4096
     g = dev.Graph.from_numpy(rp, col, val)
-    x_np = np.random.default_rng(3).uniform(-1, 1, (12000, 128)).astype(np.float32)
+    x_np = np.random.default_rng(3).uniform(-1, 1, (12000, f)).astype(np.float32)
     x = torch.from_numpy(x_np).cuda()
     try:
         capi.check(L.aes_dev_spmm_set_schedule(sched))
