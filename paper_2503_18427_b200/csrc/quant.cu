@@ -20,7 +20,7 @@ namespace aes {
 namespace {
 
 constexpr int kFitThreads = 256;
-constexpr int kFitBlocks = 148 * 8;
+constexpr int kFitBlocks = 148 * 16;  // partials fit aes_dev_scan_workspace_bytes (2 * 148 * 8 * 32 B)
 
 struct MinMax {
     float lo, hi;
@@ -132,7 +132,7 @@ fit_final_kernel(const float* __restrict__ x, const MinMax* __restrict__ part, i
 
 // Codes through the fp32 fast path with the exact fp64 fallback
 // (quantize.cuh): bit-identical to the reference, off the fp64 pipe.
-constexpr int kQuantBlocks = 148 * 8;
+constexpr int kQuantBlocks = 148 * 32;
 template <typename CodeT>
 __global__ void __launch_bounds__(256)
 quantize_fast_kernel(const float* __restrict__ x, uint64_t rows, uint64_t cols, uint64_t ldx, float lo_f,
