@@ -180,6 +180,30 @@ __global__ void dequantize_kernel(const CodeT* __restrict__ q, uint64_t rows, ui
     }
 }
 
+// u8 codes, contiguous rows: 4 codes -> one float4 through the 256-entry
+// table (each CTA builds it: float(double(q) * step + lo), the same value
+// per code as dequantize_kernel, quantize.cpp:53-64), grid-stride with
+// 4 loads in flight per thread.
+__global__ void __launch_bounds__(256)
+dequantize_u8_flat_kernel(const uchar4* __restrict__ q, uint64_t n4, double lo, double step, uint32_t levels,
+                          float4* __restrict__ x) {
+    __shared__ float lut[256];
+    const uint32_t t = threadIdx.x;
+    lut[t] = t <= levels ? __double2float_rn(__dadd_rn(__dmul_rn((double)t, step), lo)) : 0.f;
+    __syncthreads();
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    auto put = [&](uint64_t e, uchar4 c) { __stcs(x + e, make_float4(lut[c.x], lut[c.y], lut[c.z], lut[c.w])); };
+    uint64_t e = blockIdx.x * (uint64_t)blockDim.x + t;
+    for (; e + 3 * stride < n4; e += 4 * stride) {
+        uchar4 c[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) c[u] = __ldcs(q + e + u * stride);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) put(e + u * stride, c[u]);
+    }
+    for (; e < n4; e += stride) put(e, __ldcs(q + e));
+}
+
 __global__ void lut_kernel(double lo, double step, uint32_t levels, float* __restrict__ lut) {
     const uint32_t q = threadIdx.x;
     lut[q] = q <= levels ? __double2float_rn(__dadd_rn(__dmul_rn((double)q, step), lo)) : 0.f;
@@ -235,7 +259,12 @@ int aes_dev_dequantize(const void* codes, uint64_t rows, uint64_t cols, uint64_t
     if (total == 0) return AES_OK;
     const double step = ((double)hi - (double)lo) / (double)((1u << bits) - 1u);
     const unsigned grid = grid_for(total, 256, 148 * 32);
-    if (bits <= 8)
+    if (bits <= 8 && ldq == cols && ldx == cols && total % 4 == 0 && (uintptr_t)codes % 4 == 0 &&
+        (uintptr_t)x % 16 == 0) {
+        dequantize_u8_flat_kernel<<<grid_for(total / 4, 256, 148 * 32), 256, 0, st>>>(
+            static_cast<const uchar4*>(codes), total / 4, (double)lo, step, (1u << bits) - 1u,
+            reinterpret_cast<float4*>(x));
+    } else if (bits <= 8)
         dequantize_kernel<uint8_t><<<grid, 256, 0, st>>>(static_cast<const uint8_t*>(codes), rows, cols,
                                                          ldq, (double)lo, step, x, ldx);
     else

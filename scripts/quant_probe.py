@@ -26,3 +26,8 @@ ms = t(lambda: device.quantize(x, 8, params=(-1.0, 1.0)))
 print(f"quantize u8: {ms:.3f} ms, {(nb + nb / 4) / ms / 1e6:.0f} GB/s (5 B per element)")
 ms = t(lambda: device.fit_params_raw(x))
 print(f"fit_params: {ms:.3f} ms, {nb / ms / 1e6:.0f} GB/s")
+q = device.quantize(x, 8, params=(-1.0, 1.0))
+codes = q.codes.contiguous()
+qc = device.QuantizedDevice(codes, q.x_min, q.x_max, 8, q.lut)
+ms = t(lambda: device.dequantize(qc))
+print(f"dequantize u8: {ms:.3f} ms, {(nb + nb / 4) / ms / 1e6:.0f} GB/s (5 B per element)")

@@ -26,6 +26,10 @@ def to_np(t):
     return t.detach().cpu().numpy()
 
 
+def bits_of(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
 @pytest.mark.parametrize("f", [16, 128, 602])
 def test_device_spmm_matches_oracle(dev, f):
     import torch
@@ -393,6 +397,10 @@ def test_quantize_threshold_table_extremes(dev, bits, shape):
         want = port.quantize(x, lo, hi, bits)
         got = to_np(q.codes).astype(np.uint16)
         assert np.array_equal(got, want), (lo, hi, bits, int((got != want).sum()))
+        # and back: the table-driven flat dequantize (contiguous rows) or the
+        # strided one, bit-equal to the reference formula
+        deq = to_np(dev.dequantize(q))
+        assert np.array_equal(bits_of(deq), bits_of(port.dequantize(want, lo, hi, bits)))
 
 
 def test_gcn_forward_sharded_c_abi_nccl(dev):
