@@ -34,3 +34,7 @@ for name in sys.argv[1:] or ["arxiv", "products"]:
     alg = 8 * (n + 1) + 8 * nnz + 512 * nnz + 512 * n
     deg = torch.diff(rp).max().item()
     print(f"{name}: exact SpMM F=128 {ms:.3f} ms, {alg / ms / 1e6:.0f} GB/s alg, max row {deg}", flush=True)
+    q = device.quantize(b)
+    ms = t(lambda: device.spmm_q8(g.row_ptr, g.col, g.val, q, out=out))
+    alg8 = 8 * (n + 1) + 8 * nnz + 128 * nnz + 512 * n
+    print(f"{name}: exact int8 SpMM F=128 {ms:.3f} ms, {alg8 / ms / 1e6:.0f} GB/s alg", flush=True)
