@@ -1043,7 +1043,18 @@ int aes_dense_matmul(const float* a, uint64_t m, uint64_t k, const float* b, uin
     AES_TRY(upload_dense(b, k, n, db, ldb));
     const uint64_t ldc = round4(n ? n : 1);
     AES_TRY(dc.alloc(m * ldc));
-    AES_TRY(aes_dev_gemm_bias_act(da.p, m, k, lda, db.p, n, ldb, nullptr, 0, dc.p, ldc, lib_stream()));
+    // finite B makes the reference's zero-skip result-neutral (gemm.cu): the
+    // select-free kernel then runs (one scalar read-back)
+    unsigned int b_bad = 1;
+    if (k * n) {
+        DBuf<unsigned int> bad;
+        AES_TRY(bad.alloc(1));
+        AES_TRY(aes_dev_all_finite(db.p, k * ldb, bad.p, lib_stream()));
+        AES_TRY(d2h_scalar(bad.p, &b_bad));
+    }
+    float* dsts[1] = {dc.p};
+    AES_TRY(aes_dev_gemm_bias_act_ex(da.p, m, k, lda, db.p, n, ldb, nullptr, 0, b_bad == 0, dsts, nullptr, 1, 0, ldc,
+                                     lib_stream()));
     AES_TRY(download_dense(dc.p, ldc, m, n, c));
     return sync();
 }
