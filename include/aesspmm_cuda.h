@@ -372,6 +372,17 @@ AES_API int aes_dev_gemm_tf32_bcast(const float* a, uint64_t m, uint64_t k, uint
                                     int n_dst, uint64_t row_offset, uint64_t ldh, float* wt_scratch,
                                     void* stream);
 AES_API uint64_t aes_gemm_tf32_ctas(uint64_t m);
+/* act(A W + b) into h (as aes_dev_gemm_bias_act_ex, one destination) with
+ * fit_params (proj/src/quantize.cpp:11-21) of the output fused into the
+ * epilogue: one (min, max) partial per CTA into fit_partials
+ * (aes_gemm_fit_partial_bytes(m, n) bytes); aes_dev_fit_merge then writes
+ * result[0..2] = (x_min, x_max, non-finite flag bits) exactly as
+ * aes_dev_fit_params over the m x n output would. */
+AES_API int aes_dev_gemm_bias_act_fit(const float* a, uint64_t m, uint64_t k, uint64_t lda, const float* w,
+                                      uint64_t n, uint64_t ldw, const float* bias, int relu, int finite_w, float* h,
+                                      uint64_t ldh, void* fit_partials, void* stream);
+AES_API uint64_t aes_gemm_fit_partial_bytes(uint64_t m, uint64_t n);
+AES_API int aes_dev_fit_merge(const void* partials, uint64_t n_partials, float* result, void* stream);
 /* Number of CTAs (= arrivals per destination) the GEMM above launches. */
 AES_API uint64_t aes_gemm_ctas(uint64_t m, uint64_t n);
 /* Spin (one thread, ld.acquire.sys) until *counter >= target. */

@@ -68,6 +68,10 @@ def lib():
         L.aes_dev_wait_counter.argtypes = [vp, u64, vp]
         L.aes_dev_all_finite.argtypes = [vp, u64, vp, vp]
         L.aes_dev_signal_all.argtypes = [vp, i32, vp]
+        L.aes_dev_gemm_bias_act_fit.argtypes = [vp, u64, u64, u64, vp, u64, u64, vp, i32, i32, vp, u64, vp, vp]
+        L.aes_gemm_fit_partial_bytes.argtypes = [u64, u64]
+        L.aes_gemm_fit_partial_bytes.restype = u64
+        L.aes_dev_fit_merge.argtypes = [vp, u64, vp, vp]
         L.aes_gcn_sharded_workspace_bytes.argtypes = [u64, u64]
         L.aes_gcn_sharded_workspace_bytes.restype = u64
         L.aes_gcn_forward_sharded.argtypes = [vp, vp, vp, u64, u64, i32, vp, vp, vp, i32, vp, vp, u64, u64, vp, sz,

@@ -17,6 +17,7 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include "minmax.cuh"
 
 namespace aes {
 namespace {
@@ -31,9 +32,11 @@ struct Bcast {
     const uint8_t* need[kMaxDst];          // halo masks: row r goes to d only if need[d][r] (null: every row)
     int n;
     uint64_t row_off;                      // this shard's first row in the replica
+    MinMax* fit;                           // fused fit_params: one (min, max) partial per CTA (null: off)
+    uint64_t fit_off;                      // partial index of this launch's first CTA
 };
 
-template <bool SKIP, bool BCAST>
+template <bool SKIP, bool BCAST, bool FIT = false>
 __global__ void __launch_bounds__(kThreads, 2)
 gemm_ordered_kernel(const float* __restrict__ a, uint64_t m, uint64_t k, uint64_t lda,
                     const float* __restrict__ w, uint64_t n, uint64_t ldw, const float* __restrict__ bias,
@@ -127,6 +130,10 @@ gemm_ordered_kernel(const float* __restrict__ a, uint64_t m, uint64_t k, uint64_
     // epilogue: bias, ReLU, store (to every replica when broadcasting)
     const uint64_t gn0 = n0 + tx * TN;
     const bool vec = (gn0 + TN <= n) && (ldh % 4 == 0);
+    // fused fit_params over the output (row-major index row * n + col, the
+    // order quantize.cpp:14-19 scans): this thread meets its elements in
+    // increasing index order, so strict compares keep first occurrences
+    MinMax fm{INFINITY, -INFINITY, ~0ull, ~0ull, 0u};
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
         const uint64_t gm = m0 + ty * TM + i;
@@ -138,6 +145,7 @@ gemm_ordered_kernel(const float* __restrict__ a, uint64_t m, uint64_t k, uint64_
             if (bias && gn0 + j < n) x = __fadd_rn(x, bias[gn0 + j]);
             if (relu) x = (x < 0.f) ? 0.f : x;
             v[j] = x;
+            if (FIT && gn0 + j < n) fit_elem(fm, x, (bc.row_off + gm) * n + gn0 + j);
         }
         const int nd = BCAST ? bc.n : 1;
         for (int d = 0; d < nd; ++d) {
@@ -152,6 +160,10 @@ gemm_ordered_kernel(const float* __restrict__ a, uint64_t m, uint64_t k, uint64_
                     if (gn0 + j < n) row[gn0 + j] = v[j];
             }
         }
+    }
+    if (FIT) {  // one partial per CTA
+        fm = block_reduce<kThreads>(fm);
+        if (tid == 0) bc.fit[bc.fit_off + (uint64_t)blockIdx.y * gridDim.x + blockIdx.x] = fm;
     }
     if (BCAST) {
         // publish this CTA's tile to every destination: the barrier orders the
@@ -205,7 +217,7 @@ __global__ void all_finite_kernel(const float* __restrict__ x, uint64_t count, u
         if (!isfinite(x[i])) atomicOr(bad, 1u);
 }
 
-template <bool SKIP, bool BCAST>
+template <bool SKIP, bool BCAST, bool FIT = false>
 int launch(const float* a, uint64_t m, uint64_t k, uint64_t lda, const float* w, uint64_t n, uint64_t ldw,
            const float* bias, int relu, float* h, uint64_t ldh, const Bcast& bc, cudaStream_t st) {
     const unsigned gx = (unsigned)((n + BN - 1) / BN);
@@ -214,8 +226,9 @@ int launch(const float* a, uint64_t m, uint64_t k, uint64_t lda, const float* w,
         const uint64_t mm = m - r0 < rows_per ? m - r0 : rows_per;
         Bcast b2 = bc;
         b2.row_off += r0;
+        b2.fit_off = (r0 / BM) * gx;  // partials of the earlier row chunks
         dim3 grid(gx, (unsigned)((mm + BM - 1) / BM));
-        gemm_ordered_kernel<SKIP, BCAST><<<grid, kThreads, 0, st>>>(a + r0 * lda, mm, k, lda, w, n, ldw, bias, relu,
+        gemm_ordered_kernel<SKIP, BCAST, FIT><<<grid, kThreads, 0, st>>>(a + r0 * lda, mm, k, lda, w, n, ldw, bias, relu,
                                                                      h ? h + r0 * ldh : nullptr, ldh, b2);
     }
     AES_CUDA_TRY(cudaGetLastError());
@@ -273,6 +286,23 @@ int aes_dev_gemm_bias_act_halo(const float* a, uint64_t m, uint64_t k, uint64_t 
     return finite_w ? launch<false, true>(a, m, k, lda, w, n, ldw, bias, relu, nullptr, ldh, bc, st)
                     : launch<true, true>(a, m, k, lda, w, n, ldw, bias, relu, nullptr, ldh, bc, st);
 }
+
+int aes_dev_gemm_bias_act_fit(const float* a, uint64_t m, uint64_t k, uint64_t lda, const float* w, uint64_t n,
+                              uint64_t ldw, const float* bias, int relu, int finite_w, float* h, uint64_t ldh,
+                              void* fit_partials, void* stream) {
+    using namespace aes;
+    if (lda < k || ldw < n || ldh < n) return fail(AES_ERR_INVALID_ARG, "leading dimension too small");
+    if (!h || !fit_partials) return fail(AES_ERR_INVALID_ARG, "null argument");
+    if (m == 0 || n == 0) return AES_OK;
+    Bcast bc{};
+    bc.n = 1;
+    bc.fit = static_cast<MinMax*>(fit_partials);
+    cudaStream_t st = as_stream(stream);
+    return finite_w ? launch<false, false, true>(a, m, k, lda, w, n, ldw, bias, relu, h, ldh, bc, st)
+                    : launch<true, false, true>(a, m, k, lda, w, n, ldw, bias, relu, h, ldh, bc, st);
+}
+
+uint64_t aes_gemm_fit_partial_bytes(uint64_t m, uint64_t n) { return aes_gemm_ctas(m, n) * sizeof(aes::MinMax); }
 
 uint64_t aes_gemm_ctas(uint64_t m, uint64_t n) {
     if (m == 0 || n == 0) return 0;

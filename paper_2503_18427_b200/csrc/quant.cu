@@ -14,6 +14,7 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include "minmax.cuh"
 #include "quantize.cuh"
 
 namespace aes {
@@ -21,57 +22,6 @@ namespace {
 
 constexpr int kFitThreads = 256;
 constexpr int kFitBlocks = 148 * 16;  // partials fit aes_dev_scan_workspace_bytes (2 * 148 * 8 * 32 B)
-
-struct MinMax {
-    float lo, hi;
-    uint64_t ilo, ihi;
-    uint32_t bad;
-};
-
-__device__ __forceinline__ void mm_merge(MinMax& a, const MinMax& b) {
-    if (b.lo < a.lo || (b.lo == a.lo && b.ilo < a.ilo)) { a.lo = b.lo; a.ilo = b.ilo; }
-    if (b.hi > a.hi || (b.hi == a.hi && b.ihi < a.ihi)) { a.hi = b.hi; a.ihi = b.ihi; }
-    a.bad |= b.bad;
-}
-
-__device__ __forceinline__ MinMax mm_shfl(const MinMax& m, int o) {
-    MinMax r;
-    r.lo = __shfl_down_sync(0xffffffffu, m.lo, o);
-    r.hi = __shfl_down_sync(0xffffffffu, m.hi, o);
-    r.ilo = __shfl_down_sync(0xffffffffu, m.ilo, o);
-    r.ihi = __shfl_down_sync(0xffffffffu, m.ihi, o);
-    r.bad = __shfl_down_sync(0xffffffffu, m.bad, o);
-    return r;
-}
-
-__device__ MinMax block_reduce(MinMax m) {
-    __shared__ MinMax s[kFitThreads / 32];
-    for (int o = 16; o > 0; o >>= 1) {
-        MinMax t = mm_shfl(m, o);
-        mm_merge(m, t);
-    }
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (lane == 0) s[wid] = m;
-    __syncthreads();
-    if (wid == 0) {
-        m = s[lane < kFitThreads / 32 ? lane : 0];
-        for (int o = 16; o > 0; o >>= 1) {
-            MinMax t = mm_shfl(m, o);
-            mm_merge(m, t);
-        }
-    }
-    return m;
-}
-
-// Level 1: block b reduces the contiguous chunk [b*chunk, (b+1)*chunk).
-// A thread sees its elements in increasing index order, so the strict
-// compares alone keep the first occurrence (an equal later value never
-// replaces); the index only matters when partial results merge.
-__device__ __forceinline__ void fit_elem(MinMax& m, float v, uint64_t i) {
-    if (!isfinite(v)) { m.bad = 1; return; }
-    if (v < m.lo) { m.lo = v; m.ilo = i; }
-    if (v > m.hi) { m.hi = v; m.ihi = i; }
-}
 
 __global__ void __launch_bounds__(kFitThreads)
 fit_partial_kernel(const float* __restrict__ x, uint64_t n, uint64_t chunk, MinMax* __restrict__ part) {
@@ -108,7 +58,7 @@ fit_partial_kernel(const float* __restrict__ x, uint64_t n, uint64_t chunk, MinM
     } else {
         for (uint64_t i = b0 + threadIdx.x; i < b1; i += kFitThreads) fit_elem(m, __ldcs(x + i), i);
     }
-    m = block_reduce(m);
+    m = block_reduce<kFitThreads>(m);
     if (threadIdx.x == 0) part[blockIdx.x] = m;
 }
 
@@ -118,7 +68,7 @@ fit_final_kernel(const float* __restrict__ x, const MinMax* __restrict__ part, i
                  float* __restrict__ result) {
     MinMax m{INFINITY, -INFINITY, ~0ull, ~0ull, 0u};
     for (int i = threadIdx.x; i < nparts; i += kFitThreads) mm_merge(m, part[i]);
-    m = block_reduce(m);
+    m = block_reduce<kFitThreads>(m);
     if (threadIdx.x == 0) {
         uint32_t* flags = reinterpret_cast<uint32_t*>(result + 2);
         flags[0] = m.bad;
@@ -127,6 +77,20 @@ fit_final_kernel(const float* __restrict__ x, const MinMax* __restrict__ part, i
     }
 }
 
+
+// Partials that carry their values (the GEMM's fused fit epilogue): the
+// same merge, the winning values written directly.
+__global__ void __launch_bounds__(kFitThreads)
+fit_merge_kernel(const MinMax* __restrict__ part, int nparts, float* __restrict__ result) {
+    MinMax m{INFINITY, -INFINITY, ~0ull, ~0ull, 0u};
+    for (int i = threadIdx.x; i < nparts; i += kFitThreads) mm_merge(m, part[i]);
+    m = block_reduce<kFitThreads>(m);
+    if (threadIdx.x == 0) {
+        reinterpret_cast<uint32_t*>(result + 2)[0] = m.bad;
+        result[0] = m.bad || m.ilo == ~0ull ? 0.f : m.lo;
+        result[1] = m.bad || m.ihi == ~0ull ? 0.f : m.hi;
+    }
+}
 
 // Vector form for the common contiguous case: 4 floats -> 4 codes per thread.
 
@@ -226,6 +190,17 @@ int aes_dev_fit_params(const float* x, uint64_t n, float* result, void* workspac
     auto* part = static_cast<MinMax*>(workspace);
     fit_partial_kernel<<<nb, kFitThreads, 0, st>>>(x, n, chunk, part);
     fit_final_kernel<<<1, kFitThreads, 0, st>>>(x, part, nb, result);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
+int aes_dev_fit_merge(const void* partials, uint64_t n_partials, float* result, void* stream) {
+    using namespace aes;
+    if (!partials || !result) return fail(AES_ERR_INVALID_ARG, "null argument");
+    if (n_partials == 0) return fail(AES_ERR_EMPTY, "EmptyMatrix");
+    if (n_partials >= (1ull << 31)) return fail(AES_ERR_INVALID_ARG, "too many partials");
+    fit_merge_kernel<<<1, kFitThreads, 0, as_stream(stream)>>>(static_cast<const MinMax*>(partials),
+                                                              (int)n_partials, result);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
 }

@@ -296,6 +296,31 @@ def gemm_bias_act(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None, r
     return out
 
 
+def gemm_bias_act_fit(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None, relu: bool, out=None,
+                      stream=None, finite_w: bool = False):
+    """gemm_bias_act with fit_params of the output fused into the GEMM
+    epilogue: returns (out, res) where res = float32 [x_min, x_max, flag, -]
+    on the device (flag int32 bits: 1 = non-finite), as fit_params_raw(out)."""
+    m, k = a.shape
+    k2, n = w.shape
+    if k != k2:
+        raise ValueError("ShapeMismatch")
+    if m == 0 or n == 0:
+        raise ValueError("EmptyMatrix")
+    w = w.contiguous()
+    if out is None:
+        out = empty_padded(m, n, device=a.device)
+    L = lib()
+    parts = torch.empty(int(L.aes_gemm_fit_partial_bytes(m, n)), dtype=torch.uint8, device=a.device)
+    res = torch.empty(4, dtype=torch.float32, device=a.device)
+    st = stream_of(stream)
+    check(L.aes_dev_gemm_bias_act_fit(ptr(a), m, k, a.stride(0), ptr(w), n, w.stride(0),
+                                      ptr(bias) if bias is not None and bias.numel() else None, int(relu),
+                                      int(bool(finite_w)), ptr(out), out.stride(0), ptr(parts), st))
+    check(L.aes_dev_fit_merge(ptr(parts), parts.numel() // 32, ptr(res), st))
+    return out, res
+
+
 def gemm_tf32(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None, relu: bool, out=None,
               stream=None) -> torch.Tensor:
     """FAST MODE act(a @ w + bias) on the tcgen05 tensor cores (TF32

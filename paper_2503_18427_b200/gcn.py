@@ -280,12 +280,13 @@ class ShardedGCN:
 
         rep = self.replicas
         x = self.ops.alloc(max(rows, 1), w.shape[1], agg)
+        fit = None
         if self.fast[l]:
             device.gemm_tf32(agg[:rows], w, b, True, out=x[:rows])
-        else:
-            self.ops.gemm_bias_act(agg[:rows], w, b, relu=True, out=x)
+            fit = self.ops.fit_params(x[:rows]) if rows else None
+        elif rows:  # exact GEMM with fit_params fused into its epilogue
+            _, fit = device.gemm_bias_act_fit(agg[:rows], w, b, True, out=x[:rows], finite_w=self.finite[l])
         buf = l % 2
-        fit = self.ops.fit_params(x[:rows]) if rows else None
         rep.exchange_params(buf, fit, self.q_params[buf], self.q_luts[buf])
         if rows:
             rep.quantize_publish(buf, x[:rows], self.q_params[buf], self.lo, halo=self.halo)

@@ -450,3 +450,29 @@ def test_gcn_forward_sharded_c_abi_nccl(dev):
         assert np.array_equal(bits(got), bits(want))
     finally:
         nccl.ncclCommDestroy(comm)
+
+
+@pytest.mark.parametrize("m,k,n", [(1000, 40, 64), (3000, 128, 128), (257, 7, 300)])
+def test_gemm_fused_fit_matches_fit_params(dev, m, k, n):
+    """The GEMM epilogue's fused fit_params (first-occurrence min / max over
+    the row-major output, non-finite flag) equals fit_params of the output it
+    wrote, bit for bit — including ReLU's many +0 ties, -0 from the bias, and
+    a non-finite output."""
+    import torch
+    rng = np.random.default_rng(m + n)
+    a = torch.from_numpy(rng.uniform(-1, 1, (m, k)).astype(np.float32)).cuda()
+    w = torch.from_numpy(rng.uniform(-0.5, 0.5, (k, n)).astype(np.float32)).cuda()
+    b = torch.from_numpy(rng.uniform(-0.1, 0.1, n).astype(np.float32)).cuda()
+    b[0] = -0.0
+    for relu, finite in ((True, True), (False, True), (False, False)):
+        out, res = dev.gemm_bias_act_fit(a, w, b, relu, finite_w=finite)
+        want = dev.fit_params_raw(out.contiguous())
+        torch.cuda.synchronize()
+        assert np.array_equal(bits_of(to_np(res)[:3]), bits_of(to_np(want)[:3])), (relu, finite)
+        # and the GEMM itself is the exact one
+        assert torch.equal(out, dev.gemm_bias_act(a, w, b, relu, finite_w=finite))
+    w2 = w.clone()
+    w2[0, 0] = float("inf")
+    out, res = dev.gemm_bias_act_fit(a, w2, b, False, finite_w=False)
+    torch.cuda.synchronize()
+    assert to_np(res).view(np.int32)[2] == 1  # NonFinite
