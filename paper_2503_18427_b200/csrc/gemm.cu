@@ -36,11 +36,13 @@ struct Bcast {
     uint64_t fit_off;                      // partial index of this launch's first CTA
 };
 
-template <bool SKIP, bool BCAST, bool FIT = false>
+template <bool SKIP, bool BCAST, bool FIT = false, int TNV = 8>
 __global__ void __launch_bounds__(kThreads, 2)
 gemm_ordered_kernel(const float* __restrict__ a, uint64_t m, uint64_t k, uint64_t lda,
                     const float* __restrict__ w, uint64_t n, uint64_t ldw, const float* __restrict__ bias,
                     int relu, float* __restrict__ h, uint64_t ldh, Bcast bc) {
+    // TNV = 8: 128 x 128 tiles; TNV = 4: 128 x 64 tiles for narrow outputs (n <= 64)
+    constexpr int TN = TNV, BN = 16 * TNV, kRW = BK * BN / kThreads;
     __shared__ __align__(16) float As[2][BK][BM + 4];  // +4: conflict-free transposed stores
     __shared__ __align__(16) float Ws[2][BK][BN];
     const int tid = threadIdx.x;
@@ -54,7 +56,7 @@ gemm_ordered_kernel(const float* __restrict__ a, uint64_t m, uint64_t k, uint64_
         for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
 
     // staging: A tile BM x BK (4 elements / thread), W tile BK x BN (4 / thread)
-    float ra[4], rw[4];
+    float ra[4], rw[kRW];
     // interior tiles (every row, column and k of the slab in range) load
     // without bounds checks from per-thread base pointers (3.35 -> 3.09 ms
     // on the products layer GEMM: the checks were ~8 % of the issue slots)
@@ -64,10 +66,9 @@ gemm_ordered_kernel(const float* __restrict__ a, uint64_t m, uint64_t k, uint64_
     auto load_tiles = [&](uint64_t k0) {
         if (full_mn && k0 + BK <= k) {
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                ra[r] = __ldg(pa + (uint64_t)(r * kThreads / BK) * lda + k0);
-                rw[r] = __ldg(pw + (k0 + (uint64_t)(r * kThreads / BN)) * ldw);
-            }
+            for (int r = 0; r < 4; ++r) ra[r] = __ldg(pa + (uint64_t)(r * kThreads / BK) * lda + k0);
+#pragma unroll
+            for (int r = 0; r < kRW; ++r) rw[r] = __ldg(pw + (k0 + (uint64_t)(r * kThreads / BN)) * ldw);
             return;
         }
 #pragma unroll
@@ -76,6 +77,10 @@ gemm_ordered_kernel(const float* __restrict__ a, uint64_t m, uint64_t k, uint64_
             const int mm = e / BK, kk = e % BK;
             const uint64_t gm = m0 + mm, gk = k0 + kk;
             ra[r] = (gm < m && gk < k) ? __ldg(a + gm * lda + gk) : 0.f;  // zero fill is neutral
+        }
+#pragma unroll
+        for (int r = 0; r < kRW; ++r) {
+            const int e = tid + r * kThreads;
             const int kw = e / BN, nn = e % BN;
             const uint64_t gkw = k0 + kw, gn = n0 + nn;
             rw[r] = (gkw < k && gn < n) ? __ldg(w + gkw * ldw + gn) : 0.f;
@@ -86,6 +91,10 @@ gemm_ordered_kernel(const float* __restrict__ a, uint64_t m, uint64_t k, uint64_
         for (int r = 0; r < 4; ++r) {
             const int e = tid + r * kThreads;
             As[buf][e % BK][e / BK] = ra[r];
+        }
+#pragma unroll
+        for (int r = 0; r < kRW; ++r) {
+            const int e = tid + r * kThreads;
             Ws[buf][e / BN][e % BN] = rw[r];
         }
     };
@@ -101,10 +110,16 @@ gemm_ordered_kernel(const float* __restrict__ a, uint64_t m, uint64_t k, uint64_
         for (int kk = 0; kk < BK; ++kk) {
             const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * TM]);
             const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * TM + 4]);
-            const float4 w0 = *reinterpret_cast<const float4*>(&Ws[buf][kk][tx * TN]);
-            const float4 w1 = *reinterpret_cast<const float4*>(&Ws[buf][kk][tx * TN + 4]);
             const float av[TM] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-            const float wv[TN] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+            float wv[TN];
+#pragma unroll
+            for (int q = 0; q < TN / 4; ++q) {
+                const float4 w4 = *reinterpret_cast<const float4*>(&Ws[buf][kk][tx * TN + 4 * q]);
+                wv[4 * q] = w4.x;
+                wv[4 * q + 1] = w4.y;
+                wv[4 * q + 2] = w4.z;
+                wv[4 * q + 3] = w4.w;
+            }
 #pragma unroll
             for (int i = 0; i < TM; ++i) {
                 if (SKIP) {
@@ -152,8 +167,10 @@ gemm_ordered_kernel(const float* __restrict__ a, uint64_t m, uint64_t k, uint64_
             if (BCAST && bc.need[d] && !bc.need[d][bc.row_off + gm]) continue;  // halo: d never reads this row
             float* row = BCAST ? bc.dst[d] + (bc.row_off + gm) * ldh : h + gm * ldh;
             if (vec) {
-                reinterpret_cast<float4*>(row + gn0)[0] = make_float4(v[0], v[1], v[2], v[3]);
-                reinterpret_cast<float4*>(row + gn0)[1] = make_float4(v[4], v[5], v[6], v[7]);
+#pragma unroll
+                for (int q = 0; q < TN / 4; ++q)
+                    reinterpret_cast<float4*>(row + gn0)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2],
+                                                                         v[4 * q + 3]);
             } else {
 #pragma unroll
                 for (int j = 0; j < TN; ++j)
@@ -217,10 +234,15 @@ __global__ void all_finite_kernel(const float* __restrict__ x, uint64_t count, u
         if (!isfinite(x[i])) atomicOr(bad, 1u);
 }
 
+inline uint64_t gemm_tile_n(uint64_t n) { return n <= 64 ? 64 : 128; }
+
 template <bool SKIP, bool BCAST, bool FIT = false>
 int launch(const float* a, uint64_t m, uint64_t k, uint64_t lda, const float* w, uint64_t n, uint64_t ldw,
            const float* bias, int relu, float* h, uint64_t ldh, const Bcast& bc, cudaStream_t st) {
-    const unsigned gx = (unsigned)((n + BN - 1) / BN);
+    // narrow outputs (a GCN's last layer: 40 classes on arxiv) on 128 x 64
+    // tiles: half the dead columns of a 128-wide tile
+    const uint64_t bn = gemm_tile_n(n);
+    const unsigned gx = (unsigned)((n + bn - 1) / bn);
     const uint64_t rows_per = (uint64_t)65535 * BM;  // grid.y limit
     for (uint64_t r0 = 0; r0 < m; r0 += rows_per) {
         const uint64_t mm = m - r0 < rows_per ? m - r0 : rows_per;
@@ -228,8 +250,12 @@ int launch(const float* a, uint64_t m, uint64_t k, uint64_t lda, const float* w,
         b2.row_off += r0;
         b2.fit_off = (r0 / BM) * gx;  // partials of the earlier row chunks
         dim3 grid(gx, (unsigned)((mm + BM - 1) / BM));
-        gemm_ordered_kernel<SKIP, BCAST, FIT><<<grid, kThreads, 0, st>>>(a + r0 * lda, mm, k, lda, w, n, ldw, bias, relu,
-                                                                     h ? h + r0 * ldh : nullptr, ldh, b2);
+        if (bn == 64)
+            gemm_ordered_kernel<SKIP, BCAST, FIT, 4><<<grid, kThreads, 0, st>>>(
+                a + r0 * lda, mm, k, lda, w, n, ldw, bias, relu, h ? h + r0 * ldh : nullptr, ldh, b2);
+        else
+            gemm_ordered_kernel<SKIP, BCAST, FIT, 8><<<grid, kThreads, 0, st>>>(
+                a + r0 * lda, mm, k, lda, w, n, ldw, bias, relu, h ? h + r0 * ldh : nullptr, ldh, b2);
     }
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
@@ -306,7 +332,8 @@ uint64_t aes_gemm_fit_partial_bytes(uint64_t m, uint64_t n) { return aes_gemm_ct
 
 uint64_t aes_gemm_ctas(uint64_t m, uint64_t n) {
     if (m == 0 || n == 0) return 0;
-    return ((n + aes::BN - 1) / aes::BN) * ((m + aes::BM - 1) / aes::BM);
+    const uint64_t bn = aes::gemm_tile_n(n);
+    return ((n + bn - 1) / bn) * ((m + aes::BM - 1) / aes::BM);
 }
 
 int aes_dev_wait_counter(const unsigned long long* counter, unsigned long long target, void* stream) {
