@@ -234,3 +234,41 @@ def test_reference_python_core_loads():
     core = oref.core()
     assert core.select_strategy(100, 32).sample_cnt == 8
     assert core.hash_start(3, 100, 4) == 19
+
+
+def test_quantize_fast_path_decision_rule():
+    """quantize.cuh's fp32 fast path: floor(e) is accepted only when frac(e)
+    is farther than the margin from an integer (or e is clearly outside
+    [0, L + 1)); the error bound says that decision never differs from the
+    reference fp64 code.  Emulated here with numpy float32 (two roundings
+    where the GPU's FFMA has one — a looser estimate, same rule) against the
+    oracle's quantize over adversarial params and values."""
+    rng = np.random.default_rng(5)
+    params = [(-1.0, 1.0), (0.0, 1e-30), (-1e30, 1e30), (-3.5, -3.499996), (1e-40, 2e-40), (0.1, 0.7),
+              (-3e38, 3e38), (7.0, 7.5)]
+    for bits, margin in ((8, 1.0 / 4096), (4, 1.0 / 4096), (12, 1.0 / 32), (16, 1.0 / 32)):
+        levels = (1 << bits) - 1
+        for lo, hi in params:
+            lo32, hi32 = np.float32(lo), np.float32(hi)
+            rng_d = float(np.float64(hi32) - np.float64(lo32))
+            if rng_d == 0.0:
+                continue
+            span = float(hi32) - float(lo32)
+            with np.errstate(over="ignore", invalid="ignore"):
+                x = rng.uniform(float(lo32) - 0.2 * span, float(hi32) + 0.2 * span, 20000).astype(np.float32)
+                scale = np.float32(levels / rng_d)
+                e = (x - lo32) * scale + np.float32(0.0078125)
+            want = port.quantize(x, float(lo32), float(hi32), bits).astype(np.int64)
+            with np.errstate(invalid="ignore"):
+                fl = np.floor(e)
+                fr = e - fl
+                fast = np.isfinite(e) & (np.abs(e) < levels + 1) & (fr > margin) & (fr < 1 - margin)
+                above = np.isfinite(e) & (e >= levels + 1)
+                below = np.isfinite(e) & (e <= -1)
+            got = np.clip(fl[fast].astype(np.int64), 0, levels)
+            assert np.array_equal(got, want[fast]), (bits, lo, hi)
+            assert (want[above] == levels).all() and (want[below] == 0).all(), (bits, lo, hi)
+            # everything else (near an integer, fp32 overflow) takes the exact
+            # fp64 formula; with a representable scale that is a small remainder
+            if np.isfinite(scale) and span < 1e30:
+                assert (fast | above | below).mean() > 0.95, (bits, lo, hi)
