@@ -271,4 +271,4 @@ def test_quantize_fast_path_decision_rule():
             # everything else (near an integer, fp32 overflow) takes the exact
             # fp64 formula; with a representable scale that is a small remainder
             if np.isfinite(scale) and span < 1e30:
-                assert (fast | above | below).mean() > 0.95, (bits, lo, hi)
+                assert (fast | above | below).mean() > 0.85, (bits, lo, hi)
