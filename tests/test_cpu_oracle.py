@@ -270,5 +270,8 @@ def test_quantize_fast_path_decision_rule():
             assert (want[above] == levels).all() and (want[below] == 0).all(), (bits, lo, hi)
             # everything else (near an integer, fp32 overflow) takes the exact
             # fp64 formula; with a representable scale that is a small remainder
-            if np.isfinite(scale) and span < 1e30:
-                assert (fast | above | below).mean() > 0.85, (bits, lo, hi)
+            # (ranges a few float ulps wide quantize to a handful of e values
+            # that can all sit near integers: no coverage claim there)
+            wide = span > 1e-3 * max(abs(float(lo32)), abs(float(hi32)))
+            if np.isfinite(scale) and span < 1e30 and wide and bits <= 8:
+                assert (fast | above | below).mean() > 0.95, (bits, lo, hi)
