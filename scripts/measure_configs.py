@@ -105,8 +105,11 @@ def gcn_config(name, dims, width, cpu=True):
     ms_exact = gpu_ms(lambda: device.gcn_forward(g, x, tw, tb, None), reps=5)
     cg = device.GcnForwardGraph(g, x, tw, tb, plan)  # the same kernels, one graph launch
     ms_graph = gpu_ms(lambda: cg.run(), reps=20)
+    cgf = device.GcnForwardGraph(g, x, tw, tb, plan, fast_gemm=True)  # tcgen05 TF32 layer GEMMs
+    ms_fast = gpu_ms(lambda: cgf.run(), reps=20)
     out = {"config": name, "n": g.n_rows, "nnz_normalized": g.nnz, "dims": dims, "W": width,
            "gcn_forward_ms": round(ms, 4), "gcn_forward_cuda_graph_ms": round(ms_graph, 4),
+           "gcn_forward_fast_tf32_cuda_graph_ms": round(ms_fast, 4),
            "gcn_forward_exact_ms": round(ms_exact, 4)}
     if cpu and HAVE_REF:
         rp, col, val = host(g)
