@@ -44,6 +44,40 @@ SHAPES = {
     "products": (2_450_000, 1.7885, 17_481, 128),
 }
 METRIC = "AES-SpMM ms & achieved HBM GB/s (% of peak), F=128, at 1/2/4/8 B200"
+DATA = "synthetic (GPU power-law generator, seed %d; U(-1,1) features)"
+
+
+def load_synth():
+    """synth.py loaded by file path: the graph generator needs torch only, and
+    importing it this way does not run the package __init__ (which loads the
+    product's .so files) — the reference arm must not load them."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "aes_bench_synth", os.path.join(ROOT, "paper_2503_18427_b200", "synth.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def workload_config(args, n, nnz, slots, f, elem):
+    """The `config` dict — identical in both arms for the same flags."""
+    return {"workload": f"{args.config} W={args.width} {args.strategy} F={f} sampled SpMM"
+                        + (" + GEMM + all-gather (GCN layer)" if args.mode == "layer" else ""),
+            "n_rows": n, "nnz": nnz, "slots": slots, "F": f, "width": args.width, "strategy": args.strategy,
+            "features": "u8 codes (global min/max, quantize.cpp:23-51)" if elem == 1 else "f32",
+            "l2": "inputs larger than L2 (features %.2f GB, output %.2f GB vs 126 MB L2)"
+                  % (n * f * elem / 1e9, n * f * 4 / 1e9)}
 
 
 def alg_bytes(n_rows, slots, f, elem=4):
@@ -156,14 +190,19 @@ def run_reference(args):
     if not oref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (make -C oracle ref)"}))
         return 0
-    from paper_2503_18427_b200 import synth
+    synth = load_synth()  # by path: no product .so is loaded in this arm
     gdev = "cuda" if torch.cuda.is_available() else "cpu"
     rp, col, val = synth.power_law_csr(n, alpha, maxdeg, seed=args.seed, device=gdev)
     b = synth.features(n, f, seed=5, device=gdev, ld=f)
+    if args.dtype == "int8":
+        print(json.dumps({"impl": "reference", "unavailable": "int8 arm: the reference has no quantized SpMM "
+                          "entry point (dequantize + spmm_sampled is what it would run)"}))
+        return 0
     rp_np = rp.cpu().numpy().view(np.uint64)
     col_np = col.cpu().numpy().view(np.uint32)
     val_np = val.cpu().numpy()
     b_np = np.ascontiguousarray(b.cpu().numpy())
+    del rp, col, val, b
     csr = oref.RefCsr.from_arrays(n, n, rp_np, col_np, val_np)
     threads = os.cpu_count() or 1
     strat = {"adaptive": 0, "afs": 1, "sfs": 2, "full": 3}[args.strategy]
@@ -175,13 +214,13 @@ def run_reference(args):
     t = float(np.mean(timed))
     gbs = by / (t * 1e-3) / 1e9
     line = {
-        "impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "n_gpus": world,
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "n_gpus": max(world, args.gpus),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t, 4), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.config} W={args.width} {args.strategy} F={f} spmm_sampled",
-                   "n_rows": n, "nnz": int(rp_np[-1]), "slots": slots, "F": f, "width": args.width,
-                   "plan_ms": round(plan_ms, 3), "median_ms": round(float(np.median(timed)), 3)},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": DATA % args.seed,
+        "config": workload_config(args, n, int(rp_np[-1]), slots, f, 4),
+        "plan_ms": round(plan_ms, 3), "median_ms": round(float(np.median(timed)), 3),
         "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
+                         "cpu_model": cpu_model(),
                          "sample": f"full {args.config} workload, reference aes::spmm_sampled "
                                    f"(proj/src/spmm.cpp:40-107), {threads} std::threads, prebuilt plans"},
         "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -227,6 +266,7 @@ def cpu_baseline(args, rp_np, col_np, val_np, b_np, f):
         sample = f"first {rows} rows of the workload, oracle port (scalar C)"
     gbs = alg_bytes(rows, slots, f) / (t * 1e-3) / 1e9
     return {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": kind, "sample": sample,
+            "cpu_model": cpu_model(),
             "ms": round(t, 3)}
 
 
@@ -246,20 +286,24 @@ def run_ours(args):
     import torch
 
     rank, world, local = dist_env()
-    # one GPU per rank; AES_BENCH_BACKEND=gloo (with ranks sharing a device)
-    # is a functional check of the multi-rank path on a one-GPU box only
-    local = local % max(torch.cuda.device_count(), 1)
+    # one GPU per rank over NCCL.  With fewer devices than ranks (a one-GPU
+    # box) the ranks share devices over gloo: a functional check of the
+    # multi-rank path only, flagged in the line ("shared_devices")
+    n_dev = max(torch.cuda.device_count(), 1)
+    shared = world > n_dev
+    local = local % n_dev
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        backend = os.environ.get("AES_BENCH_BACKEND", "nccl")
+        backend = os.environ.get("AES_BENCH_BACKEND", "gloo" if shared else "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
 
-    from paper_2503_18427_b200 import capi, device, synth
+    from paper_2503_18427_b200 import capi, device
+    synth = load_synth()
     capi.check(capi.lib().aes_dev_spmm_set_schedule(args.sched))
 
     n, alpha, maxdeg, f = SHAPES[args.config]
@@ -289,10 +333,12 @@ def run_ours(args):
     if args.mode == "layer":
         w = (torch.rand(f, f, device="cuda") - 0.5)
         bias = torch.full((f,), 0.01, device="cuda")
-        h_next = device.empty_padded(max(shard_rows, 1), f)
-        gathered = torch.empty((cuts[-1] if world == 1 else max(c1 - c0 for c0, c1 in zip(cuts, cuts[1:])) * world, f),
-                               device="cuda")
-        layer = (w, bias, h_next, gathered)
+        per = max(c1 - c0 for c0, c1 in zip(cuts, cuts[1:]))
+        # the next-layer replica; this rank's GEMM writes its own slice and
+        # the all-gather runs in place on it (no send buffer, no copy)
+        gathered = torch.zeros((per * world, (f + 3) & ~3), device="cuda")
+        mine = gathered[rank * per:(rank + 1) * per]
+        layer = (w, bias, gathered, mine)
 
     def step():
         if quant is not None:
@@ -300,13 +346,11 @@ def run_ours(args):
         else:
             device.spmm(srow, full_plan.scol, full_plan.sval, b, out=out, max_row_slots=full_plan.row_bound)
         if layer is not None:
-            w, bias, h_next, gathered = layer
-            device.gemm_bias_act(out, w, bias, True, out=h_next)
+            w, bias, gathered, mine = layer
+            if shard_rows:
+                device.gemm_bias_act(out[:shard_rows], w, bias, True, out=mine[:shard_rows, :f])
             if world > 1:
-                mx = gathered.shape[0] // world
-                send = torch.zeros((mx, f), device="cuda")
-                send[:shard_rows].copy_(h_next[:shard_rows])
-                dist.all_gather_into_tensor(gathered, send)
+                dist.all_gather_into_tensor(gathered, mine)
 
     for _ in range(args.warmup):
         step()
@@ -341,12 +385,24 @@ def run_ours(args):
                 "frac": round(achieved / peak, 4),
                 # the committed ncu capture is of the full-graph launch (N = 1)
                 "traffic": load_traffic(f"spmm_{args.dtype}_{args.config}") if world == 1 else None,
+                "traffic_source": "static: dram__bytes_read.sum + dram__bytes_write.sum of this kernel from the "
+                                  "committed ncu --set full capture (profiles/ncu_summary.json), not measured in "
+                                  "this run",
                 "peak_kind": peak_kind, "alg_bytes_per_launch": my_bytes, "nominal_8000_frac": round(achieved / 8000, 4)}
+
+    # ---- kernels one step launches, counted by CUPTI (torch.profiler) on one
+    # extra step after the timed region; gpu_launches = per-step count x steps
+    launches = count_launches(step)
 
     # ---- e2e through the reference-facing C-ABI handle call, pinned host buffers
     e2e = None
     if not args.no_e2e and args.dtype == "f32":
         e2e = run_e2e(args, rp, col, val, b, lo, hi, f, n, total_bytes, dist, world)
+        if world == 1:
+            try:
+                e2e["pybind_call"] = run_pybind_call(args, rp, col, val, b, f, total_bytes)
+            except Exception as e:  # reporting only
+                e2e["pybind_call"] = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
     elif not args.no_e2e and args.dtype == "int8":
         e2e = run_e2e_q8(args, quant, full_plan, srow, shard_rows, f, total_bytes, dist)
 
@@ -373,18 +429,28 @@ def run_ours(args):
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u8" if args.dtype == "int8" else "f32",
-            "data": "synthetic (GPU power-law generator, seed %d; U(-1,1) features)" % args.seed,
-            "config": {"workload": f"{args.config} W={args.width} {args.strategy} F={f} sampled SpMM"
-                                   + (" + GEMM + all-gather (GCN layer)" if args.mode == "layer" else ""),
-                       "n_rows": n, "nnz": int(rp[-1].item()), "slots": int(srow_host[-1]), "F": f,
-                       "width": args.width, "mode": args.mode, "shard_rows": [c1 - c0 for c0, c1 in zip(cuts, cuts[1:])],
-                       "l2": "inputs larger than L2 (features %.2f GB, output %.2f GB vs 126 MB L2)"
-                             % (n * f * elem / 1e9, n * f * 4 / 1e9),
-                       "parallelism": f"row-sharded x{world}" if world > 1 else "single GPU"},
+            "data": DATA % args.seed,
+            "config": workload_config(args, n, int(rp[-1].item()), int(srow_host[-1]), f, elem),
+            "parallelism": f"row-sharded x{world}" if world > 1 else "single GPU",
+            "shard_rows": [c1 - c0 for c0, c1 in zip(cuts, cuts[1:])],
             "roofline": roofline, "clocks": clocks,
             "e2e": e2e, "cpu_baseline": cpu, "gcn_layer": gcn_layer,
-            "gpu_launches": args.steps * (1 + (1 if args.mode == "layer" else 0)),
+            "gpu_launches": launches["per_step"] * args.steps,
+            "gpu_launches_per_step": launches,
         }
+        if world > 1:
+            line["backend"] = dist.get_backend()
+            line["shared_devices"] = shared
+        if gcn_layer and "error" not in gcn_layer:
+            # N > 1 headline pair: the SpMM-only step (value) and the layer step
+            line["layer_step"] = {
+                "spmm_only_ms": round(ms_step, 5),
+                "layer_nccl_ms": gcn_layer.get("exact_nccl_allgather_ms"),
+                "layer_p2p_fused_ms": gcn_layer.get("exact_ordered_fp32_ms"),
+                "layer_p2p_fused_tf32_ms": gcn_layer.get("fast_tcgen05_tf32_ms"),
+                "what": "one GCN layer F->F: shard SpMM -> ordered GEMM + bias + ReLU -> exchange of the "
+                        "next-layer replica (NCCL in-place all-gather, or stores to every rank's replica "
+                        "from the GEMM epilogue over peer memory)"}
         print(json.dumps(line), flush=True)
     if layer_failed:  # the device context may be gone: no collective teardown
         sys.stdout.flush()
@@ -393,6 +459,49 @@ def run_ours(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def count_launches(step):
+    """Kernels one step launches, from CUPTI activity records (torch.profiler):
+    ours (the repo's .so) and any others, by name."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    try:
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            step()
+            torch.cuda.synchronize()
+        names = [e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+    except Exception as e:  # profiler unavailable: say so, claim nothing
+        return {"per_step": 0, "error": f"{type(e).__name__}: {str(e)[:120]}"}
+    kernels = [nm for nm in names if not nm.startswith(("Memcpy", "Memset", "memcpy", "memset"))]
+    other = [nm for nm in kernels if "at::" in nm or "nccl" in nm.lower() or "gloo" in nm]
+    ours = [nm for nm in kernels if nm not in other]
+    short = sorted({nm.split("<")[0].split("(")[0].replace("void ", "") for nm in ours})
+    return {"per_step": len(ours), "other_per_step": len(other), "kernels": short,
+            "how": "CUPTI kernel records of one extra step (torch.profiler), not in the timed region"}
+
+
+def run_pybind_call(args, rp, col, val, b, f, total_bytes):
+    """The call a reference Python user makes: _core.spmm_sampled(a, b, plans)
+    on numpy arrays (module.cpp:124-131) — pageable host memory, synchronous."""
+    import numpy as np
+
+    import paper_2503_18427_b200 as m
+    n = rp.numel() - 1
+    a = m.CsrMatrix(n, n, rp.cpu().numpy().view(np.uint64), col.cpu().numpy().view(np.uint32), val.cpu().numpy())
+    plans = m.build_plan_set(a, args.width, getattr(m.Strategy, args.strategy.upper()))
+    b_np = np.ascontiguousarray(b.cpu().numpy()[:, :f])
+    m.spmm_sampled(a, b_np, plans)
+    steps = 3
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        m.spmm_sampled(a, b_np, plans)
+    t = (time.perf_counter() - t0) / steps
+    return {"value": round(total_bytes / t / 1e9, 3), "ms_per_step": round(t * 1e3, 3),
+            "h2d_bytes_per_step": n * f * 4, "d2h_bytes_per_step": n * f * 4,
+            "path": "paper_2503_18427_b200._core.spmm_sampled(a, numpy b, plans) (== aes_spmm._core), "
+                    "pageable numpy buffers, synchronous, mean of %d" % steps}
 
 
 def release(model):
@@ -419,6 +528,24 @@ def run_gcn_layer(args, plan, n, f, b, dist):
     bias = torch.full((f,), 0.01, device="cuda")
     x = b[:, :f]
     out = {}
+    # SpMM -> exact GEMM (epilogue writes this rank's slice) -> in-place NCCL
+    # all-gather of the next-layer replica (gcn.ShardedGCN exchange="nccl")
+    model = ShardedGCN(plan.srow_ptr, plan.scol, plan.sval, n, [w], [bias], exchange="nccl",
+                       max_row_slots=plan.row_bound)
+    for _ in range(2):
+        model.forward(x, copy_out=False)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(3, min(args.steps, 10))
+    s.record()
+    for _ in range(steps):
+        model.forward(x, copy_out=False)
+    e.record()
+    torch.cuda.synchronize()
+    out["exact_nccl_allgather_ms"] = round(max_over_ranks(s.elapsed_time(e) / steps, dist), 4)
+    del model
     for name, fast in (("exact_ordered_fp32", False), ("fast_tcgen05_tf32", True)):
         model = ShardedGCN(plan.srow_ptr, plan.scol, plan.sval, n, [w], [bias], exchange="p2p", fast_gemm=fast,
                            max_row_slots=plan.row_bound)
@@ -600,6 +727,18 @@ def run_e2e(args, rp, col, val, b, lo, hi, f, n, total_bytes, dist, world):
                           "path": "C-ABI aes_spmm_sampled (synchronous, like the reference call)"}}
 
 
+def relaunch(args):
+    """`bench.py --gpus N` outside torchrun: start N ranks (one per GPU)
+    under torch.distributed.run on 127.0.0.1, as the driver would."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -618,10 +757,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-layer", action="store_true", help="skip the GCN layer (SpMM+GEMM+exchange) timing")
     args = ap.parse_args()
-    if args.warmup < 3 and args.impl == "ours":
-        args.warmup = max(args.warmup, 1)
     if args.impl == "reference":
-        return run_reference(args)
+        return run_reference(args)  # rank 0 alone does CPU work; no ranks needed
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
     return run_ours(args)
 
 

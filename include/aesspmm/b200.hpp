@@ -11,6 +11,10 @@
 // Differences, all documented in DESIGN.md:
 //  * SamplePlanSet additionally carries an opaque handle to the plan built in
 //    HBM by build_plan_set (the `plans` vector is still filled, eagerly).
+//    Edits to `plans`, `width` or `strategy` after build_plan_set are
+//    honoured: the handle is used only while a fingerprint of the host plans
+//    still matches; otherwise the plans are re-uploaded, as executed by the
+//    reference (spmm.cpp:40-100).
 //  * n_threads parameters are accepted and ignored (results never depend on
 //    them, in the reference or here).
 //  * Out of scope for the B200 hot path (not declared): csr_from_triplets

@@ -122,7 +122,11 @@ AES_API int aes_gcn_normalize(aes_csr_t a, int add_self_loops, aes_csr_t* out);
 AES_API int aes_build_plan_set(aes_csr_t a, uint32_t width, int strategy, aes_plan_t* out);
 /* A plan set given as host data (SamplePlanSet built or edited by the
  * caller): per-row chunk_len/sample_cnt and starts in CSR form (starts_ptr
- * n+1).  Filled in slot order exactly like a built plan (spmm.cpp:54-76). */
+ * n+1).  Filled in slot order exactly like a built plan (spmm.cpp:54-76).
+ * Validated first (the reference reads out of range instead): starts_ptr
+ * must begin at 0 and be non-decreasing with at least sample_cnt starts per
+ * row, and every window must fit its row (start + chunk_len <= row nnz);
+ * otherwise AES_ERR_INVALID_ARG "invalid plan: ... row <i>". */
 AES_API int aes_plan_from_host(aes_csr_t a, uint32_t width, int strategy, const uint32_t* chunk_len,
                                const uint32_t* sample_cnt, const uint64_t* starts_ptr,
                                const uint32_t* starts, aes_plan_t* out);
@@ -156,7 +160,9 @@ AES_API int aes_spmm_sampled(aes_csr_t a, const float* b, uint64_t b_rows, uint6
  * H2D(b) -> SpMM -> D2H(c) on `stream` (NULL = library stream) and returns.
  * b and c should be pinned; they must stay valid until the stream reaches
  * this point.  Successive calls on two streams overlap one call's H2D with
- * the previous call's D2H (both copy engines busy).  The plan must have been
+ * the previous call's D2H (both copy engines busy).  The plan (and its
+ * matrix) may be destroyed right after the call: aes_plan_destroy orders its
+ * frees after the work enqueued here on `stream`.  The plan must have been
  * built on `a`. */
 AES_API int aes_spmm_sampled_async(aes_csr_t a, const float* b, uint64_t b_rows, uint64_t f,
                                    aes_plan_t p, float* c, void* stream);
@@ -397,13 +403,16 @@ AES_API int aes_dev_all_finite(const float* x, uint64_t count, unsigned int* bad
 /* ---- row-sharded GCN forward over NCCL (sharded.cu) ----------------------
  * gcn_forward (proj/src/gnn.cpp:66-78) on one rank of an equal-row sharded
  * graph: per layer the shard's sampled SpMM, the ordered-fp32 GEMM + bias
- * (+ ReLU but on the last layer) into a [rows_per_rank, ld] block, and an
- * ncclAllGather of the blocks (rank order) into the other replica.
+ * (+ ReLU but on the last layer) into a [rows_per_rank, round4(dims[l+1])]
+ * block, and an ncclAllGather of the blocks (rank order) into the other
+ * replica, which holds that layer's output with row stride round4(dims[l+1])
+ * (the exchange moves N * round4(fout) * 4 bytes, not N * ld * 4).
  * srow_shard: the shard's shard_rows+1 row offsets into the GLOBAL sampled
  * CSR (scol, sval); replica_a holds the layer-0 input for every row
  * ([world * rows_per_rank, ld], ld % 4 == 0, dims[l] <= ld), replica_b is the
  * ping-pong partner; *out_replica receives the one holding the logits of all
- * rows.  weights / biases: host arrays of n_layers device pointers (biases
+ * rows and *out_ld (may be NULL) its row stride, round4(dims[n_layers]).
+ * After every all-gather ncclCommGetAsyncError is checked.  weights / biases: host arrays of n_layers device pointers (biases
  * may be NULL or hold NULL entries).  nccl_comm: the caller's ncclComm_t
  * (NCCL is looked up at run time in the process).  Bit-identical to the
  * single-GPU forward.  Stream-ordered; no host synchronisation. */
@@ -413,7 +422,7 @@ AES_API int aes_gcn_forward_sharded(const uint64_t* srow_shard, const uint32_t* 
                                     const float* const* weights, const float* const* biases, int finite_w,
                                     float* replica_a, float* replica_b, uint64_t ld, uint64_t max_row_slots,
                                     void* workspace, size_t workspace_bytes, void* nccl_comm, float** out_replica,
-                                    void* stream);
+                                    uint64_t* out_ld, void* stream);
 
 /* ---- int8 layer exchange over peer memory (exchange.cu) ------------------
  * Replaces, per hidden GCN layer, the reference composition

@@ -75,7 +75,7 @@ def lib():
         L.aes_gcn_sharded_workspace_bytes.argtypes = [u64, u64]
         L.aes_gcn_sharded_workspace_bytes.restype = u64
         L.aes_gcn_forward_sharded.argtypes = [vp, vp, vp, u64, u64, i32, vp, vp, vp, i32, vp, vp, u64, u64, vp, sz,
-                                              vp, vp, vp]
+                                              vp, vp, vp, vp]
         L.aes_dev_publish_params.argtypes = [vp, i32, i32, vp, vp, i32, vp]
         L.aes_dev_fold_params_lut.argtypes = [vp, i32, u32, vp, vp, vp]
         L.aes_quantize_bcast_ctas.argtypes = [u64]

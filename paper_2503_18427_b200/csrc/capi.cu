@@ -50,6 +50,8 @@ int launch_evaluate(const uint32_t*, const uint32_t*, const uint32_t*, const uin
                     unsigned long long*, unsigned long long*, cudaStream_t);
 int launch_explicit_fill(const uint64_t*, const uint32_t*, const uint64_t*, const uint32_t*, const uint32_t*,
                          const float*, uint64_t, const uint64_t*, uint32_t*, float*, cudaStream_t);
+int launch_explicit_check(const uint64_t*, const uint32_t*, const uint64_t*, const uint32_t*, uint64_t,
+                          unsigned long long*, cudaStream_t);
 int launch_explicit_rate(const uint64_t*, const uint32_t*, const uint64_t*, const uint32_t*, uint64_t, uint64_t,
                          unsigned char*, double*, unsigned long long*, cudaStream_t);
 
@@ -59,15 +61,17 @@ namespace {
 // library stream + stream-ordered device buffers
 // ---------------------------------------------------------------------------
 cudaStream_t lib_stream() {
-    static std::once_flag once;
-    static cudaStream_t s = nullptr;
-    std::call_once(once, [] {
-        cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    // one library stream per device (handles live on the device that was
+    // current when they were created; calls run on that device's stream)
+    static std::once_flag once[kMaxDevices];
+    static cudaStream_t streams[kMaxDevices] = {};
+    const int dev = cur_device();
+    std::call_once(once[dev], [dev] {
+        cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
         // keep freed stream-ordered blocks cached: per-call feature/result
         // buffers (GBs at the BASELINE shapes) are then recycled, not re-mapped
-        int dev = 0;
         cudaMemPool_t pool;
-        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
             uint64_t thr = ~0ull;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
             // and never hand a block still pending on another stream to a new
@@ -78,7 +82,7 @@ cudaStream_t lib_stream() {
             cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
         }
     });
-    return s;
+    return streams[dev];
 }
 
 template <typename T>
@@ -199,6 +203,34 @@ struct aes_plan_s {
     uint64_t* starts_ptr = nullptr;   // n+1
     uint32_t* starts = nullptr;
     uint64_t total_starts = 0;
+    // caller streams that aes_spmm_sampled_async enqueued reads of this plan
+    // on, each with an event recorded after its last use: destroy makes the
+    // library stream wait on them before freeing (stream-ordered lifetime)
+    std::mutex use_mu;
+    std::vector<std::pair<cudaStream_t, cudaEvent_t>> uses;
+    void note_use(cudaStream_t st) {
+        std::lock_guard<std::mutex> lock(use_mu);
+        for (auto& u : uses)
+            if (u.first == st) {
+                cudaEventRecord(u.second, st);
+                return;
+            }
+        cudaEvent_t e;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+            cudaStreamSynchronize(st);  // no event: make the use complete now
+            return;
+        }
+        cudaEventRecord(e, st);
+        uses.emplace_back(st, e);
+    }
+    void order_after_uses(cudaStream_t lib) {
+        std::lock_guard<std::mutex> lock(use_mu);
+        for (auto& u : uses) {
+            cudaStreamWaitEvent(lib, u.second, 0);
+            cudaEventDestroy(u.second);
+        }
+        uses.clear();
+    }
 };
 
 struct aes_qfeat_s {
@@ -606,11 +638,16 @@ int aes_plan_from_host(aes_csr_t a, uint32_t width, int strategy, const uint32_t
     cudaStream_t st = lib_stream();
     const uint64_t n = a->n_rows;
     const uint64_t tot_starts = starts_ptr ? starts_ptr[n] : 0;
-    // interleave (chunk, cnt) on the host side of the copy: plain data marshaling
+    if (n && starts_ptr[0] != 0) return fail(AES_ERR_INVALID_ARG, "invalid plan: starts offsets must begin at 0");
+    if (tot_starts && !starts) return fail(AES_ERR_INVALID_ARG, "null argument");
+    // interleave (chunk, cnt) on the host side of the copy: plain data marshaling;
+    // each row must carry at least sample_cnt window starts
     std::vector<uint32_t> params(2 * (n ? n : 1));
     for (uint64_t i = 0; i < n; ++i) {
         params[2 * i] = chunk_len[i];
         params[2 * i + 1] = sample_cnt[i];
+        if (starts_ptr[i + 1] < starts_ptr[i] || starts_ptr[i + 1] - starts_ptr[i] < sample_cnt[i])
+            return fail(AES_ERR_INVALID_ARG, "invalid plan: fewer starts than sample_cnt at row " + std::to_string(i));
     }
     DBuf<uint32_t> dpar, dst;
     DBuf<uint64_t> dsp, srow;
@@ -624,6 +661,16 @@ int aes_plan_from_host(aes_csr_t a, uint32_t width, int strategy, const uint32_t
     AES_TRY(srow.alloc(n + 1));
     size_t wsb = row_scan_workspace_bytes(n);
     AES_TRY(ws.alloc(wsb));
+    {  // every window inside its row (the fill / mark kernels read through them)
+        DBuf<unsigned long long> bad;
+        AES_TRY(bad.alloc(1));
+        AES_TRY(launch_explicit_check(a->row_ptr, dpar.p, dsp.p, dst.p, n, bad.p, st));
+        unsigned long long bad_row = 0;
+        AES_TRY(d2h_scalar(bad.p, &bad_row));
+        if (bad_row != ~0ull)
+            return fail(AES_ERR_INVALID_ARG,
+                        "invalid plan: sample window past the end of row " + std::to_string(bad_row));
+    }
     ScanArgs sa{nullptr, nullptr, n, width, strategy, 0, srow.p, dpar.p};
     AES_TRY(launch_row_scan(kScanExplicit, sa, ws.p, wsb, st));
     uint64_t total = 0;
@@ -658,6 +705,7 @@ int aes_plan_from_host(aes_csr_t a, uint32_t width, int strategy, const uint32_t
 int aes_plan_destroy(aes_plan_t p) {
     if (!p) return AES_OK;
     cudaStream_t st = lib_stream();
+    p->order_after_uses(st);  // frees below run after every async SpMM that read the plan
     cudaFreeAsync(p->srow_ptr, st);
     cudaFreeAsync(p->scol, st);
     cudaFreeAsync(p->sval, st);
@@ -827,6 +875,7 @@ int aes_spmm_sampled_async(aes_csr_t a, const float* b, uint64_t b_rows, uint64_
     AES_CUDA_TRY(cudaMemcpy2DAsync(c, f * 4, dc, ld * 4, f * 4, n, cudaMemcpyDeviceToHost, st));
     AES_CUDA_TRY(cudaFreeAsync(db, st));
     AES_CUDA_TRY(cudaFreeAsync(dc, st));
+    if (st != lib_stream()) p->note_use(st);
     return AES_OK;
 }
 
@@ -923,7 +972,7 @@ int aes_qfeat_from_codes(const uint16_t* codes, uint64_t rows, uint64_t cols, fl
             cudaMemsetAsync(c8, 0, rows * ld, st);
             cudaMemsetAsync(ovf.p, 0, 4, st);
             if (n)
-                narrow_u16_kernel<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(d16.p, rows, cols, ld,
+                narrow_u16_kernel<<<grid_for(n, 256, num_sms() * 32), 256, 0, st>>>(d16.p, rows, cols, ld,
                                                                               (uint8_t*)c8, ovf.p);
             unsigned int o = 0;
             s = d2h_scalar(ovf.p, &o);
@@ -975,7 +1024,7 @@ int aes_qfeat_codes(aes_qfeat_t q, uint16_t* codes) {
     if (q->u8) {
         DBuf<uint16_t> w;
         AES_TRY(w.alloc(n));
-        widen_u8_kernel<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>((const uint8_t*)q->codes, q->rows, q->cols,
+        widen_u8_kernel<<<grid_for(n, 256, num_sms() * 32), 256, 0, st>>>((const uint8_t*)q->codes, q->rows, q->cols,
                                                                     q->ld, w.p);
         AES_CUDA_TRY(cudaGetLastError());
         AES_CUDA_TRY(cudaMemcpyAsync(codes, w.p, n * 2, cudaMemcpyDeviceToHost, st));

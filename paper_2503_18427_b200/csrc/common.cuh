@@ -113,7 +113,25 @@ __device__ __forceinline__ void add2_rn(float& a0, float& a1, float p0, float p1
 // ---------------------------------------------------------------------------
 // Launch geometry
 // ---------------------------------------------------------------------------
-constexpr int kNumSMs = 148;
+// Per-device state: the library may drive several GPUs from one process, so
+// SM counts, shared-memory opt-ins and occupancy are cached per device.
+constexpr int kMaxDevices = 64;
+inline int cur_device() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+    return d;
+}
+// SMs of the current device (148 on B200), queried once per device.
+inline int num_sms() {
+    static int sms[kMaxDevices] = {};
+    const int d = cur_device();
+    if (sms[d] == 0) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+        sms[d] = v > 0 ? v : 148;
+    }
+    return sms[d];
+}
 
 inline unsigned grid_for(uint64_t work, unsigned per_block, unsigned cap = 1u << 30) {
     uint64_t g = (work + per_block - 1) / per_block;

@@ -44,11 +44,39 @@ struct QFeat {
     ~QFeat() { aes_qfeat_destroy(h); }
 };
 
+// FNV-1a over the host plan vectors + width + strategy.  The reference
+// always executes `plans.plans`; a caller may edit them (or width/strategy)
+// after build_plan_set, so the cached device plan is used only while this
+// fingerprint still matches.
+std::uint64_t plan_fingerprint(const SamplePlanSet& ps) {
+    std::uint64_t h = 1469598103934665603ull;
+    auto mix = [&h](std::uint64_t v) {
+        for (int i = 0; i < 8; ++i, v >>= 8) h = (h ^ (v & 0xff)) * 1099511628211ull;
+    };
+    mix(ps.width);
+    mix(static_cast<std::uint64_t>(ps.strategy));
+    mix(ps.plans.size());
+    for (const RowSamplePlan& p : ps.plans) {
+        mix((std::uint64_t)p.params.chunk_len << 32 | p.params.sample_cnt);
+        mix(p.starts.size());
+        for (std::uint32_t st : p.starts) mix(st);
+    }
+    return h;
+}
+
 // The device plan a SamplePlanSet carries; keeps its source CSR alive.
 struct DevicePlan {
     std::shared_ptr<Csr> src;
     Plan plan;
+    std::uint64_t fingerprint = 0;  // of the host plans it was exported as
 };
+
+// The cached device plan of `ps`, or null when the host plans were edited.
+aes_plan_t cached_plan(const SamplePlanSet& ps) {
+    if (!ps.device) return nullptr;
+    auto* dp = static_cast<DevicePlan*>(ps.device.get());
+    return plan_fingerprint(ps) == dp->fingerprint ? dp->plan.h : nullptr;
+}
 
 std::shared_ptr<Csr> upload(const CsrMatrix& m) {
     auto c = std::make_shared<Csr>();
@@ -77,7 +105,7 @@ void flatten(const SamplePlanSet& ps, std::vector<std::uint32_t>& chunk, std::ve
 // (re-filled from `a` inside the C ABI when `a` is another upload), or one
 // built from the host plan vectors.
 aes_plan_t plan_for(const SamplePlanSet& ps, const Csr& a, Plan& scratch) {
-    if (ps.device) return static_cast<DevicePlan*>(ps.device.get())->plan.h;
+    if (aes_plan_t cached = cached_plan(ps)) return cached;
     std::vector<std::uint32_t> chunk, cnt, starts;
     std::vector<std::uint64_t> sp;
     flatten(ps, chunk, cnt, sp, starts);
@@ -212,6 +240,7 @@ SamplePlanSet build_plan_set(const CsrMatrix& m, std::uint32_t width, Strategy s
         p.params = {chunk[i], cnt[i]};
         p.starts.assign(starts.begin() + sp[i], starts.begin() + sp[i + 1]);
     }
+    dp->fingerprint = plan_fingerprint(set);
     set.device = std::static_pointer_cast<void>(dp);
     return set;
 }
@@ -224,10 +253,8 @@ SamplingRates sampling_rate(const SamplePlanSet& plans, const RowStats& stats) {
     Csr c;
     check(aes_csr_structure(n, 0, rp.data(), &c.h));
     Plan scratch;
-    aes_plan_t p;
-    if (plans.device) {
-        p = static_cast<DevicePlan*>(plans.device.get())->plan.h;
-    } else {
+    aes_plan_t p = cached_plan(plans);
+    if (!p) {
         std::vector<std::uint32_t> chunk, cnt, starts;
         std::vector<std::uint64_t> sp;
         flatten(plans, chunk, cnt, sp, starts);

@@ -356,7 +356,7 @@ int aes_dev_all_finite(const float* x, uint64_t count, unsigned int* bad_flag, v
     using namespace aes;
     cudaStream_t st = as_stream(stream);
     AES_CUDA_TRY(cudaMemsetAsync(bad_flag, 0, sizeof(unsigned int), st));
-    if (count) all_finite_kernel<<<grid_for(count, 256, 148 * 8), 256, 0, st>>>(x, count, bad_flag);
+    if (count) all_finite_kernel<<<grid_for(count, 256, num_sms() * 8), 256, 0, st>>>(x, count, bad_flag);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
 }

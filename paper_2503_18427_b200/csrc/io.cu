@@ -57,10 +57,19 @@ struct Staging {
         return AES_OK;
     }
 };
-Staging& staging() {
-    static Staging s;
-    return s;
+Staging& staging() {  // per device: the staging stream and events belong to one device
+    static Staging s[kMaxDevices];
+    return s[cur_device()];
 }
+
+// Drains the staging stream on every exit path of stream_rows, so an error
+// return never leaves a DMA still writing into a buffer the caller frees.
+struct DrainGuard {
+    cudaStream_t st;
+    ~DrainGuard() {
+        if (st) cudaStreamSynchronize(st);
+    }
+};
 
 struct File {
     FILE* f = nullptr;
@@ -120,12 +129,16 @@ bool parallel_pread(int fd, char* dst, uint64_t bytes, int64_t pos) {
 }
 
 // Stream `rows` rows of `row_bytes` from the file into dst (row pitch
-// dst_pitch bytes), double-buffered through pinned memory.
-int stream_rows(File& fh, void* dst, uint64_t rows, uint64_t row_bytes, uint64_t dst_pitch) {
+// dst_pitch bytes), double-buffered through pinned memory.  zero_pitch:
+// clear the whole destination (row padding included) first, ordered before
+// the copies on the same stream.
+int stream_rows(File& fh, void* dst, uint64_t rows, uint64_t row_bytes, uint64_t dst_pitch, bool zero_pitch = false) {
     if (rows == 0 || row_bytes == 0) return AES_OK;
     Staging& s = staging();
     std::lock_guard<std::mutex> lock(s.mu);
     AES_TRY(s.init());
+    DrainGuard drain{s.st};
+    if (zero_pitch) AES_CUDA_TRY(cudaMemsetAsync(dst, 0, rows * dst_pitch, s.st));
     const uint64_t rows_per = row_bytes >= kChunk ? 1 : kChunk / row_bytes;
     if (row_bytes > kChunk) return io_fail("row larger than the staging chunk", fh.path);
     int b = 0;
@@ -226,8 +239,7 @@ int aes_fmat_load_qfeat(const char* path, aes_qfeat_t* out, double* load_ms) {
     const uint64_t ld = (h.cols + 15) & ~15ull;  // 16-B code rows (int8 SpMM batch kernel)
     auto* codes = static_cast<uint8_t*>(capi_alloc(h.rows * ld + 16));
     if (!codes) return fail(AES_ERR_CUDA, "alloc");
-    if (ld != h.cols) cudaMemset(codes, 0, h.rows * ld);
-    int s = stream_rows(fh, codes, h.rows, h.cols, ld);
+    int s = stream_rows(fh, codes, h.rows, h.cols, ld, ld != h.cols);
     if (!s) s = capi_make_qfeat_u8(codes, h.rows, h.cols, ld, h.lo, h.hi, out);  // takes ownership
     if (s) {
         capi_free(codes);

@@ -58,8 +58,8 @@ int launch_gcn_normalize(const uint64_t* row_ptr, const uint32_t* col, uint64_t 
                          const uint64_t* out_ptr, float* inv_scratch, uint32_t* out_col, float* out_val,
                          cudaStream_t st) {
     if (n == 0) return AES_OK;
-    inv_sqrt_deg_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(out_ptr, n, inv_scratch);
-    gcn_fill_kernel<<<grid_for(n * 32, 256, 148 * 32), 256, 0, st>>>(row_ptr, col, n, add_self_loops, out_ptr,
+    inv_sqrt_deg_kernel<<<grid_for(n, 256, num_sms() * 16), 256, 0, st>>>(out_ptr, n, inv_scratch);
+    gcn_fill_kernel<<<grid_for(n * 32, 256, num_sms() * 32), 256, 0, st>>>(row_ptr, col, n, add_self_loops, out_ptr,
                                                                      inv_scratch, out_col, out_val);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
@@ -128,14 +128,14 @@ __global__ void evaluate_kernel(const uint32_t* __restrict__ pred, const uint32_
 
 int launch_row_mean(const uint64_t* row_ptr, uint64_t n, float* val, cudaStream_t st) {
     if (n == 0) return AES_OK;
-    row_mean_kernel<<<grid_for(n * 32, 256, 148 * 32), 256, 0, st>>>(row_ptr, n, val);
+    row_mean_kernel<<<grid_for(n * 32, 256, num_sms() * 32), 256, 0, st>>>(row_ptr, n, val);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
 }
 
 int launch_argmax(const float* x, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t* out, cudaStream_t st) {
     if (rows == 0) return AES_OK;
-    argmax_kernel<<<grid_for(rows, 256, 148 * 16), 256, 0, st>>>(x, rows, cols, ld, out);
+    argmax_kernel<<<grid_for(rows, 256, num_sms() * 16), 256, 0, st>>>(x, rows, cols, ld, out);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
 }
@@ -144,7 +144,7 @@ int launch_evaluate(const uint32_t* pred, const uint32_t* labels, const uint32_t
                     uint64_t rows, uint64_t cols, unsigned long long* counts, unsigned long long* per_class,
                     cudaStream_t st) {
     if (rows == 0) return AES_OK;
-    evaluate_kernel<<<grid_for(rows, 256, 148 * 16), 256, 0, st>>>(pred, labels, ref, mask, rows, cols, counts,
+    evaluate_kernel<<<grid_for(rows, 256, num_sms() * 16), 256, 0, st>>>(pred, labels, ref, mask, rows, cols, counts,
                                                                    per_class);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;

@@ -233,10 +233,10 @@ int aes_dev_dequantize(const void* codes, uint64_t rows, uint64_t cols, uint64_t
     const uint64_t total = rows * cols;
     if (total == 0) return AES_OK;
     const double step = ((double)hi - (double)lo) / (double)((1u << bits) - 1u);
-    const unsigned grid = grid_for(total, 256, 148 * 32);
+    const unsigned grid = grid_for(total, 256, num_sms() * 32);
     if (bits <= 8 && ldq == cols && ldx == cols && total % 4 == 0 && (uintptr_t)codes % 4 == 0 &&
         (uintptr_t)x % 16 == 0) {
-        dequantize_u8_flat_kernel<<<grid_for(total / 4, 256, 148 * 32), 256, 0, st>>>(
+        dequantize_u8_flat_kernel<<<grid_for(total / 4, 256, num_sms() * 32), 256, 0, st>>>(
             static_cast<const uchar4*>(codes), total / 4, (double)lo, step, (1u << bits) - 1u,
             reinterpret_cast<float4*>(x));
     } else if (bits <= 8)

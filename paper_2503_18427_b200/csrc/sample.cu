@@ -453,6 +453,36 @@ int launch_sample_fill(const uint64_t* plan_row_ptr, const uint64_t* row_ptr, co
     return AES_OK;
 }
 
+// Caller-built plans (aes_plan_from_host) are checked before any fill or
+// mark reads through them: every window s of row r must satisfy
+// start_s + chunk <= row_nnz (or chunk == 0), the only reads the reference
+// makes (spmm.cpp:68-76).  The smallest offending row is recorded.
+__global__ void explicit_check_kernel(const uint64_t* __restrict__ row_ptr, const uint2* __restrict__ params,
+                                      const uint64_t* __restrict__ starts_ptr, const uint32_t* __restrict__ starts,
+                                      uint64_t n, unsigned long long* __restrict__ bad_row) {
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
+        const uint2 p = params[r];
+        if (p.x == 0) continue;
+        const uint64_t nnz = row_ptr[r + 1] - row_ptr[r];
+        const uint64_t sp = starts_ptr[r];
+        bool bad = false;
+        for (uint32_t s = lane; s < p.y; s += 32) bad |= (uint64_t)starts[sp + s] + p.x > nnz;
+        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(bad_row, (unsigned long long)r);
+    }
+}
+
+int launch_explicit_check(const uint64_t* row_ptr, const uint32_t* params, const uint64_t* starts_ptr,
+                          const uint32_t* starts, uint64_t n, unsigned long long* bad_row, cudaStream_t st) {
+    AES_CUDA_TRY(cudaMemsetAsync(bad_row, 0xff, sizeof(unsigned long long), st));
+    if (n == 0) return AES_OK;
+    explicit_check_kernel<<<grid_for(n * 32, 256, num_sms() * 32), 256, 0, st>>>(
+        row_ptr, reinterpret_cast<const uint2*>(params), starts_ptr, starts, n, bad_row);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
 int launch_explicit_fill(const uint64_t* row_ptr, const uint32_t* params, const uint64_t* starts_ptr,
                          const uint32_t* starts, const uint32_t* col, const float* val, uint64_t n,
                          const uint64_t* srow_ptr, uint32_t* scol, float* sval, cudaStream_t st) {
@@ -469,11 +499,11 @@ int launch_explicit_rate(const uint64_t* row_ptr, const uint32_t* params, const 
     AES_CUDA_TRY(cudaMemsetAsync(totals, 0, 3 * sizeof(unsigned long long), st));
     if (n == 0) return AES_OK;
     const uint2* pp = reinterpret_cast<const uint2*>(params);
-    explicit_slots_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(row_ptr, pp, n, per_row, totals);
+    explicit_slots_kernel<<<grid_for(n, 256, num_sms() * 16), 256, 0, st>>>(row_ptr, pp, n, per_row, totals);
     if (nnz) {
         AES_CUDA_TRY(cudaMemsetAsync(seen, 0, nnz, st));
-        explicit_mark_kernel<<<grid_for(n * 32, 256, 148 * 32), 256, 0, st>>>(row_ptr, pp, starts_ptr, starts, n, seen);
-        count_marks_kernel<<<grid_for(nnz, 256, 148 * 16), 256, 0, st>>>(seen, nnz, totals + 1);
+        explicit_mark_kernel<<<grid_for(n * 32, 256, num_sms() * 32), 256, 0, st>>>(row_ptr, pp, starts_ptr, starts, n, seen);
+        count_marks_kernel<<<grid_for(nnz, 256, num_sms() * 16), 256, 0, st>>>(seen, nnz, totals + 1);
     }
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
@@ -483,7 +513,7 @@ int launch_plan_export(const uint64_t* row_ptr, uint64_t n, uint32_t width, int 
                        const uint64_t* starts_ptr, uint32_t* chunk, uint32_t* cnt, uint32_t* starts,
                        cudaStream_t st) {
     if (n == 0) return AES_OK;
-    plan_export_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(row_ptr, n, width, strategy,
+    plan_export_kernel<<<grid_for(n, 256, num_sms() * 16), 256, 0, st>>>(row_ptr, n, width, strategy,
                                                                    starts_ptr, chunk, cnt, starts);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
@@ -493,7 +523,7 @@ int launch_sampling_rate(const uint64_t* row_ptr, uint64_t n, uint32_t width, in
                          double* per_row, unsigned long long* totals, cudaStream_t st) {
     AES_CUDA_TRY(cudaMemsetAsync(totals, 0, 3 * sizeof(unsigned long long), st));
     if (n == 0) return AES_OK;
-    sampling_rate_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(row_ptr, n, width, strategy,
+    sampling_rate_kernel<<<grid_for(n, 256, num_sms() * 16), 256, 0, st>>>(row_ptr, n, width, strategy,
                                                                      per_row, totals);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
@@ -503,7 +533,7 @@ int launch_row_stats(const uint64_t* row_ptr, uint64_t n, uint64_t* row_nnz,
                      unsigned long long* max_nnz, cudaStream_t st) {
     AES_CUDA_TRY(cudaMemsetAsync(max_nnz, 0, sizeof(unsigned long long), st));
     if (n == 0) return AES_OK;
-    row_stats_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(row_ptr, n, row_nnz, max_nnz);
+    row_stats_kernel<<<grid_for(n, 256, num_sms() * 16), 256, 0, st>>>(row_ptr, n, row_nnz, max_nnz);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
 }
@@ -512,7 +542,7 @@ int launch_validate(const uint64_t* row_ptr, const uint32_t* col, uint64_t n, ui
                     unsigned long long* scratch2, cudaStream_t st) {
     AES_CUDA_TRY(cudaMemsetAsync(scratch2, 0xff, 2 * sizeof(unsigned long long), st));
     if (n == 0) return AES_OK;
-    validate_monotonic_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(row_ptr, n, scratch2);
+    validate_monotonic_kernel<<<grid_for(n, 256, num_sms() * 16), 256, 0, st>>>(row_ptr, n, scratch2);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
 }
@@ -520,7 +550,7 @@ int launch_validate(const uint64_t* row_ptr, const uint32_t* col, uint64_t n, ui
 int launch_validate_rows(const uint64_t* row_ptr, const uint32_t* col, uint64_t n, uint64_t n_cols,
                          unsigned long long* scratch, cudaStream_t st) {
     if (n == 0) return AES_OK;
-    validate_rows_kernel<<<grid_for(n * 32, 256, 148 * 32), 256, 0, st>>>(row_ptr, col, n, n_cols,
+    validate_rows_kernel<<<grid_for(n * 32, 256, num_sms() * 32), 256, 0, st>>>(row_ptr, col, n, n_cols,
                                                                          scratch);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;

@@ -921,14 +921,15 @@ template <int C, int WARPS>
 int launch_q8_dual(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, const uint8_t* q,
                    uint64_t ldq, uint32_t f8, float4* c, uint64_t ldc4, const float* lut, cudaStream_t st) {
     const size_t smem = 256 * 256 + (size_t)WARPS * 2 * C * 128;
-    static bool attr_set = false;
+    static bool attr_set_dev[kMaxDevices] = {};
+    bool& attr_set = attr_set_dev[cur_device()];
     if (!attr_set) {
         AES_CUDA_TRY(cudaFuncSetAttribute(spmm_q8_dual_kernel<C, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
         attr_set = true;
     }
     uint32_t gr = 16;  // row ends live in the 16 lanes of a half-warp
-    while (gr > 2 && (n + gr - 1) / gr < (uint64_t)kNumSMs * 128) gr >>= 1;
+    while (gr > 2 && (n + gr - 1) / gr < (uint64_t)num_sms() * 128) gr >>= 1;
     const uint64_t groups = (n + gr - 1) / gr;
     const uint64_t warps = (groups + 1) / 2;
     const unsigned grid = (unsigned)((warps + WARPS - 1) / WARPS);
@@ -1293,7 +1294,8 @@ int launch_q8_batch_t(const uint64_t* srow, const uint32_t* scol, const float* s
                       uint64_t ldq, uint32_t f4, float4* c, uint64_t ldc4, const float* lut, cudaStream_t st,
                       int dyn) {
     const size_t smem = 256 * 256 + (size_t)WARPS * (32 * C + 144);  // LUT + rings, slot metadata, row ends
-    static int occ = 0;
+    static int occ_dev[kMaxDevices] = {};
+    int& occ = occ_dev[cur_device()];
     if (occ == 0) {
         AES_CUDA_TRY(cudaFuncSetAttribute(spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 0>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1309,17 +1311,17 @@ int launch_q8_batch_t(const uint64_t* srow, const uint32_t* scol, const float* s
     // shrink until (row groups x tiles) fills >= 64 warps per SM
     const uint32_t tiles = (f4 + 31) / 32;
     uint32_t gr = 32;
-    while (gr > 2 && (n + gr - 1) / gr * tiles < (uint64_t)kNumSMs * 64) gr >>= 1;
+    while (gr > 2 && (n + gr - 1) / gr * tiles < (uint64_t)num_sms() * 64) gr >>= 1;
     const uint64_t groups = (n + gr - 1) / gr;
     const unsigned gx = (unsigned)((groups + WARPS - 1) / WARPS);
     // auto: the 32-row-group grid when it runs >= 4 waves (0.56 ms on the
     // full products graph, vs 0.59-0.60 balanced), the balanced wave when it
     // would end in a partial wave (row shards: P = 8 0.107 -> 0.095 ms)
-    if (dyn == kSchedAuto) dyn = gx * tiles >= 4ull * kNumSMs * occ ? kSchedStatic : kSchedBal;
+    if (dyn == kSchedAuto) dyn = gx * tiles >= 4ull * num_sms() * occ ? kSchedStatic : kSchedBal;
     if (dyn == kSchedBal || dyn == kSchedBalOne) {  // one wave of resident CTAs per column tile
         // whole waves: the tiles share the resident CTA slots (rounding up
         // would leave one CTA for a second, nearly empty wave)
-        const uint64_t per_wave = (uint64_t)kNumSMs * occ / tiles;
+        const uint64_t per_wave = (uint64_t)num_sms() * occ / tiles;
         const uint64_t per_tile = (per_wave ? per_wave : 1) * bal_waves(n, per_wave * WARPS, 0);
         spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 2><<<dim3((unsigned)per_tile, tiles), WARPS * 32, smem, st>>>(
             srow, scol, sval, n, q, (uint32_t)ldq, f4, c, ldc4, lut, 32, 0, nullptr);
@@ -1332,8 +1334,8 @@ int launch_q8_batch_t(const uint64_t* srow, const uint32_t* scol, const float* s
         AES_CUDA_TRY(cudaMallocAsync((void**)&ws, ws_bytes, st));
         AES_CUDA_TRY(cudaMemsetAsync(ws, 0, 16, st));
         AES_CUDA_TRY(cudaMemsetAsync(reinterpret_cast<unsigned int*>(ws->heavy) + groups, 0, tiles * 4, st));
-        heavy_scan_kernel<<<grid_for(groups, 256, kNumSMs * 8), 256, 0, st>>>(srow, n, gr, groups, ws);
-        const uint64_t per_tile = ((uint64_t)kNumSMs * occ + tiles - 1) / tiles;
+        heavy_scan_kernel<<<grid_for(groups, 256, num_sms() * 8), 256, 0, st>>>(srow, n, gr, groups, ws);
+        const uint64_t per_tile = ((uint64_t)num_sms() * occ + tiles - 1) / tiles;
         const dim3 grid((unsigned)(gx < per_tile ? gx : per_tile), tiles);
         spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 1><<<grid, WARPS * 32, smem, st>>>(
             srow, scol, sval, n, q, (uint32_t)ldq, f4, c, ldc4, lut, gr, groups, ws);
@@ -1387,7 +1389,8 @@ int launch_ring_t(const uint64_t* srow, const uint32_t* scol, const float* sval,
                   float4* c, uint64_t ldc4, const float* lut, cudaStream_t st, int dyn) {
     typedef typename RingOf<G>::type R;
     const size_t smem = (size_t)R::kLutBytes + (size_t)W * C * NV * 32 * R::kBytes;
-    static int occ = 0;  // per template instance: resident blocks per SM (balanced / dynamic kernels)
+    static int occ_dev[kMaxDevices] = {};  // per template instance and device: resident blocks per SM
+    int& occ = occ_dev[cur_device()];
     if (occ == 0) {
         AES_CUDA_TRY(cudaFuncSetAttribute(spmm_ring_kernel<R, NV, C, W, FULL>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1401,13 +1404,14 @@ int launch_ring_t(const uint64_t* srow, const uint32_t* scol, const float* sval,
     }
     if (dyn == kSchedAuto) dyn = kSchedBal;  // fp32 ring: balanced waves at every size (1.17 vs 1.18 ms full graph)
     if (dyn == kSchedBal || dyn == kSchedBalOne) {  // waves of resident CTAs, slot-balanced row ranges
-        const uint64_t waves = dyn == kSchedBalOne ? 1 : bal_waves(n, (uint64_t)kNumSMs * occ * W, 20);
-        const uint64_t grid = waves * kNumSMs * occ;
+        const uint64_t waves = dyn == kSchedBalOne ? 1 : bal_waves(n, (uint64_t)num_sms() * occ * W, 20);
+        const uint64_t grid = waves * num_sms() * occ;
         // rows of unknown length, fp32 rows of <= 128 floats: hub rows go to
         // spmm_hub_kernel (column-split CTA per row), the balanced kernel skips them
         const int hubs = dyn == kSchedBalOne && R::kLutBytes == 0 && NV == 1;
         if (hubs) {
-            static bool hub_attr = false;
+            static bool hub_attr_dev[kMaxDevices] = {};
+            bool& hub_attr = hub_attr_dev[cur_device()];
             const size_t hub_smem = (size_t)kHubWarps * kHubRing * 128;
             if (!hub_attr) {
                 AES_CUDA_TRY(cudaFuncSetAttribute(spmm_hub_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1427,15 +1431,15 @@ int launch_ring_t(const uint64_t* srow, const uint32_t* scol, const float* sval,
     // rows per warp: 32 when the graph fills >= 8 warps per SM slot at that
     // size, otherwise shrink (power of 2, >= 2) so the grid still covers the GPU
     uint32_t gr = 32;
-    while (gr > 2 && (n + gr - 1) / gr < (uint64_t)kNumSMs * 64) gr >>= 1;
+    while (gr > 2 && (n + gr - 1) / gr < (uint64_t)num_sms() * 64) gr >>= 1;
     const uint64_t groups = (n + gr - 1) / gr;
     const unsigned grid = (unsigned)((groups + W - 1) / W);
     if (dyn == kSchedDyn && groups < (1ull << 31)) {
         DynSched* ws = nullptr;
         AES_CUDA_TRY(cudaMallocAsync((void**)&ws, sizeof(DynSched) + groups * sizeof(unsigned int), st));
         AES_CUDA_TRY(cudaMemsetAsync(ws, 0, 16, st));
-        heavy_scan_kernel<<<grid_for(groups, 256, kNumSMs * 8), 256, 0, st>>>(srow, n, gr, groups, ws);
-        const unsigned pgrid = (unsigned)((uint64_t)grid < (uint64_t)kNumSMs * occ ? (uint64_t)grid : (uint64_t)kNumSMs * occ);
+        heavy_scan_kernel<<<grid_for(groups, 256, num_sms() * 8), 256, 0, st>>>(srow, n, gr, groups, ws);
+        const unsigned pgrid = (unsigned)((uint64_t)grid < (uint64_t)num_sms() * occ ? (uint64_t)grid : (uint64_t)num_sms() * occ);
         spmm_ring_dyn_kernel<R, NV, C, W, FULL><<<pgrid, W * 32, smem, st>>>(
             srow, scol, sval, n, g.base(), (uint32_t)g.ld4, f4, c, ldc4, lut, gr, groups, ws);
         AES_CUDA_TRY(cudaGetLastError());
@@ -1571,7 +1575,7 @@ int aes_dev_spmm_f32_ex(const uint64_t* srow_ptr, const uint32_t* scol, const fl
         return launch_vector(srow_ptr, scol, sval, n_rows, g, (uint32_t)f4,
                              reinterpret_cast<float4*>(c), ldc / 4, nullptr, st, dyn);
     }
-    spmm_scalar_kernel<4><<<grid_for(n_rows * 32, kThreads, 148 * 64), kThreads, 0, st>>>(
+    spmm_scalar_kernel<4><<<grid_for(n_rows * 32, kThreads, num_sms() * 64), kThreads, 0, st>>>(
         srow_ptr, scol, sval, n_rows, b, ldb, f, c, ldc);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;

@@ -350,7 +350,8 @@ int launch_tc_gemm(const float* a, uint64_t m, uint64_t k, uint64_t lda, const f
     const uint32_t n_slabs = (uint32_t)((n + 31) / 32);
     const size_t smem = (size_t)kStages * kSlabBytes + (size_t)k_slabs * n_pad * 128 + (size_t)n_slabs * kSlabBytes +
                         sizeof(Barriers) + 1024;
-    static bool attr = false;
+    static bool attr_dev[kMaxDevices] = {};
+    bool& attr = attr_dev[cur_device()];
     if (!attr) {
         AES_CUDA_TRY(cudaFuncSetAttribute(
             tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -358,7 +359,7 @@ int launch_tc_gemm(const float* a, uint64_t m, uint64_t k, uint64_t lda, const f
         attr = true;
     }
     const uint64_t tiles = (m + kTileM - 1) / kTileM;
-    const unsigned grid = (unsigned)(tiles < (uint64_t)kNumSMs ? tiles : (uint64_t)kNumSMs);
+    const unsigned grid = (unsigned)(tiles < (uint64_t)num_sms() ? tiles : (uint64_t)num_sms());
     tc_gemm_kernel<<<grid, kThreads, smem, st>>>(map_a, map_w, outs, m, k_slabs, (uint32_t)n, n_pad, tmem_cols, bias,
                                                  relu);
     AES_CUDA_TRY(cudaGetLastError());

@@ -191,14 +191,20 @@ def dequant_lut(lo: float, hi: float, bits: int = 8, dev="cuda", stream=None) ->
     return lut
 
 
-def quantize(x: torch.Tensor, bits: int = 8, params=None, stream=None) -> QuantizedDevice:
-    """quantize(x, fit_params(x, bits)) — quantize.cpp:23-51, codes kept as u8."""
+def quantize(x: torch.Tensor, bits: int = 8, params=None, stream=None, out=None) -> QuantizedDevice:
+    """quantize(x, fit_params(x, bits)) — quantize.cpp:23-51, codes kept as u8.
+    out: optional u8 [rows, cols] view (row stride free) the codes go into."""
     if not 1 <= bits <= 8:
         raise ValueError("device int8 path takes bits in 1..8")
     L = lib()
     lo, hi = params if params is not None else fit_params(x, stream)
     rows, cols = x.shape
-    codes = empty_padded(rows, cols, dtype=torch.uint8, device=x.device)
+    if out is not None:
+        if out.dtype != torch.uint8 or tuple(out.shape) != (rows, cols) or out.stride(1) != 1:
+            raise ValueError("out must be a uint8 [rows, cols] row-major view")
+        codes = out
+    else:
+        codes = empty_padded(rows, cols, dtype=torch.uint8, device=x.device)
     st = stream_of(stream)
     check(L.aes_dev_quantize(ptr(x), rows, cols, x.stride(0), lo, hi, bits, ptr(codes), codes.stride(0), st))
     lut = torch.zeros(256, dtype=torch.float32, device=x.device)

@@ -46,6 +46,13 @@ import torch
 import torch.distributed as dist
 
 
+def _into(dst: torch.Tensor, res: torch.Tensor) -> None:
+    """Ops write into `out=` when they can (the CUDA ops always do); an op
+    that returned a fresh tensor instead is copied into place."""
+    if res.data_ptr() != dst.data_ptr():
+        dst.copy_(res)
+
+
 def equal_row_cuts(n_rows: int, world: int):
     per = -(-n_rows // world) if world else n_rows
     return [min(r * per, n_rows) for r in range(world)] + [n_rows], per
@@ -74,7 +81,7 @@ class Ops:
     alloc: Callable  # alloc(rows, cols, like) -> tensor (row stride padded as needed)
     # int8 exchange (exchange_dtype="int8"):
     #   fit_params(A) -> float32 tensor [lo, hi, flag] (flag: int32 bits, 1 = non-finite)
-    #   quantize(A, lo, hi) -> uint8 codes [rows, cols] (8-bit, quantize.cpp:23-51)
+    #   quantize(A, lo, hi, out=None) -> uint8 codes [rows, cols] (8-bit, quantize.cpp:23-51)
     #   spmm_q8(srow, scol, sval, codes, lo, hi, out) -> spmm over dequantize(codes)
     fit_params: Callable | None = None
     quantize: Callable | None = None
@@ -92,7 +99,7 @@ def cuda_ops(max_row_slots: int = 0) -> Ops:
         gemm_bias_act=lambda a, w, b, relu, out=None: device.gemm_bias_act(a, w, b, relu, out=out),
         alloc=lambda rows, cols, like: device.empty_padded(rows, cols, device=like.device),
         fit_params=device.fit_params_raw,
-        quantize=lambda a, lo, hi: device.quantize(a, 8, params=(lo, hi)).codes,
+        quantize=lambda a, lo, hi, out=None: device.quantize(a, 8, params=(lo, hi), out=out).codes,
         spmm_q8=lambda srow, scol, sval, codes, lo, hi, out=None: device.spmm_q8(
             srow, scol, sval, device.QuantizedDevice(codes, lo, hi, 8, device.dequant_lut(lo, hi, 8, codes.device)),
             out=out, max_row_slots=max_row_slots),
@@ -133,6 +140,7 @@ class ShardedGCN:
         self.srow = srow_ptr[lo:hi + 1]
         self.scol, self.sval = scol, sval
         self.exchange = exchange
+        self._xbufs = {}  # NCCL exchange: persistent per-layer all-gather buffers
         self.replicas = None
         self.halo = False
         if halo and exchange != "p2p":
@@ -211,22 +219,33 @@ class ShardedGCN:
             raise ValueError("EmptyMatrix")
         return float(lo), float(hi)
 
-    def _gather(self, out_rows: torch.Tensor, f: int, like: torch.Tensor) -> torch.Tensor:
-        rows = self.hi - self.lo
-        if self.world == 1:
-            return out_rows[:rows]
-        # the send buffer must be exactly `per` rows; padded rows hold zeros
-        # (u8 code rows are padded to 16 B for the int8 SpMM's 16-B gathers)
-        fw = -(-f // 16) * 16 if out_rows.dtype == torch.uint8 else f
-        send = torch.zeros((self.per, fw), dtype=out_rows.dtype, device=out_rows.device)
-        send[:rows].copy_(out_rows[:rows, :f])
-        gathered = torch.empty((self.world * self.per, fw), dtype=out_rows.dtype, device=out_rows.device)
-        dist.all_gather_into_tensor(gathered, send, group=self.group)
-        if self.balance == "slots":
-            parts = [gathered[r * self.per: r * self.per + (c1 - c0)]
+    def _exchange_buf(self, l: int, f: int, dtype: torch.dtype, like: torch.Tensor) -> torch.Tensor:
+        """Persistent [world * per, ld] all-gather buffer of layer l (NCCL
+        exchange).  Each rank's GEMM / quantize writes its rows straight into
+        its own slice and the all-gather runs in place on it: no send buffer,
+        no copy.  Zeroed once, so the pad rows / columns stay zero."""
+        ld = -(-f // 16) * 16 if dtype == torch.uint8 else (f + 3) & ~3
+        key = (l, f, dtype)
+        buf = self._xbufs.get(key)
+        if buf is None:
+            buf = torch.zeros((self.world * self.per, ld), dtype=dtype, device=like.device)
+            self._xbufs[key] = buf
+        return buf
+
+    def _my_slice(self, buf: torch.Tensor, f: int) -> torch.Tensor:
+        """This rank's rows of the exchange buffer, columns [0, f)."""
+        return buf[self.rank * self.per: self.rank * self.per + (self.hi - self.lo), :f]
+
+    def _gather_inplace(self, buf: torch.Tensor, f: int) -> torch.Tensor:
+        """In-place all-gather of the layer buffer; returns the [n, f] replica."""
+        if self.world > 1:
+            mine = buf[self.rank * self.per: (self.rank + 1) * self.per]
+            dist.all_gather_into_tensor(buf, mine, group=self.group)
+        if self.balance == "slots" and self.world > 1:
+            parts = [buf[r * self.per: r * self.per + (c1 - c0)]
                      for r, (c0, c1) in enumerate(zip(self.cuts, self.cuts[1:]))]
             return torch.cat(parts)[:, :f]
-        return gathered[: self.n, :f]
+        return buf[: self.n, :f]
 
     def input_view(self) -> torch.Tensor:
         """The layer-0 replica buffer [n, F0] (p2p exchange): fill it once and
@@ -319,15 +338,27 @@ class ShardedGCN:
                 codes, lo, hi = hq
                 agg = self.ops.spmm_q8(self.srow, self.scol, self.sval, codes, lo, hi,
                                        out=self.ops.alloc(max(rows, 1), codes.shape[1], x))
-            out = self.ops.gemm_bias_act(agg[:rows] if rows else agg[:0], w, b, relu=l + 1 < n_layers,
-                                         out=self.ops.alloc(max(rows, 1), w.shape[1], x))
-            if return_shard and l + 1 == n_layers:
-                return out[:rows]
-            if self.qx and l + 1 < n_layers:
+            fo = w.shape[1]
+            last = l + 1 == n_layers
+            quant = self.qx and not last
+            if return_shard and last:
+                return self.ops.gemm_bias_act(agg[:rows] if rows else agg[:0], w, b, relu=False,
+                                              out=self.ops.alloc(max(rows, 1), fo, x))[:rows]
+            if quant:
+                out = self.ops.gemm_bias_act(agg[:rows] if rows else agg[:0], w, b, relu=True,
+                                             out=self.ops.alloc(max(rows, 1), fo, x))
                 lo, hi = self._global_params(out)
-                codes = self.ops.quantize(out[:rows], lo, hi) if rows else \
-                    torch.zeros((0, w.shape[1]), dtype=torch.uint8, device=out.device)
-                hq = (self._gather(codes, w.shape[1], codes), lo, hi)
+                cbuf = self._exchange_buf(l, fo, torch.uint8, x)
+                if rows:
+                    _into(self._my_slice(cbuf, fo), self.ops.quantize(out[:rows], lo, hi,
+                                                                      out=self._my_slice(cbuf, fo)))
+                hq = (self._gather_inplace(cbuf, fo), lo, hi)
             else:
-                h = self._gather(out, w.shape[1], h)
-        return h
+                # the GEMM epilogue writes this rank's rows of the next replica
+                hbuf = self._exchange_buf(l, fo, torch.float32, x)
+                if rows:
+                    dst = self._my_slice(hbuf, fo)
+                    _into(dst, self.ops.gemm_bias_act(agg[:rows], w, b, relu=not last, out=dst))
+                h = self._gather_inplace(hbuf, fo)
+                hq = None
+        return h.clone() if copy_out else h

@@ -151,6 +151,28 @@ int main() {
             }
         }
     }
+    {   // edits to a built plan set are executed, as the reference executes
+        // plans.plans (spmm.cpp:57-76); invalid windows are rejected
+        std::mt19937_64 rng(21);
+        CsrMatrix a = random_graph(60, 0.4, rng);
+        DenseMatrix b = random_dense(60, 5, rng);
+        SamplePlanSet ps = build_plan_set(a, 8, Strategy::Adaptive);
+        std::size_t r = 0;
+        while (r < ps.plans.size() && (ps.plans[r].params.sample_cnt == 0 || a.row_nnz(r) < 2)) ++r;
+        CHECK(r < ps.plans.size());
+        const DenseMatrix before = spmm_sampled(a, b, ps);
+        ps.plans[r].params = {1, 1};
+        ps.plans[r].starts = {static_cast<std::uint32_t>(a.row_nnz(r) - 1)};  // last nonzero only
+        SamplePlanSet host = ps;
+        host.device.reset();
+        const DenseMatrix edited = spmm_sampled(a, b, ps);
+        CHECK(same_bits(edited, spmm_sampled(a, b, host)));
+        CHECK(!same_bits(edited, before));
+        ps.plans[r].starts = {static_cast<std::uint32_t>(a.row_nnz(r))};  // window past the row end
+        CHECK_THROWS(spmm_sampled(a, b, ps));
+        ps.plans[r].starts.clear();  // fewer starts than sample_cnt
+        CHECK_THROWS(spmm_sampled(a, b, ps));
+    }
     {
         CsrMatrix a(3, 4);
         DenseMatrix b(5, 2);

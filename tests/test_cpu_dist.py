@@ -46,7 +46,7 @@ def _oracle_ops():
         out.view(np.int32)[2] = flag
         return torch.from_numpy(out)
 
-    def quantize(a, lo, hi):
+    def quantize(a, lo, hi, out=None):
         return torch.from_numpy(port.quantize(np.ascontiguousarray(a.numpy()), lo, hi).astype(np.uint8))
 
     def spmm_q8(srow, scol, sval, codes, lo, hi, out=None):

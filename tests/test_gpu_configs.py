@@ -1,0 +1,102 @@
+"""Parity at the BASELINE configurations' full sizes, checked against the
+UNMODIFIED reference (oracle/_ref) directly.
+
+For every (shape, W, dtype) the bench or DESIGN reports, the whole graph is
+generated on the GPU, the product path runs over ALL rows (the same launch
+geometry / schedule the bench times: e.g. the int8 batch kernel's static
+32-row-group schedule only engages at full size), and a seeded sample of
+20 000 rows (all rows when the graph has fewer) is recomputed by the
+reference's own build_plan_set + spmm_sampled (proj/src/sampling.cpp:104-118,
+spmm.cpp:40-107) on a CSR holding just those rows and the full feature
+matrix.  int8 follows the reference composition
+spmm_sampled(A, dequantize(quantize(B, fit_params(B)))) (quantize.cpp:11-64).
+Bit-exact: outputs compared as uint32 bit patterns, slots per row compared
+with the reference plans, codes compared with the reference quantize.
+"""
+import numpy as np
+import pytest
+
+from oracle import ref as oref
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow,
+              pytest.mark.skipif(not oref.available(), reason="oracle/_ref not built")]
+
+SAMPLE = 20_000
+
+CASES = [
+    ("pubmed", 32, "f32"), ("pubmed", 64, "f32"), ("pubmed", 32, "int8"), ("pubmed", 64, "int8"),
+    ("arxiv", 32, "int8"),
+    ("reddit", 32, "f32"), ("reddit", 64, "f32"), ("reddit", 32, "int8"), ("reddit", 64, "int8"),
+    ("products", 32, "int8"), ("products", 64, "int8"), ("products", 64, "f32"),
+]
+
+_cache = {}
+
+
+def _shape(name):
+    """(graph on device, features on device, host arrays) — one per shape."""
+    import torch
+
+    from paper_2503_18427_b200 import device, synth
+    if name in _cache:
+        return _cache[name]
+    _cache.clear()  # one shape resident at a time (reddit + products together are ~4 GB host)
+    torch.cuda.empty_cache()
+    n, alpha, maxdeg, f = synth.SHAPES[name]
+    rp, col, val = synth.power_law_csr(n, alpha, maxdeg, seed=1, device="cuda")
+    g = device.Graph(rp, col, val, n)
+    b = synth.features(n, f, seed=5, device="cuda")
+    host = (rp.cpu().numpy().view(np.uint64), col.cpu().numpy().view(np.uint32), val.cpu().numpy(),
+            np.ascontiguousarray(b.cpu().numpy()))
+    _cache[name] = (g, b, host, n, f)
+    return _cache[name]
+
+
+def _sub_csr(rp, col, val, rows):
+    starts, ends = rp[rows], rp[rows + 1]
+    sub_rp = np.zeros(rows.size + 1, np.uint64)
+    sub_rp[1:] = np.cumsum(ends - starts)
+    lens = (ends - starts).astype(np.int64)
+    idx = np.repeat(starts.astype(np.int64) - np.concatenate([[0], np.cumsum(lens)[:-1]]), lens) + \
+        np.arange(int(lens.sum()), dtype=np.int64)
+    return sub_rp, col[idx], val[idx]
+
+
+@pytest.mark.parametrize("shape,width,dtype", CASES, ids=[f"{s}-W{w}-{d}" for s, w, d in CASES])
+def test_config_scale_parity_vs_reference(shape, width, dtype):
+    import torch
+
+    from paper_2503_18427_b200 import device
+    g, b, (rp, col, val, b_np), n, f = _shape(shape)
+    plan = device.SampledPlan(g, width)
+    if dtype == "int8":
+        q = device.quantize(b)
+        out = device.spmm_q8(plan.srow_ptr, plan.scol, plan.sval, q, max_row_slots=plan.row_bound)
+    else:
+        out = device.spmm_plan(plan, b)
+    torch.cuda.synchronize()
+
+    rows = np.arange(n) if n <= SAMPLE else np.sort(np.random.default_rng(width + n).choice(n, SAMPLE, replace=False))
+    sub_rp, sub_col, sub_val = _sub_csr(rp, col, val, rows)
+    csr = oref.RefCsr.from_arrays(rows.size, n, sub_rp, sub_col, sub_val)
+
+    # plans: slots per sampled row == the reference plan's chunk * cnt
+    chunk, cnt, _, _ = oref.build_plans(csr, width, 0)
+    srow = plan.srow_ptr.cpu().numpy().view(np.uint64)
+    got_slots = (srow[rows + 1] - srow[rows]).astype(np.uint64)
+    assert np.array_equal(got_slots, chunk[: rows.size].astype(np.uint64) * cnt[: rows.size].astype(np.uint64))
+
+    if dtype == "int8":
+        lo, hi = oref.fit_params(b_np)
+        assert (np.float32(q.x_min), np.float32(q.x_max)) == (np.float32(lo), np.float32(hi))
+        codes = oref.quantize(b_np, lo, hi)
+        got_codes = q.codes.cpu().numpy()[:, :f]
+        assert np.array_equal(got_codes[rows].astype(np.uint16), codes[rows])
+        feats = oref.dequantize(codes, lo, hi)
+        del codes
+    else:
+        feats = b_np
+    want = oref.spmm_sampled(csr, feats, width, 0)
+    got = out.cpu().numpy()[:, :f][rows]
+    assert np.array_equal(np.ascontiguousarray(got).view(np.uint32), want.view(np.uint32)), \
+        f"{shape} W={width} {dtype}: {(got != want).sum()} elements differ"

@@ -440,12 +440,15 @@ def test_gcn_forward_sharded_c_abi_nccl(dev):
         wp = (ctypes.c_void_p * 3)(*[t.data_ptr() for t in tw])
         bp = (ctypes.c_void_p * 3)(*[t.data_ptr() for t in tb])
         out = ctypes.c_void_p()
+        out_ld = ctypes.c_uint64()
         capi.check(L.aes_gcn_forward_sharded(plan.srow_ptr.data_ptr(), plan.scol.data_ptr(), plan.sval.data_ptr(),
                                              n, n, 3, dims_h, wp, bp, 1, ra.data_ptr(), rb.data_ptr(), ld,
                                              plan.row_bound, work.data_ptr(), wsb, comm, ctypes.byref(out),
-                                             capi.stream_of(None)))
+                                             ctypes.byref(out_ld), capi.stream_of(None)))
         torch.cuda.synchronize()
-        got = (ra if out.value == ra.data_ptr() else rb)[:, : dims[-1]].cpu().numpy()
+        assert out_ld.value == 8  # round4(7): the class layer moved 8 floats per row, not ld = 64
+        rep = ra if out.value == ra.data_ptr() else rb
+        got = rep.view(-1)[: n * 8].view(n, 8)[:, : dims[-1]].cpu().numpy()
         want = port.gcn_forward(nrp, ncol, nval, x, ws, bs, 16)
         assert np.array_equal(bits(got), bits(want))
     finally:
