@@ -468,7 +468,7 @@ def count_launches(step):
     from torch.profiler import ProfilerActivity, profile
     torch.cuda.synchronize()
     try:
-        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        with profile(activities=[ProfilerActivity.CUDA], acc_events=True) as prof:
             step()
             torch.cuda.synchronize()
         names = [e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
@@ -477,7 +477,7 @@ def count_launches(step):
     kernels = [nm for nm in names if not nm.startswith(("Memcpy", "Memset", "memcpy", "memset"))]
     other = [nm for nm in kernels if "at::" in nm or "nccl" in nm.lower() or "gloo" in nm]
     ours = [nm for nm in kernels if nm not in other]
-    short = sorted({nm.split("<")[0].split("(")[0].replace("void ", "") for nm in ours})
+    short = sorted({nm.split("<")[0].split("::")[-1].split("(")[0].replace("void ", "") for nm in ours})
     return {"per_step": len(ours), "other_per_step": len(other), "kernels": short,
             "how": "CUPTI kernel records of one extra step (torch.profiler), not in the timed region"}
 
