@@ -75,13 +75,19 @@ def workload_config(args, n, nnz, slots, f, elem):
     return {"workload": f"{args.config} W={args.width} {args.strategy} F={f} sampled SpMM"
                         + (" + GEMM + all-gather (GCN layer)" if args.mode == "layer" else ""),
             "n_rows": n, "nnz": nnz, "slots": slots, "F": f, "width": args.width, "strategy": args.strategy,
-            "features": "u8 codes (global min/max, quantize.cpp:23-51)" if elem == 1 else "f32",
+            "features": {"int8": "u8 codes (global min/max, quantize.cpp:23-51)",
+                         "int8-row": "u8 codes, per-row (scale, offset) — fast mode, bounded error",
+                         "int8-feature": "u8 codes, per-feature (scale, offset) — fast mode, bounded error"
+                         }.get(getattr(args, "dtype", "f32"), "f32"),
             "l2": "inputs larger than L2 (features %.2f GB, output %.2f GB vs 126 MB L2)"
                   % (n * f * elem / 1e9, n * f * 4 / 1e9)}
 
 
-def alg_bytes(n_rows, slots, f, elem=4):
-    return 8 * (n_rows + 1) + 8 * slots + elem * f * slots + 4 * f * n_rows
+def alg_bytes(n_rows, slots, f, elem=4, slot_extra=0):
+    """8(N+1) [srow_ptr] + 8S [scol, sval] + e*F*S [gathered rows] + 4FN [C]
+    (+ slot_extra*S: the int8 fast ROW mode gathers an 8-B (scale, offset)
+    pair with every row)."""
+    return 8 * (n_rows + 1) + 8 * slots + elem * f * slots + 4 * f * n_rows + slot_extra * slots
 
 
 def peaks():
@@ -322,9 +328,15 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
 
     quant = None
+    qaff = None
+    slot_extra = 0
     if args.dtype == "int8":
         quant = device.quantize(b)
         elem = 1
+    elif args.dtype in ("int8-row", "int8-feature"):  # fast mode (affine.cu), not bit-exact
+        qaff = device.quantize_affine(b, args.dtype.split("-")[1])
+        elem = 1
+        slot_extra = 8 if args.dtype == "int8-row" else 0
     else:
         elem = 4
     out = device.empty_padded(max(shard_rows, 1), f)
@@ -341,7 +353,9 @@ def run_ours(args):
         layer = (w, bias, gathered, mine)
 
     def step():
-        if quant is not None:
+        if qaff is not None:
+            device.spmm_q8_affine(srow, full_plan.scol, full_plan.sval, qaff, out=out)
+        elif quant is not None:
             device.spmm_q8(srow, full_plan.scol, full_plan.sval, quant, out=out, max_row_slots=full_plan.row_bound)
         else:
             device.spmm(srow, full_plan.scol, full_plan.sval, b, out=out, max_row_slots=full_plan.row_bound)
@@ -374,8 +388,8 @@ def run_ours(args):
     clocks = sampler.stop()
     ms_total = start.elapsed_time(end)
     ms_step = max_over_ranks(ms_total, dist) / args.steps
-    total_bytes = alg_bytes(n, int(srow_host[-1]), f, elem)
-    my_bytes = alg_bytes(shard_rows, shard_slots, f, elem)
+    total_bytes = alg_bytes(n, int(srow_host[-1]), f, elem, slot_extra)
+    my_bytes = alg_bytes(shard_rows, shard_slots, f, elem, slot_extra)
     value = total_bytes / (ms_step * 1e-3) / 1e9
     # kernel-level roofline for this rank (the step is the SpMM kernel alone in spmm mode)
     k_ms = ms_total / args.steps
@@ -428,7 +442,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u8" if args.dtype == "int8" else "f32",
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8" if args.dtype.startswith("int8") else "f32",
             "data": DATA % args.seed,
             "config": workload_config(args, n, int(rp[-1].item()), int(srow_host[-1]), f, elem),
             "parallelism": f"row-sharded x{world}" if world > 1 else "single GPU",
@@ -748,7 +762,8 @@ def main():
     ap.add_argument("--config", choices=list(SHAPES), default="products")
     ap.add_argument("--width", type=int, default=32)
     ap.add_argument("--strategy", default="adaptive", choices=["adaptive", "afs", "sfs", "full"])
-    ap.add_argument("--dtype", default="f32", choices=["f32", "int8"])
+    ap.add_argument("--dtype", default="f32", choices=["f32", "int8", "int8-row", "int8-feature"],
+                    help="int8: the reference's exact global codes; int8-row / int8-feature: fast mode")
     ap.add_argument("--mode", default="spmm", choices=["spmm", "layer"])
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--sched", type=int, default=0,

@@ -25,6 +25,7 @@
 #include <cstdint>
 #include <memory>
 #include <string>
+#include <utility>
 #include <vector>
 
 #define AES_CXX_API __attribute__((visibility("default")))
@@ -126,6 +127,11 @@ struct SamplingRates {
 };
 
 AES_CXX_API SamplingRates sampling_rate(const SamplePlanSet& plans, const RowStats& stats);
+
+// ----------------------------------------------------------------- bench.hpp
+/// Empirical CDF of per-row sampling rates as (rate, cumulative fraction)
+/// (proj/include/aesspmm/bench.hpp:58-59); sorted and tie-merged on the GPU.
+AES_CXX_API std::vector<std::pair<double, double>> cdf_stats(std::vector<double> rates);
 
 // ------------------------------------------------------------------ spmm.hpp
 struct WorkCounter {

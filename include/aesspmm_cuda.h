@@ -150,6 +150,23 @@ AES_API int aes_sampling_rate(aes_plan_t p, aes_csr_t a, double* aggregate,
 /* spmm_exact(a, b) — spmm.hpp:19-20, spmm.cpp:18-36, module.cpp:118-123.
  * b: host row-major b_rows x f; c: host row-major a.n_rows x f. */
 AES_API int aes_spmm_exact(aes_csr_t a, const float* b, uint64_t b_rows, uint64_t f, float* c);
+/* cdf_stats(rates) — bench.hpp:58-59, bench.cpp:124-138: the empirical CDF
+ * of per-row sampling rates as steps (rate, cumulative fraction), sorted by
+ * rate, ties (==) merged into one step carrying the last fraction.
+ * out_rate / out_frac hold up to n entries; *n_steps gets the step count.
+ * n == 0: AES_ERR_INVALID_ARG "rates must be nonempty".  Bit-exact. */
+AES_API int aes_cdf_stats(const double* rates, uint64_t n, double* out_rate, double* out_frac,
+                          uint64_t* n_steps);
+/* cdf_stats(sampling_rate(plans, row_stats(a)).per_row) with the per-row
+ * rates kept on the device (outputs as above, capacity n_rows). */
+AES_API int aes_sampling_rate_cdf(aes_plan_t p, aes_csr_t a, double* out_rate, double* out_frac,
+                                  uint64_t* n_steps);
+/* Device tier: rates, outputs and *n_steps in device memory; workspace of
+ * aes_cdf_workspace_bytes(n) bytes; stream-ordered (radix sort + scan). */
+AES_API uint64_t aes_cdf_workspace_bytes(uint64_t n);
+AES_API int aes_dev_cdf_stats(const double* rates, uint64_t n, double* out_rate, double* out_frac,
+                              uint64_t* n_steps, void* workspace, size_t workspace_bytes, void* stream);
+
 /* spmm_sampled(a, b, plans) — spmm.hpp:25-26, spmm.cpp:40-107, module.cpp:124-131.
  * fma/loads counters (spmm_sampled_instrumented, spmm.cpp:109-114) may be NULL. */
 AES_API int aes_spmm_sampled(aes_csr_t a, const float* b, uint64_t b_rows, uint64_t f,
@@ -399,6 +416,36 @@ AES_API int aes_dev_wait_counter(const unsigned long long* counter, unsigned lon
 AES_API int aes_dev_signal_all(unsigned long long* const* counters, int n, void* stream);
 /* *bad_flag = 1 if any of x[0..count) is inf/NaN (stream-ordered). */
 AES_API int aes_dev_all_finite(const float* x, uint64_t count, unsigned int* bad_flag, void* stream);
+
+/* ---- int8 FAST MODE: per-row / per-feature affine scales (affine.cu) -----
+ * Opt-in beside the reference's exact global min/max path (quantize.cpp:
+ * 11-64); not bit-exact, bounded instead.  codes u8 [rows, ldq];
+ * params float2 (scale s, offset m) per row (ROW) or per column (FEATURE);
+ * x^ = q * s + m, q = clamp(rint((x - m) / s), 0, 255).
+ * Bounds: |x^ - x| <= s/2 + 2^-22 (|m| + 255 s) per element, and
+ * |C - A B| <= sum_k |v_k| (s_k/2 + 2^-22 (|m_k| + 255 s_k))
+ *            + (slots + 2) 2^-23 sum_k |v_k| (|m_k| + 255 s_k)
+ * for the fused SpMM.  Non-finite input sets *bad_flag (stream-ordered). */
+#define AES_QAFFINE_ROW 0
+#define AES_QAFFINE_FEATURE 1
+AES_API uint64_t aes_quantize_affine_workspace_bytes(uint64_t rows, uint64_t cols, int mode);
+AES_API int aes_dev_quantize_affine(const float* x, uint64_t rows, uint64_t cols, uint64_t ldx, int mode,
+                                    uint8_t* q, uint64_t ldq, float* params, unsigned int* bad_flag,
+                                    void* workspace, size_t workspace_bytes, void* stream);
+AES_API int aes_dev_dequantize_affine(const uint8_t* q, uint64_t rows, uint64_t cols, uint64_t ldq, int mode,
+                                      const float* params, float* x, uint64_t ldx, void* stream);
+/* C[r, :] = sum_k v_k * x^[scol_k, :] over the (sampled) CSR, dequantizing
+ * in the gather (no table).  ldq % 4 == 0, ldc % 4 == 0, C 16-B aligned. */
+/* Handle tier: quantize host x [rows, cols] in the given mode into a
+ * QuantizedFeatures handle; aes_spmm_sampled_q8 and aes_dequantize then use
+ * the affine decode (codes are 8-bit; x_min/x_max of aes_qfeat_info are 0).
+ * aes_qfeat_affine: the handle's mode (-1 = global exact) and its params
+ * (float2 per row / column) to host memory (params may be NULL). */
+AES_API int aes_quantize_affine(const float* x, uint64_t rows, uint64_t cols, int mode, aes_qfeat_t* out);
+AES_API int aes_qfeat_affine(aes_qfeat_t q, int* mode, float* params);
+AES_API int aes_dev_spmm_q8_affine(const uint64_t* srow_ptr, const uint32_t* scol, const float* sval,
+                                   uint64_t n_rows, const uint8_t* q, uint64_t ldq, uint64_t f, int mode,
+                                   const float* params, float* c, uint64_t ldc, void* stream);
 
 /* ---- row-sharded GCN forward over NCCL (sharded.cu) ----------------------
  * gcn_forward (proj/src/gnn.cpp:66-78) on one rank of an equal-row sharded

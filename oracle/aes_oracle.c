@@ -21,6 +21,7 @@
 #include <math.h>
 #include <stddef.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 enum { OR_ADAPTIVE = 0, OR_AFS = 1, OR_SFS = 2, OR_FULL = 3 };
@@ -320,4 +321,29 @@ int or_sampling_rate(uint64_t n, const uint64_t *row_ptr, uint32_t w, int strate
     *aggregate = tot_nnz == 0 ? 1.0 : (double)tot_slots / (double)tot_nnz;
     *unique = tot_nnz == 0 ? 1.0 : (double)tot_unique / (double)tot_nnz;
     return OR_OK;
+}
+
+/* cdf_stats (proj/src/bench.cpp:124-138): sort ascending, then one step per
+ * run of equal (==) values: (first value of the run, (last index + 1) / n).
+ * Sorts `rates` in place.  Returns the step count, or 0 for n == 0 (the
+ * reference throws "rates must be nonempty"). */
+static int or_cmp_double(const void *a, const void *b) {
+    double x = *(const double *)a, y = *(const double *)b;
+    return (x < y) ? -1 : (y < x) ? 1 : 0;
+}
+uint64_t or_cdf_stats(double *rates, uint64_t n, double *out_rate, double *out_frac) {
+    uint64_t i, steps = 0;
+    if (n == 0) return 0;
+    qsort(rates, n, sizeof(double), or_cmp_double);
+    for (i = 0; i < n; ++i) {
+        double fraction = (double)(i + 1) / (double)n;
+        if (steps && out_rate[steps - 1] == rates[i]) {
+            out_frac[steps - 1] = fraction;
+        } else {
+            out_rate[steps] = rates[i];
+            out_frac[steps] = fraction;
+            ++steps;
+        }
+    }
+    return steps;
 }

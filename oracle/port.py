@@ -50,6 +50,8 @@ def lib():
         L.or_gcn_normalize.argtypes = [u64, vp, vp, i32, vp, vp, vp, vp]
         L.or_gcn_normalize.restype = None
         L.or_sampling_rate.argtypes = [u64, vp, u32, i32, vp, vp, vp]
+        L.or_cdf_stats.argtypes = [vp, u64, vp, vp]
+        L.or_cdf_stats.restype = u64
         _lib = L
     return _lib
 
@@ -252,3 +254,13 @@ def sampling_rate(row_ptr, w: int, strategy: int = ADAPTIVE):
     agg, uni = np.zeros(1), np.zeros(1)
     _check(lib().or_sampling_rate(n, _p(row_ptr), w, strategy, _p(seen), _p(agg), _p(uni)))
     return float(agg[0]), float(uni[0])
+
+
+def cdf_stats(rates):
+    """cdf_stats (bench.cpp:124-138) -> (step rates, cumulative fractions)."""
+    r = np.array(rates, np.float64)
+    if r.size == 0:
+        raise ValueError("rates must be nonempty")
+    vals, frac = np.zeros(r.size), np.zeros(r.size)
+    k = int(lib().or_cdf_stats(_p(r), r.size, _p(vals), _p(frac)))
+    return vals[:k], frac[:k]

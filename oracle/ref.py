@@ -62,6 +62,8 @@ def shim():
         L.ref_gcn_normalize.restype = vp
         L.ref_build_plans.argtypes = [vp, u32, i32, vp, vp, vp, vp, u64]
         L.ref_sampling_rate.argtypes = [vp, u32, i32, vp, vp]
+        L.ref_sampling_rate_per_row.argtypes = [vp, u32, i32, vp]
+        L.ref_cdf_stats.argtypes = [vp, u64, vp, vp, vp]
         L.ref_spmm_sampled.argtypes = [vp, vp, u64, u64, u32, i32, C.c_uint, vp]
         L.ref_spmm_exact.argtypes = [vp, vp, u64, u64, C.c_uint, vp]
         L.ref_time_spmm_sampled.argtypes = [vp, vp, u64, u64, u32, i32, C.c_uint, i32, vp, vp, vp]
@@ -142,6 +144,21 @@ def build_plans(csr: RefCsr, width, strategy):
     _chk(shim().ref_build_plans(csr.h, width, strategy, _p(chunk), _p(cnt), _p(sp), _p(starts),
                                 starts.size))
     return chunk[:n], cnt[:n], sp, starts[: int(sp[-1])]
+
+
+def sampling_rate_per_row(csr: RefCsr, width, strategy=0):
+    out = np.zeros(max(csr.n_rows, 1), np.float64)
+    _chk(shim().ref_sampling_rate_per_row(csr.h, width, strategy, _p(out)))
+    return out[: csr.n_rows]
+
+
+def cdf_stats(rates):
+    """The reference's cdf_stats (bench.cpp:124-138) -> (rates, fractions)."""
+    r = np.ascontiguousarray(rates, np.float64)
+    vals, frac = np.zeros(max(r.size, 1)), np.zeros(max(r.size, 1))
+    n = np.zeros(1, np.uint64)
+    _chk(shim().ref_cdf_stats(_p(r), r.size, _p(vals), _p(frac), _p(n)))
+    return vals[: int(n[0])], frac[: int(n[0])]
 
 
 def spmm_sampled(csr: RefCsr, b, width, strategy, threads=0):

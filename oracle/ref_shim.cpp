@@ -209,6 +209,28 @@ int ref_sampling_rate(void* h, std::uint32_t width, int strategy, double* aggreg
     });
 }
 
+int ref_sampling_rate_per_row(void* h, std::uint32_t width, int strategy, double* per_row) {
+    return guard([&] {
+        const CsrMatrix& m = *static_cast<CsrMatrix*>(h);
+        SamplePlanSet ps = build_plan_set(m, width, static_cast<Strategy>(strategy));
+        SamplingRates r = sampling_rate(ps, row_stats(m));
+        std::copy(r.per_row.begin(), r.per_row.end(), per_row);
+    });
+}
+
+// ---- cdf_stats (proj/src/bench.cpp:124-138) ----------------------------------
+int ref_cdf_stats(const double* rates, std::uint64_t n, double* out_rate, double* out_frac,
+                  std::uint64_t* n_steps) {
+    return guard([&] {
+        auto cdf = cdf_stats(std::vector<double>(rates, rates + n));
+        for (std::size_t i = 0; i < cdf.size(); ++i) {
+            out_rate[i] = cdf[i].first;
+            out_frac[i] = cdf[i].second;
+        }
+        *n_steps = cdf.size();
+    });
+}
+
 // ---- SpMM (proj/src/spmm.cpp) -----------------------------------------------
 int ref_spmm_sampled(void* h, const float* b, std::uint64_t b_rows, std::uint64_t f,
                      std::uint32_t width, int strategy, unsigned threads, float* c) {

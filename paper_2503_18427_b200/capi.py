@@ -51,6 +51,14 @@ def lib():
         L.aes_dev_quantize.argtypes = [vp, u64, u64, u64, f32, f32, u32, vp, u64, vp]
         L.aes_dev_dequantize.argtypes = [vp, u64, u64, u64, f32, f32, u32, vp, u64, vp]
         L.aes_dev_dequant_lut.argtypes = [f32, f32, u32, vp, vp]
+        L.aes_quantize_affine_workspace_bytes.argtypes = [u64, u64, i32]
+        L.aes_quantize_affine_workspace_bytes.restype = u64
+        L.aes_dev_quantize_affine.argtypes = [vp, u64, u64, u64, i32, vp, u64, vp, vp, vp, sz, vp]
+        L.aes_dev_dequantize_affine.argtypes = [vp, u64, u64, u64, i32, vp, vp, u64, vp]
+        L.aes_dev_spmm_q8_affine.argtypes = [vp, vp, vp, u64, vp, u64, u64, i32, vp, vp, u64, vp]
+        L.aes_dev_cdf_stats.argtypes = [vp, u64, vp, vp, vp, vp, sz, vp]
+        L.aes_cdf_workspace_bytes.argtypes = [u64]
+        L.aes_cdf_workspace_bytes.restype = u64
         L.aes_dev_gemm_bias_act.argtypes = [vp, u64, u64, u64, vp, u64, u64, vp, i32, vp, u64, vp]
         L.aes_dev_gemm_bias_act_ex.argtypes = [vp, u64, u64, u64, vp, u64, u64, vp, i32, i32, vp, vp, i32, u64,
                                                u64, vp]

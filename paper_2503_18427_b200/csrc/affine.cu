@@ -1,0 +1,402 @@
+// int8 FAST MODE (opt-in, not bit-exact): per-row or per-feature-scale affine
+// quantization with the dequantization fused into the SpMM gather —
+// north_star item (3).  It sits beside the reference's global min/max path
+// (proj/src/quantize.cpp:11-64, reproduced bit-exactly in quant.cu/spmm.cu):
+// the reference has no per-row / per-feature mode, so this one is measured
+// against stated error bounds instead of bit patterns.
+//
+// Quantization (codes u8, 8 bits, levels 255):
+//   ROW mode      params[r] = (s_r, m_r), m_r = min_j x[r,j], s_r = (max_j - m_r)/255
+//   FEATURE mode  params[j] = (s_j, m_j) over the rows of column j
+//   q = clamp(rint((x - m) * (255 / (max - m))), 0, 255);  x^ = q * s + m
+//   A constant row / column gets s = 0 and decodes to m exactly.
+//
+// SpMM over the codes (no table, no shared-memory LUT):
+//   ROW      C[i,:] = sum_k (v_k s_{c_k}) q_{c_k,:} + sum_k v_k m_{c_k}
+//   FEATURE  C[i,j] = s_j * sum_k v_k q_{c_k,j} + m_j * sum_k v_k
+// Per code: one PRMT places the byte in the mantissa of 2^23 (the float
+// 2^23 + q), one packed FADD2 per two codes removes 2^23 exactly, one packed
+// FFMA2 per two codes accumulates — 2 instructions per code against 3.5 for
+// the exact LUT decode.
+//
+// Error bounds (tests/test_gpu_affine.py):
+//   quantize   |x^ - x| <= s/2 + 2^-22 (|m| + 255 s)     per element
+//   SpMM       |C - A B| <= sum_k |v_k| (s_k/2 + 2^-22 (|m_k| + 255 s_k))
+//                           + (slots + 2) 2^-23 sum_k |v_k| (|m_k| + 255 s_k)
+// (s_k, m_k: the params that apply to gathered element k).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace aes {
+namespace {
+
+constexpr float kTwo23 = 8388608.0f;
+constexpr uint32_t kTwo23Bits = 0x4B000000u;
+
+__device__ __forceinline__ void fma2(float& a0, float& a1, float x, float y0, float y1) {
+    // (a0, a1) = (fma(x, y0, a0), fma(x, y1, a1)) — one FFMA2
+    unsigned long long a, y, xx;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(a0), "f"(a1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(y) : "f"(y0), "f"(y1));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(xx) : "f"(x));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a) : "l"(xx), "l"(y));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(a));
+}
+
+// the 4 codes of one u32 as exact floats
+__device__ __forceinline__ void decode4(uint32_t w, float& q0, float& q1, float& q2, float& q3) {
+    const float t0 = __uint_as_float(__byte_perm(w, kTwo23Bits, 0x7650));
+    const float t1 = __uint_as_float(__byte_perm(w, kTwo23Bits, 0x7651));
+    const float t2 = __uint_as_float(__byte_perm(w, kTwo23Bits, 0x7652));
+    const float t3 = __uint_as_float(__byte_perm(w, kTwo23Bits, 0x7653));
+    q0 = t0;
+    q1 = t1;
+    q2 = t2;
+    q3 = t3;
+    add2_rn(q0, q1, -kTwo23, -kTwo23);
+    add2_rn(q2, q3, -kTwo23, -kTwo23);
+}
+
+__device__ __forceinline__ uint32_t quant1(float x, float m, float inv) {
+    const float t = rintf((x - m) * inv);
+    return (uint32_t)fminf(fmaxf(t, 0.f), 255.f);
+}
+
+// ---------------------------------------------------------------- quantize
+// ROW mode: one warp per row; lane l handles codes 4l + 128i.
+__global__ void __launch_bounds__(256)
+quant_row_kernel(const float* __restrict__ x, uint64_t rows, uint64_t cols, uint64_t ldx,
+                 uint8_t* __restrict__ q, uint64_t ldq, float2* __restrict__ params, unsigned int* __restrict__ bad) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t r = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += warps) {
+        const float* xr = x + r * ldx;
+        float lo = INFINITY, hi = -INFINITY;
+        bool finite = true;
+        for (uint64_t j = lane; j < cols; j += 32) {
+            const float v = __ldcs(xr + j);
+            finite &= isfinite(v);
+            lo = fminf(lo, v);
+            hi = fmaxf(hi, v);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (__any_sync(0xffffffffu, !finite)) {
+            if (lane == 0) atomicExch(bad, 1u);
+            continue;
+        }
+        const float range = hi - lo;
+        const float s = range > 0.f ? range / 255.f : 0.f;
+        const float inv = range > 0.f ? 255.f / range : 0.f;
+        if (lane == 0) params[r] = make_float2(s, lo);
+        uint8_t* qr = q + r * ldq;
+        for (uint64_t j = 4 * lane; j < cols; j += 128) {
+            if (j + 4 <= cols) {
+                const float4 v = make_float4(xr[j], xr[j + 1], xr[j + 2], xr[j + 3]);
+                const uint32_t w = quant1(v.x, lo, inv) | quant1(v.y, lo, inv) << 8 | quant1(v.z, lo, inv) << 16 |
+                                   quant1(v.w, lo, inv) << 24;
+                *reinterpret_cast<uint32_t*>(qr + j) = w;  // ldq % 4 == 0
+            } else {
+                for (uint64_t e = j; e < cols; ++e) qr[e] = (uint8_t)quant1(xr[e], lo, inv);
+            }
+        }
+    }
+}
+
+// FEATURE mode, pass 1: per-column partial (min, max) of a block of rows.
+// CTA = 256 threads = 8 row lanes x 32 column lanes; grid.x over row blocks,
+// grid.y over 32-column tiles.
+constexpr int kColRowsPerCta = 1024;
+__global__ void __launch_bounds__(256)
+col_minmax_kernel(const float* __restrict__ x, uint64_t rows, uint64_t cols, uint64_t ldx,
+                  float2* __restrict__ partial, unsigned int* __restrict__ bad) {
+    __shared__ float s_lo[8][32], s_hi[8][32];
+    const uint32_t cl = threadIdx.x & 31, rl = threadIdx.x >> 5;
+    const uint64_t j = (uint64_t)blockIdx.y * 32 + cl;
+    const uint64_t r0 = (uint64_t)blockIdx.x * kColRowsPerCta;
+    const uint64_t r1 = min(rows, r0 + kColRowsPerCta);
+    float lo = INFINITY, hi = -INFINITY;
+    bool finite = true;
+    if (j < cols)
+        for (uint64_t r = r0 + rl; r < r1; r += 8) {
+            const float v = __ldcs(x + r * ldx + j);
+            finite &= isfinite(v);
+            lo = fminf(lo, v);
+            hi = fmaxf(hi, v);
+        }
+    if (!finite) atomicExch(bad, 1u);
+    s_lo[rl][cl] = lo;
+    s_hi[rl][cl] = hi;
+    __syncthreads();
+    if (rl == 0 && j < cols) {
+#pragma unroll
+        for (int k = 1; k < 8; ++k) {
+            lo = fminf(lo, s_lo[k][cl]);
+            hi = fmaxf(hi, s_hi[k][cl]);
+        }
+        partial[(uint64_t)blockIdx.x * cols + j] = make_float2(lo, hi);
+    }
+}
+
+// FEATURE mode, pass 2: fold the partials into (s_j, m_j)
+__global__ void col_params_kernel(const float2* __restrict__ partial, uint64_t blocks, uint64_t cols,
+                                  float2* __restrict__ params) {
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j >= cols) return;
+    float lo = INFINITY, hi = -INFINITY;
+    for (uint64_t b = 0; b < blocks; ++b) {
+        const float2 p = partial[b * cols + j];
+        lo = fminf(lo, p.x);
+        hi = fmaxf(hi, p.y);
+    }
+    const float range = hi - lo;
+    params[j] = make_float2(range > 0.f ? range / 255.f : 0.f, lo);
+}
+
+// FEATURE mode, pass 3: element-wise codes (4 per thread)
+__global__ void __launch_bounds__(256)
+quant_col_kernel(const float* __restrict__ x, uint64_t rows, uint64_t cols, uint64_t ldx,
+                 const float2* __restrict__ params, uint8_t* __restrict__ q, uint64_t ldq) {
+    const uint64_t c4 = (cols + 3) / 4;
+    const uint64_t total = rows * c4;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = e / c4, j0 = (e - r * c4) * 4;
+        uint32_t w = 0;
+        for (int u = 0; u < 4 && j0 + u < cols; ++u) {
+            const float2 p = params[j0 + u];  // (s, m); 1/s == 255/range up to rounding
+            w |= quant1(x[r * ldx + j0 + u], p.y, p.x > 0.f ? 1.f / p.x : 0.f) << (8 * u);
+        }
+        *reinterpret_cast<uint32_t*>(q + r * ldq + j0) = w;
+    }
+}
+
+// x^ = q * s + m (the values the fast SpMM aggregates)
+template <int MODE>
+__global__ void dequant_affine_kernel(const uint8_t* __restrict__ q, uint64_t rows, uint64_t cols, uint64_t ldq,
+                                      const float2* __restrict__ params, float* __restrict__ x, uint64_t ldx) {
+    const uint64_t total = rows * cols;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = e / cols, j = e - r * cols;
+        const float2 p = params[MODE == 0 ? r : j];
+        x[r * ldx + j] = fmaf((float)q[r * ldq + j], p.x, p.y);
+    }
+}
+
+// ---------------------------------------------------------------- SpMM
+// Warp per 32-row group, one flattened slot stream.  Lane l owns codes
+// 4l..4l+3 of the 128-code column tile blockIdx.y.  Slot metadata of 32
+// slots is loaded by the 32 lanes (coalesced) and staged in shared memory as
+// {col, a = v*s_c, b = v*m_c} (ROW) or {col, v} (FEATURE) so every lane reads
+// a slot's metadata with one broadcast LDS.128; the code gathers of U slots
+// are issued before any is consumed.
+struct SlotMeta {
+    uint32_t col;
+    float a;  // ROW: v * s_col   FEATURE: v
+    float b;  // ROW: v * m_col
+    float pad;
+};
+
+template <int MODE, int U, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+spmm_q8a_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
+                const float* __restrict__ sval, uint64_t n_rows, const uint8_t* __restrict__ q, uint64_t ldq,
+                uint32_t f, const float2* __restrict__ params, float* __restrict__ c, uint64_t ldc) {
+    __shared__ __align__(16) SlotMeta s_meta[WARPS][32];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t r0 = ((uint64_t)blockIdx.x * WARPS + warp) * 32;
+    if (r0 >= n_rows) return;
+    const uint32_t nr = (uint32_t)min((uint64_t)32, n_rows - r0);
+    const uint32_t col0 = blockIdx.y * 128 + 4 * lane;  // first code of this lane
+    const uint32_t ne = col0 < f ? min(4u, f - col0) : 0u;  // codes this lane owns
+    const uint8_t* qb = q + col0;
+    float sj[4] = {0.f, 0.f, 0.f, 0.f}, mj[4] = {0.f, 0.f, 0.f, 0.f};
+    if (MODE == 1)
+        for (uint32_t u = 0; u < ne; ++u) {
+            const float2 p = params[col0 + u];
+            sj[u] = p.x;
+            mj[u] = p.y;
+        }
+    const uint64_t g0 = srow[r0];
+    const uint32_t my_end = (uint32_t)(srow[r0 + 1 + min(lane, nr - 1)] - g0);
+    const uint32_t total = __shfl_sync(0xffffffffu, my_end, nr - 1);
+    float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f, bsum = 0.f;
+    uint32_t row = 0;
+    uint32_t row_end = __shfl_sync(0xffffffffu, my_end, 0);
+    float* crow = c + r0 * ldc + col0;
+
+    auto store_row = [&]() {
+        float o0, o1, o2, o3;
+        if (MODE == 0) {
+            o0 = acc0 + bsum; o1 = acc1 + bsum; o2 = acc2 + bsum; o3 = acc3 + bsum;
+        } else {
+            o0 = fmaf(sj[0], acc0, mj[0] * bsum); o1 = fmaf(sj[1], acc1, mj[1] * bsum);
+            o2 = fmaf(sj[2], acc2, mj[2] * bsum); o3 = fmaf(sj[3], acc3, mj[3] * bsum);
+        }
+        float* dst = crow + (uint64_t)row * ldc;
+        if (ne == 4) {
+            __stcs(reinterpret_cast<float4*>(dst), make_float4(o0, o1, o2, o3));  // ldc % 4 == 0
+        } else {
+            if (ne > 0) dst[0] = o0;
+            if (ne > 1) dst[1] = o1;
+            if (ne > 2) dst[2] = o2;
+        }
+        acc0 = acc1 = acc2 = acc3 = bsum = 0.f;
+    };
+    auto advance = [&](uint32_t pos) {
+        do {
+            store_row();
+            ++row;
+            row_end = __shfl_sync(0xffffffffu, my_end, min(row, nr - 1));
+        } while (row < nr && row_end == pos);
+    };
+    if (total == 0 || row_end == 0) {
+        if (total == 0) {
+            for (; row < nr; ++row) store_row();
+            return;
+        }
+        advance(0);
+    }
+
+    for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+        const uint32_t nb = min(32u, total - t0);
+        // stage this batch's metadata
+        __syncwarp();
+        if (lane < nb) {
+            const uint32_t cc = __ldcs(scol + g0 + t0 + lane);
+            const float v = __ldcs(sval + g0 + t0 + lane);
+            SlotMeta m;
+            m.col = cc;
+            if (MODE == 0) {
+                const float2 p = __ldg(params + cc);
+                m.a = v * p.x;
+                m.b = v * p.y;
+            } else {
+                m.a = v;
+                m.b = v;
+            }
+            m.pad = 0.f;
+            s_meta[warp][lane] = m;
+        }
+        __syncwarp();
+        for (uint32_t k0 = 0; k0 < nb; k0 += U) {
+            uint32_t raw[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                raw[u] = 0;
+                if (k0 + u < nb && ne) {
+                    const uint32_t cc = s_meta[warp][k0 + u].col;
+                    raw[u] = __ldg(reinterpret_cast<const uint32_t*>(qb + (uint64_t)cc * ldq));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (k0 + u < nb) {
+                    const float4 mm = *reinterpret_cast<const float4*>(&s_meta[warp][k0 + u]);
+                    const float a = mm.y;
+                    float q0, q1, q2, q3;
+                    decode4(raw[u], q0, q1, q2, q3);
+                    fma2(acc0, acc1, a, q0, q1);
+                    fma2(acc2, acc3, a, q2, q3);
+                    bsum += mm.z;
+                    const uint32_t pos = t0 + k0 + u + 1;
+                    if (pos == row_end) advance(pos);
+                }
+            }
+        }
+    }
+    for (; row < nr; ++row) store_row();  // rows after the last slot (empty tails)
+}
+
+template <int MODE>
+int launch_q8a(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, const uint8_t* q,
+               uint64_t ldq, uint64_t f, const float2* params, float* c, uint64_t ldc, cudaStream_t st) {
+    constexpr int kWarps = 8, kU = 16;
+    const uint64_t groups = (n + 31) / 32;
+    const dim3 grid((unsigned)((groups + kWarps - 1) / kWarps), (unsigned)((f + 127) / 128));
+    spmm_q8a_kernel<MODE, kU, kWarps><<<grid, kWarps * 32, 0, st>>>(srow, scol, sval, n, q, ldq, (uint32_t)f, params,
+                                                                    c, ldc);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
+}  // namespace
+}  // namespace aes
+
+extern "C" {
+
+uint64_t aes_quantize_affine_workspace_bytes(uint64_t rows, uint64_t cols, int mode) {
+    using namespace aes;
+    if (mode != AES_QAFFINE_FEATURE) return 256;
+    const uint64_t blocks = (rows + kColRowsPerCta - 1) / kColRowsPerCta;
+    return 256 + (blocks ? blocks : 1) * (cols ? cols : 1) * sizeof(float2);
+}
+
+int aes_dev_quantize_affine(const float* x, uint64_t rows, uint64_t cols, uint64_t ldx, int mode, uint8_t* q,
+                            uint64_t ldq, float* params, unsigned int* bad_flag, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+    using namespace aes;
+    if (mode != AES_QAFFINE_ROW && mode != AES_QAFFINE_FEATURE) return fail(AES_ERR_INVALID_ARG, "unknown affine mode");
+    if (!x || !q || !params || !bad_flag) return fail(AES_ERR_INVALID_ARG, "null argument");
+    if (ldq % 4 || (uintptr_t)q % 4 || ldq < ((cols + 3) & ~3ull) || ldx < cols)
+        return fail(AES_ERR_UNSUPPORTED, "affine quantize needs ldq % 4 == 0 and ldq >= round_up(cols, 4)");
+    if (workspace_bytes < aes_quantize_affine_workspace_bytes(rows, cols, mode) || !workspace)
+        return fail(AES_ERR_INVALID_ARG, "affine quantize workspace too small");
+    cudaStream_t st = as_stream(stream);
+    AES_CUDA_TRY(cudaMemsetAsync(bad_flag, 0, sizeof(unsigned int), st));
+    if (rows == 0 || cols == 0) return AES_OK;
+    float2* p2 = reinterpret_cast<float2*>(params);
+    if (mode == AES_QAFFINE_ROW) {
+        quant_row_kernel<<<grid_for(rows * 32, 256, num_sms() * 16), 256, 0, st>>>(x, rows, cols, ldx, q, ldq, p2,
+                                                                                   bad_flag);
+    } else {
+        const uint64_t blocks = (rows + kColRowsPerCta - 1) / kColRowsPerCta;
+        float2* partial = reinterpret_cast<float2*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
+        col_minmax_kernel<<<dim3((unsigned)blocks, (unsigned)((cols + 31) / 32)), 256, 0, st>>>(x, rows, cols, ldx,
+                                                                                             partial, bad_flag);
+        col_params_kernel<<<grid_for(cols, 128), 128, 0, st>>>(partial, blocks, cols, p2);
+        quant_col_kernel<<<grid_for(rows * ((cols + 3) / 4), 256, num_sms() * 32), 256, 0, st>>>(x, rows, cols, ldx,
+                                                                                                 p2, q, ldq);
+    }
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
+int aes_dev_dequantize_affine(const uint8_t* q, uint64_t rows, uint64_t cols, uint64_t ldq, int mode,
+                              const float* params, float* x, uint64_t ldx, void* stream) {
+    using namespace aes;
+    if (mode != AES_QAFFINE_ROW && mode != AES_QAFFINE_FEATURE) return fail(AES_ERR_INVALID_ARG, "unknown affine mode");
+    cudaStream_t st = as_stream(stream);
+    if (rows == 0 || cols == 0) return AES_OK;
+    const float2* p2 = reinterpret_cast<const float2*>(params);
+    const unsigned grid = grid_for(rows * cols, 256, num_sms() * 32);
+    if (mode == AES_QAFFINE_ROW)
+        dequant_affine_kernel<0><<<grid, 256, 0, st>>>(q, rows, cols, ldq, p2, x, ldx);
+    else
+        dequant_affine_kernel<1><<<grid, 256, 0, st>>>(q, rows, cols, ldq, p2, x, ldx);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
+int aes_dev_spmm_q8_affine(const uint64_t* srow_ptr, const uint32_t* scol, const float* sval, uint64_t n_rows,
+                           const uint8_t* q, uint64_t ldq, uint64_t f, int mode, const float* params, float* c,
+                           uint64_t ldc, void* stream) {
+    using namespace aes;
+    if (mode != AES_QAFFINE_ROW && mode != AES_QAFFINE_FEATURE) return fail(AES_ERR_INVALID_ARG, "unknown affine mode");
+    if (n_rows == 0 || f == 0) return AES_OK;
+    if (ldq % 4 || (uintptr_t)q % 4 || ldq < ((f + 3) & ~3ull) || ldc % 4 || (uintptr_t)c % 16 || ldc < f)
+        return fail(AES_ERR_UNSUPPORTED, "affine spmm needs ldq % 4 == 0, ldc % 4 == 0, 16-B aligned C");
+    if (f > 0xffffffffull) return fail(AES_ERR_UNSUPPORTED, "F too large");
+    cudaStream_t st = as_stream(stream);
+    const float2* p2 = reinterpret_cast<const float2*>(params);
+    if (mode == AES_QAFFINE_ROW) return launch_q8a<0>(srow_ptr, scol, sval, n_rows, q, ldq, f, p2, c, ldc, st);
+    return launch_q8a<1>(srow_ptr, scol, sval, n_rows, q, ldq, f, p2, c, ldc, st);
+}
+
+}  // extern "C"

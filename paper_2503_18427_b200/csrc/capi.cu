@@ -240,6 +240,10 @@ struct aes_qfeat_s {
     bool u8 = true;       // codes stored as u8 (bits <= 8 and all codes <= 255)
     void* codes = nullptr;
     float* lut = nullptr;  // 256 floats when u8
+    // fast mode (affine.cu): AES_QAFFINE_ROW / _FEATURE, -1 = the reference's
+    // global min/max codes; params: float2 (scale, offset) per row / column
+    int affine = -1;
+    float* aparams = nullptr;
 };
 
 namespace {
@@ -830,6 +834,58 @@ int aes_sampling_rate(aes_plan_t p, aes_csr_t a, double* aggregate, double* uniq
     return AES_OK;
 }
 
+// cdf_stats (bench.cpp:124-138) over host rates, and over a plan's per-row
+// rates straight from the device (no per-row read-back).  Outputs hold at
+// most n steps; *n_steps receives the count.
+static int cdf_device(const double* d_rates, uint64_t n, double* out_rate, double* out_frac, uint64_t* n_steps) {
+    cudaStream_t st = lib_stream();
+    DBuf<char> ws;
+    DBuf<double> dr, df;
+    DBuf<uint64_t> dn;
+    const size_t wsb = aes_cdf_workspace_bytes(n);
+    AES_TRY(ws.alloc(wsb));
+    AES_TRY(dr.alloc(n));
+    AES_TRY(df.alloc(n));
+    AES_TRY(dn.alloc(1));
+    AES_TRY(aes_dev_cdf_stats(d_rates, n, dr.p, df.p, dn.p, ws.p, wsb, st));
+    uint64_t steps = 0;
+    AES_TRY(d2h_scalar(dn.p, &steps));
+    AES_CUDA_TRY(cudaMemcpyAsync(out_rate, dr.p, steps * 8, cudaMemcpyDeviceToHost, st));
+    AES_CUDA_TRY(cudaMemcpyAsync(out_frac, df.p, steps * 8, cudaMemcpyDeviceToHost, st));
+    AES_TRY(sync());
+    *n_steps = steps;
+    return AES_OK;
+}
+
+int aes_cdf_stats(const double* rates, uint64_t n, double* out_rate, double* out_frac, uint64_t* n_steps) {
+    if (n == 0) return fail(AES_ERR_INVALID_ARG, "rates must be nonempty");
+    if (!rates || !out_rate || !out_frac || !n_steps) return fail(AES_ERR_INVALID_ARG, "null argument");
+    DBuf<double> d;
+    AES_TRY(d.alloc(n));
+    AES_CUDA_TRY(cudaMemcpyAsync(d.p, rates, n * 8, cudaMemcpyHostToDevice, lib_stream()));
+    return cdf_device(d.p, n, out_rate, out_frac, n_steps);
+}
+
+int aes_sampling_rate_cdf(aes_plan_t p, aes_csr_t a, double* out_rate, double* out_frac, uint64_t* n_steps) {
+    if (!p || !a || !out_rate || !out_frac || !n_steps) return fail(AES_ERR_INVALID_ARG, "null argument");
+    if (p->n_rows != a->n_rows) return fail(AES_ERR_INVALID_ARG, "plan/stats row count mismatch");
+    if (a->n_rows == 0) return fail(AES_ERR_INVALID_ARG, "rates must be nonempty");
+    cudaStream_t st = lib_stream();
+    DBuf<unsigned long long> tot;
+    DBuf<double> pr;
+    DBuf<unsigned char> seen;
+    AES_TRY(tot.alloc(3));
+    AES_TRY(pr.alloc(a->n_rows));
+    if (p->explicit_plan) {
+        AES_TRY(seen.alloc(a->nnz ? a->nnz : 1));
+        AES_TRY(launch_explicit_rate(a->row_ptr, p->params, p->starts_ptr, p->starts, a->n_rows, a->nnz, seen.p,
+                                     pr.p, tot.p, st));
+    } else {
+        AES_TRY(launch_sampling_rate(a->row_ptr, a->n_rows, p->width, p->strategy, pr.p, tot.p, st));
+    }
+    return cdf_device(pr.p, a->n_rows, out_rate, out_frac, n_steps);
+}
+
 // ---- SpMM ------------------------------------------------------------------------
 int aes_spmm_exact(aes_csr_t a, const float* b, uint64_t b_rows, uint64_t f, float* c) {
     if (!a) return fail(AES_ERR_INVALID_ARG, "null csr");
@@ -997,11 +1053,65 @@ int aes_qfeat_from_codes(const uint16_t* codes, uint64_t rows, uint64_t cols, fl
     return AES_OK;
 }
 
+// Fast mode: per-row / per-feature affine codes (affine.cu).
+int aes_quantize_affine(const float* x, uint64_t rows, uint64_t cols, int mode, aes_qfeat_t* out) {
+    if (!out) return fail(AES_ERR_INVALID_ARG, "null out");
+    if (mode != AES_QAFFINE_ROW && mode != AES_QAFFINE_FEATURE) return fail(AES_ERR_INVALID_ARG, "unknown affine mode");
+    const uint64_t n = rows * cols;
+    if (n == 0) return fail(AES_ERR_EMPTY, "EmptyMatrix");
+    cudaStream_t st = lib_stream();
+    DBuf<float> dx;
+    DBuf<char> ws;
+    DBuf<unsigned int> bad;
+    AES_TRY(dx.alloc(n));
+    AES_CUDA_TRY(cudaMemcpyAsync(dx.p, x, n * 4, cudaMemcpyHostToDevice, st));
+    const size_t wsb = aes_quantize_affine_workspace_bytes(rows, cols, mode);
+    AES_TRY(ws.alloc(wsb));
+    AES_TRY(bad.alloc(1));
+    auto* q = new aes_qfeat_s;
+    q->rows = rows;
+    q->cols = cols;
+    q->bits = 8;
+    q->u8 = true;
+    q->affine = mode;
+    q->ld = round16(cols);
+    int s = AES_OK;
+    const uint64_t np = mode == AES_QAFFINE_ROW ? rows : cols;
+    if (cudaMallocAsync(&q->codes, rows * q->ld + 16, st) != cudaSuccess ||
+        cudaMallocAsync((void**)&q->aparams, np * 2 * sizeof(float), st) != cudaSuccess)
+        s = fail(AES_ERR_CUDA, "alloc");
+    if (!s && q->ld != cols) s = cudaMemsetAsync(q->codes, 0, rows * q->ld, st) == cudaSuccess ? AES_OK
+                                                                                              : fail(AES_ERR_CUDA, "memset");
+    if (!s) s = aes_dev_quantize_affine(dx.p, rows, cols, cols, mode, (uint8_t*)q->codes, q->ld, q->aparams, bad.p,
+                                        ws.p, wsb, st);
+    unsigned int flag = 0;
+    if (!s) s = d2h_scalar(bad.p, &flag);
+    if (!s && flag) s = fail(AES_ERR_NONFINITE, "NonFinite");
+    if (s) {
+        aes_qfeat_destroy(q);
+        return s;
+    }
+    *out = q;
+    return AES_OK;
+}
+
+int aes_qfeat_affine(aes_qfeat_t q, int* mode, float* params) {
+    if (!q) return fail(AES_ERR_INVALID_ARG, "null qfeat");
+    if (mode) *mode = q->affine;
+    if (params && q->affine >= 0) {
+        const uint64_t np = q->affine == AES_QAFFINE_ROW ? q->rows : q->cols;
+        AES_CUDA_TRY(cudaMemcpyAsync(params, q->aparams, np * 8, cudaMemcpyDeviceToHost, lib_stream()));
+        return sync();
+    }
+    return AES_OK;
+}
+
 int aes_qfeat_destroy(aes_qfeat_t q) {
     if (!q) return AES_OK;
     cudaStream_t st = lib_stream();
     if (q->codes) cudaFreeAsync(q->codes, st);
     if (q->lut) cudaFreeAsync(q->lut, st);
+    if (q->aparams) cudaFreeAsync(q->aparams, st);
     delete q;
     return AES_OK;
 }
@@ -1039,6 +1149,9 @@ static int dequant_device(aes_qfeat_t q, DBuf<float>& out, uint64_t& ld) {
     AES_TRY(out.alloc(q->rows * ld));
     cudaStream_t st = lib_stream();
     if (ld != q->cols) AES_CUDA_TRY(cudaMemsetAsync(out.p, 0, q->rows * ld * 4, st));
+    if (q->affine >= 0)
+        return aes_dev_dequantize_affine((const uint8_t*)q->codes, q->rows, q->cols, q->ld, q->affine, q->aparams,
+                                         out.p, ld, st);
     return aes_dev_dequantize(q->codes, q->rows, q->cols, q->ld, q->x_min, q->x_max, q->bits, out.p, ld, st);
 }
 
@@ -1071,7 +1184,10 @@ int aes_spmm_sampled_q8(aes_csr_t a, aes_qfeat_t q, aes_plan_t p, float* c) {
     const uint64_t ldc = round4(f);
     DBuf<float> dc;
     AES_TRY(dc.alloc(n * ldc));
-    if (q->u8) {
+    if (q->affine >= 0) {  // fast mode: affine decode fused into the gather
+        AES_TRY(aes_dev_spmm_q8_affine(rp, scol, sval, n, (const uint8_t*)q->codes, q->ld, f, q->affine, q->aparams,
+                                       dc.p, ldc, st));
+    } else if (q->u8) {
         AES_TRY(aes_dev_spmm_q8_ex(rp, scol, sval, n, (const uint8_t*)q->codes, q->ld, f, q->lut, dc.p, ldc,
                                    plan_row_bound(p), st));
     } else {  // 9..16-bit codes: dequantize on the GPU, then the fp32 kernel
@@ -1361,6 +1477,7 @@ int capi_csr_from_device(uint64_t n_rows, uint64_t n_cols, uint64_t nnz, uint64_
 
 int capi_qfeat_device(aes_qfeat_t q, const void** codes, uint64_t* ld, int* u8) {
     if (!q) return fail(AES_ERR_INVALID_ARG, "null qfeat");
+    if (q->affine >= 0) return fail(AES_ERR_INVALID_ARG, "FMAT dtype 1 stores global-params codes only");
     *codes = q->codes;
     *ld = q->ld;
     *u8 = q->u8 ? 1 : 0;

@@ -268,6 +268,17 @@ SamplingRates sampling_rate(const SamplePlanSet& plans, const RowStats& stats) {
     return r;
 }
 
+// ----------------------------------------------------------------- bench
+std::vector<std::pair<double, double>> cdf_stats(std::vector<double> rates) {
+    if (rates.empty()) throw std::invalid_argument("rates must be nonempty");  // bench.cpp:125
+    std::vector<double> r(rates.size()), f(rates.size());
+    std::uint64_t steps = 0;
+    check(aes_cdf_stats(rates.data(), rates.size(), r.data(), f.data(), &steps));
+    std::vector<std::pair<double, double>> cdf(steps);
+    for (std::uint64_t i = 0; i < steps; ++i) cdf[i] = {r[i], f[i]};
+    return cdf;
+}
+
 // ------------------------------------------------------------------ spmm
 DenseMatrix spmm_exact(const CsrMatrix& a, const DenseMatrix& b, unsigned) {
     if (a.n_cols != b.n_rows) throw std::invalid_argument("ShapeMismatch");

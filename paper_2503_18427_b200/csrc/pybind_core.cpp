@@ -227,6 +227,24 @@ PYBIND11_MODULE(_core, mod) {
             uint16_t* p = a.mutable_data();
             check(nogil([&] { return aes_qfeat_codes(q.h, p); }));
             return a;
+        })
+        // fast mode (quantize_affine): "row" / "feature", None for the
+        // reference's global min/max codes
+        .def_property_readonly("affine_mode", [](const QFeat& q) -> py::object {
+            int mode = -1;
+            check(aes_qfeat_affine(q.h, &mode, nullptr));
+            if (mode < 0) return py::none();
+            return py::str(mode == AES_QAFFINE_ROW ? "row" : "feature");
+        })
+        .def_property_readonly("affine_params", [](const QFeat& q) -> py::object {
+            int mode = -1;
+            check(aes_qfeat_affine(q.h, &mode, nullptr));
+            if (mode < 0) return py::none();
+            const uint64_t np = mode == AES_QAFFINE_ROW ? q.n_rows : q.n_cols;
+            py::array_t<float> a({(py::ssize_t)np, (py::ssize_t)2});
+            float* p = a.mutable_data();
+            check(nogil([&] { return aes_qfeat_affine(q.h, &mode, p); }));
+            return a;
         });
 
     mod.def(
@@ -276,6 +294,32 @@ PYBIND11_MODULE(_core, mod) {
             return pr;
         },
         py::arg("plans"), py::arg("matrix"));
+    // cdf_stats (bench.hpp:58-59, bench.cpp:124-138): [(rate, fraction), ...]
+    mod.def(
+        "cdf_stats",
+        [](py::array_t<double, py::array::c_style | py::array::forcecast> rates) {
+            const uint64_t n = (uint64_t)rates.size();
+            std::vector<double> r(n ? n : 1), fr(n ? n : 1);
+            uint64_t steps = 0;
+            const double* pr = rates.data();
+            check(nogil([&] { return aes_cdf_stats(pr, n, r.data(), fr.data(), &steps); }));
+            py::list out;
+            for (uint64_t i = 0; i < steps; ++i) out.append(py::make_tuple(r[i], fr[i]));
+            return out;
+        },
+        py::arg("rates"), "empirical CDF of per-row sampling rates (sorted steps, ties merged)");
+    mod.def(
+        "sampling_rate_cdf",
+        [](const PlanSet& plans, const Csr& m) {
+            std::vector<double> r(m.n_rows ? m.n_rows : 1), fr(m.n_rows ? m.n_rows : 1);
+            uint64_t steps = 0;
+            check(nogil([&] { return aes_sampling_rate_cdf(plans.h, m.h, r.data(), fr.data(), &steps); }));
+            py::array_t<double> ra(steps), fa(steps);
+            std::copy(r.begin(), r.begin() + steps, ra.mutable_data());
+            std::copy(fr.begin(), fr.begin() + steps, fa.mutable_data());
+            return py::make_tuple(ra, fa);
+        },
+        py::arg("plans"), py::arg("matrix"), "cdf_stats of the per-row sampling rates, computed on the device");
 
     mod.def(
         "spmm_exact",
@@ -342,6 +386,21 @@ PYBIND11_MODULE(_core, mod) {
             return std::make_shared<QFeat>(h);
         },
         py::arg("x"), py::arg("bits") = 8);
+    mod.def(
+        "quantize_affine",
+        [](F32In x, const std::string& mode) {
+            x = as_2d(x);
+            int m = mode == "row" ? AES_QAFFINE_ROW : mode == "feature" ? AES_QAFFINE_FEATURE : -1;
+            if (m < 0) throw py::value_error("mode must be 'row' or 'feature'");
+            aes_qfeat_t h = nullptr;
+            uint64_t r = x.shape(0), c = x.shape(1);
+            const float* px = x.data();
+            check(nogil([&] { return aes_quantize_affine(px, r, c, m, &h); }));
+            return std::make_shared<QFeat>(h);
+        },
+        py::arg("x"), py::arg("mode") = "row",
+        "FAST MODE int8 codes with per-row or per-feature (scale, offset); spmm_sampled_q8 / dequantize "
+        "decode them (not bit-exact; error bounds in include/aesspmm_cuda.h)");
     mod.def(
         "quantize_with",
         [](F32In x, const QuantParams& p) {

@@ -33,22 +33,21 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
     return v;
 }
 
+// Row count of row r, with the row's offsets b = row_ptr[r], e = row_ptr[r+1]
+// already at hand (the tile stages row_ptr in shared memory).
 template <int KIND>
-__device__ __forceinline__ uint64_t row_count(const ScanArgs& a, uint64_t r) {
+__device__ __forceinline__ uint64_t row_count(const ScanArgs& a, uint64_t r, uint64_t b, uint64_t e) {
     if (KIND == kScanExplicit) {  // host-supplied plans: slots = chunk * cnt
         const uint2 p = reinterpret_cast<const uint2*>(a.row_params)[r];
         return (uint64_t)p.x * p.y;
     }
-    uint64_t b = a.row_ptr[r], e = a.row_ptr[r + 1];
-    uint64_t nnz = e - b;
+    const uint64_t nnz = e - b;
     if (KIND == kScanSlots) {
-        RowParams p = row_params(nnz, a.width, a.strategy);
-        if (a.row_params) {
-            reinterpret_cast<uint2*>(a.row_params)[r] = make_uint2(p.chunk, p.cnt);
-        }
+        const RowParams p = row_params(nnz, a.width, a.strategy);
+        if (a.row_params) reinterpret_cast<uint2*>(a.row_params)[r] = make_uint2(p.chunk, p.cnt);
         return (uint64_t)p.chunk * p.cnt;
     } else if (KIND == kScanStarts) {
-        RowParams p = row_params(nnz, a.width, a.strategy);
+        const RowParams p = row_params(nnz, a.width, a.strategy);
         return row_num_starts(nnz, a.width, a.strategy, p);
     } else {  // kScanGcnNnz: rows are sorted (validated); probe the diagonal
         if (!a.add_self_loops) return nnz;
@@ -57,14 +56,25 @@ __device__ __forceinline__ uint64_t row_count(const ScanArgs& a, uint64_t r) {
             uint64_t mid = (lo + hi) >> 1;
             if (a.col_ind[mid] < r) lo = mid + 1; else hi = mid;
         }
-        bool has_diag = lo < e && a.col_ind[lo] == r;
+        const bool has_diag = lo < e && a.col_ind[lo] == r;
         return nnz + (has_diag ? 0 : 1);
     }
 }
 
+// shared-memory index of tile row i: one u64 of padding per 16 so that the
+// blocked per-thread reads (thread t: rows 8t..8t+7) spread over the banks
+__device__ __forceinline__ int pad_idx(int i) { return i + (i >> 4); }
+
+// One tile = 2048 rows.  The tile's row_ptr (2049 values) is staged in shared
+// memory with coalesced loads; thread t counts rows 8t..8t+7 (one thread-
+// serial prefix, ONE block scan per tile instead of one per 256 rows); warp 0
+// looks back over up to 32 predecessor tiles at a time; the inclusive
+// prefixes go back through shared memory so the srow_ptr stores are coalesced.
 template <int KIND>
 __global__ void __launch_bounds__(kScanThreads)
 row_scan_kernel(ScanArgs a, unsigned long long* tile_state, unsigned int* tile_counter) {
+    constexpr int kPadded = kScanTile + 1 + (kScanTile + 1) / 16 + 1;
+    __shared__ uint64_t s_rp[kPadded];
     __shared__ uint64_t warp_tot[kScanThreads / 32];
     __shared__ uint64_t s_excl;
     __shared__ unsigned int s_tile;
@@ -74,62 +84,95 @@ row_scan_kernel(ScanArgs a, unsigned long long* tile_state, unsigned int* tile_c
     __syncthreads();
     const uint64_t tile = s_tile;
     const uint64_t base = tile * kScanTile;
+    const int nr = (int)min((uint64_t)kScanTile, a.n - base);
+    if (KIND != kScanExplicit)
+        for (int i = tid; i <= nr; i += kScanThreads) s_rp[pad_idx(i)] = a.row_ptr[base + i];
+    __syncthreads();
 
     uint64_t incl[kScanIters];
-    uint64_t carry = 0;
+    uint64_t run = 0;
 #pragma unroll
-    for (int it = 0; it < kScanIters; ++it) {
-        uint64_t r = base + (uint64_t)it * kScanThreads + tid;
-        uint64_t c = r < a.n ? row_count<KIND>(a, r) : 0;
-        // warp inclusive scan
-        uint64_t v = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint64_t t = __shfl_up_sync(0xffffffffu, v, o);
-            if (lane >= o) v += t;
+    for (int u = 0; u < kScanIters; ++u) {
+        const int i = tid * kScanIters + u;
+        uint64_t c = 0;
+        if (i < nr) {
+            const uint64_t b = KIND != kScanExplicit ? s_rp[pad_idx(i)] : 0;
+            const uint64_t e = KIND != kScanExplicit ? s_rp[pad_idx(i + 1)] : 0;
+            c = row_count<KIND>(a, base + i, b, e);
         }
-        if (lane == 31) warp_tot[wid] = v;
-        __syncthreads();
-        uint64_t woff = 0, tot = 0;
-#pragma unroll
-        for (int w = 0; w < kScanThreads / 32; ++w) {
-            uint64_t x = warp_tot[w];
-            woff += (w < wid) ? x : 0;
-            tot += x;
-        }
-        incl[it] = carry + woff + v;
-        carry += tot;
-        __syncthreads();
+        run += c;
+        incl[u] = run;
     }
+    // block exclusive scan of the per-thread totals
+    uint64_t v = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    if (lane == 31) warp_tot[wid] = v;
+    __syncthreads();
+    uint64_t woff = 0, tile_tot = 0;
+#pragma unroll
+    for (int w = 0; w < kScanThreads / 32; ++w) {
+        const uint64_t x = warp_tot[w];
+        woff += (w < wid) ? x : 0;
+        tile_tot += x;
+    }
+    const uint64_t thread_excl = woff + v - run;
 
-    // publish aggregate / look back
-    if (tid == 0) {
+    // publish the aggregate, look back (warp 0, 32 predecessors per step)
+    if (wid == 0) {
         uint64_t excl = 0;
         if (tile == 0) {
-            st_release(&tile_state[0], (carry << 2) | 2ull);
+            if (lane == 0) st_release(&tile_state[0], (tile_tot << 2) | 2ull);
         } else {
-            st_release(&tile_state[tile], (carry << 2) | 1ull);
-            int64_t j = (int64_t)tile - 1;
-            while (j >= 0) {
-                unsigned long long s;
-                do {
-                    s = ld_acquire(&tile_state[j]);
-                } while ((s & 3ull) == 0);
-                excl += s >> 2;
-                if ((s & 3ull) == 2ull) break;
-                --j;
-            }
-            st_release(&tile_state[tile], ((excl + carry) << 2) | 2ull);
-        }
-        s_excl = excl;
-    }
-    __syncthreads();
-    const uint64_t excl = s_excl;
+            if (lane == 0) st_release(&tile_state[tile], (tile_tot << 2) | 1ull);
+            // 128 predecessors per step (4 per lane, lane l at distances
+            // 4l+1 .. 4l+4): every first-wave tile publishes its aggregate at
+            // about the same time, so the walk length — not waiting — is what
+            // costs, one L2 round trip per step
+            int64_t hi = (int64_t)tile - 1;
+            while (true) {
+                unsigned long long st[4];
 #pragma unroll
-    for (int it = 0; it < kScanIters; ++it) {
-        uint64_t r = base + (uint64_t)it * kScanThreads + tid;
-        if (r < a.n) a.out[r + 1] = excl + incl[it];
+                for (int i = 0; i < 4; ++i) {
+                    const int64_t j = hi - (4 * lane + i);
+                    st[i] = 2ull;  // below tile 0: an empty inclusive prefix
+                    if (j >= 0) {
+                        do {
+                            st[i] = ld_acquire(&tile_state[j]);
+                        } while ((st[i] & 3ull) == 0);
+                    }
+                }
+                int first = 4;  // nearest inclusive prefix among this lane's four
+#pragma unroll
+                for (int i = 3; i >= 0; --i)
+                    if ((st[i] & 3ull) == 2ull) first = i;
+                const unsigned inc = __ballot_sync(0xffffffffu, first < 4);
+                const int stop = inc ? __ffs(inc) - 1 : 32;
+                uint64_t val = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const bool take = lane < stop || (lane == stop && i <= first);
+                    if (take && hi - (4 * lane + i) >= 0) val += st[i] >> 2;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+                excl += val;
+                if (inc) break;
+                hi -= 128;
+            }
+            if (lane == 0) st_release(&tile_state[tile], ((excl + tile_tot) << 2) | 2ull);
+        }
+        if (lane == 0) s_excl = excl;
     }
+    __syncthreads();  // s_excl visible; every s_rp read above is done
+    const uint64_t excl = s_excl + thread_excl;
+#pragma unroll
+    for (int u = 0; u < kScanIters; ++u) s_rp[pad_idx(tid * kScanIters + u)] = excl + incl[u];
+    __syncthreads();
+    for (int i = tid; i < nr; i += kScanThreads) a.out[base + i + 1] = s_rp[pad_idx(i)];
     if (tile == 0 && tid == 0) a.out[0] = 0;
 }
 
@@ -179,46 +222,125 @@ int launch_row_scan(int kind, const ScanArgs& a, void* ws, size_t ws_bytes, cuda
 namespace {
 
 constexpr int kFillRows = 256;
+constexpr int kFillMap = 8192;  // slots per pass of the slot -> row map (u8 entries)
 
+// Per-row fill parameters, computed once per row (not per slot).
+struct FillRow {
+    uint64_t src;     // row_ptr[row] of the matrix being filled
+    uint32_t first;   // first slot, relative to the CTA's first slot
+    uint32_t cnt;     // sample_cnt
+    uint32_t shift;   // log2(cnt) when cnt is a power of two, else 0xff
+    uint32_t range;   // hash modulus nnz - chunk + 1 (adaptive, sampled rows), saturated to 2^32-1
+    uint32_t mode;    // 0: start 0 (whole row / prefix), 1: hashed windows, 2: AFS starts
+    uint32_t nnz;     // plan row nnz (AFS)
+};
+
+// The CTA owns kFillRows consecutive rows and writes their slots in slot
+// order (coalesced scol / sval stores; each window's reads are contiguous).
+// Thread i derives row i's parameters once and writes i into the slot -> row
+// map for the row's slots, so a slot finds its row with one shared load (no
+// search); the slot's window index s and offset j come from a shift/mask
+// (sample_cnt is a power of two in every Table-1 branch when W >= 32), and a
+// hashed start needs at most a 32-bit modulo: s*1429 < 32*1429, and
+// hash_start is s*1429 itself whenever the modulus exceeds it.  CTAs whose
+// slots exceed the map (W > 32, FULL) run several passes.
 __global__ void __launch_bounds__(kFillRows)
 sample_fill_kernel(const uint64_t* __restrict__ plan_row_ptr, const uint64_t* __restrict__ row_ptr,
                    const uint32_t* __restrict__ col_ind, const float* __restrict__ val,
                    uint64_t n, uint32_t width, int strategy, const uint64_t* __restrict__ srow_ptr,
                    uint32_t* __restrict__ scol, float* __restrict__ sval) {
-    __shared__ uint64_t s_srow[kFillRows + 1];
-    __shared__ uint64_t s_prp[kFillRows + 1];
-    __shared__ uint64_t s_rp[kFillRows];
+    __shared__ FillRow s_row[kFillRows];
+    __shared__ unsigned char s_map[kFillMap];
+    __shared__ uint64_t s_g0, s_total;
+    const int tid = threadIdx.x;
     const uint64_t r0 = (uint64_t)blockIdx.x * kFillRows;
     const int nr = (int)min((uint64_t)kFillRows, n - r0);
-    for (int i = threadIdx.x; i <= nr; i += blockDim.x) {
-        s_srow[i] = srow_ptr[r0 + i];
-        s_prp[i] = plan_row_ptr[r0 + i];
-        if (i < nr) s_rp[i] = row_ptr[r0 + i];
+    if (tid == 0) {
+        s_g0 = srow_ptr[r0];
+        s_total = srow_ptr[r0 + nr] - s_g0;
     }
     __syncthreads();
-    const uint64_t g0 = s_srow[0];
-    const uint64_t total = s_srow[nr] - g0;
-    for (uint64_t t = threadIdx.x; t < total; t += blockDim.x) {
-        const uint64_t pos = g0 + t;
-        // last row with start <= pos (skips empty rows sharing the start)
-        int lo = 0, hi = nr;  // invariant: s_srow[lo] <= pos < s_srow[hi]
-        while (hi - lo > 1) {
-            int mid = (lo + hi) >> 1;
-            if (s_srow[mid] <= pos) lo = mid; else hi = mid;
-        }
-        const uint64_t nnz = s_prp[lo + 1] - s_prp[lo];
+    const uint64_t g0 = s_g0, total = s_total;
+    uint32_t my_first = 0, my_slots = 0;
+    if (tid < nr) {
+        const uint64_t r = r0 + tid;
+        const uint64_t nnz = plan_row_ptr[r + 1] - plan_row_ptr[r];
         const RowParams p = row_params(nnz, width, strategy);
-        const uint64_t k = pos - s_srow[lo];
-        uint64_t s, j;
-        if (p.cnt == 1) {
-            s = 0; j = k;
+        FillRow fr;
+        fr.src = row_ptr[r];
+        my_first = (uint32_t)(srow_ptr[r] - g0);
+        my_slots = p.chunk * p.cnt;
+        fr.first = my_first;
+        fr.cnt = p.cnt;
+        fr.shift = (p.cnt && (p.cnt & (p.cnt - 1)) == 0) ? (uint32_t)__ffs(p.cnt) - 1 : 0xffu;
+        fr.nnz = (uint32_t)nnz;
+        if (strategy == AES_AFS) {
+            fr.mode = 2;
+        } else if (strategy == AES_ADAPTIVE && nnz > width) {
+            fr.mode = 1;
         } else {
-            uint32_t k32 = (uint32_t)k;  // adaptive/afs rows have <= W slots
-            s = k32 % p.cnt; j = k32 / p.cnt;
+            fr.mode = 0;
         }
-        const uint64_t src = s_rp[lo] + row_start(nnz, width, strategy, p, (uint32_t)s) + j;
-        scol[pos] = col_ind[src];
-        sval[pos] = val[src];
+        const uint64_t range = nnz - (uint64_t)p.chunk + 1ull;
+        fr.range = range > 0xffffffffull ? 0xffffffffu : (uint32_t)range;
+        s_row[tid] = fr;
+    }
+    // (total < 2^32 slots per CTA: 256 rows of u32 nonzeros each at most)
+    for (uint32_t pass = 0; pass < total; pass += kFillMap) {
+        const uint32_t pend = (uint32_t)min((uint64_t)pass + kFillMap, total);
+        __syncthreads();  // previous pass done with the map
+        if (tid < nr && my_slots) {
+            const uint32_t a = max(my_first, pass), b = min(my_first + my_slots, pend);
+            for (uint32_t t = a; t < b; ++t) s_map[t - pass] = (unsigned char)tid;
+        }
+        __syncthreads();
+        // four slots per thread per step: their loads are all in flight
+        // before the first store (the map / row lookups are shared-memory hits)
+        for (uint32_t t0 = pass + tid; t0 < pend; t0 += 4 * kFillRows) {
+            uint64_t src[4];
+            bool ok[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t t = t0 + u * kFillRows;
+                ok[u] = t < pend;
+                src[u] = 0;
+                if (ok[u]) {
+                    const FillRow& fr = s_row[s_map[t - pass]];
+                    const uint32_t k = t - fr.first;
+                    uint32_t sidx, j;
+                    if (fr.shift != 0xffu) {
+                        sidx = k & (fr.cnt - 1);
+                        j = k >> fr.shift;
+                    } else {
+                        sidx = k % fr.cnt;
+                        j = k / fr.cnt;
+                    }
+                    uint32_t start = 0;
+                    if (fr.mode == 1) {
+                        const uint32_t prod = sidx * 1429u;  // sidx < cnt <= 32 on hashed rows
+                        start = prod < fr.range ? prod : prod % fr.range;
+                    } else if (fr.mode == 2) {
+                        start = (uint32_t)((uint64_t)sidx * fr.nnz / fr.cnt);
+                    }
+                    src[u] = fr.src + start + j;
+                }
+            }
+            uint32_t cv[4];
+            float vv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (ok[u]) {
+                    cv[u] = __ldg(col_ind + src[u]);
+                    vv[u] = __ldg(val + src[u]);
+                }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (ok[u]) {
+                    const uint64_t pos = g0 + t0 + u * kFillRows;
+                    __stcs(scol + pos, cv[u]);
+                    __stcs(sval + pos, vv[u]);
+                }
+        }
     }
 }
 

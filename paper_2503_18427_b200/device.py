@@ -259,6 +259,59 @@ def spmm_q8(srow_ptr, scol, sval, q: QuantizedDevice, out=None, stream=None, max
     return out
 
 
+AFFINE_MODES = {"row": 0, "feature": 1}
+
+
+@dataclass
+class QuantizedAffine:
+    """FAST MODE int8 codes (affine.cu): u8 codes with a (scale, offset) pair
+    per row ("row") or per column ("feature"); x^ = q * s + m.  Not the
+    reference's global min/max codes — bounded, not bit-exact."""
+
+    codes: torch.Tensor   # uint8 [rows, cols] view, ld % 16 == 0
+    params: torch.Tensor  # float32 [rows or cols, 2] = (s, m)
+    mode: str
+
+
+def quantize_affine(x: torch.Tensor, mode: str = "row", stream=None) -> QuantizedAffine:
+    """Per-row / per-feature 8-bit codes of x (one pass for "row", three
+    small passes for "feature"); raises ValueError("NonFinite") on inf/NaN."""
+    if mode not in AFFINE_MODES:
+        raise ValueError("mode must be 'row' or 'feature'")
+    L = lib()
+    rows, cols = x.shape
+    codes = empty_padded(rows, cols, dtype=torch.uint8, device=x.device)
+    params = torch.empty((rows if mode == "row" else cols, 2), dtype=torch.float32, device=x.device)
+    wsb = int(L.aes_quantize_affine_workspace_bytes(rows, cols, AFFINE_MODES[mode]))
+    ws = torch.empty(wsb, dtype=torch.uint8, device=x.device)
+    bad = torch.zeros(1, dtype=torch.int32, device=x.device)
+    check(L.aes_dev_quantize_affine(ptr(x), rows, cols, x.stride(0), AFFINE_MODES[mode], ptr(codes),
+                                    codes.stride(0), ptr(params), ptr(bad), ptr(ws), wsb, stream_of(stream)))
+    if int(bad.item()):
+        raise ValueError("NonFinite")
+    return QuantizedAffine(codes, params, mode)
+
+
+def dequantize_affine(q: QuantizedAffine, stream=None) -> torch.Tensor:
+    rows, cols = q.codes.shape
+    out = empty_padded(rows, cols, device=q.codes.device)
+    check(lib().aes_dev_dequantize_affine(ptr(q.codes), rows, cols, q.codes.stride(0), AFFINE_MODES[q.mode],
+                                          ptr(q.params), ptr(out), out.stride(0), stream_of(stream)))
+    return out
+
+
+def spmm_q8_affine(srow_ptr, scol, sval, q: QuantizedAffine, out=None, stream=None) -> torch.Tensor:
+    """spmm(A, dequantize_affine(Q)) with the affine decode fused into the u8 gather."""
+    n = srow_ptr.numel() - 1
+    f = q.codes.shape[1]
+    if out is None:
+        out = empty_padded(n, f, device=q.codes.device)
+    check(lib().aes_dev_spmm_q8_affine(ptr(srow_ptr), ptr(scol), ptr(sval), n, ptr(q.codes), q.codes.stride(0), f,
+                                       AFFINE_MODES[q.mode], ptr(q.params), ptr(out), out.stride(0),
+                                       stream_of(stream)))
+    return out
+
+
 def weights_finite(w: torch.Tensor, stream=None) -> bool:
     """True when w has no inf/NaN (device reduction, one sync)."""
     flag = torch.zeros(1, dtype=torch.int32, device=w.device)

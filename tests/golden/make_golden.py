@@ -73,6 +73,11 @@ def main():
             c = core.CsrMatrix(2708, 2708, rp, col, val)
             agg, uni = core.sampling_rate(core.build_plan_set(c, w, getattr(core.Strategy, name.upper())), c)
             fx[f"rate_{name}_{w}"] = np.array([agg, uni])
+            # per-row rates and their CDF (bench.cpp:124-138, Fig. 5/6 reporting)
+            per_row = ref.sampling_rate_per_row(graw, w, code)
+            fx[f"rate_per_row_{name}_{w}"] = digest(per_row)
+            cr, cf = ref.cdf_stats(per_row)
+            fx[f"cdf_{name}_{w}_rate"], fx[f"cdf_{name}_{w}_frac"] = cr, cf
     fx["spmm_exact"] = digest(ref.spmm_exact(graw, b))
     ws = [rng.uniform(-0.5, 0.5, (16, 16)).astype(np.float32), rng.uniform(-0.5, 0.5, (16, 7)).astype(np.float32)]
     bs = [np.full(16, 0.01, np.float32), np.zeros(7, np.float32)]
@@ -102,6 +107,8 @@ def main():
         chunk, cnt, sp, starts = ref.build_plans(hg, w, 0)
         hx[f"plan_{w}_chunk"], hx[f"plan_{w}_cnt"] = chunk, cnt
         hx[f"plan_{w}_starts_ptr"], hx[f"plan_{w}_starts"] = sp, starts
+        cr, cf = ref.cdf_stats(ref.sampling_rate_per_row(hg, w, 0))
+        hx[f"cdf_{w}_rate"], hx[f"cdf_{w}_frac"] = cr, cf
     np.savez_compressed(os.path.join(OUT, "heavy_tail.npz"), **hx)
     for f in ("cora_shape.npz", "heavy_tail.npz"):
         print(f, os.path.getsize(os.path.join(OUT, f)), "bytes")

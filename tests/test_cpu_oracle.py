@@ -275,3 +275,47 @@ def test_quantize_fast_path_decision_rule():
             wide = span > 1e-3 * max(abs(float(lo32)), abs(float(hi32)))
             if np.isfinite(scale) and span < 1e30 and wide and bits <= 8:
                 assert (fast | above | below).mean() > 0.95, (bits, lo, hi)
+
+
+# ----------------------------------------------------------------- cdf_stats
+def test_cdf_known_answers():
+    # test_io_bench.cpp:177-187
+    r, f = port.cdf_stats([1.0, 1.0, 1.0])
+    assert list(zip(r, f)) == [(1.0, 1.0)]
+    r, f = port.cdf_stats([1.0, 0.5])
+    assert list(zip(r, f)) == [(0.5, 0.5), (1.0, 1.0)]
+    with pytest.raises(ValueError):
+        port.cdf_stats([])
+
+
+def _per_row_rates(rp, w, strat):
+    """sampling_rate(...).per_row (sampling.cpp:120-152): slots / nnz, 1.0 for empty rows."""
+    out = np.ones(rp.size - 1)
+    for i in range(rp.size - 1):
+        nnz = int(rp[i + 1] - rp[i])
+        if nnz:
+            ch, cn, _ = port.row_plan(nnz, w, strat)
+            out[i] = float(ch * cn) / float(nnz)
+    return out
+
+
+@pytest.mark.parametrize("name", list(gu.STRATS))
+@pytest.mark.parametrize("w", [8, 32])
+def test_golden_cora_cdf(name, w):
+    fx = gu.cora()
+    per_row = _per_row_rates(fx["row_ptr"], w, gu.STRATS[name])
+    assert gu.digest(per_row) == fx[f"rate_per_row_{name}_{w}"]
+    r, f = port.cdf_stats(per_row)
+    assert np.array_equal(r.view(np.uint64), fx[f"cdf_{name}_{w}_rate"].view(np.uint64))
+    assert np.array_equal(f.view(np.uint64), fx[f"cdf_{name}_{w}_frac"].view(np.uint64))
+
+
+@pytest.mark.skipif(not oref.available(), reason="oracle/_ref not built")
+def test_cdf_port_matches_reference_live():
+    rng = np.random.default_rng(7)
+    for n in (1, 2, 17, 5000):
+        r = np.round(rng.random(n) * 13) / 13  # many ties
+        r[: n // 3] = np.where(rng.random(n // 3) < 0.5, 0.0, -0.0)  # +0 and -0 merge (==)
+        a, b = port.cdf_stats(r), oref.cdf_stats(r)
+        assert np.array_equal(a[0].view(np.uint64), b[0].view(np.uint64))
+        assert np.array_equal(a[1].view(np.uint64), b[1].view(np.uint64))

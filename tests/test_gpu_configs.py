@@ -100,3 +100,18 @@ def test_config_scale_parity_vs_reference(shape, width, dtype):
     got = out.cpu().numpy()[:, :f][rows]
     assert np.array_equal(np.ascontiguousarray(got).view(np.uint32), want.view(np.uint32)), \
         f"{shape} W={width} {dtype}: {(got != want).sum()} elements differ"
+
+
+@pytest.mark.parametrize("shape,width", [("products", 32), ("reddit", 64)])
+def test_config_scale_rate_cdf_vs_reference(shape, width):
+    """sampling_rate_cdf over every row of the full graph (device sort + tie
+    merge) == the reference's cdf_stats(sampling_rate(...).per_row)."""
+    import paper_2503_18427_b200 as m
+
+    _, _, (rp, col, val, _), n, _ = _shape(shape)
+    a = m.CsrMatrix(n, n, rp, col, val)
+    r, f = m.sampling_rate_cdf(m.build_plan_set(a, width), a)
+    csr = oref.RefCsr.from_arrays(n, n, rp, col, val)
+    wr, wf = oref.cdf_stats(oref.sampling_rate_per_row(csr, width, 0))
+    assert np.array_equal(r.view(np.uint64), wr.view(np.uint64))
+    assert np.array_equal(f.view(np.uint64), wf.view(np.uint64))

@@ -89,3 +89,48 @@ def test_sharded_driver_world1_on_gpu(m):
     out = ShardedGCN(plan.srow_ptr, plan.scol, plan.sval, n, ws, bs).forward(x)
     torch.cuda.synchronize()
     assert gu.digest(np.ascontiguousarray(out.cpu().numpy())) == fx["gcn_w32"]
+
+
+@pytest.mark.parametrize("name", list(gu.STRATS))
+@pytest.mark.parametrize("w", [8, 32])
+def test_cora_rates_cdf(m, cora, name, w):
+    """Per-row rates and their CDF (bench.cpp:124-138) on the device, bit-exact
+    vs the reference's outputs."""
+    n = cora["row_ptr"].size - 1
+    a = m.CsrMatrix(n, n, cora["row_ptr"], cora["col"], cora["val"])
+    ps = m.build_plan_set(a, w, getattr(m.Strategy, name.upper()))
+    per_row = m.sampling_rate_per_row(ps, a)
+    assert gu.digest(per_row) == cora[f"rate_per_row_{name}_{w}"]
+    want_r, want_f = cora[f"cdf_{name}_{w}_rate"], cora[f"cdf_{name}_{w}_frac"]
+    steps = m.cdf_stats(per_row)
+    assert np.array_equal(np.array([s[0] for s in steps]).view(np.uint64), want_r.view(np.uint64))
+    assert np.array_equal(np.array([s[1] for s in steps]).view(np.uint64), want_f.view(np.uint64))
+    r, f = m.sampling_rate_cdf(ps, a)  # per-row rates never leave the device
+    assert np.array_equal(r.view(np.uint64), want_r.view(np.uint64))
+    assert np.array_equal(f.view(np.uint64), want_f.view(np.uint64))
+
+
+@pytest.mark.parametrize("w", [16, 32, 64])
+def test_heavy_tail_cdf(m, w):
+    fx = gu.heavy()
+    n = fx["row_ptr"].size - 1
+    a = m.CsrMatrix(n, n, fx["row_ptr"], fx["col"], fx["val"])
+    r, f = m.sampling_rate_cdf(m.build_plan_set(a, w), a)
+    assert np.array_equal(r.view(np.uint64), fx[f"cdf_{w}_rate"].view(np.uint64))
+    assert np.array_equal(f.view(np.uint64), fx[f"cdf_{w}_frac"].view(np.uint64))
+
+
+def test_cdf_known_answers_and_errors(m):
+    assert m.cdf_stats([1.0, 1.0, 1.0]) == [(1.0, 1.0)]  # test_io_bench.cpp:177-187
+    assert m.cdf_stats([1.0, 0.5]) == [(0.5, 0.5), (1.0, 1.0)]
+    with pytest.raises(ValueError, match="rates must be nonempty"):
+        m.cdf_stats([])
+    # ties by == : +0 and -0 are one step; large random input vs the oracle port
+    from oracle import port
+    rng = np.random.default_rng(3)
+    x = np.round(rng.random(300_000) * 997) / 997
+    x[:1000] = -0.0
+    got = m.cdf_stats(x)
+    wr, wf = port.cdf_stats(x)
+    assert np.array_equal(np.array([s[0] for s in got]).view(np.uint64), wr.view(np.uint64))
+    assert np.array_equal(np.array([s[1] for s in got]).view(np.uint64), wf.view(np.uint64))
