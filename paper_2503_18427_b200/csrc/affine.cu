@@ -191,31 +191,35 @@ __global__ void dequant_affine_kernel(const uint8_t* __restrict__ q, uint64_t ro
 
 // ---------------------------------------------------------------- SpMM
 // Warp per 32-row group, one flattened slot stream.  Lane l owns codes
-// 4l..4l+3 of the 128-code column tile blockIdx.y.  Slot metadata of 32
-// slots is loaded by the 32 lanes (coalesced) and staged in shared memory as
-// {col, a = v*s_c, b = v*m_c} (ROW) or {col, v} (FEATURE) so every lane reads
-// a slot's metadata with one broadcast LDS.128; the code gathers of U slots
-// are issued before any is consumed.
+// 4l..4l+3 of the 128-code column tile blockIdx.y.  Slot metadata goes
+// through shared memory in batches of 32 slots as {col, a = v*s_col,
+// b = v*m_col} (ROW) or {col, v, v} (FEATURE): lane l loads slot t0+l's
+// (col, v) two batches ahead and its row params one batch ahead, so neither
+// dependent load is on the critical path.  The last batch is padded with
+// {col 0, a 0, b 0} slots (adds of +0, past every row end), so the inner
+// loop has no bounds tests; U code gathers are in flight before the first
+// is consumed.
 struct SlotMeta {
-    uint32_t col;
     float a;  // ROW: v * s_col   FEATURE: v
-    float b;  // ROW: v * m_col
-    float pad;
+    float b;  // ROW: v * m_col   FEATURE: v
+    uint32_t col;
+    uint32_t pad;
 };
 
 template <int MODE, int U, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32)
+__global__ void __launch_bounds__(WARPS * 32, 4)
 spmm_q8a_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
-                const float* __restrict__ sval, uint64_t n_rows, const uint8_t* __restrict__ q, uint64_t ldq,
+                const float* __restrict__ sval, uint64_t n_rows, const uint8_t* __restrict__ q, uint32_t ldq,
                 uint32_t f, const float2* __restrict__ params, float* __restrict__ c, uint64_t ldc) {
-    __shared__ __align__(16) SlotMeta s_meta[WARPS][32];
+    __shared__ __align__(16) SlotMeta s_meta[WARPS][64];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t r0 = ((uint64_t)blockIdx.x * WARPS + warp) * 32;
     if (r0 >= n_rows) return;
     const uint32_t nr = (uint32_t)min((uint64_t)32, n_rows - r0);
     const uint32_t col0 = blockIdx.y * 128 + 4 * lane;  // first code of this lane
     const uint32_t ne = col0 < f ? min(4u, f - col0) : 0u;  // codes this lane owns
-    const uint8_t* qb = q + col0;
+    // lanes past the row read (and ignore) the row's last 4 bytes: in bounds
+    const uint8_t* qb = q + min(col0, ldq - 4);
     float sj[4] = {0.f, 0.f, 0.f, 0.f}, mj[4] = {0.f, 0.f, 0.f, 0.f};
     if (MODE == 1)
         for (uint32_t u = 0; u < ne; ++u) {
@@ -229,7 +233,7 @@ spmm_q8a_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ 
     float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f, bsum = 0.f;
     uint32_t row = 0;
     uint32_t row_end = __shfl_sync(0xffffffffu, my_end, 0);
-    float* crow = c + r0 * ldc + col0;
+    float* cptr = c + r0 * ldc + col0;
 
     auto store_row = [&]() {
         float o0, o1, o2, o3;
@@ -239,14 +243,14 @@ spmm_q8a_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ 
             o0 = fmaf(sj[0], acc0, mj[0] * bsum); o1 = fmaf(sj[1], acc1, mj[1] * bsum);
             o2 = fmaf(sj[2], acc2, mj[2] * bsum); o3 = fmaf(sj[3], acc3, mj[3] * bsum);
         }
-        float* dst = crow + (uint64_t)row * ldc;
         if (ne == 4) {
-            __stcs(reinterpret_cast<float4*>(dst), make_float4(o0, o1, o2, o3));  // ldc % 4 == 0
+            __stcs(reinterpret_cast<float4*>(cptr), make_float4(o0, o1, o2, o3));  // ldc % 4 == 0
         } else {
-            if (ne > 0) dst[0] = o0;
-            if (ne > 1) dst[1] = o1;
-            if (ne > 2) dst[2] = o2;
+            if (ne > 0) cptr[0] = o0;
+            if (ne > 1) cptr[1] = o1;
+            if (ne > 2) cptr[2] = o2;
         }
+        cptr += ldc;
         acc0 = acc1 = acc2 = acc3 = bsum = 0.f;
     };
     auto advance = [&](uint32_t pos) {
@@ -256,7 +260,7 @@ spmm_q8a_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ 
             row_end = __shfl_sync(0xffffffffu, my_end, min(row, nr - 1));
         } while (row < nr && row_end == pos);
     };
-    if (total == 0 || row_end == 0) {
+    if (row_end == 0) {
         if (total == 0) {
             for (; row < nr; ++row) store_row();
             return;
@@ -264,64 +268,100 @@ spmm_q8a_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ 
         advance(0);
     }
 
-    for (uint32_t t0 = 0; t0 < total; t0 += 32) {
-        const uint32_t nb = min(32u, total - t0);
-        // stage this batch's metadata
-        __syncwarp();
-        if (lane < nb) {
-            const uint32_t cc = __ldcs(scol + g0 + t0 + lane);
-            const float v = __ldcs(sval + g0 + t0 + lane);
-            SlotMeta m;
-            m.col = cc;
-            if (MODE == 0) {
-                const float2 p = __ldg(params + cc);
-                m.a = v * p.x;
-                m.b = v * p.y;
-            } else {
-                m.a = v;
-                m.b = v;
-            }
-            m.pad = 0.f;
-            s_meta[warp][lane] = m;
+    // Metadata: a 64-entry ring per warp (two 32-slot batches).  Batch j
+    // lives in half j & 1; it is staged at the start of batch j - 1, from
+    // (col, v) loaded two batches ahead and row params one batch ahead.
+    // Code gathers: sub-batches of U slots, sub-batch s+1's loads issued
+    // before sub-batch s is consumed (U..2U gathers in flight per warp at
+    // every point of the stream, across batch and row boundaries).
+    auto load_cv = [&](uint32_t t0, uint32_t& cc, float& v) {
+        cc = 0;
+        v = 0.f;
+        if (t0 + lane < total) {
+            cc = __ldcs(scol + g0 + t0 + lane);
+            v = __ldcs(sval + g0 + t0 + lane);
         }
-        __syncwarp();
-        for (uint32_t k0 = 0; k0 < nb; k0 += U) {
-            uint32_t raw[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                raw[u] = 0;
-                if (k0 + u < nb && ne) {
-                    const uint32_t cc = s_meta[warp][k0 + u].col;
-                    raw[u] = __ldg(reinterpret_cast<const uint32_t*>(qb + (uint64_t)cc * ldq));
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                if (k0 + u < nb) {
-                    const float4 mm = *reinterpret_cast<const float4*>(&s_meta[warp][k0 + u]);
-                    const float a = mm.y;
-                    float q0, q1, q2, q3;
-                    decode4(raw[u], q0, q1, q2, q3);
-                    fma2(acc0, acc1, a, q0, q1);
-                    fma2(acc2, acc3, a, q2, q3);
-                    bsum += mm.z;
-                    const uint32_t pos = t0 + k0 + u + 1;
-                    if (pos == row_end) advance(pos);
-                }
-            }
+    };
+    auto stage = [&](uint32_t j, uint32_t cc, float v, float2 p) {
+        SlotMeta m;
+        m.col = cc;
+        m.a = MODE == 0 ? v * p.x : v;
+        m.b = MODE == 0 ? v * p.y : v;
+        m.pad = 0u;
+        s_meta[warp][(j & 1) * 32 + lane] = m;
+    };
+    uint32_t c1, c2;  // (col, v) of batches j+1 and j+2
+    float v1, v2;
+    float2 p1 = make_float2(0.f, 0.f);
+    {
+        uint32_t c0;
+        float v0;
+        load_cv(0, c0, v0);
+        load_cv(32, c1, v1);
+        load_cv(64, c2, v2);
+        float2 p0 = make_float2(0.f, 0.f);
+        if (MODE == 0) {
+            p0 = __ldg(params + c0);
+            p1 = __ldg(params + c1);
         }
+        stage(0, c0, v0, p0);
     }
-    for (; row < nr; ++row) store_row();  // rows after the last slot (empty tails)
+    __syncwarp();
+    const uint32_t n_sub = (total + U - 1) / U;
+    uint32_t raw[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+        raw[u] = __ldg(reinterpret_cast<const uint32_t*>(qb + (uint64_t)s_meta[warp][u].col * ldq));
+    for (uint32_t sb = 0; sb < n_sub; ++sb) {
+        const uint32_t p0 = sb * U;  // first slot of this sub-batch
+        if ((p0 & 31) == 0) {
+            // entering batch j = p0 / 32: stage batch j+1 (its half held
+            // batch j-1, consumed — the syncwarp below orders it), rotate
+            // the prefetches
+            const uint32_t j = p0 >> 5;
+            __syncwarp();  // every lane is done reading batch j-1's half
+            stage(j + 1, c1, v1, p1);
+            c1 = c2;
+            v1 = v2;
+            if (MODE == 0) p1 = __ldg(params + c1);
+            load_cv(p0 + 96, c2, v2);
+            __syncwarp();
+        }
+        // gathers of the next sub-batch (its metadata is staged: same or next batch)
+        uint32_t nxt[U];
+        const uint32_t pn = p0 + U;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            nxt[u] = __ldg(reinterpret_cast<const uint32_t*>(qb + (uint64_t)s_meta[warp][(pn + u) & 63].col * ldq));
+        const uint32_t base = p0 + 1;  // position after slot p0
+        uint32_t rel = row_end - base;  // the row ends after slot p0 + rel
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const float2 ab = *reinterpret_cast<const float2*>(&s_meta[warp][(p0 + u) & 63]);
+            float q0, q1, q2, q3;
+            decode4(raw[u], q0, q1, q2, q3);
+            fma2(acc0, acc1, ab.x, q0, q1);
+            fma2(acc2, acc3, ab.x, q2, q3);
+            bsum += ab.y;
+            if (rel == (uint32_t)u) {
+                advance(base + u);
+                rel = row_end - base;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) raw[u] = nxt[u];
+    }
+    for (; row < nr; ++row) store_row();  // (only rows after the last slot)
 }
 
 template <int MODE>
 int launch_q8a(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, const uint8_t* q,
                uint64_t ldq, uint64_t f, const float2* params, float* c, uint64_t ldc, cudaStream_t st) {
-    constexpr int kWarps = 8, kU = 16;
+    constexpr int kWarps = 8, kU = 8;
     const uint64_t groups = (n + 31) / 32;
     const dim3 grid((unsigned)((groups + kWarps - 1) / kWarps), (unsigned)((f + 127) / 128));
-    spmm_q8a_kernel<MODE, kU, kWarps><<<grid, kWarps * 32, 0, st>>>(srow, scol, sval, n, q, ldq, (uint32_t)f, params,
-                                                                    c, ldc);
+    spmm_q8a_kernel<MODE, kU, kWarps><<<grid, kWarps * 32, 0, st>>>(srow, scol, sval, n, q, (uint32_t)ldq,
+                                                                    (uint32_t)f, params, c, ldc);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
 }
@@ -392,7 +432,7 @@ int aes_dev_spmm_q8_affine(const uint64_t* srow_ptr, const uint32_t* scol, const
     if (n_rows == 0 || f == 0) return AES_OK;
     if (ldq % 4 || (uintptr_t)q % 4 || ldq < ((f + 3) & ~3ull) || ldc % 4 || (uintptr_t)c % 16 || ldc < f)
         return fail(AES_ERR_UNSUPPORTED, "affine spmm needs ldq % 4 == 0, ldc % 4 == 0, 16-B aligned C");
-    if (f > 0xffffffffull) return fail(AES_ERR_UNSUPPORTED, "F too large");
+    if (f > 0xffffffffull || ldq > 0xffffffffull) return fail(AES_ERR_UNSUPPORTED, "F too large");
     cudaStream_t st = as_stream(stream);
     const float2* p2 = reinterpret_cast<const float2*>(params);
     if (mode == AES_QAFFINE_ROW) return launch_q8a<0>(srow_ptr, scol, sval, n_rows, q, ldq, f, p2, c, ldc, st);

@@ -23,16 +23,6 @@ constexpr int kScanThreads = 256;
 constexpr int kScanIters = 8;                        // rows per thread per tile
 constexpr int kScanTile = kScanThreads * kScanIters; // 2048 rows per tile
 
-// tile state word: (value << 2) | flag ; flag 1 = aggregate, 2 = inclusive prefix
-__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
 // Row count of row r, with the row's offsets b = row_ptr[r], e = row_ptr[r+1]
 // already at hand (the tile stages row_ptr in shared memory).
 template <int KIND>
@@ -65,31 +55,27 @@ __device__ __forceinline__ uint64_t row_count(const ScanArgs& a, uint64_t r, uin
 // blocked per-thread reads (thread t: rows 8t..8t+7) spread over the banks
 __device__ __forceinline__ int pad_idx(int i) { return i + (i >> 4); }
 
-// One tile = 2048 rows.  The tile's row_ptr (2049 values) is staged in shared
-// memory with coalesced loads; thread t counts rows 8t..8t+7 (one thread-
-// serial prefix, ONE block scan per tile instead of one per 256 rows); warp 0
-// looks back over up to 32 predecessor tiles at a time; the inclusive
-// prefixes go back through shared memory so the srow_ptr stores are coalesced.
-template <int KIND>
-__global__ void __launch_bounds__(kScanThreads)
-row_scan_kernel(ScanArgs a, unsigned long long* tile_state, unsigned int* tile_counter) {
-    constexpr int kPadded = kScanTile + 1 + (kScanTile + 1) / 16 + 1;
-    __shared__ uint64_t s_rp[kPadded];
-    __shared__ uint64_t warp_tot[kScanThreads / 32];
-    __shared__ uint64_t s_excl;
-    __shared__ unsigned int s_tile;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+// Reduce-then-scan over 2048-row tiles, two kernels with no inter-CTA waits
+// (a decoupled look-back measured latency-bound here: ~1 200 tiles chained
+// through L2 round trips took 40 us for 39 MB).
+//   pass 1  tile totals: tile_tot[t] = sum of the tile's row counts
+//   pass 2  each tile sums the totals before it (<= a few thousand u64 from
+//           L2, a block reduction), scans its rows and writes srow_ptr
+// The tile's row_ptr (2049 values) is staged in shared memory with coalesced
+// loads; thread t owns rows 8t..8t+7 (one thread-serial prefix, one block
+// scan per tile); prefixes go back through shared memory so the srow_ptr
+// stores are coalesced.
+constexpr int kPadded = kScanTile + 1 + (kScanTile + 1) / 16 + 1;
 
-    if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
-    __syncthreads();
-    const uint64_t tile = s_tile;
-    const uint64_t base = tile * kScanTile;
-    const int nr = (int)min((uint64_t)kScanTile, a.n - base);
+template <int KIND>
+__device__ __forceinline__ uint64_t tile_counts(const ScanArgs& a, uint64_t base, int nr, uint64_t* s_rp,
+                                                uint64_t (&incl)[kScanIters], bool write_params) {
+    const int tid = threadIdx.x;
     if (KIND != kScanExplicit)
         for (int i = tid; i <= nr; i += kScanThreads) s_rp[pad_idx(i)] = a.row_ptr[base + i];
     __syncthreads();
-
-    uint64_t incl[kScanIters];
+    ScanArgs aa = a;
+    if (!write_params) aa.row_params = KIND == kScanExplicit ? a.row_params : nullptr;
     uint64_t run = 0;
 #pragma unroll
     for (int u = 0; u < kScanIters; ++u) {
@@ -98,13 +84,18 @@ row_scan_kernel(ScanArgs a, unsigned long long* tile_state, unsigned int* tile_c
         if (i < nr) {
             const uint64_t b = KIND != kScanExplicit ? s_rp[pad_idx(i)] : 0;
             const uint64_t e = KIND != kScanExplicit ? s_rp[pad_idx(i + 1)] : 0;
-            c = row_count<KIND>(a, base + i, b, e);
+            c = row_count<KIND>(aa, base + i, b, e);
         }
         run += c;
         incl[u] = run;
     }
-    // block exclusive scan of the per-thread totals
-    uint64_t v = run;
+    return run;
+}
+
+// block-wide exclusive scan of one u64 per thread; *total gets the sum
+__device__ __forceinline__ uint64_t block_excl_scan(uint64_t x, uint64_t* warp_tot, uint64_t* total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint64_t v = x;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint64_t t = __shfl_up_sync(0xffffffffu, v, o);
@@ -112,63 +103,52 @@ row_scan_kernel(ScanArgs a, unsigned long long* tile_state, unsigned int* tile_c
     }
     if (lane == 31) warp_tot[wid] = v;
     __syncthreads();
-    uint64_t woff = 0, tile_tot = 0;
+    uint64_t woff = 0, tot = 0;
 #pragma unroll
     for (int w = 0; w < kScanThreads / 32; ++w) {
-        const uint64_t x = warp_tot[w];
-        woff += (w < wid) ? x : 0;
-        tile_tot += x;
+        const uint64_t y = warp_tot[w];
+        woff += (w < wid) ? y : 0;
+        tot += y;
     }
-    const uint64_t thread_excl = woff + v - run;
+    *total = tot;
+    return woff + v - x;
+}
 
-    // publish the aggregate, look back (warp 0, 32 predecessors per step)
-    if (wid == 0) {
-        uint64_t excl = 0;
-        if (tile == 0) {
-            if (lane == 0) st_release(&tile_state[0], (tile_tot << 2) | 2ull);
-        } else {
-            if (lane == 0) st_release(&tile_state[tile], (tile_tot << 2) | 1ull);
-            // 128 predecessors per step (4 per lane, lane l at distances
-            // 4l+1 .. 4l+4): every first-wave tile publishes its aggregate at
-            // about the same time, so the walk length — not waiting — is what
-            // costs, one L2 round trip per step
-            int64_t hi = (int64_t)tile - 1;
-            while (true) {
-                unsigned long long st[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int64_t j = hi - (4 * lane + i);
-                    st[i] = 2ull;  // below tile 0: an empty inclusive prefix
-                    if (j >= 0) {
-                        do {
-                            st[i] = ld_acquire(&tile_state[j]);
-                        } while ((st[i] & 3ull) == 0);
-                    }
-                }
-                int first = 4;  // nearest inclusive prefix among this lane's four
-#pragma unroll
-                for (int i = 3; i >= 0; --i)
-                    if ((st[i] & 3ull) == 2ull) first = i;
-                const unsigned inc = __ballot_sync(0xffffffffu, first < 4);
-                const int stop = inc ? __ffs(inc) - 1 : 32;
-                uint64_t val = 0;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const bool take = lane < stop || (lane == stop && i <= first);
-                    if (take && hi - (4 * lane + i) >= 0) val += st[i] >> 2;
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
-                excl += val;
-                if (inc) break;
-                hi -= 128;
-            }
-            if (lane == 0) st_release(&tile_state[tile], ((excl + tile_tot) << 2) | 2ull);
-        }
-        if (lane == 0) s_excl = excl;
-    }
-    __syncthreads();  // s_excl visible; every s_rp read above is done
-    const uint64_t excl = s_excl + thread_excl;
+template <int KIND>
+__global__ void __launch_bounds__(kScanThreads)
+row_tile_total_kernel(ScanArgs a, unsigned long long* tile_tot) {
+    __shared__ uint64_t s_rp[kPadded];
+    __shared__ uint64_t warp_tot[kScanThreads / 32];
+    const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
+    const int nr = (int)min((uint64_t)kScanTile, a.n - base);
+    uint64_t incl[kScanIters];
+    const uint64_t run = tile_counts<KIND>(a, base, nr, s_rp, incl, false);
+    uint64_t tot;
+    block_excl_scan(run, warp_tot, &tot);
+    if (threadIdx.x == 0) tile_tot[blockIdx.x] = tot;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kScanThreads)
+row_scan_kernel(ScanArgs a, const unsigned long long* __restrict__ tile_tot) {
+    __shared__ uint64_t s_rp[kPadded];
+    __shared__ uint64_t warp_tot[kScanThreads / 32];
+    __shared__ uint64_t s_excl;
+    const int tid = threadIdx.x;
+    const uint64_t tile = blockIdx.x;
+    const uint64_t base = tile * kScanTile;
+    const int nr = (int)min((uint64_t)kScanTile, a.n - base);
+    // exclusive offset of this tile: the totals of every tile before it
+    uint64_t pre = 0;
+    for (uint64_t t = tid; t < tile; t += kScanThreads) pre += tile_tot[t];
+    uint64_t incl[kScanIters];
+    const uint64_t run = tile_counts<KIND>(a, base, nr, s_rp, incl, true);
+    uint64_t pre_tot, tile_sum;
+    block_excl_scan(pre, warp_tot, &pre_tot);
+    __syncthreads();  // warp_tot reused
+    const uint64_t thread_excl = block_excl_scan(run, warp_tot, &tile_sum);
+    const uint64_t excl = pre_tot + thread_excl;
+    __syncthreads();  // every s_rp read is done
 #pragma unroll
     for (int u = 0; u < kScanIters; ++u) s_rp[pad_idx(tid * kScanIters + u)] = excl + incl[u];
     __syncthreads();
@@ -191,22 +171,24 @@ int launch_row_scan(int kind, const ScanArgs& a, void* ws, size_t ws_bytes, cuda
         AES_CUDA_TRY(cudaMemsetAsync(a.out, 0, sizeof(uint64_t), st));
         return AES_OK;
     }
-    uint64_t tiles = (a.n + kScanTile - 1) / kScanTile;
-    AES_CUDA_TRY(cudaMemsetAsync(ws, 0, need, st));
-    auto* counter = static_cast<unsigned int*>(ws);
-    auto* state = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 256);
+    const unsigned tiles = (unsigned)((a.n + kScanTile - 1) / kScanTile);
+    auto* tot = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 256);
     switch (kind) {
         case kScanSlots:
-            row_scan_kernel<kScanSlots><<<(unsigned)tiles, kScanThreads, 0, st>>>(a, state, counter);
+            row_tile_total_kernel<kScanSlots><<<tiles, kScanThreads, 0, st>>>(a, tot);
+            row_scan_kernel<kScanSlots><<<tiles, kScanThreads, 0, st>>>(a, tot);
             break;
         case kScanStarts:
-            row_scan_kernel<kScanStarts><<<(unsigned)tiles, kScanThreads, 0, st>>>(a, state, counter);
+            row_tile_total_kernel<kScanStarts><<<tiles, kScanThreads, 0, st>>>(a, tot);
+            row_scan_kernel<kScanStarts><<<tiles, kScanThreads, 0, st>>>(a, tot);
             break;
         case kScanExplicit:
-            row_scan_kernel<kScanExplicit><<<(unsigned)tiles, kScanThreads, 0, st>>>(a, state, counter);
+            row_tile_total_kernel<kScanExplicit><<<tiles, kScanThreads, 0, st>>>(a, tot);
+            row_scan_kernel<kScanExplicit><<<tiles, kScanThreads, 0, st>>>(a, tot);
             break;
         default:
-            row_scan_kernel<kScanGcnNnz><<<(unsigned)tiles, kScanThreads, 0, st>>>(a, state, counter);
+            row_tile_total_kernel<kScanGcnNnz><<<tiles, kScanThreads, 0, st>>>(a, tot);
+            row_scan_kernel<kScanGcnNnz><<<tiles, kScanThreads, 0, st>>>(a, tot);
             break;
     }
     AES_CUDA_TRY(cudaGetLastError());
@@ -244,31 +226,37 @@ struct FillRow {
 // hashed start needs at most a 32-bit modulo: s*1429 < 32*1429, and
 // hash_start is s*1429 itself whenever the modulus exceeds it.  CTAs whose
 // slots exceed the map (W > 32, FULL) run several passes.
-__global__ void __launch_bounds__(kFillRows)
+__global__ void __launch_bounds__(kFillRows, 6)
 sample_fill_kernel(const uint64_t* __restrict__ plan_row_ptr, const uint64_t* __restrict__ row_ptr,
                    const uint32_t* __restrict__ col_ind, const float* __restrict__ val,
                    uint64_t n, uint32_t width, int strategy, const uint64_t* __restrict__ srow_ptr,
                    uint32_t* __restrict__ scol, float* __restrict__ sval) {
     __shared__ FillRow s_row[kFillRows];
     __shared__ unsigned char s_map[kFillMap];
-    __shared__ uint64_t s_g0, s_total;
+    __shared__ uint64_t s_first[kFillRows + 1];
     const int tid = threadIdx.x;
     const uint64_t r0 = (uint64_t)blockIdx.x * kFillRows;
     const int nr = (int)min((uint64_t)kFillRows, n - r0);
-    if (tid == 0) {
-        s_g0 = srow_ptr[r0];
-        s_total = srow_ptr[r0 + nr] - s_g0;
-    }
-    __syncthreads();
-    const uint64_t g0 = s_g0, total = s_total;
-    uint32_t my_first = 0, my_slots = 0;
+    // one round of independent loads per row (no dependent load chain before
+    // the map is built): sampled offsets, plan row length, source row start
+    uint64_t my_s0 = 0, my_nnz = 0, my_src = 0;
     if (tid < nr) {
         const uint64_t r = r0 + tid;
-        const uint64_t nnz = plan_row_ptr[r + 1] - plan_row_ptr[r];
+        my_s0 = srow_ptr[r];
+        my_nnz = plan_row_ptr[r + 1] - plan_row_ptr[r];
+        my_src = row_ptr[r];
+        s_first[tid] = my_s0;
+        if (tid == nr - 1) s_first[nr] = srow_ptr[r + 1];
+    }
+    __syncthreads();
+    const uint64_t g0 = s_first[0], total = s_first[nr] - g0;
+    uint32_t my_first = 0, my_slots = 0;
+    if (tid < nr) {
+        const uint64_t nnz = my_nnz;
         const RowParams p = row_params(nnz, width, strategy);
         FillRow fr;
-        fr.src = row_ptr[r];
-        my_first = (uint32_t)(srow_ptr[r] - g0);
+        fr.src = my_src;
+        my_first = (uint32_t)(my_s0 - g0);
         my_slots = p.chunk * p.cnt;
         fr.first = my_first;
         fr.cnt = p.cnt;

@@ -1055,9 +1055,10 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
     float4 acc = f4_zero();
     uint32_t row = 0;
     uint32_t row_end = lds_u32(ends0);
-    auto store_row = [&](uint32_t r) {
-        // row index and stride fit 32 bits (u32 column indices bound n_rows)
-        if (FULL || lane < f4) __stcs(c + (uint64_t)((uint32_t)r0 + r) * (uint32_t)ldc4 + lane, acc);
+    float4* cptr = c + r0 * ldc4 + lane;  // rows are stored in order: a running pointer
+    auto store_row = [&](uint32_t) {
+        if (FULL || lane < f4) __stcs(cptr, acc);
+        cptr += ldc4;
         acc = f4_zero();
     };
     auto advance_rows = [&](uint32_t pos) {
@@ -1096,11 +1097,15 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
 #pragma unroll
                 for (int u = 0; u < 4; ++u) consume(4 * b + u, vv[u]);
             } else {
+                const uint32_t base = t0 + 4 * b + 1;  // position after this batch's first slot
+                uint32_t rel = row_end - base;           // the row ends after slot 4b + rel
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const int p = 4 * b + u;
-                    consume(p, vv[u]);
-                    if (t0 + p + 1 == row_end) advance_rows(t0 + p + 1);
+                    consume(4 * b + u, vv[u]);
+                    if (rel == (uint32_t)u) {
+                        advance_rows(base + u);
+                        rel = row_end - base;
+                    }
                 }
             }
             __syncwarp();  // every lane is done reading these holes
@@ -1170,8 +1175,10 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
     uint32_t ri = 0;  // next row to store (relative to rb)
     uint32_t wi = 0;  // its index in the window
     uint32_t row_end = lds_u32(ends0);
+    float4* cptr = crow;  // rows are stored in order: a running pointer
     auto store_row = [&]() {
-        if (FULL || lane < f4) __stcs(crow + (uint64_t)ri * (uint32_t)ldc4, acc);
+        if (FULL || lane < f4) __stcs(cptr, acc);
+        cptr += ldc4;
         acc = f4_zero();
     };
     auto advance_rows = [&](uint32_t pos) {
@@ -1217,11 +1224,15 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
 #pragma unroll
                 for (int u = 0; u < 4; ++u) consume(4 * b + u, vv[u]);
             } else {
+                const uint32_t base = t0 + 4 * b + 1;  // position after this batch's first slot
+                uint32_t rel = row_end - base;           // the row ends after slot 4b + rel
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const int p = 4 * b + u;
-                    consume(p, vv[u]);
-                    if (t0 + p + 1 == row_end) advance_rows(t0 + p + 1);
+                    consume(4 * b + u, vv[u]);
+                    if (rel == (uint32_t)u) {
+                        advance_rows(base + u);
+                        rel = row_end - base;
+                    }
                 }
             }
             __syncwarp();  // every lane is done reading these holes
@@ -1322,7 +1333,11 @@ int launch_q8_batch_t(const uint64_t* srow, const uint32_t* scol, const float* s
         // whole waves: the tiles share the resident CTA slots (rounding up
         // would leave one CTA for a second, nearly empty wave)
         const uint64_t per_wave = (uint64_t)num_sms() * occ / tiles;
-        const uint64_t per_tile = (per_wave ? per_wave : 1) * bal_waves(n, per_wave * WARPS, 0);
+        uint64_t per_tile = (per_wave ? per_wave : 1) * bal_waves(n, per_wave * WARPS, 0);
+        // small graphs (pubmed: 20 k rows): at least 8 rows per warp, so the
+        // 64 KB LUT fill of a CTA is not paid for a handful of slots
+        const uint64_t cap = (n + (uint64_t)WARPS * 8 - 1) / ((uint64_t)WARPS * 8);
+        if (cap < per_tile) per_tile = cap ? cap : 1;
         spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 2><<<dim3((unsigned)per_tile, tiles), WARPS * 32, smem, st>>>(
             srow, scol, sval, n, q, (uint32_t)ldq, f4, c, ldc4, lut, 32, 0, nullptr);
         AES_CUDA_TRY(cudaGetLastError());
