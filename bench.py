@@ -311,6 +311,8 @@ def run_ours(args):
     from paper_2503_18427_b200 import capi, device
     synth = load_synth()
     capi.check(capi.lib().aes_dev_spmm_set_schedule(args.sched))
+    capi.lib().aes_dev_spmm_set_variant.argtypes = [ctypes.c_int]
+    capi.check(capi.lib().aes_dev_spmm_set_variant(args.variant))
 
     n, alpha, maxdeg, f = SHAPES[args.config]
     rp, col, val = synth.power_law_csr(n, alpha, maxdeg, seed=args.seed, device="cuda")
@@ -768,6 +770,8 @@ def main():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--sched", type=int, default=0,
                     help="SpMM row schedule (aes_dev_spmm_set_schedule; 0 = library default)")
+    ap.add_argument("--variant", type=int, default=0,
+                    help="SpMM kernel variant (aes_dev_spmm_set_variant; 0 = library default, tuning only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-layer", action="store_true", help="skip the GCN layer (SpMM+GEMM+exchange) timing")

@@ -354,6 +354,217 @@ spmm_q8a_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ 
     for (; row < nr; ++row) store_row();  // (only rows after the last slot)
 }
 
+// ---------------------------------------------------------------- ring kernel
+// The default fast-mode SpMM: the cp.async ring schedule of the exact int8
+// batch kernel (spmm.cu) — one warp per 32-row group, one slot stream, the
+// gathers four slots per 16-B LDGSTS (lane (g, j) copies bytes 16j.. of slot
+// g), slot metadata two ring rounds ahead — with the table decode replaced by
+// the affine one: no 64 KB table per CTA, no table reads (4 of the ~7 shared
+// wavefronts per slot of the exact kernel), and 8 instead of 14 decode /
+// accumulate instructions per slot.  ROW mode stages each gathered row's
+// (s, m) next to the metadata, one round ahead of its use.
+constexpr int kRC = 16;            // ring slots per warp
+constexpr int kRB = kRC / 4;       // 4-slot batches per round
+constexpr uint32_t kREnds = 160;   // 33 row ends (padded)
+
+template <int MODE, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 3)
+spmm_q8r_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
+                const float* __restrict__ sval, uint64_t n_rows, const uint8_t* __restrict__ q, uint32_t ldq,
+                uint32_t f, const float2* __restrict__ params, float4* __restrict__ c, uint64_t ldc4) {
+    // per warp: ring kRC x 128 B | meta 4 rounds x (kRC cols + kRC vals) | row params 4 rounds x kRC x 8 B | ends
+    constexpr uint32_t kRing = kRC * 128, kMeta = 4 * 8 * kRC, kPar = MODE == 0 ? 4 * 8 * kRC : 0;
+    constexpr uint32_t kPerWarp = kRing + kMeta + kPar + kREnds;
+    extern __shared__ __align__(16) unsigned char rsm[];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(rsm) + warp * kPerWarp;
+    const uint32_t ring0 = base, meta0 = base + kRing, par0 = meta0 + kMeta, ends0 = par0 + kPar;
+    const uint32_t tile = blockIdx.y;
+    q += (size_t)tile * 128;
+    const uint32_t col0 = tile * 128 + 4 * lane;
+    const uint32_t f4 = min(32u, (f + 3) / 4 - tile * 32);
+    const bool st_ok = lane < f4;
+    uint32_t nb = 16;  // bytes this lane copies per gathered row (partial last tile)
+    {
+        const uint32_t rowb = min(128u, f - tile * 128), j16 = (lane & 7) * 16;
+        nb = rowb > j16 ? min(16u, rowb - j16) : 0u;
+    }
+    float sj[4] = {0.f, 0.f, 0.f, 0.f}, mj[4] = {0.f, 0.f, 0.f, 0.f};
+    if (MODE == 1)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (col0 + u < f) {
+                const float2 p = params[col0 + u];
+                sj[u] = p.x;
+                mj[u] = p.y;
+            }
+    const uint64_t r0 = ((uint64_t)blockIdx.x * WARPS + warp) * 32;
+    if (r0 >= n_rows) return;
+    const uint32_t nr = (uint32_t)min((uint64_t)32, n_rows - r0);
+    const uint64_t g0 = srow[r0];
+    const uint64_t my_end = srow[r0 + 1 + min(lane, nr - 1)];
+    const uint32_t total = (uint32_t)(__shfl_sync(0xffffffffu, my_end, nr - 1) - g0);
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(ends0 + lane * 4), "r"((uint32_t)(my_end - g0)) : "memory");
+    if (lane == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(ends0 + 128), "r"(total) : "memory");
+
+    auto issue_meta = [&](uint32_t k) {  // round k -> buffer k & 3 (lanes 0..15 cols, 16..31 vals)
+        const uint32_t i = lane & 15, s = k * kRC + i;
+        if (s < total) {
+            const void* src = lane < 16 ? (const void*)(scol + g0 + s) : (const void*)(sval + g0 + s);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(meta0 + (k & 3) * (8 * kRC) +
+                                                                           (lane >> 4) * (4 * kRC) + i * 4),
+                         "l"(src)
+                         : "memory");
+        }
+    };
+    auto issue_par = [&](uint32_t k) {  // ROW: (s, m) of round k's gathered rows -> buffer k & 3
+        if (MODE == 0 && lane < (uint32_t)kRC && k * kRC + lane < total) {
+            uint32_t cc;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cc) : "r"(meta0 + (k & 3) * (8 * kRC) + lane * 4));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(par0 + (k & 3) * (8 * kRC) + lane * 8),
+                         "l"(params + cc)
+                         : "memory");
+        }
+    };
+    auto issue = [&](int p0, uint32_t k) {  // gathers for ring positions p0..p0+3 of round k
+        const uint32_t t = k * kRC + p0 + (lane >> 3);
+        if (t < total && nb) {
+            uint32_t cc;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cc) : "r"(meta0 + (k & 3) * (8 * kRC) + (p0 + (lane >> 3)) * 4));
+            const unsigned char* src = q + (uint64_t)cc * ldq + (lane & 7) * 16;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(ring0 + (p0 + (lane >> 3)) * 128 +
+                                                                                 (lane & 7) * 16),
+                         "l"(src), "r"(nb)
+                         : "memory");
+        }
+    };
+    issue_meta(0);
+    issue_meta(1);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncwarp();
+    issue_par(0);
+#pragma unroll
+    for (int b = 0; b < kRB; ++b) {
+        issue(4 * b, 0);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, bs = 0.f;
+    uint32_t row = 0, row_end;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(row_end) : "r"(ends0));
+    float4* cptr = c + r0 * ldc4 + tile * 32 + lane;
+    auto store_row = [&]() {
+        if (st_ok) {
+            float4 o;
+            if (MODE == 0)
+                o = make_float4(a0 + bs, a1 + bs, a2 + bs, a3 + bs);
+            else
+                o = make_float4(fmaf(sj[0], a0, mj[0] * bs), fmaf(sj[1], a1, mj[1] * bs), fmaf(sj[2], a2, mj[2] * bs),
+                                fmaf(sj[3], a3, mj[3] * bs));
+            __stcs(cptr, o);
+        }
+        cptr += ldc4;
+        a0 = a1 = a2 = a3 = bs = 0.f;
+    };
+    auto advance_rows = [&](uint32_t pos) {
+        do {
+            store_row();
+            ++row;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(row_end) : "r"(ends0 + row * 4));
+        } while (row < nr && row_end == pos);
+    };
+    if (row_end == 0) advance_rows(0);
+    const uint32_t rd0 = ring0 + lane * 4;
+    auto consume = [&](int p, float a, float b) {
+        uint32_t r;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(rd0 + p * 128));
+        float q0 = __uint_as_float(__byte_perm(r, 0x4B000000u, 0x7650));
+        float q1 = __uint_as_float(__byte_perm(r, 0x4B000000u, 0x7651));
+        float q2 = __uint_as_float(__byte_perm(r, 0x4B000000u, 0x7652));
+        float q3 = __uint_as_float(__byte_perm(r, 0x4B000000u, 0x7653));
+        add2_rn(q0, q1, -kTwo23, -kTwo23);
+        add2_rn(q2, q3, -kTwo23, -kTwo23);
+        fma2(a0, a1, a, q0, q1);
+        fma2(a2, a3, a, q2, q3);
+        bs += b;
+    };
+
+    // every round consumes all kRC positions; past `total` (last round only)
+    // garbage accumulates after the last row was stored and is never written
+    for (uint32_t k = 0, t0 = 0; t0 < total; t0 += kRC, ++k) {
+#pragma unroll
+        for (int b = 0; b < kRB; ++b) {
+            asm volatile("cp.async.wait_group %0;\n" ::"n"(kRB - 1) : "memory");
+            __syncwarp();
+            float4 v4;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(v4.x), "=f"(v4.y), "=f"(v4.z), "=f"(v4.w)
+                         : "r"(meta0 + (k & 3) * (8 * kRC) + 4 * kRC + 16 * b));
+            float av[4] = {v4.x, v4.y, v4.z, v4.w}, bv[4] = {v4.x, v4.y, v4.z, v4.w};
+            if (MODE == 0) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    float2 sm;
+                    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(sm.x), "=f"(sm.y)
+                                 : "r"(par0 + (k & 3) * (8 * kRC) + (4 * b + u) * 8));
+                    bv[u] = av[u] * sm.y;
+                    av[u] = av[u] * sm.x;
+                }
+            }
+            if (row_end > t0 + 4 * b + 4) {  // no row ends in this batch
+#pragma unroll
+                for (int u = 0; u < 4; ++u) consume(4 * b + u, av[u], bv[u]);
+            } else {
+                const uint32_t pb = t0 + 4 * b + 1;
+                uint32_t rel = row_end - pb;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    consume(4 * b + u, av[u], bv[u]);
+                    if (rel == (uint32_t)u) {
+                        advance_rows(pb + u);
+                        rel = row_end - pb;
+                    }
+                }
+            }
+            __syncwarp();  // every lane is done reading these ring slots
+            if (b == 0) {
+                issue_meta(k + 2);
+                issue_par(k + 1);  // round k+1's metadata landed with the wait above
+            }
+            issue(4 * b, k + 1);
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
+        }
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    while (row < nr) {
+        store_row();
+        ++row;
+    }
+}
+
+template <int MODE>
+int launch_q8r(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, const uint8_t* q,
+               uint64_t ldq, uint64_t f, const float2* params, float* c, uint64_t ldc, cudaStream_t st) {
+    constexpr int kWarps = 16;
+    constexpr uint32_t kPerWarp = kRC * 128 + 4 * 8 * kRC + (MODE == 0 ? 4 * 8 * kRC : 0) + kREnds;
+    const size_t smem = (size_t)kWarps * kPerWarp;
+    static bool attr_dev[kMaxDevices] = {};
+    bool& attr = attr_dev[cur_device()];
+    if (!attr) {
+        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_q8r_kernel<MODE, kWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+        attr = true;
+    }
+    const uint64_t groups = (n + 31) / 32;
+    const dim3 grid((unsigned)((groups + kWarps - 1) / kWarps), (unsigned)((f + 127) / 128));
+    spmm_q8r_kernel<MODE, kWarps><<<grid, kWarps * 32, smem, st>>>(srow, scol, sval, n, q, (uint32_t)ldq,
+                                                                   (uint32_t)f, params, reinterpret_cast<float4*>(c),
+                                                                   ldc / 4);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
 template <int MODE>
 int launch_q8a(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, const uint8_t* q,
                uint64_t ldq, uint64_t f, const float2* params, float* c, uint64_t ldc, cudaStream_t st) {
@@ -367,6 +578,11 @@ int launch_q8a(const uint64_t* srow, const uint32_t* scol, const float* sval, ui
 }
 
 }  // namespace
+
+int launch_spmm_q8_tma(int dec, const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n,
+                       const uint8_t* q, uint64_t ldq, uint64_t f, const float* lut, const float* fparams, float* c,
+                       uint64_t ldc, cudaStream_t st);  // spmm_tma.cu
+int spmm_variant();                                     // spmm.cu
 }  // namespace aes
 
 extern "C" {
@@ -435,6 +651,17 @@ int aes_dev_spmm_q8_affine(const uint64_t* srow_ptr, const uint32_t* scol, const
     if (f > 0xffffffffull || ldq > 0xffffffffull) return fail(AES_ERR_UNSUPPORTED, "F too large");
     cudaStream_t st = as_stream(stream);
     const float2* p2 = reinterpret_cast<const float2*>(params);
+    const int v = spmm_variant();
+    // tuning variants: 51 the TMA-gather kernel (FEATURE), 50 the register-pipelined one
+    if (v == 51 && mode == AES_QAFFINE_FEATURE) {
+        const int s = launch_spmm_q8_tma(1, srow_ptr, scol, sval, n_rows, q, ldq, f, nullptr, params, c, ldc, st);
+        if (s != AES_ERR_UNSUPPORTED) return s;
+    }
+    // default: the cp.async ring kernel (16-B code rows, 16-B aligned C)
+    if (v != 50 && ldq % 16 == 0 && (uintptr_t)q % 16 == 0 && n_rows < (1ull << 31)) {
+        if (mode == AES_QAFFINE_ROW) return launch_q8r<0>(srow_ptr, scol, sval, n_rows, q, ldq, f, p2, c, ldc, st);
+        return launch_q8r<1>(srow_ptr, scol, sval, n_rows, q, ldq, f, p2, c, ldc, st);
+    }
     if (mode == AES_QAFFINE_ROW) return launch_q8a<0>(srow_ptr, scol, sval, n_rows, q, ldq, f, p2, c, ldc, st);
     return launch_q8a<1>(srow_ptr, scol, sval, n_rows, q, ldq, f, p2, c, ldc, st);
 }

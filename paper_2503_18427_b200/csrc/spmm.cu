@@ -1246,9 +1246,9 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
     __syncwarp();  // the next range reuses this warp's ring, metadata and row ends
   };
 
-    if (SCHED == 0) {
-        const uint64_t r0 = ((uint64_t)blockIdx.x * WARPS + warp) * group_rows;
-        if (r0 < n_rows) run_group32(r0);
+    if (SCHED == 0) {  // 32-row groups, grid-stride (persistent CTAs fill the 64 KB table once)
+        for (uint64_t gi = (uint64_t)blockIdx.x * WARPS + warp; gi < groups; gi += (uint64_t)gridDim.x * WARPS)
+            run_group32(gi * group_rows);
         return;
     }
     if (SCHED == 2) {  // balanced persistent: this warp's slot-balanced row range
@@ -1358,7 +1358,11 @@ int launch_q8_batch_t(const uint64_t* srow, const uint32_t* scol, const float* s
         AES_CUDA_TRY(cudaFreeAsync(ws, st));
         return AES_OK;
     }
-    spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 0><<<dim3(gx, tiles), WARPS * 32, smem, st>>>(
+    // static: persistent, one wave of resident CTAs per column tile walking the groups
+    uint64_t gs = (uint64_t)num_sms() * occ / tiles;
+    if (gs == 0) gs = 1;
+    const unsigned gxs = (unsigned)(gx < gs ? gx : gs);
+    spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 0><<<dim3(gxs, tiles), WARPS * 32, smem, st>>>(
         srow, scol, sval, n, q, (uint32_t)ldq, f4, c, ldc4, lut, gr, groups, nullptr);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
@@ -1553,6 +1557,11 @@ int launch_vector(const uint64_t* srow, const uint32_t* scol, const float* sval,
 }
 
 }  // namespace
+
+int launch_spmm_q8_tma(int dec, const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n,
+                       const uint8_t* q, uint64_t ldq, uint64_t f, const float* lut, const float* fparams, float* c,
+                       uint64_t ldc, cudaStream_t st);  // spmm_tma.cu
+int spmm_variant() { return g_spmm_variant; }  // read by affine.cu (tuning variants 50, 51)
 }  // namespace aes
 
 extern "C" {
@@ -1633,7 +1642,16 @@ int aes_dev_spmm_q8_ex(const uint64_t* srow_ptr, const uint32_t* scol, const flo
     // batch kernel (variants 30-37; the default for F > 64 with 16-B aligned
     // code rows).  Wider rows run as 128-code column tiles (grid.y): every
     // tile re-reads only the 8-B slot metadata next to its 128-B gathers.
-    if ((v == 0 || v >= 30) && f4 > 16 && ldq % 16 == 0 && (uintptr_t)q % 16 == 0 && f4 / 32 < 65535) {
+    // TMA-gather kernel (spmm_tma.cu), variant 40 only: it moves the code
+    // rows off the LSU (l1tex 88 -> 72 %) but issues more instructions than it
+    // saves (562 M vs 460 M per products launch, the elected-lane TMA issue
+    // converts its operands to uniform registers), 0.655 vs 0.566 ms
+    if (v == 40 && f4 > 16) {
+        const int s = launch_spmm_q8_tma(0, srow_ptr, scol, sval, n_rows, q, ldq, f, lut, nullptr, c, ldc, st);
+        if (s != AES_ERR_UNSUPPORTED) return s;
+    }
+    if ((v == 0 || (v >= 30 && v <= 40)) && f4 > 16 && ldq % 16 == 0 && (uintptr_t)q % 16 == 0 &&
+        f4 / 32 < 65535) {
         float4* c4 = reinterpret_cast<float4*>(c);
         const uint32_t f4u = (uint32_t)f4;
         switch (v) {

@@ -1,0 +1,11 @@
+cd ${GRAFT_REPO_ROOT:-.}
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
+for cfg in products reddit pubmed arxiv; do for dt in int8 int8-feature int8-row f32; do
+  timeout 300 python bench.py --config $cfg --dtype $dt --no-cpu-baseline --no-e2e --no-layer --steps 20 --warmup 5 > /tmp/b.json 2>/tmp/b.err; python -c "import json;d=json.load(open('/tmp/b.json'));print('$cfg $dt', d['ms_per_step'], d['roofline']['frac'])" 2>/dev/null || tail -3 /tmp/b.err
+done; done
+bash scripts/ncu_capture.sh q8r "spmm_q8r" 2 1 -- python bench.py --dtype int8-feature --steps 2 --warmup 2 --no-e2e --no-cpu-baseline --no-layer
+bash scripts/ncu_capture.sh q8rr "spmm_q8r" 2 1 -- python bench.py --dtype int8-row --steps 2 --warmup 2 --no-e2e --no-cpu-baseline --no-layer
+bash scripts/ncu_capture.sh q8b2 "spmm_q8_batch" 2 1 -- python bench.py --dtype int8 --steps 2 --warmup 2 --no-e2e --no-cpu-baseline --no-layer
+bash scripts/sanitize.sh
+du -sh gpurun_out
