@@ -311,8 +311,10 @@ AES_API int aes_dev_spmm_set_variant(int variant);
  * group w), 2 = heavy-first dynamic (groups with > 4096 slots first, then
  * the rest, by ticket from one counter), 3 = balanced persistent (one wave of
  * resident warps, each owning a contiguous row range with an equal share of
- * slots + rows), 0 = auto (balanced).  Results are bit-identical under every
- * schedule (each row group is one warp's ordered stream). */
+ * slots + rows), 0 = auto (balanced), 6 = int8 batch kernel only: static
+ * 32-row groups walked grid-stride by one persistent wave (tuning).  Results
+ * are bit-identical under every schedule (each row group is one warp's
+ * ordered stream). */
 AES_API int aes_dev_spmm_set_schedule(int schedule);
 
 /* Int8 variant: Q is u8 codes (ldq bytes per row), lut[256] the exact

@@ -230,6 +230,12 @@ __device__ __forceinline__ uint32_t pin_u32(uint32_t x) {
     asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
     return y;
 }
+template <class T>
+__device__ __forceinline__ T* pin_ptr(T* p) {
+    uint64_t y;
+    asm volatile("mov.b64 %0, %1;" : "=l"(y) : "l"(reinterpret_cast<uint64_t>(p)));
+    return reinterpret_cast<T*>(y);
+}
 // Offset of the dynamic shared-memory window inside the CTA's shared window
 // on sm_100a (1 KB reserved; the SASS of cvta.shared is (CgaCtaId<<24)+0x400).
 constexpr uint32_t kDynSmemOffset = 0x400;
@@ -485,6 +491,7 @@ constexpr uint32_t kHeavySlots = 4096;
 constexpr int kSchedStatic = 1, kSchedDyn = 2, kSchedBal = 3;
 constexpr int kSchedBalOne = 4;  // balanced, one wave (rows of unknown length: hub rows stay spread)
 constexpr int kSchedAuto = 5;    // bounded rows, per-kernel choice (see the launchers)
+constexpr int kSchedStaticPersist = 6;  // int8 batch kernel: persistent grid-stride 32-row groups (tuning only)
 struct DynSched {
     unsigned int next;     // ticket counter
     unsigned int n_heavy;  // heavy groups listed
@@ -961,12 +968,17 @@ template <int C, int WARPS, bool FULL, bool FASTB, int SCHED>  // SCHED: 0 stati
 // tile form (F % 128 != 0, e.g. reddit's 602) runs faster at 2 CTAs with room
 // for 64 registers (reddit int8 0.64 -> 0.59 ms; products, whole tiles, loses
 // 4-20 % that way)
-__global__ void __launch_bounds__(WARPS * 32, FULL ? 3 : 2)
+__global__ void __launch_bounds__(WARPS * 32, WARPS >= 32 ? 1 : FULL ? 3 : 2)
 spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
                      const float* __restrict__ sval, uint64_t n_rows, const unsigned char* __restrict__ q,
                      uint32_t ldq, uint32_t f4, float4* __restrict__ c, uint64_t ldc4,
                      const float* __restrict__ lut_g, uint32_t group_rows, uint64_t groups, DynSched* ws) {
-    static_assert(C % 4 == 0 && C >= 8 && C <= 16 && C * WARPS <= 256, "the rings live in the LUT's 256 holes");
+    static_assert(C % 4 == 0 && C >= 8 && C <= 16 && WARPS <= 32, "ring shape");
+    // rings in the LUT's 256 holes (256-B stride) while they fit, else in
+    // their own region after the row ends (128-B stride; one 32-warp CTA per
+    // SM with room for 64 registers)
+    constexpr bool kSep = C * WARPS > 256;
+    constexpr uint32_t RS = kSep ? 128 : 256;
     constexpr int B = C / 4;  // batches per ring round
     constexpr uint32_t kEndsBytes = 144;  // 33 row ends per warp
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -987,13 +999,18 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
     const uint32_t lane4 = pin_u32((smem0 & 0xFF000000u) | (lane * 4));
     // ring slot p of this warp: hole warp*C + p; lane reads its 4 codes at
     // rd0 + p*256 and copies its 16 B of batch slot p0 + lane/8 to wr0 + p0*256
-    const uint32_t rd0 = pin_u32(smem0 + warp * (C * 256) + 128 + lane * 4);
-    const uint32_t wr0 = smem0 + warp * (C * 256) + 128 + (lane >> 3) * 256 + (lane & 7) * 16;
+    const uint32_t ring0 = kSep ? smem0 + 65536 + WARPS * (32 * C + kEndsBytes) + warp * (C * 128)
+                                : smem0 + warp * (C * 256) + 128;
+    const uint32_t rd0 = pin_u32(ring0 + lane * 4);
+    const uint32_t wr0 = pin_u32(ring0 + (lane >> 3) * RS + (lane & 7) * 16);
     // slot metadata of ring round k: cols at meta0 + (k&3)*8C, vals 4C later
     const uint32_t meta0 = pin_u32(smem0 + 65536 + warp * (32 * C));
+    const uint32_t mcol = pin_u32(meta0 + (lane >> 3) * 4);  // this lane's gather column, batch slot lane/8
+    const uint32_t tl = pin_u32(lane >> 3);
     // column tile blockIdx.y: codes 128y.., output float4 columns 32y..
     q += (size_t)blockIdx.y * 128;
     c += (size_t)blockIdx.y * 32;
+    const unsigned char* qlane = pin_ptr(q + (lane & 7) * 16);
     f4 = min(32u, f4 - blockIdx.y * 32);
     uint32_t nb = 16;  // bytes this lane copies per slot
     if (!FULL) {
@@ -1026,17 +1043,19 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
                          : "memory");
         }
     };
-    // gathers for ring positions p0..p0+3 of round k (slots k*C + p0 ..)
+    // gathers for ring positions p0..p0+3 of round k (slots k*C + p0 ..);
+    // every per-lane term is pinned (qlane, mcol, tl), so the issue is one
+    // compare, one LDS, one IMAD.WIDE and the LDGSTS
     auto issue = [&](int p0, uint32_t k) {
-        const uint32_t t = k * C + p0 + (lane >> 3);
+        const uint32_t t = k * C + p0 + tl;
         if (t < total && (FULL || nb != 0)) {
-            const uint32_t col = lds_u32(meta0 + (k & 3) * (8 * C) + (p0 + (lane >> 3)) * 4);
-            const unsigned char* src = q + (uint64_t)col * ldq + (lane & 7) * 16;
+            const uint32_t col = lds_u32(mcol + (k & 3) * (8 * C) + p0 * 4);
+            const unsigned char* src = qlane + (uint64_t)col * ldq;
             if (FULL)
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(wr0 + p0 * 256), "l"(src)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(wr0 + p0 * RS), "l"(src)
                              : "memory");
             else
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(wr0 + p0 * 256), "l"(src),
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(wr0 + p0 * RS), "l"(src),
                              "r"(nb)
                              : "memory");
         }
@@ -1071,7 +1090,7 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
     if (row_end == 0) advance_rows(0);
 
     auto consume = [&](int p, float v) {
-        const uint32_t r = lds_u32(rd0 + p * 256);
+        const uint32_t r = lds_u32(rd0 + p * RS);
         const float d0 = lds_lut(__byte_perm(r, lane4, 0x7604u));
         const float d1 = lds_lut(__byte_perm(r, lane4, 0x7614u));
         const float d2 = lds_lut(__byte_perm(r, lane4, 0x7624u));
@@ -1145,17 +1164,19 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
                          : "memory");
         }
     };
-    // gathers for ring positions p0..p0+3 of round k (slots k*C + p0 ..)
+    // gathers for ring positions p0..p0+3 of round k (slots k*C + p0 ..);
+    // every per-lane term is pinned (qlane, mcol, tl), so the issue is one
+    // compare, one LDS, one IMAD.WIDE and the LDGSTS
     auto issue = [&](int p0, uint32_t k) {
-        const uint32_t t = k * C + p0 + (lane >> 3);
+        const uint32_t t = k * C + p0 + tl;
         if (t < total && (FULL || nb != 0)) {
-            const uint32_t col = lds_u32(meta0 + (k & 3) * (8 * C) + (p0 + (lane >> 3)) * 4);
-            const unsigned char* src = q + (uint64_t)col * ldq + (lane & 7) * 16;
+            const uint32_t col = lds_u32(mcol + (k & 3) * (8 * C) + p0 * 4);
+            const unsigned char* src = qlane + (uint64_t)col * ldq;
             if (FULL)
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(wr0 + p0 * 256), "l"(src)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(wr0 + p0 * RS), "l"(src)
                              : "memory");
             else
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(wr0 + p0 * 256), "l"(src),
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(wr0 + p0 * RS), "l"(src),
                              "r"(nb)
                              : "memory");
         }
@@ -1198,7 +1219,7 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
     if (row_end == 0) advance_rows(0);
 
     auto consume = [&](int p, float v) {
-        const uint32_t r = lds_u32(rd0 + p * 256);
+        const uint32_t r = lds_u32(rd0 + p * RS);
         const float d0 = lds_lut(__byte_perm(r, lane4, 0x7604u));
         const float d1 = lds_lut(__byte_perm(r, lane4, 0x7614u));
         const float d2 = lds_lut(__byte_perm(r, lane4, 0x7624u));
@@ -1246,7 +1267,7 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
     __syncwarp();  // the next range reuses this warp's ring, metadata and row ends
   };
 
-    if (SCHED == 0) {  // 32-row groups, grid-stride (persistent CTAs fill the 64 KB table once)
+    if (SCHED == 0) {  // 32-row groups, grid-stride (one group per warp unless the grid is persistent)
         for (uint64_t gi = (uint64_t)blockIdx.x * WARPS + warp; gi < groups; gi += (uint64_t)gridDim.x * WARPS)
             run_group32(gi * group_rows);
         return;
@@ -1304,7 +1325,8 @@ template <int C, int WARPS, bool FULL, bool FASTB>
 int launch_q8_batch_t(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, const uint8_t* q,
                       uint64_t ldq, uint32_t f4, float4* c, uint64_t ldc4, const float* lut, cudaStream_t st,
                       int dyn) {
-    const size_t smem = 256 * 256 + (size_t)WARPS * (32 * C + 144);  // LUT + rings, slot metadata, row ends
+    // LUT (+ rings in its holes), slot metadata, row ends (+ separate rings)
+    const size_t smem = 256 * 256 + (size_t)WARPS * (32 * C + 144) + (C * WARPS > 256 ? (size_t)WARPS * C * 128 : 0);
     static int occ_dev[kMaxDevices] = {};
     int& occ = occ_dev[cur_device()];
     if (occ == 0) {
@@ -1358,10 +1380,13 @@ int launch_q8_batch_t(const uint64_t* srow, const uint32_t* scol, const float* s
         AES_CUDA_TRY(cudaFreeAsync(ws, st));
         return AES_OK;
     }
-    // static: persistent, one wave of resident CTAs per column tile walking the groups
+    // static: one 32-row group per warp; the hardware block scheduler balances
+    // the CTAs (products 0.56 ms).  A persistent grid-stride grid fills the
+    // 64 KB table once per SM slot but loses that balancing (0.61 ms), so it
+    // is tuning-only (kSchedStaticPersist).
     uint64_t gs = (uint64_t)num_sms() * occ / tiles;
     if (gs == 0) gs = 1;
-    const unsigned gxs = (unsigned)(gx < gs ? gx : gs);
+    const unsigned gxs = (unsigned)(dyn == kSchedStaticPersist && gx > gs ? gs : gx);
     spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 0><<<dim3(gxs, tiles), WARPS * 32, smem, st>>>(
         srow, scol, sval, n, q, (uint32_t)ldq, f4, c, ldc4, lut, gr, groups, nullptr);
     AES_CUDA_TRY(cudaGetLastError());
@@ -1572,7 +1597,7 @@ int aes_dev_spmm_set_variant(int variant) {
 }
 
 int aes_dev_spmm_set_schedule(int schedule) {
-    if (schedule < 0 || schedule > 3) return aes::fail(AES_ERR_INVALID_ARG, "schedule must be 0, 1, 2 or 3");
+    if (schedule < 0 || schedule > 6) return aes::fail(AES_ERR_INVALID_ARG, "schedule must be 0..6");
     aes::g_spmm_sched = schedule;
     return AES_OK;
 }
@@ -1662,6 +1687,8 @@ int aes_dev_spmm_q8_ex(const uint64_t* srow_ptr, const uint32_t* scol, const flo
             case 35: return launch_q8_batch<16, 4>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st, dyn);
             case 36: return launch_q8_batch<16, 16, false>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st, dyn);
             case 37: return launch_q8_batch<12, 16, false>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st, dyn);
+            case 38: return launch_q8_batch<16, 32>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st, dyn);
+            case 39: return launch_q8_batch<12, 32>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st, dyn);
             default: return launch_q8_batch<16, 16>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st, dyn);
         }
     }

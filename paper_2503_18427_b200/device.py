@@ -40,9 +40,16 @@ def padded(x: torch.Tensor) -> torch.Tensor:
 
 
 def empty_padded(rows: int, cols: int, dtype=torch.float32, device="cuda") -> torch.Tensor:
-    """[rows, cols] view of a buffer whose rows are padded to 16 bytes."""
+    """[rows, cols] view of a buffer whose rows are padded to 16 bytes.  The
+    pad columns are zeroed: the vector kernels gather whole 16-B units, so a
+    padded buffer read as an operand never feeds uninitialized bytes (they
+    only ever reach pad output columns, but compute-sanitizer initcheck
+    flags the read)."""
     per16 = max(1, 16 // torch.empty((), dtype=dtype).element_size())
-    buf = torch.empty((rows, -(-max(cols, 1) // per16) * per16), dtype=dtype, device=device)
+    width = -(-max(cols, 1) // per16) * per16
+    buf = torch.empty((rows, width), dtype=dtype, device=device)
+    if width != cols and rows:
+        buf[:, cols:].zero_()
     return buf[:, :cols]
 
 
@@ -163,7 +170,7 @@ def fit_params(x: torch.Tensor, stream=None):
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=x.device)
     res = torch.empty(4, dtype=torch.float32, device=x.device)
     check(L.aes_dev_fit_params(ptr(x), n, ptr(res), ptr(ws), ws_bytes, stream_of(stream)))
-    r = res.cpu()
+    r = res[:3].cpu()  # word 3 is padding the kernel never writes
     if r.view(torch.int32)[2].item() != 0:
         raise ValueError("NonFinite")
     return float(r[0]), float(r[1])

@@ -182,11 +182,11 @@ def test_async_host_call_matches_sync():
     L.aes_csr_destroy(h)
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5, 6, 7, 8, 21, 22, 23, 24, 30, 31, 32, 33, 34, 35, 36, 37])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5, 6, 7, 8, 21, 22, 23, 24, 30, 31, 32, 33, 34, 35, 36, 37, 38, 39, 40])
 def test_every_spmm_schedule_is_bit_exact(dev, variant):
     """All schedule variants (aes_dev_spmm_set_variant) give the oracle's bits,
     fp32 and int8 (int8 dual-stream kernel: variants 21-24; int8 batch kernel:
-    30-37, the default for 64 < F <= 128)."""
+    30-39, the default for 64 < F <= 128; TMA-gather kernel: 40)."""
     import torch
 
     from paper_2503_18427_b200 import capi
@@ -237,7 +237,7 @@ def test_ring_schedules_bit_exact(dev, sched, f):
     assert np.array_equal(bits(to_np(sampled)), bits(port.spmm_sampled(rp, col, val, x_np, 32)))
 
 
-@pytest.mark.parametrize("sched", [0, 1, 2, 3])
+@pytest.mark.parametrize("sched", [0, 1, 2, 3, 6])
 @pytest.mark.parametrize("f", [128, 300])
 def test_q8_schedules_bit_exact(dev, sched, f):
     """int8 batch kernel under every schedule, exact (unbounded rows) and
