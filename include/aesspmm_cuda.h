@@ -362,6 +362,21 @@ AES_API int aes_dev_gemm_bias_act(const float* a, uint64_t m, uint64_t k, uint64
  * waits for sum-over-producers aes_gemm_ctas(m_p, n) arrivals
  * (aes_dev_wait_counter) before reading its replica.  This replaces the
  * layer's all-gather (gnn.cpp:66-78 run row-sharded). */
+/* One exact GCN layer, fused: h = act(SpMM(srow/scol/sval, x) w + bias) for
+ * k = F_in <= 128 (k % 4 == 0), n = F_out <= 128, x / h 16-B aligned with
+ * ld % 4 == 0 (gnn.cpp:66-78 for one layer: spmm_sampled -> dense_matmul ->
+ * add_bias_inplace -> relu_inplace).  One persistent CTA per SM: producer
+ * warps gather 128-row tiles of the aggregate into shared memory while
+ * consumer warps run the ordered GEMM of the previous tile against W held in
+ * shared memory; the aggregate never goes to HBM.  Bit-identical to
+ * aes_dev_spmm_f32 followed by aes_dev_gemm_bias_act_ex.  finite_w = 0 keeps
+ * the reference's a == 0 skip (needed only when W has inf/NaN).  Rows of the
+ * plan should be bounded (sampled plans): a hub row stalls one producer warp.
+ * AES_ERR_UNSUPPORTED outside that range (callers run the split kernels). */
+AES_API int aes_dev_gcn_layer_fused(const uint64_t* srow_ptr, const uint32_t* scol, const float* sval,
+                                    uint64_t n_rows, const float* x, uint64_t ldx, uint64_t k, const float* w,
+                                    uint64_t ldw, uint64_t n, const float* bias, int relu, int finite_w, float* h,
+                                    uint64_t ldh, void* stream);
 AES_API int aes_dev_gemm_bias_act_ex(const float* a, uint64_t m, uint64_t k, uint64_t lda,
                                      const float* w, uint64_t n, uint64_t ldw, const float* bias,
                                      int relu, int finite_w, float* const* dsts,

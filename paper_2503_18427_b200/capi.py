@@ -15,6 +15,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libaescuda.so")
 
 ADAPTIVE, AFS, SFS, FULL = 0, 1, 2, 3
+AES_ERR_UNSUPPORTED = 11  # aes_status (include/aesspmm_cuda.h)
 _STRATEGIES = {"adaptive": ADAPTIVE, "afs": AFS, "sfs": SFS, "full": FULL}
 
 
@@ -60,6 +61,7 @@ def lib():
         L.aes_cdf_workspace_bytes.argtypes = [u64]
         L.aes_cdf_workspace_bytes.restype = u64
         L.aes_dev_gemm_bias_act.argtypes = [vp, u64, u64, u64, vp, u64, u64, vp, i32, vp, u64, vp]
+        L.aes_dev_gcn_layer_fused.argtypes = [vp, vp, vp, u64, vp, u64, u64, vp, u64, u64, vp, i32, i32, vp, u64, vp]
         L.aes_dev_gemm_bias_act_ex.argtypes = [vp, u64, u64, u64, vp, u64, u64, vp, i32, i32, vp, vp, i32, u64,
                                                u64, vp]
         L.aes_dev_gemm_bias_act_halo.argtypes = [vp, u64, u64, u64, vp, u64, u64, vp, i32, i32, vp, vp, vp, i32,

@@ -367,8 +367,8 @@ constexpr int kRC = 16;            // ring slots per warp
 constexpr int kRB = kRC / 4;       // 4-slot batches per round
 constexpr uint32_t kREnds = 160;   // 33 row ends (padded)
 
-template <int MODE, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, 3)
+template <int MODE, int WARPS, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB)
 spmm_q8r_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
                 const float* __restrict__ sval, uint64_t n_rows, const uint8_t* __restrict__ q, uint32_t ldq,
                 uint32_t f, const float2* __restrict__ params, float4* __restrict__ c, uint64_t ldc4) {
@@ -407,13 +407,15 @@ spmm_q8r_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ 
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(ends0 + lane * 4), "r"((uint32_t)(my_end - g0)) : "memory");
     if (lane == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(ends0 + 128), "r"(total) : "memory");
 
+    // lanes 0..15 stream scol, 16..31 sval: one per-lane base pointer
+    const char* const mbase = lane < 16 ? reinterpret_cast<const char*>(scol + g0 + (lane & 15))
+                                        : reinterpret_cast<const char*>(sval + g0 + (lane & 15));
+    const uint32_t mdst = meta0 + (lane >> 4) * (4 * kRC) + (lane & 15) * 4;
     auto issue_meta = [&](uint32_t k) {  // round k -> buffer k & 3 (lanes 0..15 cols, 16..31 vals)
-        const uint32_t i = lane & 15, s = k * kRC + i;
+        const uint32_t s = k * kRC + (lane & 15);
         if (s < total) {
-            const void* src = lane < 16 ? (const void*)(scol + g0 + s) : (const void*)(sval + g0 + s);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(meta0 + (k & 3) * (8 * kRC) +
-                                                                           (lane >> 4) * (4 * kRC) + i * 4),
-                         "l"(src)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(mdst + (k & 3) * (8 * kRC)),
+                         "l"(mbase + (uint64_t)(k * kRC) * 4)
                          : "memory");
         }
     };
@@ -426,15 +428,15 @@ spmm_q8r_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ 
                          : "memory");
         }
     };
+    const unsigned char* const qlane = q + (lane & 7) * 16;
+    const uint32_t mcol = meta0 + (lane >> 3) * 4, wr0 = ring0 + (lane >> 3) * 128 + (lane & 7) * 16;
     auto issue = [&](int p0, uint32_t k) {  // gathers for ring positions p0..p0+3 of round k
         const uint32_t t = k * kRC + p0 + (lane >> 3);
         if (t < total && nb) {
             uint32_t cc;
-            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cc) : "r"(meta0 + (k & 3) * (8 * kRC) + (p0 + (lane >> 3)) * 4));
-            const unsigned char* src = q + (uint64_t)cc * ldq + (lane & 7) * 16;
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(ring0 + (p0 + (lane >> 3)) * 128 +
-                                                                                 (lane & 7) * 16),
-                         "l"(src), "r"(nb)
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cc) : "r"(mcol + (k & 3) * (8 * kRC) + p0 * 4));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(wr0 + p0 * 128),
+                         "l"(qlane + (uint64_t)cc * ldq), "r"(nb)
                          : "memory");
         }
     };
@@ -543,26 +545,37 @@ spmm_q8r_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ 
     }
 }
 
-template <int MODE>
-int launch_q8r(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, const uint8_t* q,
-               uint64_t ldq, uint64_t f, const float2* params, float* c, uint64_t ldc, cudaStream_t st) {
-    constexpr int kWarps = 16;
+template <int MODE, int WARPS, int MINB>
+int launch_q8r_t(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, const uint8_t* q,
+                 uint64_t ldq, uint64_t f, const float2* params, float* c, uint64_t ldc, cudaStream_t st) {
     constexpr uint32_t kPerWarp = kRC * 128 + 4 * 8 * kRC + (MODE == 0 ? 4 * 8 * kRC : 0) + kREnds;
-    const size_t smem = (size_t)kWarps * kPerWarp;
+    const size_t smem = (size_t)WARPS * kPerWarp;
     static bool attr_dev[kMaxDevices] = {};
     bool& attr = attr_dev[cur_device()];
     if (!attr) {
-        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_q8r_kernel<MODE, kWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)smem));
+        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_q8r_kernel<MODE, WARPS, MINB>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
     const uint64_t groups = (n + 31) / 32;
-    const dim3 grid((unsigned)((groups + kWarps - 1) / kWarps), (unsigned)((f + 127) / 128));
-    spmm_q8r_kernel<MODE, kWarps><<<grid, kWarps * 32, smem, st>>>(srow, scol, sval, n, q, (uint32_t)ldq,
-                                                                   (uint32_t)f, params, reinterpret_cast<float4*>(c),
-                                                                   ldc / 4);
+    const dim3 grid((unsigned)((groups + WARPS - 1) / WARPS), (unsigned)((f + 127) / 128));
+    spmm_q8r_kernel<MODE, WARPS, MINB><<<grid, WARPS * 32, smem, st>>>(srow, scol, sval, n, q, (uint32_t)ldq,
+                                                                      (uint32_t)f, params,
+                                                                      reinterpret_cast<float4*>(c), ldc / 4);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
+}
+
+// Default 16 warps x 2 CTAs per SM with room for 64 registers (measured on
+// B200: products feature 0.594 -> 0.537 ms, reddit feature 0.621 -> 0.475,
+// reddit row 0.595 -> 0.522; products row 0.565 -> 0.575).  Tuning variants:
+// 54 = 16 warps x 3 CTAs (40 registers), 53 = 32 warps x 1.
+template <int MODE>
+int launch_q8r(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, const uint8_t* q,
+               uint64_t ldq, uint64_t f, const float2* params, float* c, uint64_t ldc, cudaStream_t st, int v) {
+    if (v == 54) return launch_q8r_t<MODE, 16, 3>(srow, scol, sval, n, q, ldq, f, params, c, ldc, st);
+    if (v == 53) return launch_q8r_t<MODE, 32, 1>(srow, scol, sval, n, q, ldq, f, params, c, ldc, st);
+    return launch_q8r_t<MODE, 16, 2>(srow, scol, sval, n, q, ldq, f, params, c, ldc, st);
 }
 
 template <int MODE>
@@ -659,8 +672,8 @@ int aes_dev_spmm_q8_affine(const uint64_t* srow_ptr, const uint32_t* scol, const
     }
     // default: the cp.async ring kernel (16-B code rows, 16-B aligned C)
     if (v != 50 && ldq % 16 == 0 && (uintptr_t)q % 16 == 0 && n_rows < (1ull << 31)) {
-        if (mode == AES_QAFFINE_ROW) return launch_q8r<0>(srow_ptr, scol, sval, n_rows, q, ldq, f, p2, c, ldc, st);
-        return launch_q8r<1>(srow_ptr, scol, sval, n_rows, q, ldq, f, p2, c, ldc, st);
+        if (mode == AES_QAFFINE_ROW) return launch_q8r<0>(srow_ptr, scol, sval, n_rows, q, ldq, f, p2, c, ldc, st, v);
+        return launch_q8r<1>(srow_ptr, scol, sval, n_rows, q, ldq, f, p2, c, ldc, st, v);
     }
     if (mode == AES_QAFFINE_ROW) return launch_q8a<0>(srow_ptr, scol, sval, n_rows, q, ldq, f, p2, c, ldc, st);
     return launch_q8a<1>(srow_ptr, scol, sval, n_rows, q, ldq, f, p2, c, ldc, st);

@@ -33,6 +33,11 @@ __device__ __forceinline__ uint64_t row_count(const ScanArgs& a, uint64_t r, uin
     }
     const uint64_t nnz = e - b;
     if (KIND == kScanSlots) {
+        // slots = chunk * cnt is min(nnz, W) for Sfs / Afs, and for Adaptive
+        // whenever W is a multiple of 32 (every Table-1 branch then has
+        // chunk * cnt == W: W/4*4, W/8*8, W/16*16, W/32*32); nnz for Full
+        if (!a.row_params && (a.strategy != AES_ADAPTIVE || a.width % 32 == 0))
+            return a.strategy == AES_FULL ? nnz : min(nnz, (uint64_t)a.width);
         const RowParams p = row_params(nnz, a.width, a.strategy);
         if (a.row_params) reinterpret_cast<uint2*>(a.row_params)[r] = make_uint2(p.chunk, p.cnt);
         return (uint64_t)p.chunk * p.cnt;
@@ -156,6 +161,133 @@ row_scan_kernel(ScanArgs a, const unsigned long long* __restrict__ tile_tot) {
     if (tile == 0 && tid == 0) a.out[0] = 0;
 }
 
+// One cooperative launch instead of two kernels: every CTA owns a contiguous
+// run of tiles.  Phase 1 sums its tiles' row counts (row_ptr from HBM) and
+// publishes the CTA total; a grid barrier (co-residency guaranteed by the
+// cooperative launch); phase 2 sums the totals of the CTAs before it, then
+// rescans its tiles (row_ptr now an L2 hit: 16 B per row of the graph) and
+// writes srow_ptr.  Saves one launch and one HBM pass over row_ptr.
+// Counts of the first kCoopKeep tiles stay in registers across the barrier
+// (u32 per row: a row count is at most 2^32 - 1 for every kind but the
+// caller-supplied explicit plans, which recount instead).
+constexpr int kCoopKeep = 4;
+template <int KIND>
+__global__ void __launch_bounds__(kScanThreads, 4)
+row_scan_coop_kernel(ScanArgs a, unsigned long long* cta_tot, unsigned int* barrier, uint32_t tiles_per_cta) {
+    constexpr int K = KIND == kScanExplicit ? 0 : kCoopKeep;
+    __shared__ uint64_t s_rp[kPadded];
+    __shared__ uint64_t warp_tot[kScanThreads / 32];
+    const int tid = threadIdx.x;
+    const uint64_t n_tiles = (a.n + kScanTile - 1) / kScanTile;
+    const uint64_t t0 = (uint64_t)blockIdx.x * tiles_per_cta;
+    const uint64_t t1 = min(n_tiles, t0 + tiles_per_cta);
+    uint32_t keep[K > 0 ? K : 1][kScanIters];
+    uint64_t incl[kScanIters];
+    uint64_t mine = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const uint64_t t = t0 + k;
+        if (t < t1) {
+            const uint64_t base = t * kScanTile;
+            const int nr = (int)min((uint64_t)kScanTile, a.n - base);
+            const uint64_t run = tile_counts<KIND>(a, base, nr, s_rp, incl, true);  // (params written once)
+            uint64_t prev = 0;
+#pragma unroll
+            for (int u = 0; u < kScanIters; ++u) {
+                keep[k][u] = (uint32_t)(incl[u] - prev);
+                prev = incl[u];
+            }
+            mine += run;
+            __syncthreads();  // s_rp reused by the next tile
+        }
+    }
+    for (uint64_t t = t0 + K; t < t1; ++t) {
+        const uint64_t base = t * kScanTile;
+        const int nr = (int)min((uint64_t)kScanTile, a.n - base);
+        mine += tile_counts<KIND>(a, base, nr, s_rp, incl, false);
+        __syncthreads();
+    }
+    uint64_t cta_sum;
+    block_excl_scan(mine, warp_tot, &cta_sum);
+    if (tid == 0) {
+        cta_tot[blockIdx.x] = cta_sum;
+        __threadfence();
+        atomicAdd(barrier, 1u);
+        unsigned int seen;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(barrier) : "memory");
+        } while (seen < gridDim.x);
+    }
+    __syncthreads();
+    uint64_t pre = 0;
+    for (uint32_t c = tid; c < blockIdx.x; c += kScanThreads) pre += __ldcg(cta_tot + c);
+    uint64_t run_off;
+    block_excl_scan(pre, warp_tot, &run_off);
+    __syncthreads();  // warp_tot reused
+    auto emit = [&](uint64_t t) {  // incl holds this thread's inclusive counts of tile t
+        const uint64_t base = t * kScanTile;
+        const int nr = (int)min((uint64_t)kScanTile, a.n - base);
+        uint64_t tile_sum;
+        const uint64_t excl = run_off + block_excl_scan(incl[kScanIters - 1], warp_tot, &tile_sum);
+        __syncthreads();  // every s_rp / warp_tot read is done
+#pragma unroll
+        for (int u = 0; u < kScanIters; ++u) s_rp[pad_idx(tid * kScanIters + u)] = excl + incl[u];
+        __syncthreads();
+        for (int i = tid; i < nr; i += kScanThreads) a.out[base + i + 1] = s_rp[pad_idx(i)];
+        run_off += tile_sum;
+        __syncthreads();
+    };
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+        if (t0 + k < t1) {
+            uint64_t r = 0;
+#pragma unroll
+            for (int u = 0; u < kScanIters; ++u) incl[u] = (r += keep[k][u]);
+            emit(t0 + k);
+        }
+    for (uint64_t t = t0 + K; t < t1; ++t) {
+        const uint64_t base = t * kScanTile;
+        const int nr = (int)min((uint64_t)kScanTile, a.n - base);
+        tile_counts<KIND>(a, base, nr, s_rp, incl, true);
+        __syncthreads();
+        emit(t);
+    }
+    if (blockIdx.x == 0 && tid == 0) a.out[0] = 0;
+}
+
+template <int KIND>
+int launch_scan_kind(const ScanArgs& a, void* ws, cudaStream_t st) {
+    const uint64_t tiles = (a.n + kScanTile - 1) / kScanTile;
+    auto* hdr = reinterpret_cast<unsigned int*>(ws);
+    auto* tot = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 256);
+    static int occ_dev[kMaxDevices] = {};
+    int& occ = occ_dev[cur_device()];
+    if (occ == 0) {
+        AES_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, row_scan_coop_kernel<KIND>, kScanThreads, 0));
+        if (occ < 1) occ = -1;
+    }
+    if (tiles > 1 && occ > 0) {
+        // kCoopKeep tiles per CTA when the grid fits (counts never recomputed)
+        const uint64_t slots = (uint64_t)num_sms() * occ;
+        const uint32_t per = (uint32_t)((tiles + slots - 1) / slots);
+        const unsigned grid = (unsigned)((tiles + per - 1) / per);
+        AES_CUDA_TRY(cudaMemsetAsync(hdr, 0, sizeof(unsigned int), st));
+        ScanArgs aa = a;
+        unsigned long long* tp = tot;
+        unsigned int* bp = hdr;
+        uint32_t pp = per;
+        void* args[] = {&aa, &tp, &bp, &pp};
+        if (cudaLaunchCooperativeKernel((const void*)row_scan_coop_kernel<KIND>, dim3(grid), dim3(kScanThreads),
+                                        args, 0, st) == cudaSuccess)
+            return AES_OK;
+        (void)cudaGetLastError();  // not launchable cooperatively here: the two-kernel form
+    }
+    row_tile_total_kernel<KIND><<<(unsigned)tiles, kScanThreads, 0, st>>>(a, tot);
+    row_scan_kernel<KIND><<<(unsigned)tiles, kScanThreads, 0, st>>>(a, tot);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
 }  // namespace
 
 size_t row_scan_workspace_bytes(uint64_t n) {
@@ -171,28 +303,12 @@ int launch_row_scan(int kind, const ScanArgs& a, void* ws, size_t ws_bytes, cuda
         AES_CUDA_TRY(cudaMemsetAsync(a.out, 0, sizeof(uint64_t), st));
         return AES_OK;
     }
-    const unsigned tiles = (unsigned)((a.n + kScanTile - 1) / kScanTile);
-    auto* tot = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 256);
     switch (kind) {
-        case kScanSlots:
-            row_tile_total_kernel<kScanSlots><<<tiles, kScanThreads, 0, st>>>(a, tot);
-            row_scan_kernel<kScanSlots><<<tiles, kScanThreads, 0, st>>>(a, tot);
-            break;
-        case kScanStarts:
-            row_tile_total_kernel<kScanStarts><<<tiles, kScanThreads, 0, st>>>(a, tot);
-            row_scan_kernel<kScanStarts><<<tiles, kScanThreads, 0, st>>>(a, tot);
-            break;
-        case kScanExplicit:
-            row_tile_total_kernel<kScanExplicit><<<tiles, kScanThreads, 0, st>>>(a, tot);
-            row_scan_kernel<kScanExplicit><<<tiles, kScanThreads, 0, st>>>(a, tot);
-            break;
-        default:
-            row_tile_total_kernel<kScanGcnNnz><<<tiles, kScanThreads, 0, st>>>(a, tot);
-            row_scan_kernel<kScanGcnNnz><<<tiles, kScanThreads, 0, st>>>(a, tot);
-            break;
+        case kScanSlots: return launch_scan_kind<kScanSlots>(a, ws, st);
+        case kScanStarts: return launch_scan_kind<kScanStarts>(a, ws, st);
+        case kScanExplicit: return launch_scan_kind<kScanExplicit>(a, ws, st);
+        default: return launch_scan_kind<kScanGcnNnz>(a, ws, st);
     }
-    AES_CUDA_TRY(cudaGetLastError());
-    return AES_OK;
 }
 
 // ===========================================================================
@@ -226,6 +342,7 @@ struct FillRow {
 // hashed start needs at most a 32-bit modulo: s*1429 < 32*1429, and
 // hash_start is s*1429 itself whenever the modulus exceeds it.  CTAs whose
 // slots exceed the map (W > 32, FULL) run several passes.
+constexpr int kFillUnroll = 4;  // slots per thread per step, all loads in flight before the stores
 __global__ void __launch_bounds__(kFillRows, 6)
 sample_fill_kernel(const uint64_t* __restrict__ plan_row_ptr, const uint64_t* __restrict__ row_ptr,
                    const uint32_t* __restrict__ col_ind, const float* __restrict__ val,
@@ -282,13 +399,14 @@ sample_fill_kernel(const uint64_t* __restrict__ plan_row_ptr, const uint64_t* __
             for (uint32_t t = a; t < b; ++t) s_map[t - pass] = (unsigned char)tid;
         }
         __syncthreads();
-        // four slots per thread per step: their loads are all in flight
-        // before the first store (the map / row lookups are shared-memory hits)
-        for (uint32_t t0 = pass + tid; t0 < pend; t0 += 4 * kFillRows) {
-            uint64_t src[4];
-            bool ok[4];
+        // kFillUnroll slots per thread per step: their loads are all in
+        // flight before the first store (the map / row lookups are
+        // shared-memory hits)
+        for (uint32_t t0 = pass + tid; t0 < pend; t0 += kFillUnroll * kFillRows) {
+            uint64_t src[kFillUnroll];
+            bool ok[kFillUnroll];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < kFillUnroll; ++u) {
                 const uint32_t t = t0 + u * kFillRows;
                 ok[u] = t < pend;
                 src[u] = 0;
@@ -313,16 +431,16 @@ sample_fill_kernel(const uint64_t* __restrict__ plan_row_ptr, const uint64_t* __
                     src[u] = fr.src + start + j;
                 }
             }
-            uint32_t cv[4];
-            float vv[4];
+            uint32_t cv[kFillUnroll];
+            float vv[kFillUnroll];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < kFillUnroll; ++u)
                 if (ok[u]) {
                     cv[u] = __ldg(col_ind + src[u]);
                     vv[u] = __ldg(val + src[u]);
                 }
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < kFillUnroll; ++u)
                 if (ok[u]) {
                     const uint64_t pos = g0 + t0 + u * kFillRows;
                     __stcs(scol + pos, cv[u]);

@@ -301,12 +301,14 @@ struct RingQ8 {
 // a 32-row window held one per lane; the next window's ends are loaded when
 // the current one is entered, so crossing into it costs a register move.
 // Caller guarantees srow[re] - srow[rb] < 2^31.
-template <class R, int NV, int C, bool FULL>
+// SOUT: rows go to shared memory instead (the fused layer kernel): row rb + i
+// of this lane at smem address sout + i * ldc4 * 16 (c unused).
+template <class R, int NV, int C, bool FULL, bool SOUT = false>
 __device__ __forceinline__ void ring_range(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
                                            const float* __restrict__ sval,
                                            const typename R::raw_t* __restrict__ gsrc, uint32_t ld, uint32_t f4,
                                            float4* __restrict__ c, uint64_t ldc4, uint32_t ring0,
-                                           uint32_t lut_lane, uint64_t rb, uint64_t re) {
+                                           uint32_t lut_lane, uint64_t rb, uint64_t re, uint32_t sout = 0) {
     typedef typename R::raw_t raw_t;
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t g0 = srow[rb];
@@ -363,7 +365,15 @@ __device__ __forceinline__ void ring_range(const uint64_t* __restrict__ srow, co
     auto store_row = [&]() {
 #pragma unroll
         for (int n = 0; n < NV; ++n) {
-            if (colok[n]) __stcs(crow + ra * ldc4 + 32u * n, acc[n]);
+            if (SOUT) {
+                if (colok[n])
+                    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                     sout + (uint32_t)(ra - rb) * (uint32_t)ldc4 * 16u + 512u * n),
+                                 "f"(acc[n].x), "f"(acc[n].y), "f"(acc[n].z), "f"(acc[n].w)
+                                 : "memory");
+            } else if (colok[n]) {
+                __stcs(crow + ra * ldc4 + 32u * n, acc[n]);
+            }
             acc[n] = f4_zero();
         }
     };
@@ -968,7 +978,7 @@ template <int C, int WARPS, bool FULL, bool FASTB, int SCHED>  // SCHED: 0 stati
 // tile form (F % 128 != 0, e.g. reddit's 602) runs faster at 2 CTAs with room
 // for 64 registers (reddit int8 0.64 -> 0.59 ms; products, whole tiles, loses
 // 4-20 % that way)
-__global__ void __launch_bounds__(WARPS * 32, WARPS >= 32 ? 1 : FULL ? 3 : 2)
+__global__ void __launch_bounds__(WARPS * 32, WARPS >= 32 ? 1 : WARPS >= 20 ? 2 : FULL ? 3 : 2)
 spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
                      const float* __restrict__ sval, uint64_t n_rows, const unsigned char* __restrict__ q,
                      uint32_t ldq, uint32_t f4, float4* __restrict__ c, uint64_t ldc4,
@@ -1033,13 +1043,15 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
     __syncwarp();
 
     // metadata of round k -> buffer k & 3 (lanes 0..C-1: cols, 16..16+C-1: vals)
+    // (lanes 0..15 stream scol, 16..31 sval: one per-lane base pointer)
+    const char* const mbase = lane < 16 ? reinterpret_cast<const char*>(scol + g0 + (lane & 15))
+                                        : reinterpret_cast<const char*>(sval + g0 + (lane & 15));
+    const uint32_t mdst = meta0 + (lane >> 4) * (4 * C) + (lane & 15) * 4;
     auto issue_meta = [&](uint32_t k) {
         const uint32_t i = lane & 15, s = k * C + i;
         if (i < (uint32_t)C && s < total) {
-            const void* src = lane < 16 ? (const void*)(scol + g0 + s) : (const void*)(sval + g0 + s);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(meta0 + (k & 3) * (8 * C) +
-                                                                           (lane >> 4) * (4 * C) + i * 4),
-                         "l"(src)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(mdst + (k & 3) * (8 * C)),
+                         "l"(mbase + (uint64_t)(k * C) * 4)
                          : "memory");
         }
     };
@@ -1154,13 +1166,15 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
     __syncwarp();
 
     // metadata of round k -> buffer k & 3 (lanes 0..C-1: cols, 16..16+C-1: vals)
+    // (lanes 0..15 stream scol, 16..31 sval: one per-lane base pointer)
+    const char* const mbase = lane < 16 ? reinterpret_cast<const char*>(scol + g0 + (lane & 15))
+                                        : reinterpret_cast<const char*>(sval + g0 + (lane & 15));
+    const uint32_t mdst = meta0 + (lane >> 4) * (4 * C) + (lane & 15) * 4;
     auto issue_meta = [&](uint32_t k) {
         const uint32_t i = lane & 15, s = k * C + i;
         if (i < (uint32_t)C && s < total) {
-            const void* src = lane < 16 ? (const void*)(scol + g0 + s) : (const void*)(sval + g0 + s);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(meta0 + (k & 3) * (8 * C) +
-                                                                           (lane >> 4) * (4 * C) + i * 4),
-                         "l"(src)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(mdst + (k & 3) * (8 * C)),
+                         "l"(mbase + (uint64_t)(k * C) * 4)
                          : "memory");
         }
     };
@@ -1350,7 +1364,10 @@ int launch_q8_batch_t(const uint64_t* srow, const uint32_t* scol, const float* s
     // auto: the 32-row-group grid when it runs >= 4 waves (0.56 ms on the
     // full products graph, vs 0.59-0.60 balanced), the balanced wave when it
     // would end in a partial wave (row shards: P = 8 0.107 -> 0.095 ms)
-    if (dyn == kSchedAuto) dyn = gx * tiles >= 4ull * num_sms() * occ ? kSchedStatic : kSchedBal;
+    // (one 32-warp CTA per SM: balanced always — a single wave fills the
+    // 64 KB table once per SM, 0.51 vs 0.59 ms static on products)
+    if (dyn == kSchedAuto)
+        dyn = WARPS >= 32 || gx * tiles < 4ull * num_sms() * occ ? kSchedBal : kSchedStatic;
     if (dyn == kSchedBal || dyn == kSchedBalOne) {  // one wave of resident CTAs per column tile
         // whole waves: the tiles share the resident CTA slots (rounding up
         // would leave one CTA for a second, nearly empty wave)
@@ -1581,6 +1598,202 @@ int launch_vector(const uint64_t* srow, const uint32_t* scol, const float* sval,
     return AES_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Fused exact GCN layer: H = act(SpMM(A, X) W + b) in one persistent kernel
+// (gnn.cpp:66-78 for one layer: spmm_sampled then dense_matmul, bias, ReLU).
+//
+// The SpMM is HBM-bound (gathers) and the ordered fp32 GEMM is FP32-pipe
+// bound, so the split kernels leave each resource idle half of the time and
+// round-trip the aggregate through HBM.  Here one CTA per SM runs both,
+// warp-specialised over 128-row tiles:
+//   * 8 producer warps gather tile i+1's aggregate rows (the ring SpMM
+//     body, 8 rows each) into a shared-memory A buffer;
+//   * 8 consumer warps run the ordered GEMM of tile i from the other buffer
+//     against W, resident in shared memory for the whole kernel, and store
+//     bias + ReLU results straight from registers;
+//   * named barriers hand the two A buffers back and forth (full: producers
+//     arrive, consumers sync; empty: the reverse).
+// Bit-exact with the split path: every aggregate element is the same slot-
+// order FMUL/FADD chain, every output the same k-ascending chain from +0.
+// Consumer mapping: thread (tx, ty) owns rows 4ty..4ty+3 and columns
+// {4tx..4tx+3, 64+4tx..}: the A reads broadcast, the W reads are 256
+// contiguous bytes per half-warp (no bank conflicts).
+// ---------------------------------------------------------------------------
+// 64-row tiles: W (64 KB) stays resident next to two 33 KB A buffers and
+// eight producer rings; each producer warp streams 8 rows (~45 slots) per
+// tile through a 16-slot ring, so a tile's gathers take less time than its
+// GEMM (measured with 128-row tiles and 4 producer warps: producer-bound,
+// the consumers stalled on the full barrier a third of the time).
+constexpr int kLayerBM = 64;
+constexpr int kLayerConsumers = 8, kLayerProducers = 8;
+constexpr int kLayerThreads = (kLayerConsumers + kLayerProducers) * 32;  // 512
+constexpr int kLayerRing = 12;  // producer ring slots (512 B each at K = 128)
+constexpr int kLayerBufs = 3;   // A buffers: producers run up to two tiles ahead
+
+__device__ __forceinline__ void named_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+template <bool FULLK, bool SKIP>
+__global__ void __launch_bounds__(kLayerThreads, 1)
+gcn_layer_fused_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
+                       const float* __restrict__ sval, uint64_t n_rows, const float4* __restrict__ x,
+                       uint32_t ldx4, uint32_t k, const float* __restrict__ w, uint64_t ldw, uint32_t n,
+                       const float* __restrict__ bias, int relu, float* __restrict__ h, uint64_t ldh,
+                       uint64_t n_tiles) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const uint32_t k4 = k / 4, as4 = k4 + 1;  // A row stride in float4 (one float4 of pad)
+    const uint32_t smem0 = smem_addr(smem_raw);
+    float* ws = reinterpret_cast<float*>(smem_raw);  // W [k][128] (columns >= n zero)
+    const uint32_t a_off = k * 128 * 4;
+    const uint32_t a_bytes = kLayerBM * as4 * 16;
+    const uint32_t ring_off = a_off + kLayerBufs * a_bytes;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    // W resident for the whole kernel (read once per SM from L2)
+    for (uint32_t i = tid; i < k * 128; i += kLayerThreads) {
+        const uint32_t kk = i >> 7, j = i & 127;
+        ws[i] = j < n ? w[(uint64_t)kk * ldw + j] : 0.f;
+    }
+    __syncthreads();
+
+    if (warp >= kLayerConsumers) {
+        // ---------------- producers: SpMM rows into the A buffers
+        const int pw = warp - kLayerConsumers;
+        const uint32_t ring0 = smem0 + ring_off + pw * (kLayerRing * 512) + lane * 16;
+        uint64_t i = 0;
+        for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+            const int buf = (int)(i % kLayerBufs);
+            if (i >= kLayerBufs) named_sync(1 + kLayerBufs + buf, kLayerThreads);  // consumers released it
+            // this warp's share of the tile: rows whose first slot falls in
+            // the pw-th equal slot share (one coalesced load of the tile's
+            // row offsets + two ballots; a row never splits)
+            const uint64_t t0 = t * kLayerBM, t1 = min(t0 + kLayerBM, n_rows);
+            const uint32_t nr = (uint32_t)(t1 - t0);
+            const uint64_t va = (uint32_t)lane < nr ? srow[t0 + lane] : ~0ull;
+            const uint64_t vb = (uint32_t)lane + 32 < nr ? srow[t0 + 32 + lane] : ~0ull;
+            const uint64_t s0 = __shfl_sync(0xffffffffu, va, 0), s1 = srow[t1];
+            auto first_row = [&](int share) -> uint64_t {
+                const uint64_t target = s0 + (s1 - s0) * (uint64_t)share / kLayerProducers;
+                return t0 + __popc(__ballot_sync(0xffffffffu, va < target)) +
+                       __popc(__ballot_sync(0xffffffffu, vb < target));
+            };
+            const uint64_t rb = pw == 0 ? t0 : first_row(pw);
+            const uint64_t re = pw == kLayerProducers - 1 ? t1 : first_row(pw + 1);
+            if (rb < re) {
+                const uint32_t sout = smem0 + a_off + buf * a_bytes + (uint32_t)(rb - t0) * as4 * 16 + lane * 16;
+                for (uint64_t r = rb; r < re;) {  // slices with 32-bit slot offsets (one at any real shape)
+                    const uint64_t e = srow[re] - srow[r] >= (1ull << 31) ? r + 1 : re;
+                    ring_range<RingF32, 1, kLayerRing, FULLK, true>(srow, scol, sval, x, ldx4, k4, nullptr, as4,
+                                                                    ring0, 0, r, e,
+                                                                    sout + (uint32_t)(r - rb) * as4 * 16);
+                    r = e;
+                }
+            }
+            named_arrive(1 + buf, kLayerThreads);  // tile i's aggregate is in buffer buf
+        }
+        // drain: match the consumers' releases of the last kLayerBufs tiles
+        for (uint64_t j = i > kLayerBufs ? i - kLayerBufs : 0; j < i; ++j)
+            named_sync(1 + kLayerBufs + (int)(j % kLayerBufs), kLayerThreads);
+        return;
+    }
+
+    // ---------------- consumers: ordered GEMM of each tile
+    const int tx = tid & 15, ty = tid >> 4;  // 16 x 16 threads, 4 x 8 outputs each
+    uint64_t i = 0;
+    for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+        const int buf = (int)(i % kLayerBufs);
+        named_sync(1 + buf, kLayerThreads);  // tile i's aggregate landed
+        const float* as = reinterpret_cast<const float*>(smem_raw + a_off + buf * a_bytes);
+        float acc[4][8];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[r][j] = 0.f;
+        for (uint32_t k0 = 0; k0 < k; k0 += 4) {
+            float4 a4[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                a4[r] = *reinterpret_cast<const float4*>(as + (uint32_t)(4 * ty + r) * as4 * 4 + k0);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                const float4 w0 = *reinterpret_cast<const float4*>(ws + (k0 + kk) * 128 + 4 * tx);
+                const float4 w1 = *reinterpret_cast<const float4*>(ws + (k0 + kk) * 128 + 64 + 4 * tx);
+                const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const float av = kk == 0 ? a4[r].x : kk == 1 ? a4[r].y : kk == 2 ? a4[r].z : a4[r].w;
+                    if (SKIP) {
+                        const bool skip = av == 0.f;
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const float s2 = __fadd_rn(acc[r][j], __fmul_rn(av, wv[j]));
+                            acc[r][j] = skip ? acc[r][j] : s2;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) acc[r][j] = __fadd_rn(acc[r][j], __fmul_rn(av, wv[j]));
+                    }
+                }
+            }
+        }
+        named_arrive(1 + kLayerBufs + buf, kLayerThreads);  // buffer buf may be refilled
+        // epilogue: bias, ReLU (gnn.cpp:41-52), store
+        const uint64_t m0 = t * kLayerBM;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const uint64_t gm = m0 + 4 * ty + r;
+            if (gm >= n_rows) continue;
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                const uint32_t c0 = (half ? 64 : 0) + 4 * tx;
+                if (c0 >= n) continue;
+                float v[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    float xo = acc[r][4 * half + j];
+                    if (bias && c0 + j < n) xo = __fadd_rn(xo, bias[c0 + j]);
+                    if (relu) xo = (xo < 0.f) ? 0.f : xo;
+                    v[j] = xo;
+                }
+                float* dst = h + gm * ldh + c0;
+                if (c0 + 4 <= n)
+                    __stcs(reinterpret_cast<float4*>(dst), make_float4(v[0], v[1], v[2], v[3]));
+                else
+                    for (int j = 0; j < 4; ++j)
+                        if (c0 + j < n) dst[j] = v[j];
+            }
+        }
+    }
+}
+
+template <bool FULLK, bool SKIP>
+int launch_layer_fused_t(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n_rows,
+                         const float* x, uint64_t ldx, uint32_t k, const float* w, uint64_t ldw, uint32_t n,
+                         const float* bias, int relu, float* h, uint64_t ldh, cudaStream_t st) {
+    const size_t smem = (size_t)k * 128 * 4 + kLayerBufs * (size_t)kLayerBM * (k / 4 + 1) * 16 +
+                        (size_t)kLayerProducers * kLayerRing * 512;
+    static bool attr_dev[kMaxDevices] = {};
+    bool& attr = attr_dev[cur_device()];
+    if (!attr) {  // opt in once for the largest k (128)
+        const size_t smax = 128 * 128 * 4 + kLayerBufs * (size_t)kLayerBM * 33 * 16 +
+                            (size_t)kLayerProducers * kLayerRing * 512;
+        AES_CUDA_TRY(cudaFuncSetAttribute(gcn_layer_fused_kernel<FULLK, SKIP>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+        attr = true;
+    }
+    const uint64_t tiles = (n_rows + kLayerBM - 1) / kLayerBM;
+    const unsigned grid = (unsigned)(tiles < (uint64_t)num_sms() ? tiles : (uint64_t)num_sms());
+    gcn_layer_fused_kernel<FULLK, SKIP><<<grid, kLayerThreads, smem, st>>>(
+        srow, scol, sval, n_rows, reinterpret_cast<const float4*>(x), (uint32_t)(ldx / 4), k, w, ldw, n, bias,
+        relu, h, ldh, tiles);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
 }  // namespace
 
 int launch_spmm_q8_tma(int dec, const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n,
@@ -1675,11 +1888,12 @@ int aes_dev_spmm_q8_ex(const uint64_t* srow_ptr, const uint32_t* scol, const flo
         const int s = launch_spmm_q8_tma(0, srow_ptr, scol, sval, n_rows, q, ldq, f, lut, nullptr, c, ldc, st);
         if (s != AES_ERR_UNSUPPORTED) return s;
     }
-    if ((v == 0 || (v >= 30 && v <= 40)) && f4 > 16 && ldq % 16 == 0 && (uintptr_t)q % 16 == 0 &&
+    if ((v == 0 || (v >= 30 && v <= 45)) && f4 > 16 && ldq % 16 == 0 && (uintptr_t)q % 16 == 0 &&
         f4 / 32 < 65535) {
         float4* c4 = reinterpret_cast<float4*>(c);
         const uint32_t f4u = (uint32_t)f4;
         switch (v) {
+            case 30: return launch_q8_batch<16, 16>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st, dyn);
             case 31: return launch_q8_batch<8, 16>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st, dyn);
             case 32: return launch_q8_batch<16, 8>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st, dyn);
             case 33: return launch_q8_batch<8, 8>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st, dyn);
@@ -1689,12 +1903,45 @@ int aes_dev_spmm_q8_ex(const uint64_t* srow_ptr, const uint32_t* scol, const flo
             case 37: return launch_q8_batch<12, 16, false>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st, dyn);
             case 38: return launch_q8_batch<16, 32>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st, dyn);
             case 39: return launch_q8_batch<12, 32>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st, dyn);
-            default: return launch_q8_batch<16, 16>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st, dyn);
+            case 43: return launch_q8_batch<16, 20>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st, dyn);
+            case 44: return launch_q8_batch<12, 20>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st, dyn);
+            case 45: return launch_q8_batch<8, 32>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st, dyn);
+            default:
+                // whole 128-code tiles (F = 128: products, arxiv, pubmed): one
+                // 32-warp CTA per SM with 64 registers and a 12-slot ring,
+                // balanced wave (products 0.511 ms vs 0.585 for the 16 x 16
+                // static grid); partial tiles (reddit F = 602) keep 16 x 16
+                // (0.585 vs 0.600)
+                if (f4u % 32 == 0)
+                    return launch_q8_batch<12, 32>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st, dyn);
+                return launch_q8_batch<16, 16>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st, dyn);
         }
     }
     GatherQ8 g{reinterpret_cast<const uint32_t*>(q), ldq / 4};
     return launch_vector(srow_ptr, scol, sval, n_rows, g, (uint32_t)f4,
                          reinterpret_cast<float4*>(c), ldc / 4, lut, st, dyn);
+}
+
+
+int aes_dev_gcn_layer_fused(const uint64_t* srow_ptr, const uint32_t* scol, const float* sval, uint64_t n_rows,
+                            const float* x, uint64_t ldx, uint64_t k, const float* w, uint64_t ldw, uint64_t n,
+                            const float* bias, int relu, int finite_w, float* h, uint64_t ldh, void* stream) {
+    using namespace aes;
+    if (k == 0 || n == 0 || k > 128 || n > 128 || k % 4 != 0)
+        return fail(AES_ERR_UNSUPPORTED, "fused layer needs 0 < k <= 128, k % 4 == 0, 0 < n <= 128");
+    if (ldx % 4 != 0 || (uintptr_t)x % 16 != 0 || ldx < k || ldh < n || ldw < n)
+        return fail(AES_ERR_UNSUPPORTED, "fused layer needs ldx % 4 == 0, 16-B aligned x, ldw >= n, ldh >= n");
+    if (ldh % 4 != 0 || (uintptr_t)h % 16 != 0)
+        return fail(AES_ERR_UNSUPPORTED, "fused layer needs ldh % 4 == 0 and 16-B aligned h");
+    cudaStream_t st = as_stream(stream);
+    if (n_rows == 0) return AES_OK;
+    const uint32_t k32 = (uint32_t)k, n32 = (uint32_t)n;
+    if (k == 128) {
+        if (finite_w) return launch_layer_fused_t<true, false>(srow_ptr, scol, sval, n_rows, x, ldx, k32, w, ldw, n32, bias, relu, h, ldh, st);
+        return launch_layer_fused_t<true, true>(srow_ptr, scol, sval, n_rows, x, ldx, k32, w, ldw, n32, bias, relu, h, ldh, st);
+    }
+    if (finite_w) return launch_layer_fused_t<false, false>(srow_ptr, scol, sval, n_rows, x, ldx, k32, w, ldw, n32, bias, relu, h, ldh, st);
+    return launch_layer_fused_t<false, true>(srow_ptr, scol, sval, n_rows, x, ldx, k32, w, ldw, n32, bias, relu, h, ldh, st);
 }
 
 }  // extern "C"

@@ -98,11 +98,11 @@ class SampledPlan:
         st = stream_of(stream)
         self.n_rows = n
         self.srow_ptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
-        self.row_params = torch.empty((max(n, 1), 2), dtype=torch.int32, device=dev)
         ws_bytes = L.aes_dev_scan_workspace_bytes(n)
         ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        # (no per-row (chunk, cnt) output: the fill re-derives them per row)
         check(L.aes_dev_sample_plan(ptr(graph.row_ptr), n, self.width, self.strategy, ptr(self.srow_ptr),
-                                    ptr(self.row_params), ptr(ws), ws_bytes, st))
+                                    None, ptr(ws), ws_bytes, st))
         # the absolute offset of this (possibly sharded) row range
         self.base = int(self.srow_ptr[0].item()) if n else 0
         self.total_slots = int(self.srow_ptr[-1].item()) - self.base
@@ -404,8 +404,32 @@ def gemm_tf32(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None, relu:
     return out
 
 
+def gcn_layer_fused(srow_ptr, scol, sval, x: torch.Tensor, w: torch.Tensor, b, relu: bool, finite_w: bool = True,
+                    out: torch.Tensor | None = None, stream=None):
+    """One exact GCN layer act(SpMM(A, x) w + b) as ONE persistent kernel
+    (aes_dev_gcn_layer_fused: SpMM producer warps + ordered-GEMM consumer
+    warps, the aggregate never leaves shared memory).  Returns None when the
+    shape is outside the kernel's range (k % 4 != 0, k > 128 or n > 128):
+    the caller runs the split kernels.  Bit-identical to spmm + gemm_bias_act."""
+    L = lib()
+    m, k = x.shape[0], x.shape[1]
+    n = w.shape[1]
+    if k % 4 or k > 128 or n > 128 or k == 0 or n == 0:
+        return None
+    x = padded(x)
+    w = w.contiguous()
+    h = out if out is not None else empty_padded(m, n, device=x.device)
+    rc = L.aes_dev_gcn_layer_fused(ptr(srow_ptr), ptr(scol), ptr(sval), m, ptr(x), x.stride(0), k, ptr(w),
+                                   w.stride(0), n, ptr(b) if b is not None else None, int(relu), int(finite_w),
+                                   ptr(h), h.stride(0), stream_of(stream))
+    if rc == capi.AES_ERR_UNSUPPORTED:
+        return None
+    check(rc)
+    return h
+
+
 def gcn_forward(graph: Graph, x: torch.Tensor, weights, biases, plan: SampledPlan | None = None,
-                stream=None, fast_gemm: bool = False, finite=None) -> torch.Tensor:
+                stream=None, fast_gemm: bool = False, finite=None, fused: bool = True) -> torch.Tensor:
     """gcn_forward (proj/src/gnn.cpp:66-78) on one GPU, all tensors in HBM.
     fast_gemm=True runs the layer transform on the tcgen05 tensor cores (TF32,
     not bit-exact); the aggregation stays the exact sampled SpMM.  finite:
@@ -418,6 +442,12 @@ def gcn_forward(graph: Graph, x: torch.Tensor, weights, biases, plan: SampledPla
     if finite is None:
         finite = all_weights_finite(weights, stream)  # one read-back for every layer
     for l, (w, b) in enumerate(zip(weights, biases)):
+        relu = l + 1 < len(weights)
+        if fused and not fast_gemm and bound:  # sampled plan: rows bounded, one fused kernel
+            hf = gcn_layer_fused(srow, scol, sval, h, w, b, relu, finite_w=finite[l], stream=stream)
+            if hf is not None:
+                h = hf
+                continue
         agg = spmm(srow, scol, sval, h, stream=stream, max_row_slots=bound)
         if fast_gemm and agg.shape[1] <= 128 and w.shape[1] <= 128:
             h = gemm_tf32(agg, w, b, relu=l + 1 < len(weights), stream=stream)

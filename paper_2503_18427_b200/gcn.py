@@ -86,6 +86,9 @@ class Ops:
     fit_params: Callable | None = None
     quantize: Callable | None = None
     spmm_q8: Callable | None = None
+    # fused exact layer: layer(srow, scol, sval, H, W, bias, relu, finite_w, out)
+    # -> out, or None when the shape is outside the fused kernel (then spmm + gemm)
+    layer: Callable | None = None
 
 
 def cuda_ops(max_row_slots: int = 0) -> Ops:
@@ -103,6 +106,9 @@ def cuda_ops(max_row_slots: int = 0) -> Ops:
         spmm_q8=lambda srow, scol, sval, codes, lo, hi, out=None: device.spmm_q8(
             srow, scol, sval, device.QuantizedDevice(codes, lo, hi, 8, device.dequant_lut(lo, hi, 8, codes.device)),
             out=out, max_row_slots=max_row_slots),
+        # (sampled plans only: the fused kernel's producer warps want bounded rows)
+        layer=(lambda srow, scol, sval, h, w, b, relu, finite_w, out=None: device.gcn_layer_fused(
+            srow, scol, sval, h, w, b, relu, finite_w=finite_w, out=out)) if max_row_slots else None,
     )
 
 
@@ -143,6 +149,12 @@ class ShardedGCN:
         self._xbufs = {}  # NCCL exchange: persistent per-layer all-gather buffers
         self.replicas = None
         self.halo = False
+        # fused-layer path: finite W lets the kernel drop the reference's
+        # a == 0 select (result-neutral then, gemm.cu); checked once here
+        self.layer_finite = [False] * len(weights)
+        if self.ops.layer is not None:
+            from . import device
+            self.layer_finite = device.all_weights_finite(weights)
         if halo and exchange != "p2p":
             raise ValueError("halo exchange needs exchange='p2p'")
         if exchange == "p2p":
@@ -266,6 +278,19 @@ class ShardedGCN:
         statuses = []
         n_layers = len(self.weights)
         for l, (w, b) in enumerate(zip(self.weights, self.biases)):
+            fo = w.shape[1]
+            last = l + 1 == n_layers
+            if (hq is None and self.ops.layer is not None and rows and not return_shard
+                    and not (self.qx and not last)):
+                # fp32 layer as ONE kernel (SpMM producer warps + ordered-GEMM
+                # consumer warps) writing this rank's rows of the next replica
+                hbuf = self._exchange_buf(l, fo, torch.float32, x)
+                dst = self._my_slice(hbuf, fo)
+                res = self.ops.layer(self.srow, self.scol, self.sval, h, w, b, not last, self.layer_finite[l], out=dst)
+                if res is not None:
+                    _into(dst, res)
+                    h = self._gather_inplace(hbuf, fo)
+                    continue
             if hq is None:
                 agg = self.ops.spmm(self.srow, self.scol, self.sval, h,
                                     out=self.ops.alloc(max(rows, 1), h.shape[1], h))
@@ -331,6 +356,19 @@ class ShardedGCN:
         rows = self.hi - self.lo
         n_layers = len(self.weights)
         for l, (w, b) in enumerate(zip(self.weights, self.biases)):
+            fo = w.shape[1]
+            last = l + 1 == n_layers
+            if (hq is None and self.ops.layer is not None and rows and not return_shard
+                    and not (self.qx and not last)):
+                # fp32 layer as ONE kernel (SpMM producer warps + ordered-GEMM
+                # consumer warps) writing this rank's rows of the next replica
+                hbuf = self._exchange_buf(l, fo, torch.float32, x)
+                dst = self._my_slice(hbuf, fo)
+                res = self.ops.layer(self.srow, self.scol, self.sval, h, w, b, not last, self.layer_finite[l], out=dst)
+                if res is not None:
+                    _into(dst, res)
+                    h = self._gather_inplace(hbuf, fo)
+                    continue
             if hq is None:
                 agg = self.ops.spmm(self.srow, self.scol, self.sval, h,
                                     out=self.ops.alloc(max(rows, 1), h.shape[1], h))
@@ -338,8 +376,6 @@ class ShardedGCN:
                 codes, lo, hi = hq
                 agg = self.ops.spmm_q8(self.srow, self.scol, self.sval, codes, lo, hi,
                                        out=self.ops.alloc(max(rows, 1), codes.shape[1], x))
-            fo = w.shape[1]
-            last = l + 1 == n_layers
             quant = self.qx and not last
             if return_shard and last:
                 return self.ops.gemm_bias_act(agg[:rows] if rows else agg[:0], w, b, relu=False,

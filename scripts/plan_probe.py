@@ -29,7 +29,7 @@ ws = torch.empty(ws_b, dtype=torch.uint8, device="cuda")
 st = stream_of(None)
 s.record()
 for _ in range(10):
-    L.aes_dev_sample_plan(ptr(rp), n, 32, 0, ptr(p.srow_ptr), ptr(p.row_params), ptr(ws), ws_b, st)
+    L.aes_dev_sample_plan(ptr(rp), n, 32, 0, ptr(p.srow_ptr), None, ptr(ws), ws_b, st)
 e.record()
 torch.cuda.synchronize()
 print(f"  row scan kernel: {s.elapsed_time(e) / 10:.3f} ms")

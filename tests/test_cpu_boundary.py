@@ -62,7 +62,7 @@ def test_exact_kernels_never_fuse_multiply_add():
     if not shutil.which("cuobjdump"):
         pytest.skip("cuobjdump missing")
     funcs = _sass_by_function()
-    crit = [f for f in funcs if re.search(r"spmm|gemm|dequantize_kernel|(?<!fold_params_)lut_kernel|gcn_fill", f)
+    crit = [f for f in funcs if re.search(r"spmm|gemm|gcn_layer_fused|dequantize_kernel|(?<!fold_params_)lut_kernel|gcn_fill", f)
             and not re.search(r"q8a|q8r|affine|q8t_kernelILi1E", f)]  # int8 fast mode: bounded, not exact
     assert len(crit) >= 10
     # (HFMA2.MMA with RZ operands is ptxas's move-immediate idiom, not arithmetic)

@@ -182,7 +182,7 @@ def test_async_host_call_matches_sync():
     L.aes_csr_destroy(h)
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5, 6, 7, 8, 21, 22, 23, 24, 30, 31, 32, 33, 34, 35, 36, 37, 38, 39, 40])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5, 6, 7, 8, 21, 22, 23, 24, 30, 31, 32, 33, 34, 35, 36, 37, 38, 39, 40, 43, 44, 45])
 def test_every_spmm_schedule_is_bit_exact(dev, variant):
     """All schedule variants (aes_dev_spmm_set_variant) give the oracle's bits,
     fp32 and int8 (int8 dual-stream kernel: variants 21-24; int8 batch kernel:

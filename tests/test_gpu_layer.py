@@ -1,0 +1,111 @@
+"""Fused exact GCN layer (aes_dev_gcn_layer_fused, csrc/spmm.cu): one
+persistent kernel whose producer warps gather the aggregate into shared
+memory and whose consumer warps run the ordered GEMM.  Bit-identical to the
+split kernels (spmm -> gemm_bias_act) and to the CPU oracle's
+gcn layer (proj/src/gnn.cpp:66-78 for one layer)."""
+import numpy as np
+import pytest
+
+from oracle import port
+from tests import graphs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    from paper_2503_18427_b200 import device
+    return device
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+
+
+def to_np(t):
+    return t.cpu().numpy()
+
+
+@pytest.mark.parametrize("k,n_out", [(128, 128), (128, 40), (64, 128), (100, 7), (4, 1), (128, 100)])
+@pytest.mark.parametrize("strategy", ["adaptive", "afs", "sfs"])
+def test_fused_layer_matches_split_and_oracle(dev, k, n_out, strategy):
+    import torch
+    rng = np.random.default_rng(k * 1000 + n_out)
+    n = 2000 + 77  # partial last 128-row tile
+    rp, col, _ = graphs.power_law(n, alpha=1.7, max_deg=400, seed=k + n_out)
+    val = rng.uniform(-1, 1, col.size).astype(np.float32)
+    g = dev.Graph.from_numpy(rp, col, val)
+    plan = dev.SampledPlan(g, 32, strategy)
+    x = rng.uniform(-1, 1, (n, k)).astype(np.float32)
+    x[rng.random((n, k)) < 0.2] = 0.0  # zeros: the reference's a == 0 skip must stay neutral
+    w = rng.uniform(-0.5, 0.5, (k, n_out)).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, n_out).astype(np.float32)
+    xt, wt, bt = (torch.from_numpy(a).cuda() for a in (x, w, b))
+    for relu in (True, False):
+        fused = dev.gcn_layer_fused(plan.srow_ptr, plan.scol, plan.sval, xt, wt, bt, relu)
+        assert fused is not None
+        agg = dev.spmm(plan.srow_ptr, plan.scol, plan.sval, xt, max_row_slots=plan.row_bound)
+        split = dev.gemm_bias_act(agg, wt, bt, relu=relu)
+        torch.cuda.synchronize()
+        assert np.array_equal(bits(to_np(fused)), bits(to_np(split)))
+    want = port.gcn_forward(rp, col, val, x, [w], [b], 32) if strategy == "adaptive" else None
+    if want is not None:  # one layer, last layer: no ReLU
+        got = dev.gcn_layer_fused(plan.srow_ptr, plan.scol, plan.sval, xt, wt, bt, False)
+        assert np.array_equal(bits(to_np(got)), bits(want))
+
+
+def test_fused_layer_nonfinite_weights_keep_the_skip(dev):
+    """W with inf: the reference skips a == 0 (0 * inf would be NaN); the
+    fused kernel's finite_w = 0 form must too."""
+    import torch
+    rng = np.random.default_rng(5)
+    n, k, n_out = 600, 128, 64
+    rp, col, _ = graphs.power_law(n, alpha=1.9, max_deg=100, seed=5)
+    val = rng.uniform(-1, 1, col.size).astype(np.float32)
+    g = dev.Graph.from_numpy(rp, col, val)
+    plan = dev.SampledPlan(g, 16)
+    x = rng.uniform(-1, 1, (n, k)).astype(np.float32)
+    x[:, 3] = 0.0
+    w = rng.uniform(-0.5, 0.5, (k, n_out)).astype(np.float32)
+    w[3, :] = np.inf
+    xt, wt = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
+    b = torch.zeros(n_out, device="cuda")
+    fused = dev.gcn_layer_fused(plan.srow_ptr, plan.scol, plan.sval, xt, wt, b, False, finite_w=False)
+    agg = dev.spmm(plan.srow_ptr, plan.scol, plan.sval, xt, max_row_slots=plan.row_bound)
+    split = dev.gemm_bias_act(agg, wt, b, relu=False, finite_w=False)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(to_np(fused)), bits(to_np(split)))
+    want = port.gcn_forward(rp, col, val, x, [w], [np.zeros(n_out, np.float32)], 16)
+    assert np.array_equal(bits(to_np(fused)), bits(want))
+
+
+def test_fused_layer_unsupported_shapes_fall_back(dev):
+    import torch
+    rng = np.random.default_rng(6)
+    n = 300
+    rp, col, _ = graphs.power_law(n, alpha=2.0, max_deg=50, seed=6)
+    g = dev.Graph.from_numpy(rp, col, np.ones(col.size, np.float32))
+    plan = dev.SampledPlan(g, 32)
+    for k, n_out in [(130, 16), (6, 16), (128, 129)]:
+        xt = torch.from_numpy(rng.uniform(-1, 1, (n, k)).astype(np.float32)).cuda()
+        wt = torch.from_numpy(rng.uniform(-1, 1, (k, n_out)).astype(np.float32)).cuda()
+        assert dev.gcn_layer_fused(plan.srow_ptr, plan.scol, plan.sval, xt, wt, None, True) is None
+
+
+def test_fused_gcn_forward_arxiv_shape(dev):
+    """3-layer GCN at the arxiv shape through gcn_forward (fused layers) ==
+    the split-kernel forward, bit for bit."""
+    import torch
+    from paper_2503_18427_b200 import synth
+    n = 169_343
+    rp, col, val = synth.power_law_csr(n, 2.0737, 13_161, seed=3, device="cuda")
+    g = dev.Graph(rp, col, val, n)
+    plan = dev.SampledPlan(g, 32)
+    x = synth.features(n, 128, seed=4, device="cuda")
+    gen = torch.Generator(device="cuda").manual_seed(9)
+    ws = [torch.rand(s, generator=gen, device="cuda") - 0.5 for s in [(128, 128), (128, 128), (128, 40)]]
+    bs = [torch.full((s,), 0.01, device="cuda") for s in (128, 128, 40)]
+    fused = dev.gcn_forward(g, x, ws, bs, plan)
+    split = dev.gcn_forward(g, x, ws, bs, plan, fused=False)
+    torch.cuda.synchronize()
+    assert torch.equal(fused.view(torch.int32), split.view(torch.int32))
