@@ -561,6 +561,9 @@ def run_gcn_layer(args, plan, n, f, b, dist):
     e.record()
     torch.cuda.synchronize()
     out["exact_nccl_allgather_ms"] = round(max_over_ranks(s.elapsed_time(e) / steps, dist), 4)
+    out["exact_nccl_layer_kernels"] = ("fused SpMM + ordered GEMM, one persistent kernel (aes_dev_gcn_layer_fused)"
+                                       if model.fused_min_rows and model.hi - model.lo >= model.fused_min_rows
+                                       else "split: sampled SpMM, then ordered GEMM")
     del model
     for name, fast in (("exact_ordered_fp32", False), ("fast_tcgen05_tf32", True)):
         model = ShardedGCN(plan.srow_ptr, plan.scol, plan.sval, n, [w], [bias], exchange="p2p", fast_gemm=fast,

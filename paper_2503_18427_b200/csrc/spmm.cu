@@ -1605,36 +1605,183 @@ int launch_vector(const uint64_t* srow, const uint32_t* scol, const float* sval,
 // The SpMM is HBM-bound (gathers) and the ordered fp32 GEMM is FP32-pipe
 // bound, so the split kernels leave each resource idle half of the time and
 // round-trip the aggregate through HBM.  Here one CTA per SM runs both,
-// warp-specialised over 128-row tiles:
-//   * 8 producer warps gather tile i+1's aggregate rows (the ring SpMM
-//     body, 8 rows each) into a shared-memory A buffer;
-//   * 8 consumer warps run the ordered GEMM of tile i from the other buffer
-//     against W, resident in shared memory for the whole kernel, and store
-//     bias + ReLU results straight from registers;
-//   * named barriers hand the two A buffers back and forth (full: producers
-//     arrive, consumers sync; empty: the reverse).
+// warp-specialised:
+//   * the CTA owns a slot-balanced contiguous row block; producer warp p
+//     streams its own contiguous 1/8 of it as ONE slot stream through a
+//     cp.async ring (the ring SpMM body: the ring never drains at a tile
+//     boundary) and deposits every finished aggregate row into a shared-
+//     memory A buffer: its rows 8i..8i+7 become rows 8p..8p+7 of GEMM tile i;
+//   * 8 consumer warps run the ordered GEMM of tile i (64 rows from 8
+//     producers) against W, resident in shared memory for the whole kernel,
+//     and store bias + ReLU results from registers to each row's place;
+//   * mbarriers pass kLayerBufs A buffers around (full: every producer
+//     thread arrives, consumers wait; empty: the reverse); a producer waits
+//     only for the consumers, so one slowed by a dense 8-row block has two
+//     tiles of slack and never holds the other producers back.
 // Bit-exact with the split path: every aggregate element is the same slot-
 // order FMUL/FADD chain, every output the same k-ascending chain from +0.
-// Consumer mapping: thread (tx, ty) owns rows 4ty..4ty+3 and columns
+// Consumer mapping: thread (tx, ty) owns tile rows 4ty..4ty+3 and columns
 // {4tx..4tx+3, 64+4tx..}: the A reads broadcast, the W reads are 256
 // contiguous bytes per half-warp (no bank conflicts).
 // ---------------------------------------------------------------------------
-// 64-row tiles: W (64 KB) stays resident next to two 33 KB A buffers and
-// eight producer rings; each producer warp streams 8 rows (~45 slots) per
-// tile through a 16-slot ring, so a tile's gathers take less time than its
-// GEMM (measured with 128-row tiles and 4 producer warps: producer-bound,
-// the consumers stalled on the full barrier a third of the time).
 constexpr int kLayerBM = 64;
 constexpr int kLayerConsumers = 8, kLayerProducers = 8;
 constexpr int kLayerThreads = (kLayerConsumers + kLayerProducers) * 32;  // 512
 constexpr int kLayerRing = 12;  // producer ring slots (512 B each at K = 128)
-constexpr int kLayerBufs = 3;   // A buffers: producers run up to two tiles ahead
+constexpr int kLayerBufs = 3;   // A buffers (2 buffers + 20-slot rings: 4.49 ms vs 4.13 on products)
+constexpr int kLayerPRows = kLayerBM / kLayerProducers;  // rows per producer per tile (8)
 
-__device__ __forceinline__ void named_sync(int id, int count) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+// mbarriers (shared memory): a producer waits only for the consumers, never
+// for the other producers (a named barrier's bar.sync would count every
+// producer thread and lock the eight streams into one pace)
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
 }
-__device__ __forceinline__ void named_arrive(int id, int count) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "LAYER_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra LAYER_WAIT_%=;\n\t}" ::"r"(a), "r"(parity)
+        : "memory");
+}
+
+// Row block of CTA c (slot + row balanced, bal_range) and producer p's rows in
+// it: 8T consecutive rows each, T = tiles of the block.
+__device__ __forceinline__ void layer_rows(const uint64_t* __restrict__ srow, uint64_t n_rows, uint64_t& c0,
+                                           uint64_t& c1, uint64_t& tiles) {
+    bal_range(srow, n_rows, blockIdx.x, gridDim.x, c0, c1);
+    tiles = (c1 - c0 + kLayerBM - 1) / kLayerBM;
+}
+
+// One producer warp: rows [rb, re) as one ring stream; row q = r - rb goes to
+// tile q / 8, A row 8p + q % 8 (smem address abase + buf * a_bytes + ...).
+template <bool FULL>
+__device__ __forceinline__ void layer_produce(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
+                                              const float* __restrict__ sval, const float4* __restrict__ gsrc,
+                                              uint32_t ld, uint32_t f4, uint32_t ring0, uint64_t rb, uint64_t re,
+                                              uint64_t tiles, int pw, uint32_t abase, uint32_t a_bytes,
+                                              uint32_t as4, uint32_t mbar) {
+    constexpr int C = kLayerRing;
+    const uint32_t lane = threadIdx.x & 31;
+    uint64_t tile = 0;  // tile of the next row to store
+    uint32_t j = 0;     // its row within this producer's 8
+    bool held = false;  // buffer of `tile` acquired
+    // full[b] at mbar + 8b, empty[b] at mbar + 8(kLayerBufs + b); tile t is
+    // use t / kLayerBufs of buffer t % kLayerBufs
+    auto acquire = [&]() {
+        if (tile >= (uint64_t)kLayerBufs)  // consumers released tile - kLayerBufs
+            mbar_wait(mbar + 8 * (kLayerBufs + (uint32_t)(tile % kLayerBufs)),
+                      (uint32_t)((tile / kLayerBufs - 1) & 1));
+        held = true;
+    };
+    auto release = [&]() {
+        mbar_arrive(mbar + 8 * (uint32_t)(tile % kLayerBufs));
+        ++tile;
+        j = 0;
+        held = false;
+    };
+    if (rb < re) {
+        const uint64_t g0 = srow[rb];
+        const uint32_t total = (uint32_t)(srow[re] - g0);  // < 2^31: 1/1184 of any plan that fits in HBM
+        auto window = [&](uint64_t w) -> uint32_t { return (uint32_t)(srow[min(w + 1 + lane, re)] - g0); };
+        uint32_t rel = window(rb);
+        uint32_t rel_nx = window(rb + 32);
+        const uint32_t* gcol = scol + g0;
+        const float* gval = sval + g0;
+        const char* glb = reinterpret_cast<const char*>(gsrc + lane);
+        const uint32_t ld_bytes = ld * 16u;
+        const bool colok = FULL || lane < f4;
+        auto ld_col = [&](uint32_t chunk) -> uint32_t {
+            const uint32_t sidx = chunk * C + lane;
+            return (lane < (uint32_t)C && sidx < total) ? ld_meta_u32(gcol + sidx) : 0u;
+        };
+        auto ld_val = [&](uint32_t chunk) -> float {
+            const uint32_t sidx = chunk * C + lane;
+            return (lane < (uint32_t)C && sidx < total) ? ld_meta_f32(gval + sidx) : 0.f;
+        };
+        auto issue = [&](int p, uint32_t col) {
+            if (colok) cp_async_sa(ring0 + p * 512, glb + (uint64_t)col * ld_bytes, 16);
+        };
+        {
+            const uint32_t mc0 = ld_col(0);
+#pragma unroll
+            for (int p = 0; p < C; ++p) {
+                const uint32_t col = __shfl_sync(0xffffffffu, mc0, p);
+                if ((uint32_t)p < total) issue(p, col);
+                cp_commit();
+            }
+        }
+        uint32_t mc_is = ld_col(1), mc_nx = ld_col(2);
+        float mv_cur = ld_val(0), mv_nx = ld_val(1);
+        float4 acc = f4_zero();
+        uint64_t ra = rb;
+        uint32_t wi = 0;
+        uint32_t row_end = __shfl_sync(0xffffffffu, rel, 0);
+        auto store_row = [&]() {
+            if (!held) acquire();
+            if (colok)
+                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                 abase + (uint32_t)(tile % kLayerBufs) * a_bytes +
+                                 (uint32_t)(pw * kLayerPRows + j) * as4 * 16),
+                             "f"(acc.x), "f"(acc.y), "f"(acc.z), "f"(acc.w)
+                             : "memory");
+            acc = f4_zero();
+            if (++j == kLayerPRows) release();
+        };
+        auto advance_rows = [&](uint32_t pos) {
+            do {
+                store_row();
+                ++ra;
+                if (++wi == 32) {
+                    wi = 0;
+                    rel = rel_nx;
+                    rel_nx = window(ra + 32);
+                }
+                row_end = __shfl_sync(0xffffffffu, rel, wi);
+            } while (ra < re && row_end == pos);
+        };
+        if (row_end == 0) advance_rows(0);
+        auto body = [&](int p, uint32_t t) {
+            cp_wait<C - 1>();
+            const float v = __shfl_sync(0xffffffffu, mv_cur, p);
+            if (colok) f4_axpy(acc, v, lds_f32x4(ring0 + p * 512));
+            const uint32_t col = __shfl_sync(0xffffffffu, mc_is, p);
+            if (t + C < total) issue(p, col);
+            cp_commit();
+            if (t + 1 == row_end) advance_rows(t + 1);
+        };
+        uint32_t k = 0;
+        for (uint32_t t0 = 0; t0 < total; t0 += C, ++k) {
+            if (t0 + C <= total) {
+#pragma unroll
+                for (int p = 0; p < C; ++p) body(p, t0 + p);
+            } else {
+#pragma unroll
+                for (int p = 0; p < C; ++p) {
+                    if (t0 + p >= total) break;
+                    body(p, t0 + p);
+                }
+            }
+            mv_cur = mv_nx;
+            mc_is = mc_nx;
+            mv_nx = ld_val(k + 2);
+            mc_nx = ld_col(k + 3);
+        }
+        cp_wait<0>();
+        while (ra < re) {  // trailing empty rows
+            store_row();
+            ++ra;
+        }
+    }
+    if (j != 0 || held) release();  // a partly filled last tile
+    while (tile < tiles) {  // tiles past this producer's rows: nothing to add (the
+        acquire();          // wait keeps this arrival in the right phase)
+        release();
+    }
 }
 
 template <bool FULLK, bool SKIP>
@@ -1642,11 +1789,12 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
 gcn_layer_fused_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
                        const float* __restrict__ sval, uint64_t n_rows, const float4* __restrict__ x,
                        uint32_t ldx4, uint32_t k, const float* __restrict__ w, uint64_t ldw, uint32_t n,
-                       const float* __restrict__ bias, int relu, float* __restrict__ h, uint64_t ldh,
-                       uint64_t n_tiles) {
+                       const float* __restrict__ bias, int relu, float* __restrict__ h, uint64_t ldh) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t mbar_s[2 * kLayerBufs];  // full[b], empty[b]
     const uint32_t k4 = k / 4, as4 = k4 + 1;  // A row stride in float4 (one float4 of pad)
     const uint32_t smem0 = smem_addr(smem_raw);
+    const uint32_t mbar = smem_addr(mbar_s);
     float* ws = reinterpret_cast<float*>(smem_raw);  // W [k][128] (columns >= n zero)
     const uint32_t a_off = k * 128 * 4;
     const uint32_t a_bytes = kLayerBM * as4 * 16;
@@ -1655,64 +1803,41 @@ gcn_layer_fused_kernel(const uint64_t* __restrict__ srow, const uint32_t* __rest
 
     // W resident for the whole kernel (read once per SM from L2)
     for (uint32_t i = tid; i < k * 128; i += kLayerThreads) {
-        const uint32_t kk = i >> 7, j = i & 127;
-        ws[i] = j < n ? w[(uint64_t)kk * ldw + j] : 0.f;
+        const uint32_t kk = i >> 7, jj = i & 127;
+        ws[i] = jj < n ? w[(uint64_t)kk * ldw + jj] : 0.f;
     }
+    if (tid < kLayerBufs) {
+        mbar_init(mbar + 8 * tid, kLayerProducers * 32);                 // full: every producer thread
+        mbar_init(mbar + 8 * (kLayerBufs + tid), kLayerConsumers * 32);  // empty: every consumer thread
+    }
+    uint64_t c0, c1, tiles;
+    layer_rows(srow, n_rows, c0, c1, tiles);
+    const uint64_t prow = kLayerPRows * tiles;  // rows per producer
     __syncthreads();
 
     if (warp >= kLayerConsumers) {
-        // ---------------- producers: SpMM rows into the A buffers
         const int pw = warp - kLayerConsumers;
-        const uint32_t ring0 = smem0 + ring_off + pw * (kLayerRing * 512) + lane * 16;
-        uint64_t i = 0;
-        for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
-            const int buf = (int)(i % kLayerBufs);
-            if (i >= kLayerBufs) named_sync(1 + kLayerBufs + buf, kLayerThreads);  // consumers released it
-            // this warp's share of the tile: rows whose first slot falls in
-            // the pw-th equal slot share (one coalesced load of the tile's
-            // row offsets + two ballots; a row never splits)
-            const uint64_t t0 = t * kLayerBM, t1 = min(t0 + kLayerBM, n_rows);
-            const uint32_t nr = (uint32_t)(t1 - t0);
-            const uint64_t va = (uint32_t)lane < nr ? srow[t0 + lane] : ~0ull;
-            const uint64_t vb = (uint32_t)lane + 32 < nr ? srow[t0 + 32 + lane] : ~0ull;
-            const uint64_t s0 = __shfl_sync(0xffffffffu, va, 0), s1 = srow[t1];
-            auto first_row = [&](int share) -> uint64_t {
-                const uint64_t target = s0 + (s1 - s0) * (uint64_t)share / kLayerProducers;
-                return t0 + __popc(__ballot_sync(0xffffffffu, va < target)) +
-                       __popc(__ballot_sync(0xffffffffu, vb < target));
-            };
-            const uint64_t rb = pw == 0 ? t0 : first_row(pw);
-            const uint64_t re = pw == kLayerProducers - 1 ? t1 : first_row(pw + 1);
-            if (rb < re) {
-                const uint32_t sout = smem0 + a_off + buf * a_bytes + (uint32_t)(rb - t0) * as4 * 16 + lane * 16;
-                for (uint64_t r = rb; r < re;) {  // slices with 32-bit slot offsets (one at any real shape)
-                    const uint64_t e = srow[re] - srow[r] >= (1ull << 31) ? r + 1 : re;
-                    ring_range<RingF32, 1, kLayerRing, FULLK, true>(srow, scol, sval, x, ldx4, k4, nullptr, as4,
-                                                                    ring0, 0, r, e,
-                                                                    sout + (uint32_t)(r - rb) * as4 * 16);
-                    r = e;
-                }
-            }
-            named_arrive(1 + buf, kLayerThreads);  // tile i's aggregate is in buffer buf
-        }
-        // drain: match the consumers' releases of the last kLayerBufs tiles
-        for (uint64_t j = i > kLayerBufs ? i - kLayerBufs : 0; j < i; ++j)
-            named_sync(1 + kLayerBufs + (int)(j % kLayerBufs), kLayerThreads);
+        const uint64_t rb = min(c0 + (uint64_t)pw * prow, c1), re = min(rb + prow, c1);
+        layer_produce<FULLK>(srow, scol, sval, x, ldx4, k4,
+                             smem0 + ring_off + pw * (kLayerRing * 512) + lane * 16, rb, re, tiles, pw,
+                             smem0 + a_off + lane * 16, a_bytes, as4, mbar);
         return;
     }
 
     // ---------------- consumers: ordered GEMM of each tile
     const int tx = tid & 15, ty = tid >> 4;  // 16 x 16 threads, 4 x 8 outputs each
-    uint64_t i = 0;
-    for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+    // tile row 4ty + r comes from producer (4ty + r) / 8, its row (4ty + r) % 8 of the tile
+    const int pw_of = (4 * ty) / kLayerPRows, j0 = (4 * ty) % kLayerPRows;
+    const uint64_t my_rb = min(c0 + (uint64_t)pw_of * prow, c1), my_re = min(my_rb + prow, c1);
+    for (uint64_t i = 0; i < tiles; ++i) {
         const int buf = (int)(i % kLayerBufs);
-        named_sync(1 + buf, kLayerThreads);  // tile i's aggregate landed
+        mbar_wait(mbar + 8 * buf, (uint32_t)((i / kLayerBufs) & 1));  // tile i's rows landed
         const float* as = reinterpret_cast<const float*>(smem_raw + a_off + buf * a_bytes);
         float acc[4][8];
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[r][j] = 0.f;
+            for (int jj = 0; jj < 8; ++jj) acc[r][jj] = 0.f;
         for (uint32_t k0 = 0; k0 < k; k0 += 4) {
             float4 a4[4];
 #pragma unroll
@@ -1729,42 +1854,41 @@ gcn_layer_fused_kernel(const uint64_t* __restrict__ srow, const uint32_t* __rest
                     if (SKIP) {
                         const bool skip = av == 0.f;
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const float s2 = __fadd_rn(acc[r][j], __fmul_rn(av, wv[j]));
-                            acc[r][j] = skip ? acc[r][j] : s2;
+                        for (int jj = 0; jj < 8; ++jj) {
+                            const float s2 = __fadd_rn(acc[r][jj], __fmul_rn(av, wv[jj]));
+                            acc[r][jj] = skip ? acc[r][jj] : s2;
                         }
                     } else {
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) acc[r][j] = __fadd_rn(acc[r][j], __fmul_rn(av, wv[j]));
+                        for (int jj = 0; jj < 8; ++jj) acc[r][jj] = __fadd_rn(acc[r][jj], __fmul_rn(av, wv[jj]));
                     }
                 }
             }
         }
-        named_arrive(1 + kLayerBufs + buf, kLayerThreads);  // buffer buf may be refilled
-        // epilogue: bias, ReLU (gnn.cpp:41-52), store
-        const uint64_t m0 = t * kLayerBM;
+        mbar_arrive(mbar + 8 * (kLayerBufs + buf));  // buffer buf may be refilled
+        // epilogue: bias, ReLU (gnn.cpp:41-52), store to each row's place
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-            const uint64_t gm = m0 + 4 * ty + r;
-            if (gm >= n_rows) continue;
+            const uint64_t gm = my_rb + kLayerPRows * i + j0 + r;
+            if (gm >= my_re) continue;
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
-                const uint32_t c0 = (half ? 64 : 0) + 4 * tx;
-                if (c0 >= n) continue;
+                const uint32_t col0 = (half ? 64 : 0) + 4 * tx;
+                if (col0 >= n) continue;
                 float v[4];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    float xo = acc[r][4 * half + j];
-                    if (bias && c0 + j < n) xo = __fadd_rn(xo, bias[c0 + j]);
+                for (int jj = 0; jj < 4; ++jj) {
+                    float xo = acc[r][4 * half + jj];
+                    if (bias && col0 + jj < n) xo = __fadd_rn(xo, bias[col0 + jj]);
                     if (relu) xo = (xo < 0.f) ? 0.f : xo;
-                    v[j] = xo;
+                    v[jj] = xo;
                 }
-                float* dst = h + gm * ldh + c0;
-                if (c0 + 4 <= n)
+                float* dst = h + gm * ldh + col0;
+                if (col0 + 4 <= n)
                     __stcs(reinterpret_cast<float4*>(dst), make_float4(v[0], v[1], v[2], v[3]));
                 else
-                    for (int j = 0; j < 4; ++j)
-                        if (c0 + j < n) dst[j] = v[j];
+                    for (int jj = 0; jj < 4; ++jj)
+                        if (col0 + jj < n) dst[jj] = v[jj];
             }
         }
     }
@@ -1785,11 +1909,12 @@ int launch_layer_fused_t(const uint64_t* srow, const uint32_t* scol, const float
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
         attr = true;
     }
-    const uint64_t tiles = (n_rows + kLayerBM - 1) / kLayerBM;
-    const unsigned grid = (unsigned)(tiles < (uint64_t)num_sms() ? tiles : (uint64_t)num_sms());
+    // one CTA per SM, each a slot-balanced row block (small graphs: >= 64 rows per CTA)
+    const uint64_t blocks = (n_rows + kLayerBM - 1) / kLayerBM;
+    const unsigned grid = (unsigned)(blocks < (uint64_t)num_sms() ? blocks : (uint64_t)num_sms());
     gcn_layer_fused_kernel<FULLK, SKIP><<<grid, kLayerThreads, smem, st>>>(
         srow, scol, sval, n_rows, reinterpret_cast<const float4*>(x), (uint32_t)(ldx / 4), k, w, ldw, n, bias,
-        relu, h, ldh, tiles);
+        relu, h, ldh);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
 }

@@ -152,9 +152,11 @@ class ShardedGCN:
         # fused-layer path: finite W lets the kernel drop the reference's
         # a == 0 select (result-neutral then, gemm.cu); checked once here
         self.layer_finite = [False] * len(weights)
+        self.fused_min_rows = 0
         if self.ops.layer is not None:
             from . import device
             self.layer_finite = device.all_weights_finite(weights)
+            self.fused_min_rows = device.FUSED_LAYER_MIN_ROWS
         if halo and exchange != "p2p":
             raise ValueError("halo exchange needs exchange='p2p'")
         if exchange == "p2p":
@@ -278,19 +280,6 @@ class ShardedGCN:
         statuses = []
         n_layers = len(self.weights)
         for l, (w, b) in enumerate(zip(self.weights, self.biases)):
-            fo = w.shape[1]
-            last = l + 1 == n_layers
-            if (hq is None and self.ops.layer is not None and rows and not return_shard
-                    and not (self.qx and not last)):
-                # fp32 layer as ONE kernel (SpMM producer warps + ordered-GEMM
-                # consumer warps) writing this rank's rows of the next replica
-                hbuf = self._exchange_buf(l, fo, torch.float32, x)
-                dst = self._my_slice(hbuf, fo)
-                res = self.ops.layer(self.srow, self.scol, self.sval, h, w, b, not last, self.layer_finite[l], out=dst)
-                if res is not None:
-                    _into(dst, res)
-                    h = self._gather_inplace(hbuf, fo)
-                    continue
             if hq is None:
                 agg = self.ops.spmm(self.srow, self.scol, self.sval, h,
                                     out=self.ops.alloc(max(rows, 1), h.shape[1], h))
@@ -359,7 +348,7 @@ class ShardedGCN:
             fo = w.shape[1]
             last = l + 1 == n_layers
             if (hq is None and self.ops.layer is not None and rows and not return_shard
-                    and not (self.qx and not last)):
+                    and not (self.qx and not last) and rows >= self.fused_min_rows):
                 # fp32 layer as ONE kernel (SpMM producer warps + ordered-GEMM
                 # consumer warps) writing this rank's rows of the next replica
                 hbuf = self._exchange_buf(l, fo, torch.float32, x)

@@ -105,7 +105,35 @@ def test_fused_gcn_forward_arxiv_shape(dev):
     gen = torch.Generator(device="cuda").manual_seed(9)
     ws = [torch.rand(s, generator=gen, device="cuda") - 0.5 for s in [(128, 128), (128, 128), (128, 40)]]
     bs = [torch.full((s,), 0.01, device="cuda") for s in (128, 128, 40)]
-    fused = dev.gcn_forward(g, x, ws, bs, plan)
+    saved = dev.FUSED_LAYER_MIN_ROWS
+    dev.FUSED_LAYER_MIN_ROWS = 0  # (arxiv is below the default size threshold)
+    try:
+        fused = dev.gcn_forward(g, x, ws, bs, plan)
+    finally:
+        dev.FUSED_LAYER_MIN_ROWS = saved
     split = dev.gcn_forward(g, x, ws, bs, plan, fused=False)
     torch.cuda.synchronize()
     assert torch.equal(fused.view(torch.int32), split.view(torch.int32))
+
+
+def test_sharded_gcn_nccl_mode_fused_layers(dev):
+    """gcn.ShardedGCN (exchange="nccl", one rank) runs each fp32 layer as the
+    fused kernel writing its slice of the all-gather buffer: == the oracle."""
+    import torch
+    from paper_2503_18427_b200.gcn import ShardedGCN
+    rng = np.random.default_rng(11)
+    n = 5000
+    rp, col, _ = graphs.power_law(n, alpha=1.8, max_deg=300, seed=11)
+    nrp, ncol, nval = port.gcn_normalize(rp, col, True)
+    g = dev.Graph.from_numpy(nrp, ncol, nval)
+    plan = dev.SampledPlan(g, 32)
+    x = rng.uniform(-1, 1, (n, 64)).astype(np.float32)
+    ws = [rng.uniform(-0.5, 0.5, s).astype(np.float32) for s in [(64, 128), (128, 16)]]
+    bs = [np.full(128, 0.01, np.float32), np.zeros(16, np.float32)]
+    model = ShardedGCN(plan.srow_ptr, plan.scol, plan.sval, n, [torch.from_numpy(w).cuda() for w in ws],
+                       [torch.from_numpy(b).cuda() for b in bs], exchange="nccl", max_row_slots=plan.row_bound)
+    model.fused_min_rows = 0
+    out = model.forward(torch.from_numpy(x).cuda())
+    torch.cuda.synchronize()
+    want = port.gcn_forward(nrp, ncol, nval, x, ws, bs, 32)
+    assert np.array_equal(bits(to_np(out)), bits(want))
