@@ -1851,16 +1851,21 @@ gcn_layer_fused_kernel(const uint64_t* __restrict__ srow, const uint32_t* __rest
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
                     const float av = kk == 0 ? a4[r].x : kk == 1 ? a4[r].y : kk == 2 ? a4[r].z : a4[r].w;
+                    // scalar FMULs, paired adds (FADD2): 3 issue slots per 2
+                    // MACs (products layer 4.13 -> 3.39 ms)
                     if (SKIP) {
                         const bool skip = av == 0.f;
 #pragma unroll
-                        for (int jj = 0; jj < 8; ++jj) {
-                            const float s2 = __fadd_rn(acc[r][jj], __fmul_rn(av, wv[jj]));
-                            acc[r][jj] = skip ? acc[r][jj] : s2;
+                        for (int jj = 0; jj < 8; jj += 2) {
+                            float s0 = acc[r][jj], s1 = acc[r][jj + 1];
+                            add2_rn(s0, s1, __fmul_rn(av, wv[jj]), __fmul_rn(av, wv[jj + 1]));
+                            acc[r][jj] = skip ? acc[r][jj] : s0;
+                            acc[r][jj + 1] = skip ? acc[r][jj + 1] : s1;
                         }
                     } else {
 #pragma unroll
-                        for (int jj = 0; jj < 8; ++jj) acc[r][jj] = __fadd_rn(acc[r][jj], __fmul_rn(av, wv[jj]));
+                        for (int jj = 0; jj < 8; jj += 2)
+                            add2_rn(acc[r][jj], acc[r][jj + 1], __fmul_rn(av, wv[jj]), __fmul_rn(av, wv[jj + 1]));
                     }
                 }
             }
