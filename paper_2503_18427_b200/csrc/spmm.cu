@@ -684,12 +684,23 @@ spmm_hub_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ 
                 const uint32_t base = ring + (k % kChunks) * 32 * 128;
                 const uint32_t left = total - k * 32;  // >= 1
                 if (left >= 32) {  // whole chunk: no per-slot bound checks
+                    // per batch: every ring read and product first, then the
+                    // dependent add chain, then the refills — the chain is the
+                    // only serial part (one slot per ~4-cycle FADD instead of
+                    // a load-multiply-add round trip per slot)
 #pragma unroll
-                    for (uint32_t j = 0; j < 32; ++j) {
-                        if (j % kHubBatch == 0) cp_wait<kHubRing / kHubBatch - 1>();
-                        acc = __fadd_rn(acc, __fmul_rn(__shfl_sync(0xffffffffu, mv, j), lds_f32(base + j * 128)));
-                        issue_chunk_slot(base, j, __shfl_sync(0xffffffffu, mc_ahead, j));
-                        if (j % kHubBatch == kHubBatch - 1) cp_commit();
+                    for (uint32_t j0 = 0; j0 < 32; j0 += kHubBatch) {
+                        cp_wait<kHubRing / kHubBatch - 1>();
+                        float pr[kHubBatch];
+#pragma unroll
+                        for (uint32_t j = 0; j < kHubBatch; ++j)
+                            pr[j] = __fmul_rn(__shfl_sync(0xffffffffu, mv, j0 + j), lds_f32(base + (j0 + j) * 128));
+#pragma unroll
+                        for (uint32_t j = 0; j < kHubBatch; ++j) acc = __fadd_rn(acc, pr[j]);
+#pragma unroll
+                        for (uint32_t j = 0; j < kHubBatch; ++j)
+                            issue_chunk_slot(base, j0 + j, __shfl_sync(0xffffffffu, mc_ahead, j0 + j));
+                        cp_commit();
                     }
                 } else {  // last, partial chunk: nothing more is committed, so wait for all
                     cp_wait<0>();
@@ -1373,9 +1384,11 @@ int launch_q8_batch_t(const uint64_t* srow, const uint32_t* scol, const float* s
         // would leave one CTA for a second, nearly empty wave)
         const uint64_t per_wave = (uint64_t)num_sms() * occ / tiles;
         uint64_t per_tile = (per_wave ? per_wave : 1) * bal_waves(n, per_wave * WARPS, 0);
-        // small graphs (pubmed: 20 k rows): at least 8 rows per warp, so the
-        // 64 KB LUT fill of a CTA is not paid for a handful of slots
-        const uint64_t cap = (n + (uint64_t)WARPS * 8 - 1) / ((uint64_t)WARPS * 8);
+        // small graphs (pubmed: 20 k rows): at least 8 rows per warp (4 for
+        // the one-CTA-per-SM form, which would otherwise leave half the SMs
+        // idle), so the 64 KB LUT fill of a CTA is not paid for a handful of slots
+        const uint64_t min_rows = WARPS >= 32 ? 4 : 8;
+        const uint64_t cap = (n + (uint64_t)WARPS * min_rows - 1) / ((uint64_t)WARPS * min_rows);
         if (cap < per_tile) per_tile = cap ? cap : 1;
         spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 2><<<dim3((unsigned)per_tile, tiles), WARPS * 32, smem, st>>>(
             srow, scol, sval, n, q, (uint32_t)ldq, f4, c, ldc4, lut, 32, 0, nullptr);

@@ -1,8 +1,11 @@
 """Fused GEMM + exchange over CUDA-IPC peer memory (gcn.ShardedGCN with
-exchange="p2p").  This run has one GPU, so two ranks share cuda:0 as two
-processes: the IPC mapping, P2P epilogue stores, per-CTA system-scope
-arrivals and the device-side step barrier are exercised exactly as across
-NVLink peers.  The result must equal the single-process oracle bit for bit."""
+exchange="p2p").  Rank r runs on cuda:(r % device_count): on a multi-GPU box
+the ranks sit on distinct devices and the epilogue stores cross NVLink; on a
+one-GPU box two ranks share cuda:0 as two processes, and the IPC mapping,
+P2P epilogue stores, per-CTA system-scope arrivals and the device-side step
+barrier are exercised exactly as across NVLink peers.  The result must
+equal the single-process oracle bit for bit.  The NCCL all-gather mode runs
+across two real devices when the box has them (skipped otherwise)."""
 import os
 import socket
 
@@ -38,7 +41,7 @@ def _run(rank, world, port_no, q, fast=False, exchange_dtype="f32", halo=False):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
-    torch.cuda.set_device(0)
+    torch.cuda.set_device(rank % torch.cuda.device_count())  # distinct devices when the box has them
     if world > 1:
         dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -174,3 +177,56 @@ def test_p2p_halo_exchange_matches_oracle(exchange_dtype):
         if exchange_dtype == "f32":
             n_unsent, untouched, sent_filled = outs[3]
             assert n_unsent > 0 and untouched and sent_filled > 0.9
+
+
+def _run_nccl(rank, world, port_no, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        from paper_2503_18427_b200 import device
+        from paper_2503_18427_b200.gcn import ShardedGCN
+        nrp, ncol, nval, x, ws, bs = _problem()
+        g = device.Graph.from_numpy(nrp, ncol, nval)
+        plan = device.SampledPlan(g, 16)
+        outs = []
+        for fused_min in (0, 1 << 40):  # the fused layer kernel, then the split kernels
+            model = ShardedGCN(plan.srow_ptr, plan.scol, plan.sval, g.n_rows,
+                               [torch.from_numpy(w).cuda() for w in ws], [torch.from_numpy(b).cuda() for b in bs],
+                               exchange="nccl", max_row_slots=plan.row_bound)
+            model.fused_min_rows = fused_min
+            outs.append(model.forward(torch.from_numpy(x).cuda()).cpu().numpy())
+        q.put((rank, outs))
+    except Exception:
+        import traceback
+        q.put((rank, traceback.format_exc()))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_exchange_across_two_devices():
+    """ShardedGCN(exchange="nccl") with one rank per device over a real NCCL
+    communicator (NVLink between the two GPUs): bit-exact vs the oracle."""
+    import torch
+    import torch.multiprocessing as mp
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs (this box has one)")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = _free_port()
+    procs = [ctx.Process(target=_run_nccl, args=(r, 2, p, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = sorted([q.get(timeout=300) for _ in procs], key=lambda t: t[0])
+    for pr in procs:
+        pr.join(timeout=120)
+    for _, outs in res:
+        assert not isinstance(outs, str), outs
+    nrp, ncol, nval, x, ws, bs = _problem()
+    want = port.gcn_forward(nrp, ncol, nval, x, ws, bs, 16)
+    for _, outs in res:
+        for o in outs:
+            assert np.array_equal(np.ascontiguousarray(o).view(np.uint32), want.view(np.uint32))
