@@ -684,23 +684,12 @@ spmm_hub_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ 
                 const uint32_t base = ring + (k % kChunks) * 32 * 128;
                 const uint32_t left = total - k * 32;  // >= 1
                 if (left >= 32) {  // whole chunk: no per-slot bound checks
-                    // per batch: every ring read and product first, then the
-                    // dependent add chain, then the refills — the chain is the
-                    // only serial part (one slot per ~4-cycle FADD instead of
-                    // a load-multiply-add round trip per slot)
 #pragma unroll
-                    for (uint32_t j0 = 0; j0 < 32; j0 += kHubBatch) {
-                        cp_wait<kHubRing / kHubBatch - 1>();
-                        float pr[kHubBatch];
-#pragma unroll
-                        for (uint32_t j = 0; j < kHubBatch; ++j)
-                            pr[j] = __fmul_rn(__shfl_sync(0xffffffffu, mv, j0 + j), lds_f32(base + (j0 + j) * 128));
-#pragma unroll
-                        for (uint32_t j = 0; j < kHubBatch; ++j) acc = __fadd_rn(acc, pr[j]);
-#pragma unroll
-                        for (uint32_t j = 0; j < kHubBatch; ++j)
-                            issue_chunk_slot(base, j0 + j, __shfl_sync(0xffffffffu, mc_ahead, j0 + j));
-                        cp_commit();
+                    for (uint32_t j = 0; j < 32; ++j) {
+                        if (j % kHubBatch == 0) cp_wait<kHubRing / kHubBatch - 1>();
+                        acc = __fadd_rn(acc, __fmul_rn(__shfl_sync(0xffffffffu, mv, j), lds_f32(base + j * 128)));
+                        issue_chunk_slot(base, j, __shfl_sync(0xffffffffu, mc_ahead, j));
+                        if (j % kHubBatch == kHubBatch - 1) cp_commit();
                     }
                 } else {  // last, partial chunk: nothing more is committed, so wait for all
                     cp_wait<0>();

@@ -137,3 +137,28 @@ def test_sharded_gcn_nccl_mode_fused_layers(dev):
     torch.cuda.synchronize()
     want = port.gcn_forward(nrp, ncol, nval, x, ws, bs, 32)
     assert np.array_equal(bits(to_np(out)), bits(want))
+
+
+@pytest.mark.parametrize("n", [1, 2, 63, 64, 65, 1000, 9473 + 64 * 148])
+def test_fused_layer_small_and_ragged_graphs(dev, n):
+    """Row blocks smaller than one tile, CTAs with empty blocks, rows with no
+    slots (isolated rows), the partial last tile of every producer."""
+    import torch
+    rng = np.random.default_rng(n)
+    rp, col, _ = graphs.power_law(n, alpha=1.5, max_deg=min(n, 200), seed=n)
+    keep = rng.random(n) < 0.85  # ~15 % of the rows lose all their nonzeros
+    rows = [col[rp[i]:rp[i + 1]] if keep[i] else col[:0] for i in range(n)]
+    rp2 = np.zeros(n + 1, np.uint64)
+    rp2[1:] = np.cumsum([r.size for r in rows])
+    col2 = np.concatenate(rows).astype(np.uint32) if rp2[-1] else np.zeros(0, np.uint32)
+    val2 = rng.uniform(-1, 1, col2.size).astype(np.float32)
+    g = dev.Graph.from_numpy(rp2, col2, val2)
+    plan = dev.SampledPlan(g, 32)
+    x = rng.uniform(-1, 1, (n, 32)).astype(np.float32)
+    w = rng.uniform(-0.5, 0.5, (32, 24)).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, 24).astype(np.float32)
+    xt, wt, bt = (torch.from_numpy(a).cuda() for a in (x, w, b))
+    fused = dev.gcn_layer_fused(plan.srow_ptr, plan.scol, plan.sval, xt, wt, bt, True)
+    torch.cuda.synchronize()
+    want = port.bias_act(port.dense_matmul(port.spmm_sampled(rp2, col2, val2, x, 32), w), b, True)
+    assert np.array_equal(bits(to_np(fused)), bits(want))
