@@ -132,17 +132,11 @@ int upload_dense(const float* h, uint64_t rows, uint64_t cols, DBuf<float>& d, u
     if (rows == 0) return AES_OK;
     cudaStream_t st = lib_stream();
     if (ld != cols) AES_CUDA_TRY(cudaMemsetAsync(d.p, 0, rows * ld * sizeof(float), st));
-    if (cols)
-        AES_CUDA_TRY(cudaMemcpy2DAsync(d.p, ld * sizeof(float), h, cols * sizeof(float), cols * sizeof(float),
-                                       rows, cudaMemcpyHostToDevice, st));
-    return AES_OK;
+    return h2d_dense(h, rows, cols, d.p, ld, st);  // (pageable sources through the staging ring)
 }
 
 int download_dense(const float* d, uint64_t ld, uint64_t rows, uint64_t cols, float* h) {
-    if (rows == 0 || cols == 0) return AES_OK;
-    AES_CUDA_TRY(cudaMemcpy2DAsync(h, cols * sizeof(float), d, ld * sizeof(float), cols * sizeof(float), rows,
-                                   cudaMemcpyDeviceToHost, lib_stream()));
-    return AES_OK;
+    return d2h_dense(d, ld, rows, cols, h, lib_stream());
 }
 
 template <typename T>

@@ -156,6 +156,11 @@ struct ScanArgs {
     uint32_t* row_params;    // kScanSlots: optional output; kScanExplicit: input (uint2 per row)
 };
 int launch_row_scan(int kind, const ScanArgs& a, void* ws, size_t ws_bytes, cudaStream_t st);
+// Dense host <-> device copies (hostio.cu): pageable host buffers go through a
+// pinned staging ring with multi-threaded host copies; h2d returns once the
+// host buffer may be reused, d2h once the host buffer holds the data.
+int h2d_dense(const float* h, uint64_t rows, uint64_t cols, float* d, uint64_t ld, cudaStream_t st);
+int d2h_dense(const float* d, uint64_t ld, uint64_t rows, uint64_t cols, float* h, cudaStream_t st);
 size_t row_scan_workspace_bytes(uint64_t n);
 
 }  // namespace aes
