@@ -372,11 +372,26 @@ AES_API int aes_dev_gemm_bias_act(const float* a, uint64_t m, uint64_t k, uint64
  * aes_dev_spmm_f32 followed by aes_dev_gemm_bias_act_ex.  finite_w = 0 keeps
  * the reference's a == 0 skip (needed only when W has inf/NaN).  Rows of the
  * plan should be bounded (sampled plans): a hub row stalls one producer warp.
- * AES_ERR_UNSUPPORTED outside that range (callers run the split kernels). */
+ * AES_ERR_UNSUPPORTED outside that range or when h overlaps x (callers run
+ * the split kernels). */
 AES_API int aes_dev_gcn_layer_fused(const uint64_t* srow_ptr, const uint32_t* scol, const float* sval,
                                     uint64_t n_rows, const float* x, uint64_t ldx, uint64_t k, const float* w,
                                     uint64_t ldw, uint64_t n, const float* bias, int relu, int finite_w, float* h,
                                     uint64_t ldh, void* stream);
+/* The same layer with its exchange fused in (the p2p layer step of
+ * gnn.cpp:66-78 run row-sharded): output row r goes to dsts[d] at row
+ * row_offset + r for every destination d (peer replicas mapped through CUDA
+ * IPC), or only where need[d][row_offset + r] != 0 when need (halo masks, per
+ * destination, NULL entries = every row) is given; every CTA then adds one
+ * release arrival (system scope) to each counters[d].  Arrivals per launch:
+ * aes_gcn_layer_fused_ctas(n_rows).  n_dst <= 16. */
+AES_API uint64_t aes_gcn_layer_fused_ctas(uint64_t n_rows);
+AES_API int aes_dev_gcn_layer_fused_bcast(const uint64_t* srow_ptr, const uint32_t* scol, const float* sval,
+                                          uint64_t n_rows, const float* x, uint64_t ldx, uint64_t k,
+                                          const float* w, uint64_t ldw, uint64_t n, const float* bias, int relu,
+                                          int finite_w, float* const* dsts, unsigned long long* const* counters,
+                                          const uint8_t* const* need, int n_dst, uint64_t row_offset,
+                                          uint64_t ldh, void* stream);
 AES_API int aes_dev_gemm_bias_act_ex(const float* a, uint64_t m, uint64_t k, uint64_t lda,
                                      const float* w, uint64_t n, uint64_t ldw, const float* bias,
                                      int relu, int finite_w, float* const* dsts,

@@ -73,6 +73,10 @@ def lib():
                                               vp]
         L.aes_gemm_tf32_ctas.argtypes = [u64]
         L.aes_gemm_tf32_ctas.restype = u64
+        L.aes_gcn_layer_fused_ctas.argtypes = [u64]
+        L.aes_gcn_layer_fused_ctas.restype = u64
+        L.aes_dev_gcn_layer_fused_bcast.argtypes = [vp, vp, vp, u64, vp, u64, u64, vp, u64, u64, vp, i32, i32, vp, vp,
+                                                    vp, i32, u64, u64, vp]
         L.aes_gemm_ctas.argtypes = [u64, u64]
         L.aes_gemm_ctas.restype = u64
         L.aes_dev_wait_counter.argtypes = [vp, u64, vp]

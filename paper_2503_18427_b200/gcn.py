@@ -195,8 +195,21 @@ class ShardedGCN:
                 self.finite.append(int(flag.item()) == 0)
             # fast mode (tcgen05 TF32, not bit-exact) where the layer shape allows
             self.fast = [fast_gemm and w.shape[0] <= 128 and w.shape[1] <= 128 for w in weights]
-            self.arrivals = [sum(p2p.gemm_ctas(c1 - c0, w.shape[1], fast) for c0, c1 in zip(self.cuts, self.cuts[1:]))
-                             for w, fast in zip(weights, self.fast)]
+            # fused layer kernel per (layer, producer rank): fp32 exact layers
+            # whose input arrives as fp32, shapes the kernel takes, sampled
+            # plans, shards above the size threshold — decided the same way
+            # on every rank so each knows every producer's arrival count
+            dims_in = [weights[0].shape[0]] + [w.shape[1] for w in weights[:-1]]
+            self.p2p_fused = []
+            for l, (w, fast) in enumerate(zip(weights, self.fast)):
+                fp32_in = not (self.qx and l > 0)
+                shape_ok = dims_in[l] % 4 == 0 and 0 < dims_in[l] <= 128 and 0 < w.shape[1] <= 128
+                self.p2p_fused.append([fp32_in and shape_ok and not fast and not (self.qx and l + 1 < len(weights))
+                                       and max_row_slots > 0 and (c1 - c0) >= device.FUSED_LAYER_MIN_ROWS
+                                       for c0, c1 in zip(self.cuts, self.cuts[1:])])
+            self.arrivals = [sum(p2p.layer_fused_ctas(c1 - c0) if fused[r] else p2p.gemm_ctas(c1 - c0, w.shape[1], fast)
+                                 for r, (c0, c1) in enumerate(zip(self.cuts, self.cuts[1:])))
+                             for w, fast, fused in zip(weights, self.fast, self.p2p_fused)]
 
     def _global_params(self, out_rows: torch.Tensor):
         """fit_params over the whole (row-sharded) H: each rank's first-occurrence
@@ -280,6 +293,17 @@ class ShardedGCN:
         statuses = []
         n_layers = len(self.weights)
         for l, (w, b) in enumerate(zip(self.weights, self.biases)):
+            if hq is None and self.p2p_fused[l][self.rank]:
+                # the whole layer as ONE kernel: SpMM producer warps + ordered-
+                # GEMM consumer warps whose epilogue stores into every rank's
+                # replica (one arrival per CTA)
+                out_buf = (l + 1) % 2
+                ok = rep.layer_publish(out_buf, self.srow, self.scol, self.sval, h, w, b, l + 1 < n_layers,
+                                       self.finite[l], self.lo, halo=self.halo and l + 1 < n_layers)
+                assert ok, "fused layer refused a shape it was planned for"
+                rep.wait(self.arrivals[l])
+                h = rep.bufs[out_buf][: self.n, : w.shape[1]]
+                continue
             if hq is None:
                 agg = self.ops.spmm(self.srow, self.scol, self.sval, h,
                                     out=self.ops.alloc(max(rows, 1), h.shape[1], h))

@@ -118,6 +118,27 @@ class PeerReplicas:
             ctypes.cast(self.dst[out_buf], ctypes.c_void_p), ctypes.cast(self.ctr, ctypes.c_void_p), need,
             self.world, row_offset, self.ld, stream_of(stream)))
 
+    def layer_publish(self, out_buf: int, srow, scol, sval, x: torch.Tensor, w: torch.Tensor, bias, relu: bool,
+                      finite_w: bool, row_offset: int, stream=None, halo: bool = False) -> bool:
+        """The whole exact layer for this rank's rows as ONE kernel
+        (aes_dev_gcn_layer_fused_bcast: SpMM producer warps + ordered-GEMM
+        consumer warps whose epilogue stores into every rank's replica
+        `out_buf`, then one arrival per CTA).  False when the shape is outside
+        the fused kernel (the caller runs spmm + gemm_publish)."""
+        m = srow.numel() - 1
+        k, n = x.shape[1], w.shape[1]
+        w = w.contiguous()
+        need = ctypes.cast(self.need_ptrs, ctypes.c_void_p) if halo and self.need_ptrs is not None else None
+        rc = lib().aes_dev_gcn_layer_fused_bcast(
+            srow.data_ptr(), scol.data_ptr(), sval.data_ptr(), m, x.data_ptr(), x.stride(0), k, w.data_ptr(),
+            w.stride(0), n, None if bias is None or bias.numel() == 0 else bias.data_ptr(), int(relu),
+            int(finite_w), ctypes.cast(self.dst[out_buf], ctypes.c_void_p), ctypes.cast(self.ctr, ctypes.c_void_p),
+            need, self.world, row_offset, self.ld, stream_of(stream))
+        if rc == capi.AES_ERR_UNSUPPORTED:
+            return False
+        check(rc)
+        return True
+
     def barrier(self, stream=None):
         """Device-side barrier across ranks (stream-ordered): no rank starts
         writing a new step into peers' replicas while a peer still reads the
@@ -171,6 +192,11 @@ def quantize_ctas(rows: int) -> int:
     return int(lib().aes_quantize_bcast_ctas(rows))
 
 
+def layer_fused_ctas(m: int) -> int:
+    """Arrivals one producer's fused layer (layer_publish) adds to each counter."""
+    return int(lib().aes_gcn_layer_fused_ctas(m))
+
+
 def gemm_ctas(m: int, n: int, fast: bool = False) -> int:
     """Arrivals one producer's publishing GEMM adds to each counter."""
     if fast:
@@ -178,4 +204,4 @@ def gemm_ctas(m: int, n: int, fast: bool = False) -> int:
     return int(lib().aes_gemm_ctas(m, n))
 
 
-__all__ = ["PeerReplicas", "gemm_ctas", "quantize_ctas", "capi"]
+__all__ = ["PeerReplicas", "gemm_ctas", "layer_fused_ctas", "quantize_ctas", "capi"]

@@ -162,3 +162,14 @@ def test_fused_layer_small_and_ragged_graphs(dev, n):
     torch.cuda.synchronize()
     want = port.bias_act(port.dense_matmul(port.spmm_sampled(rp2, col2, val2, x, 32), w), b, True)
     assert np.array_equal(bits(to_np(fused)), bits(want))
+
+
+def test_fused_layer_refuses_in_place_output(dev):
+    import torch
+    n = 500
+    rp, col, _ = graphs.power_law(n, alpha=2.0, max_deg=50, seed=8)
+    g = dev.Graph.from_numpy(rp, col, np.ones(col.size, np.float32))
+    plan = dev.SampledPlan(g, 32)
+    x = torch.rand((n, 64), device="cuda")
+    w = torch.rand((64, 64), device="cuda")
+    assert dev.gcn_layer_fused(plan.srow_ptr, plan.scol, plan.sval, x, w, None, True, out=x) is None

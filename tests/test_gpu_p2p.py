@@ -37,7 +37,7 @@ def _problem(n=3001, f=40):
     return nrp, ncol, nval, x, ws, bs
 
 
-def _run(rank, world, port_no, q, fast=False, exchange_dtype="f32", halo=False):
+def _run(rank, world, port_no, q, fast=False, exchange_dtype="f32", halo=False, fused=False):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
@@ -47,6 +47,8 @@ def _run(rank, world, port_no, q, fast=False, exchange_dtype="f32", halo=False):
     try:
         from paper_2503_18427_b200 import device
         from paper_2503_18427_b200.gcn import ShardedGCN
+        if fused:  # every fp32 layer through the fused SpMM + GEMM + exchange kernel
+            device.FUSED_LAYER_MIN_ROWS = 0
         nrp, ncol, nval, x, ws, bs = _problem()
         g = device.Graph.from_numpy(nrp, ncol, nval)
         plan = device.SampledPlan(g, 16)
@@ -103,13 +105,15 @@ def test_p2p_tcgen05_fused_exchange_within_bound(world):
         assert np.array_equal(res[0][1][0], res[1][1][0])
 
 
-@pytest.mark.parametrize("world", [1, 2])
-def test_p2p_fused_exchange_matches_oracle(world):
+@pytest.mark.parametrize("world,fused", [(1, False), (2, False), (1, True), (2, True)])
+def test_p2p_fused_exchange_matches_oracle(world, fused):
+    """GEMM epilogue exchange, and (fused=True) the whole layer — SpMM + GEMM
+    + stores into every replica — as one kernel per rank."""
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     p = _free_port()
-    procs = [ctx.Process(target=_run, args=(r, world, p, q)) for r in range(world)]
+    procs = [ctx.Process(target=_run, args=(r, world, p, q, False, "f32", False, fused)) for r in range(world)]
     for pr in procs:
         pr.start()
     res = sorted([q.get(timeout=300) for _ in procs], key=lambda t: t[0])
@@ -149,8 +153,8 @@ def test_p2p_int8_exchange_matches_reference_composition(world):
             assert np.array_equal(np.ascontiguousarray(o).view(np.uint32), want.view(np.uint32))
 
 
-@pytest.mark.parametrize("exchange_dtype", ["f32", "int8"])
-def test_p2p_halo_exchange_matches_oracle(exchange_dtype):
+@pytest.mark.parametrize("exchange_dtype,fused", [("f32", False), ("int8", False), ("f32", True)])
+def test_p2p_halo_exchange_matches_oracle(exchange_dtype, fused):
     """Halo exchange: producers store a hidden-layer row
     into a peer's replica only where the peer's sampled slots reference it.
     Results stay bit-exact, and the rows a rank never reads are never sent."""
@@ -158,7 +162,7 @@ def test_p2p_halo_exchange_matches_oracle(exchange_dtype):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     p = _free_port()
-    procs = [ctx.Process(target=_run, args=(r, 2, p, q, False, exchange_dtype, True)) for r in range(2)]
+    procs = [ctx.Process(target=_run, args=(r, 2, p, q, False, exchange_dtype, True, fused)) for r in range(2)]
     for pr in procs:
         pr.start()
     res = sorted([q.get(timeout=300) for _ in procs], key=lambda t: t[0])
