@@ -239,6 +239,42 @@ __device__ __forceinline__ T* pin_ptr(T* p) {
 // Offset of the dynamic shared-memory window inside the CTA's shared window
 // on sm_100a (1 KB reserved; the SASS of cvta.shared is (CgaCtaId<<24)+0x400).
 constexpr uint32_t kDynSmemOffset = 0x400;
+// The batch kernel relies on it; dyn_smem_offset_ok() checks it once per
+// device with a probe launch (same dynamic-only shared memory layout) and the
+// int8 dispatch falls back to the layout-agnostic ring kernel if a driver or
+// toolkit ever places the window elsewhere — slower, never wrong.
+__global__ void dyn_smem_probe_kernel(uint32_t* out) {
+    extern __shared__ __align__(16) unsigned char probe_smem[];
+    if (threadIdx.x == 0) *out = (uint32_t)__cvta_generic_to_shared(probe_smem) & 0xFFFFFFu;
+}
+bool dyn_smem_offset_ok(cudaStream_t st) {
+    static int ok_dev[kMaxDevices] = {};  // 0 unknown, 1 ok, -1 not
+    int& ok = ok_dev[cur_device()];
+    if (ok == 0) {
+        // (no probe while the caller's stream is being captured into a graph:
+        // the batch kernel's own __trap() remains the guard)
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) return true;
+        (void)cudaGetLastError();
+        cudaStream_t ps = nullptr;
+        uint32_t* d = nullptr;
+        uint32_t h = 0;
+        ok = -1;
+        if (cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking) == cudaSuccess) {
+            if (cudaMallocAsync((void**)&d, sizeof(uint32_t), ps) == cudaSuccess) {
+                dyn_smem_probe_kernel<<<1, 32, 4096, ps>>>(d);
+                if (cudaMemcpyAsync(&h, d, sizeof(uint32_t), cudaMemcpyDeviceToHost, ps) == cudaSuccess &&
+                    cudaStreamSynchronize(ps) == cudaSuccess && h == kDynSmemOffset)
+                    ok = 1;
+                cudaFreeAsync(d, ps);
+                cudaStreamSynchronize(ps);
+            }
+            cudaStreamDestroy(ps);
+        }
+        (void)cudaGetLastError();
+    }
+    return ok == 1;
+}
 // LDS at (addr + kDynSmemOffset); not volatile so ptxas may schedule it
 __device__ __forceinline__ float lds_lut(uint32_t addr) {
     float v;
@@ -2095,6 +2131,7 @@ int aes_dev_spmm_q8_ex(const uint64_t* srow_ptr, const uint32_t* scol, const flo
         if (s != AES_ERR_UNSUPPORTED) return s;
     }
     if ((v == 0 || (v >= 30 && v <= 45)) && f4 > 16 && ldq % 16 == 0 && (uintptr_t)q % 16 == 0 &&
+        dyn_smem_offset_ok(st) &&
         f4 / 32 < 65535) {
         float4* c4 = reinterpret_cast<float4*>(c);
         const uint32_t f4u = (uint32_t)f4;
