@@ -596,6 +596,9 @@ int launch_spmm_q8_tma(int dec, const uint64_t* srow, const uint32_t* scol, cons
                        const uint8_t* q, uint64_t ldq, uint64_t f, const float* lut, const float* fparams, float* c,
                        uint64_t ldc, cudaStream_t st);  // spmm_tma.cu
 int spmm_variant();                                     // spmm.cu
+int launch_q8_feature_batch(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n,
+                            const uint8_t* q, uint64_t ldq, uint64_t f, const float2* params, float* c, uint64_t ldc,
+                            cudaStream_t st);  // spmm.cu
 }  // namespace aes
 
 extern "C" {
@@ -668,6 +671,12 @@ int aes_dev_spmm_q8_affine(const uint64_t* srow_ptr, const uint32_t* scol, const
     // tuning variants: 51 the TMA-gather kernel (FEATURE), 50 the register-pipelined one
     if (v == 51 && mode == AES_QAFFINE_FEATURE) {
         const int s = launch_spmm_q8_tma(1, srow_ptr, scol, sval, n_rows, q, ldq, f, nullptr, params, c, ldc, st);
+        if (s != AES_ERR_UNSUPPORTED) return s;
+    }
+    // FEATURE mode: the batch kernel with the affine decode (spmm.cu), unless
+    // a tuning variant asks for the ring kernel (52-54)
+    if (mode == AES_QAFFINE_FEATURE && (v == 0 || v == 55) && n_rows < (1ull << 31)) {
+        const int s = launch_q8_feature_batch(srow_ptr, scol, sval, n_rows, q, ldq, f, p2, c, ldc, st);
         if (s != AES_ERR_UNSUPPORTED) return s;
     }
     // default: the cp.async ring kernel (16-B code rows, 16-B aligned C)

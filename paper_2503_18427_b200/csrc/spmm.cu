@@ -230,6 +230,15 @@ __device__ __forceinline__ uint32_t pin_u32(uint32_t x) {
     asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
     return y;
 }
+// (a0, a1) = (fma(x, y0, a0), fma(x, y1, a1)) as one FFMA2 — int8 FAST MODE only
+__device__ __forceinline__ void fma2_rn(float& a0, float& a1, float x, float y0, float y1) {
+    unsigned long long a, y, xx;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(a0), "f"(a1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(y) : "f"(y0), "f"(y1));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(xx) : "f"(x));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a) : "l"(xx), "l"(y));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(a));
+}
 template <class T>
 __device__ __forceinline__ T* pin_ptr(T* p) {
     uint64_t y;
@@ -1009,7 +1018,13 @@ int launch_q8_dual(const uint64_t* srow, const uint32_t* scol, const float* sval
 // the per-warp gather rings in the upper 128 B of each entry ("holes"): ring
 // slot p of warp w is hole w*C + p.
 // ---------------------------------------------------------------------------
-template <int C, int WARPS, bool FULL, bool FASTB, int SCHED>  // SCHED: 0 static, 1 dynamic, 2 balanced
+// DEC 0: the reference's global codes through the exact table (bit-exact);
+// DEC 1: int8 FAST MODE per-feature affine codes, x^ = q s_j + m_j (affine.cu
+// states the bounds): no table — PRMT places the byte in the mantissa of
+// 2^23, one FADD2 per code pair removes 2^23, one FFMA2 per pair accumulates
+// v q, and each stored row is s_j * acc + m_j * sum(v) (the same arithmetic
+// as spmm_q8r_kernel, so the results are bit-identical to it)
+template <int C, int WARPS, bool FULL, bool FASTB, int SCHED, int DEC = 0>  // SCHED: 0 static, 1 dynamic, 2 balanced
 // 3 x 74 KB CTAs per SM (40 registers) for whole 128-code tiles; the partial-
 // tile form (F % 128 != 0, e.g. reddit's 602) runs faster at 2 CTAs with room
 // for 64 registers (reddit int8 0.64 -> 0.59 ms; products, whole tiles, loses
@@ -1018,7 +1033,8 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 32 ? 1 : WARPS >= 20 ? 2 
 spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
                      const float* __restrict__ sval, uint64_t n_rows, const unsigned char* __restrict__ q,
                      uint32_t ldq, uint32_t f4, float4* __restrict__ c, uint64_t ldc4,
-                     const float* __restrict__ lut_g, uint32_t group_rows, uint64_t groups, DynSched* ws) {
+                     const float* __restrict__ lut_g, uint32_t group_rows, uint64_t groups, DynSched* ws,
+                     const float2* __restrict__ fparams = nullptr, uint32_t fcols = 0) {
     static_assert(C % 4 == 0 && C >= 8 && C <= 16 && WARPS <= 32, "ring shape");
     // rings in the LUT's 256 holes (256-B stride) while they fit, else in
     // their own region after the row ends (128-B stride; one 32-warp CTA per
@@ -1028,9 +1044,11 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
     constexpr int B = C / 4;  // batches per ring round
     constexpr uint32_t kEndsBytes = 144;  // 33 row ends per warp
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    for (int i = threadIdx.x; i < 256 * 32; i += WARPS * 32)
-        reinterpret_cast<float*>(smem_raw)[(i >> 5) * 64 + (i & 31)] = lut_g[i >> 5];
-    __syncthreads();
+    if (DEC == 0) {
+        for (int i = threadIdx.x; i < 256 * 32; i += WARPS * 32)
+            reinterpret_cast<float*>(smem_raw)[(i >> 5) * 64 + (i & 31)] = lut_g[i >> 5];
+        __syncthreads();
+    }
 
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t smem0 = smem_addr(smem_raw);
@@ -1039,7 +1057,7 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
     // window base (the high byte), so one PRMT builds base_hi | code<<8 |
     // lane*4 and the offset rides in the LDS immediate: no add per code.
     // A different layout would silently read wrong entries, so trap on it.
-    if ((smem0 & 0xFFFFFFu) != kDynSmemOffset) __trap();
+    if (DEC == 0 && (smem0 & 0xFFFFFFu) != kDynSmemOffset) __trap();
     // (pinned through asm so ptxas keeps them in registers instead of
     // re-deriving them from %tid in every slot)
     const uint32_t lane4 = pin_u32((smem0 & 0xFF000000u) | (lane * 4));
@@ -1058,6 +1076,24 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
     c += (size_t)blockIdx.y * 32;
     const unsigned char* qlane = pin_ptr(q + (lane & 7) * 16);
     f4 = min(32u, f4 - blockIdx.y * 32);
+    // DEC 1: (s_j, m_j) of this lane's 4 output columns of tile blockIdx.y
+    float sj[4] = {0.f, 0.f, 0.f, 0.f}, mj[4] = {0.f, 0.f, 0.f, 0.f};
+    if (DEC == 1) {
+        const uint32_t col0 = blockIdx.y * 128 + 4 * lane;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (col0 + u < fcols) {
+                const float2 pj = fparams[col0 + u];
+                sj[u] = pj.x;
+                mj[u] = pj.y;
+            }
+    }
+    // the stored value of an output row (DEC 1: the affine epilogue)
+    auto out4 = [&](const float4& a, float bsum) -> float4 {
+        if (DEC == 0) return a;
+        return make_float4(fmaf(sj[0], a.x, mj[0] * bsum), fmaf(sj[1], a.y, mj[1] * bsum),
+                           fmaf(sj[2], a.z, mj[2] * bsum), fmaf(sj[3], a.w, mj[3] * bsum));
+    };
     uint32_t nb = 16;  // bytes this lane copies per slot
     if (!FULL) {
         const uint32_t rowb = f4 * 4, j16 = (lane & 7) * 16;
@@ -1123,10 +1159,12 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
     uint32_t row = 0;
     uint32_t row_end = lds_u32(ends0);
     float4* cptr = c + r0 * ldc4 + lane;  // rows are stored in order: a running pointer
+    float bs = 0.f;  // DEC 1: sum of the row's slot values
     auto store_row = [&](uint32_t) {
-        if (FULL || lane < f4) __stcs(cptr, acc);
+        if (FULL || lane < f4) __stcs(cptr, out4(acc, bs));
         cptr += ldc4;
         acc = f4_zero();
+        bs = 0.f;
     };
     auto advance_rows = [&](uint32_t pos) {
         do {
@@ -1139,6 +1177,18 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
 
     auto consume = [&](int p, float v) {
         const uint32_t r = lds_u32(rd0 + p * RS);
+        if (DEC == 1) {
+            float q0 = __uint_as_float(__byte_perm(r, 0x4B000000u, 0x7650));
+            float q1 = __uint_as_float(__byte_perm(r, 0x4B000000u, 0x7651));
+            float q2 = __uint_as_float(__byte_perm(r, 0x4B000000u, 0x7652));
+            float q3 = __uint_as_float(__byte_perm(r, 0x4B000000u, 0x7653));
+            add2_rn(q0, q1, -8388608.0f, -8388608.0f);  // exactly q
+            add2_rn(q2, q3, -8388608.0f, -8388608.0f);
+            fma2_rn(acc.x, acc.y, v, q0, q1);
+            fma2_rn(acc.z, acc.w, v, q2, q3);
+            bs += v;
+            return;
+        }
         const float d0 = lds_lut(__byte_perm(r, lane4, 0x7604u));
         const float d1 = lds_lut(__byte_perm(r, lane4, 0x7614u));
         const float d2 = lds_lut(__byte_perm(r, lane4, 0x7624u));
@@ -1247,10 +1297,12 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
     uint32_t wi = 0;  // its index in the window
     uint32_t row_end = lds_u32(ends0);
     float4* cptr = crow;  // rows are stored in order: a running pointer
+    float bs = 0.f;  // DEC 1: sum of the row's slot values
     auto store_row = [&]() {
-        if (FULL || lane < f4) __stcs(cptr, acc);
+        if (FULL || lane < f4) __stcs(cptr, out4(acc, bs));
         cptr += ldc4;
         acc = f4_zero();
+        bs = 0.f;
     };
     auto advance_rows = [&](uint32_t pos) {
         do {
@@ -1270,6 +1322,18 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
 
     auto consume = [&](int p, float v) {
         const uint32_t r = lds_u32(rd0 + p * RS);
+        if (DEC == 1) {
+            float q0 = __uint_as_float(__byte_perm(r, 0x4B000000u, 0x7650));
+            float q1 = __uint_as_float(__byte_perm(r, 0x4B000000u, 0x7651));
+            float q2 = __uint_as_float(__byte_perm(r, 0x4B000000u, 0x7652));
+            float q3 = __uint_as_float(__byte_perm(r, 0x4B000000u, 0x7653));
+            add2_rn(q0, q1, -8388608.0f, -8388608.0f);  // exactly q
+            add2_rn(q2, q3, -8388608.0f, -8388608.0f);
+            fma2_rn(acc.x, acc.y, v, q0, q1);
+            fma2_rn(acc.z, acc.w, v, q2, q3);
+            bs += v;
+            return;
+        }
         const float d0 = lds_lut(__byte_perm(r, lane4, 0x7604u));
         const float d1 = lds_lut(__byte_perm(r, lane4, 0x7614u));
         const float d2 = lds_lut(__byte_perm(r, lane4, 0x7624u));
@@ -1371,22 +1435,22 @@ uint32_t bal_waves(uint64_t n_rows, uint64_t resident_warps, uint64_t rows_per_r
     return (uint32_t)(w < 1 ? 1 : w > 64 ? 64 : w);
 }
 
-template <int C, int WARPS, bool FULL, bool FASTB>
+template <int C, int WARPS, bool FULL, bool FASTB, int DEC = 0>
 int launch_q8_batch_t(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, const uint8_t* q,
                       uint64_t ldq, uint32_t f4, float4* c, uint64_t ldc4, const float* lut, cudaStream_t st,
-                      int dyn) {
+                      int dyn, const float2* fparams = nullptr, uint32_t fcols = 0) {
     // LUT (+ rings in its holes), slot metadata, row ends (+ separate rings)
     const size_t smem = 256 * 256 + (size_t)WARPS * (32 * C + 144) + (C * WARPS > 256 ? (size_t)WARPS * C * 128 : 0);
     static int occ_dev[kMaxDevices] = {};
     int& occ = occ_dev[cur_device()];
     if (occ == 0) {
-        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 0>,
+        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 0, DEC>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 1>,
+        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 1, DEC>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         AES_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &occ, spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 1>, WARPS * 32, smem));
-        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 2>,
+            &occ, spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 1, DEC>, WARPS * 32, smem));
+        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 2, DEC>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         if (occ < 1) occ = 1;
     }
@@ -1415,8 +1479,8 @@ int launch_q8_batch_t(const uint64_t* srow, const uint32_t* scol, const float* s
         const uint64_t min_rows = WARPS >= 32 ? 4 : 8;
         const uint64_t cap = (n + (uint64_t)WARPS * min_rows - 1) / ((uint64_t)WARPS * min_rows);
         if (cap < per_tile) per_tile = cap ? cap : 1;
-        spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 2><<<dim3((unsigned)per_tile, tiles), WARPS * 32, smem, st>>>(
-            srow, scol, sval, n, q, (uint32_t)ldq, f4, c, ldc4, lut, 32, 0, nullptr);
+        spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 2, DEC><<<dim3((unsigned)per_tile, tiles), WARPS * 32, smem, st>>>(
+            srow, scol, sval, n, q, (uint32_t)ldq, f4, c, ldc4, lut, 32, 0, nullptr, fparams, fcols);
         AES_CUDA_TRY(cudaGetLastError());
         return AES_OK;
     }
@@ -1429,8 +1493,8 @@ int launch_q8_batch_t(const uint64_t* srow, const uint32_t* scol, const float* s
         heavy_scan_kernel<<<grid_for(groups, 256, num_sms() * 8), 256, 0, st>>>(srow, n, gr, groups, ws);
         const uint64_t per_tile = ((uint64_t)num_sms() * occ + tiles - 1) / tiles;
         const dim3 grid((unsigned)(gx < per_tile ? gx : per_tile), tiles);
-        spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 1><<<grid, WARPS * 32, smem, st>>>(
-            srow, scol, sval, n, q, (uint32_t)ldq, f4, c, ldc4, lut, gr, groups, ws);
+        spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 1, DEC><<<grid, WARPS * 32, smem, st>>>(
+            srow, scol, sval, n, q, (uint32_t)ldq, f4, c, ldc4, lut, gr, groups, ws, fparams, fcols);
         AES_CUDA_TRY(cudaGetLastError());
         AES_CUDA_TRY(cudaFreeAsync(ws, st));
         return AES_OK;
@@ -1442,19 +1506,21 @@ int launch_q8_batch_t(const uint64_t* srow, const uint32_t* scol, const float* s
     uint64_t gs = (uint64_t)num_sms() * occ / tiles;
     if (gs == 0) gs = 1;
     const unsigned gxs = (unsigned)(dyn == kSchedStaticPersist && gx > gs ? gs : gx);
-    spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 0><<<dim3(gxs, tiles), WARPS * 32, smem, st>>>(
-        srow, scol, sval, n, q, (uint32_t)ldq, f4, c, ldc4, lut, gr, groups, nullptr);
+    spmm_q8_batch_kernel<C, WARPS, FULL, FASTB, 0, DEC><<<dim3(gxs, tiles), WARPS * 32, smem, st>>>(
+        srow, scol, sval, n, q, (uint32_t)ldq, f4, c, ldc4, lut, gr, groups, nullptr, fparams, fcols);
     AES_CUDA_TRY(cudaGetLastError());
     return AES_OK;
 }
 
-template <int C, int WARPS, bool FASTB = true>
+template <int C, int WARPS, bool FASTB = true, int DEC = 0>
 int launch_q8_batch(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, const uint8_t* q,
                     uint64_t ldq, uint32_t f4, float4* c, uint64_t ldc4, const float* lut, cudaStream_t st,
-                    int dyn) {
+                    int dyn, const float2* fparams = nullptr, uint32_t fcols = 0) {
     if (f4 % 32 == 0)
-        return launch_q8_batch_t<C, WARPS, true, FASTB>(srow, scol, sval, n, q, ldq, f4, c, ldc4, lut, st, dyn);
-    return launch_q8_batch_t<C, WARPS, false, FASTB>(srow, scol, sval, n, q, ldq, f4, c, ldc4, lut, st, dyn);
+        return launch_q8_batch_t<C, WARPS, true, FASTB, DEC>(srow, scol, sval, n, q, ldq, f4, c, ldc4, lut, st, dyn,
+                                                             fparams, fcols);
+    return launch_q8_batch_t<C, WARPS, false, FASTB, DEC>(srow, scol, sval, n, q, ldq, f4, c, ldc4, lut, st, dyn,
+                                                          fparams, fcols);
 }
 
 // ---------------------------------------------------------------------------
@@ -2036,6 +2102,20 @@ int layer_fused_dispatch(const uint64_t* srow_ptr, const uint32_t* scol, const f
                                                          bias, relu, h, ldh, st, bc);
     return launch_layer_fused_t<false, true, BCAST>(srow_ptr, scol, sval, n_rows, x, ldx, k32, w, ldw, n32, bias,
                                                     relu, h, ldh, st, bc);
+}
+
+// int8 FAST MODE, per-feature affine codes (affine.cu dispatches here for
+// 16-B aligned code rows): the batch kernel with the affine decode (DEC 1),
+// one 32-warp CTA per SM on a balanced wave, no table.
+int launch_q8_feature_batch(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n,
+                            const uint8_t* q, uint64_t ldq, uint64_t f, const float2* params, float* c, uint64_t ldc,
+                            cudaStream_t st) {
+    const uint64_t f4 = (f + 3) / 4;
+    if (f4 <= 16 || ldq % 16 != 0 || (uintptr_t)q % 16 != 0 || ldc % 4 != 0 || (uintptr_t)c % 16 != 0 ||
+        f4 / 32 >= 65535 || f > 0xffffffffull)
+        return AES_ERR_UNSUPPORTED;
+    return launch_q8_batch<12, 32, true, 1>(srow, scol, sval, n, q, ldq, (uint32_t)f4, reinterpret_cast<float4*>(c),
+                                            ldc / 4, nullptr, st, kSchedBal, params, (uint32_t)f);
 }
 
 int launch_spmm_q8_tma(int dec, const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n,

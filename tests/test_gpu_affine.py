@@ -144,3 +144,29 @@ def test_affine_handle_api(dev):
         m.quantize_affine(bad, "row")
     with pytest.raises(ValueError, match="NonFinite"):
         m.quantize_affine(bad, "feature")
+
+
+@pytest.mark.parametrize("f", [128, 130, 602])
+def test_feature_batch_kernel_equals_ring_kernel(dev, f):
+    """The per-feature affine decode runs in the batch kernel by default
+    (spmm.cu, DEC 1) and in the cp.async ring kernel as variant 54: the same
+    arithmetic in the same order, so the same bits."""
+    import torch
+
+    from paper_2503_18427_b200 import capi
+    L = capi.lib()
+    n = 6000
+    rp, col, _ = graphs.power_law(n, alpha=1.5, max_deg=800, seed=f)
+    val = np.random.default_rng(f).uniform(-1, 1, col.size).astype(np.float32)
+    g = dev.Graph.from_numpy(rp, col, val)
+    plan = dev.SampledPlan(g, 32)
+    xt = torch.from_numpy(_features(np.random.default_rng(3 * f), n, f, skew=True)).cuda()
+    q = dev.quantize_affine(xt, "feature")
+    got = dev.spmm_q8_affine(plan.srow_ptr, plan.scol, plan.sval, q)
+    try:
+        L.aes_dev_spmm_set_variant(54)
+        ring = dev.spmm_q8_affine(plan.srow_ptr, plan.scol, plan.sval, q)
+        torch.cuda.synchronize()
+    finally:
+        L.aes_dev_spmm_set_variant(0)
+    assert torch.equal(got.view(torch.int32), ring.view(torch.int32))
