@@ -460,7 +460,7 @@ spmm_q8r_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ 
         if (st_ok) {
             float4 o;
             if (MODE == 0)
-                o = make_float4(a0 + bs, a1 + bs, a2 + bs, a3 + bs);
+                o = make_float4(__fadd_rn(a0, bs), __fadd_rn(a1, bs), __fadd_rn(a2, bs), __fadd_rn(a3, bs));
             else
                 o = make_float4(fmaf(sj[0], a0, mj[0] * bs), fmaf(sj[1], a1, mj[1] * bs), fmaf(sj[2], a2, mj[2] * bs),
                                 fmaf(sj[3], a3, mj[3] * bs));
@@ -489,7 +489,7 @@ spmm_q8r_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ 
         add2_rn(q2, q3, -kTwo23, -kTwo23);
         fma2(a0, a1, a, q0, q1);
         fma2(a2, a3, a, q2, q3);
-        bs += b;
+        bs = __fadd_rn(bs, b);
     };
 
     // every round consumes all kRC positions; past `total` (last round only)
@@ -510,8 +510,8 @@ spmm_q8r_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ 
                     float2 sm;
                     asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(sm.x), "=f"(sm.y)
                                  : "r"(par0 + (k & 3) * (8 * kRC) + (4 * b + u) * 8));
-                    bv[u] = av[u] * sm.y;
-                    av[u] = av[u] * sm.x;
+                    bv[u] = __fmul_rn(av[u], sm.y);  // (no contraction into the sums: the
+                    av[u] = __fmul_rn(av[u], sm.x);  // batch kernel's DEC 2 gives the same bits)
                 }
             }
             if (row_end > t0 + 4 * b + 4) {  // no row ends in this batch
@@ -599,6 +599,9 @@ int spmm_variant();                                     // spmm.cu
 int launch_q8_feature_batch(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n,
                             const uint8_t* q, uint64_t ldq, uint64_t f, const float2* params, float* c, uint64_t ldc,
                             cudaStream_t st);  // spmm.cu
+int launch_q8_row_batch(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, const uint8_t* q,
+                        uint64_t ldq, uint64_t f, const float2* params, float* c, uint64_t ldc,
+                        cudaStream_t st);  // spmm.cu
 }  // namespace aes
 
 extern "C" {
@@ -673,10 +676,17 @@ int aes_dev_spmm_q8_affine(const uint64_t* srow_ptr, const uint32_t* scol, const
         const int s = launch_spmm_q8_tma(1, srow_ptr, scol, sval, n_rows, q, ldq, f, nullptr, params, c, ldc, st);
         if (s != AES_ERR_UNSUPPORTED) return s;
     }
-    // FEATURE mode: the batch kernel with the affine decode (spmm.cu), unless
-    // a tuning variant asks for the ring kernel (52-54)
-    if (mode == AES_QAFFINE_FEATURE && (v == 0 || v == 55) && n_rows < (1ull << 31)) {
-        const int s = launch_q8_feature_batch(srow_ptr, scol, sval, n_rows, q, ldq, f, p2, c, ldc, st);
+    // the batch kernel with the affine decode (spmm.cu), unless a tuning
+    // variant asks for the ring kernel (52-54).  Per-row codes on one large
+    // 128-code tile stay on the ring kernel: products 0.564 ms vs 0.626 for
+    // the batch kernel's balanced wave (whose per-slot (s, m) read adds an
+    // LDS + 2 FMUL); with several tiles or fewer rows the batch kernel wins
+    // (reddit 0.496 vs 0.593, arxiv 0.034 vs 0.058, pubmed 0.017 vs 0.029)
+    const bool row_ring = mode == AES_QAFFINE_ROW && f <= 128 && n_rows >= (1u << 20);
+    if ((v == 0 || v == 55) && n_rows < (1ull << 31) && !(row_ring && v == 0)) {
+        const int s = mode == AES_QAFFINE_FEATURE
+                          ? launch_q8_feature_batch(srow_ptr, scol, sval, n_rows, q, ldq, f, p2, c, ldc, st)
+                          : launch_q8_row_batch(srow_ptr, scol, sval, n_rows, q, ldq, f, p2, c, ldc, st);
         if (s != AES_ERR_UNSUPPORTED) return s;
     }
     // default: the cp.async ring kernel (16-B code rows, 16-B aligned C)

@@ -1078,7 +1078,7 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
     f4 = min(32u, f4 - blockIdx.y * 32);
     // DEC 1: (s_j, m_j) of this lane's 4 output columns of tile blockIdx.y
     float sj[4] = {0.f, 0.f, 0.f, 0.f}, mj[4] = {0.f, 0.f, 0.f, 0.f};
-    if (DEC == 1) {
+    if (DEC == 1) {  // (DEC 2 reads its row params per slot instead)
         const uint32_t col0 = blockIdx.y * 128 + 4 * lane;
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -1091,6 +1091,8 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
     // the stored value of an output row (DEC 1: the affine epilogue)
     auto out4 = [&](const float4& a, float bsum) -> float4 {
         if (DEC == 0) return a;
+        if (DEC == 2)
+            return make_float4(__fadd_rn(a.x, bsum), __fadd_rn(a.y, bsum), __fadd_rn(a.z, bsum), __fadd_rn(a.w, bsum));
         return make_float4(fmaf(sj[0], a.x, mj[0] * bsum), fmaf(sj[1], a.y, mj[1] * bsum),
                            fmaf(sj[2], a.z, mj[2] * bsum), fmaf(sj[3], a.w, mj[3] * bsum));
     };
@@ -1101,6 +1103,10 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
     }
 
     const uint32_t ends0 = smem0 + 65536 + WARPS * 32 * C + warp * kEndsBytes;
+    // DEC 2: the gathered rows' (s, m) pairs, 4 rounds x C slots x 8 B per warp
+    const uint32_t par0 = smem0 + 65536 + WARPS * (32 * C + kEndsBytes) + (kSep ? WARPS * C * 128 : 0) +
+                          warp * (32 * C);
+    const float2* const rparams = fparams;
 
   // 32-row groups (static / dynamic schedules): one ring fill and drain per group
   auto run_group32 = [&](const uint64_t r0) {
@@ -1144,16 +1150,28 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
                              : "memory");
         }
     };
+    // DEC 2: (s, m) of round k's gathered rows -> params buffer k & 3 (the
+    // round's columns are in shared memory by then)
+    auto issue_par = [&](uint32_t k) {
+        if (DEC == 2 && lane < (uint32_t)C && k * C + lane < total) {
+            const uint32_t col = lds_u32(meta0 + (k & 3) * (8 * C) + lane * 4);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(par0 + (k & 3) * (8 * C) + lane * 8),
+                         "l"(rparams + col)
+                         : "memory");
+        }
+    };
     issue_meta(0);
     issue_meta(1);
     cp_commit();
     cp_wait<0>();
     __syncwarp();
+    issue_par(0);
 #pragma unroll
     for (int b = 0; b < B; ++b) {
         issue(4 * b, 0);
         cp_commit();
     }
+    uint32_t parr = par0;  // params of the round being consumed
 
     float4 acc = f4_zero();
     uint32_t row = 0;
@@ -1177,16 +1195,23 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
 
     auto consume = [&](int p, float v) {
         const uint32_t r = lds_u32(rd0 + p * RS);
-        if (DEC == 1) {
+        if (DEC != 0) {
             float q0 = __uint_as_float(__byte_perm(r, 0x4B000000u, 0x7650));
             float q1 = __uint_as_float(__byte_perm(r, 0x4B000000u, 0x7651));
             float q2 = __uint_as_float(__byte_perm(r, 0x4B000000u, 0x7652));
             float q3 = __uint_as_float(__byte_perm(r, 0x4B000000u, 0x7653));
             add2_rn(q0, q1, -8388608.0f, -8388608.0f);  // exactly q
             add2_rn(q2, q3, -8388608.0f, -8388608.0f);
-            fma2_rn(acc.x, acc.y, v, q0, q1);
-            fma2_rn(acc.z, acc.w, v, q2, q3);
-            bs += v;
+            float a = v, bv = v;
+            if (DEC == 2) {  // per-row codes: v s_c scales the codes, v m_c the offset
+                float2 sm;
+                asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(sm.x), "=f"(sm.y) : "r"(parr + p * 8));
+                bv = __fmul_rn(v, sm.y);
+                a = __fmul_rn(v, sm.x);
+            }
+            fma2_rn(acc.x, acc.y, a, q0, q1);
+            fma2_rn(acc.z, acc.w, a, q2, q3);
+            bs = __fadd_rn(bs, bv);  // (no contraction: the same bits as spmm_q8r_kernel)
             return;
         }
         const float d0 = lds_lut(__byte_perm(r, lane4, 0x7604u));
@@ -1201,6 +1226,7 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
     // (only in the last round) accumulate garbage into acc AFTER the group's
     // last row was stored — no row ends there, so nothing of it is written.
     for (uint32_t k = 0, t0 = 0; t0 < total; t0 += C, ++k) {
+        parr = par0 + (k & 3) * (8 * C);
 #pragma unroll
         for (int b = 0; b < B; ++b) {
             cp_wait<B - 1>();
@@ -1226,7 +1252,10 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
                 }
             }
             __syncwarp();  // every lane is done reading these holes
-            if (b == 0) issue_meta(k + 2);
+            if (b == 0) {
+                issue_meta(k + 2);
+                issue_par(k + 1);  // round k+1's columns landed with the wait above
+            }
             issue(4 * b, k + 1);
             cp_commit();
         }
@@ -1281,16 +1310,28 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
                              : "memory");
         }
     };
+    // DEC 2: (s, m) of round k's gathered rows -> params buffer k & 3 (the
+    // round's columns are in shared memory by then)
+    auto issue_par = [&](uint32_t k) {
+        if (DEC == 2 && lane < (uint32_t)C && k * C + lane < total) {
+            const uint32_t col = lds_u32(meta0 + (k & 3) * (8 * C) + lane * 4);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(par0 + (k & 3) * (8 * C) + lane * 8),
+                         "l"(rparams + col)
+                         : "memory");
+        }
+    };
     issue_meta(0);
     issue_meta(1);
     cp_commit();
     cp_wait<0>();
     __syncwarp();
+    issue_par(0);
 #pragma unroll
     for (int b = 0; b < B; ++b) {
         issue(4 * b, 0);
         cp_commit();
     }
+    uint32_t parr = par0;  // params of the round being consumed
 
     float4 acc = f4_zero();
     uint32_t ri = 0;  // next row to store (relative to rb)
@@ -1322,16 +1363,23 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
 
     auto consume = [&](int p, float v) {
         const uint32_t r = lds_u32(rd0 + p * RS);
-        if (DEC == 1) {
+        if (DEC != 0) {
             float q0 = __uint_as_float(__byte_perm(r, 0x4B000000u, 0x7650));
             float q1 = __uint_as_float(__byte_perm(r, 0x4B000000u, 0x7651));
             float q2 = __uint_as_float(__byte_perm(r, 0x4B000000u, 0x7652));
             float q3 = __uint_as_float(__byte_perm(r, 0x4B000000u, 0x7653));
             add2_rn(q0, q1, -8388608.0f, -8388608.0f);  // exactly q
             add2_rn(q2, q3, -8388608.0f, -8388608.0f);
-            fma2_rn(acc.x, acc.y, v, q0, q1);
-            fma2_rn(acc.z, acc.w, v, q2, q3);
-            bs += v;
+            float a = v, bv = v;
+            if (DEC == 2) {  // per-row codes: v s_c scales the codes, v m_c the offset
+                float2 sm;
+                asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(sm.x), "=f"(sm.y) : "r"(parr + p * 8));
+                bv = __fmul_rn(v, sm.y);
+                a = __fmul_rn(v, sm.x);
+            }
+            fma2_rn(acc.x, acc.y, a, q0, q1);
+            fma2_rn(acc.z, acc.w, a, q2, q3);
+            bs = __fadd_rn(bs, bv);  // (no contraction: the same bits as spmm_q8r_kernel)
             return;
         }
         const float d0 = lds_lut(__byte_perm(r, lane4, 0x7604u));
@@ -1346,6 +1394,7 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
     // (only in the last round) accumulate garbage into acc AFTER the group's
     // last row was stored — no row ends there, so nothing of it is written.
     for (uint32_t k = 0, t0 = 0; t0 < total; t0 += C, ++k) {
+        parr = par0 + (k & 3) * (8 * C);
 #pragma unroll
         for (int b = 0; b < B; ++b) {
             cp_wait<B - 1>();
@@ -1371,7 +1420,10 @@ spmm_q8_batch_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restri
                 }
             }
             __syncwarp();  // every lane is done reading these holes
-            if (b == 0) issue_meta(k + 2);
+            if (b == 0) {
+                issue_meta(k + 2);
+                issue_par(k + 1);  // round k+1's columns landed with the wait above
+            }
             issue(4 * b, k + 1);
             cp_commit();
         }
@@ -1440,7 +1492,8 @@ int launch_q8_batch_t(const uint64_t* srow, const uint32_t* scol, const float* s
                       uint64_t ldq, uint32_t f4, float4* c, uint64_t ldc4, const float* lut, cudaStream_t st,
                       int dyn, const float2* fparams = nullptr, uint32_t fcols = 0) {
     // LUT (+ rings in its holes), slot metadata, row ends (+ separate rings)
-    const size_t smem = 256 * 256 + (size_t)WARPS * (32 * C + 144) + (C * WARPS > 256 ? (size_t)WARPS * C * 128 : 0);
+    const size_t smem = 256 * 256 + (size_t)WARPS * (32 * C + 144) + (C * WARPS > 256 ? (size_t)WARPS * C * 128 : 0) +
+                        (DEC == 2 ? (size_t)WARPS * 32 * C : 0);  // (+ the per-row params buffers)
     static int occ_dev[kMaxDevices] = {};
     int& occ = occ_dev[cur_device()];
     if (occ == 0) {
@@ -2115,6 +2168,18 @@ int launch_q8_feature_batch(const uint64_t* srow, const uint32_t* scol, const fl
         f4 / 32 >= 65535 || f > 0xffffffffull)
         return AES_ERR_UNSUPPORTED;
     return launch_q8_batch<12, 32, true, 1>(srow, scol, sval, n, q, ldq, (uint32_t)f4, reinterpret_cast<float4*>(c),
+                                            ldc / 4, nullptr, st, kSchedBal, params, (uint32_t)f);
+}
+
+// int8 FAST MODE, per-row affine codes: the batch kernel with the gathered
+// rows' (s, m) staged next to the slot metadata (DEC 2).
+int launch_q8_row_batch(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, const uint8_t* q,
+                        uint64_t ldq, uint64_t f, const float2* params, float* c, uint64_t ldc, cudaStream_t st) {
+    const uint64_t f4 = (f + 3) / 4;
+    if (f4 <= 16 || ldq % 16 != 0 || (uintptr_t)q % 16 != 0 || ldc % 4 != 0 || (uintptr_t)c % 16 != 0 ||
+        f4 / 32 >= 65535 || f > 0xffffffffull)
+        return AES_ERR_UNSUPPORTED;
+    return launch_q8_batch<12, 32, true, 2>(srow, scol, sval, n, q, ldq, (uint32_t)f4, reinterpret_cast<float4*>(c),
                                             ldc / 4, nullptr, st, kSchedBal, params, (uint32_t)f);
 }
 

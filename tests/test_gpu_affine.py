@@ -146,8 +146,9 @@ def test_affine_handle_api(dev):
         m.quantize_affine(bad, "feature")
 
 
+@pytest.mark.parametrize("mode", ["feature", "row"])
 @pytest.mark.parametrize("f", [128, 130, 602])
-def test_feature_batch_kernel_equals_ring_kernel(dev, f):
+def test_feature_batch_kernel_equals_ring_kernel(dev, f, mode):
     """The per-feature affine decode runs in the batch kernel by default
     (spmm.cu, DEC 1) and in the cp.async ring kernel as variant 54: the same
     arithmetic in the same order, so the same bits."""
@@ -161,7 +162,7 @@ def test_feature_batch_kernel_equals_ring_kernel(dev, f):
     g = dev.Graph.from_numpy(rp, col, val)
     plan = dev.SampledPlan(g, 32)
     xt = torch.from_numpy(_features(np.random.default_rng(3 * f), n, f, skew=True)).cuda()
-    q = dev.quantize_affine(xt, "feature")
+    q = dev.quantize_affine(xt, mode)
     got = dev.spmm_q8_affine(plan.srow_ptr, plan.scol, plan.sval, q)
     try:
         L.aes_dev_spmm_set_variant(54)
