@@ -15,10 +15,12 @@ UNITS = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1, "ms": 1.0, "us": 1
 SOURCES = {
     "spmm_f32_products": "ncu_f32_summary.json",
     "spmm_int8_products": "ncu_q8_batch_default_summary.json",
-    "spmm_int8-row_products": "ncu_q8r_row_summary.json",
-    "spmm_int8-feature_products": "ncu_q8r_feat_summary.json",
+    "spmm_int8-row_products": "ncu_q8f_row_summary.json",
+    "spmm_int8-feature_products": "ncu_q8f_feat_summary.json",
     "spmm_f32_reddit": "ncu_f32_reddit_summary.json",
     "spmm_int8_reddit": "ncu_q8b_reddit_summary.json",
+    "spmm_int8-row_reddit": "ncu_q8f_row_reddit_summary.json",
+    "spmm_int8-feature_reddit": "ncu_q8f_feat_reddit_summary.json",
 }
 
 
