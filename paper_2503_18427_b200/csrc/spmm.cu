@@ -2076,11 +2076,12 @@ gcn_layer_fused_kernel(const uint64_t* __restrict__ srow, const uint32_t* __rest
                     put(h1 + gm * ldh + col0);
                     continue;
                 }
-                // (destinations unrolled: bc.dst[d] / bc.need[d] are constant-
-                // offset parameter loads, no dynamic indexing of the struct)
-#pragma unroll
-                for (int d = 0; d < (BCAST ? kLayerMaxDst : 1); ++d) {
-                    if (d >= bc.n) break;
+                // several destinations: a rolled loop — unrolled over 16
+                // destinations the kernel grew from 5.9 k to 9.4 k instructions
+                // and the producer / consumer loops started missing in the
+                // instruction cache (3.38 -> 3.72 ms on the products layer)
+#pragma unroll 1
+                for (int d = 0; d < bc.n; ++d) {
                     if (bc.need[d] && !bc.need[d][bc.row_off + gm]) continue;  // halo: d never reads it
                     put(bc.dst[d] + (bc.row_off + gm) * ldh + col0);
                 }
