@@ -30,7 +30,8 @@ def _round4(x: int) -> int:
 
 def padded(x: torch.Tensor) -> torch.Tensor:
     """Return a view of ``x`` whose row stride is a multiple of 4 elements."""
-    assert x.dim() == 2
+    if x.dim() != 2:
+        raise ValueError("expected a 2-D tensor")
     if x.stride(1) == 1 and x.stride(0) % 4 == 0 and x.data_ptr() % 16 == 0:
         return x
     r, f = x.shape

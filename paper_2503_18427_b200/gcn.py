@@ -300,7 +300,8 @@ class ShardedGCN:
                 out_buf = (l + 1) % 2
                 ok = rep.layer_publish(out_buf, self.srow, self.scol, self.sval, h, w, b, l + 1 < n_layers,
                                        self.finite[l], self.lo, halo=self.halo and l + 1 < n_layers)
-                assert ok, "fused layer refused a shape it was planned for"
+                if not ok:  # (the plan above mirrors the kernel's shape checks)
+                    raise RuntimeError("fused layer refused a shape it was planned for")
                 rep.wait(self.arrivals[l])
                 h = rep.bufs[out_buf][: self.n, : w.shape[1]]
                 continue
