@@ -1577,6 +1577,226 @@ int launch_q8_batch(const uint64_t* srow, const uint32_t* scol, const float* sva
 }
 
 // ---------------------------------------------------------------------------
+// int8 wide-row kernel (exact global codes, 128 < F <= 128 T, 16-B aligned
+// code rows).  The batch kernel runs wide rows as 128-code column tiles on
+// grid.y, so every tile pays the whole per-slot bookkeeping again (metadata
+// cp.async, the value LDS.128, the column LDS of each gather issue, row-end
+// tests): reddit F = 602 pays it 5 times per slot, and its last tile is 70 %
+// full.  Here ONE warp covers the whole code row: lane l decodes codes
+// 128t + 4l .. 128t + 4l + 3 of every group t < T into accumulator t, so the
+// bookkeeping is paid once per slot and only the decode (ring LDS, 4 PRMT +
+// 4 LUT LDS, 4 FMUL, 2 FADD2 per group) scales with F.  Gathers: per 4-slot
+// batch, T LDGSTS.128 per lane — lane (g, j) copies bytes 128t + 16j .. of
+// slot p0 + g, zero-filled past the row's bytes (only group T-1 is partial).
+// The LUT layout, metadata pipeline and balanced row ranges are the batch
+// kernel's (DEC 0, SCHED 2); each output element is the same slot-order
+// FMUL/FADD chain, so the results are bit-identical to it.
+// ---------------------------------------------------------------------------
+template <int T, int C, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+spmm_q8_wide_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restrict__ scol,
+                    const float* __restrict__ sval, uint64_t n_rows, const unsigned char* __restrict__ q,
+                    uint32_t ldq, uint32_t f4, float4* __restrict__ c, uint64_t ldc4,
+                    const float* __restrict__ lut_g) {
+    static_assert(T >= 2 && T <= 8 && C % 4 == 0 && C >= 8 && C <= 16, "wide ring shape");
+    constexpr int B = C / 4;               // batches per ring round
+    constexpr uint32_t RS = 128 * T;       // ring slot stride (one whole code row)
+    constexpr uint32_t kEndsBytes = 144;   // 33 row ends per warp
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    for (int i = threadIdx.x; i < 256 * 32; i += WARPS * 32)
+        reinterpret_cast<float*>(smem_raw)[(i >> 5) * 64 + (i & 31)] = lut_g[i >> 5];
+    __syncthreads();
+
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t smem0 = smem_addr(smem_raw);
+    if ((smem0 & 0xFFFFFFu) != kDynSmemOffset) __trap();  // see dyn_smem_offset_ok
+    const uint32_t lane4 = pin_u32((smem0 & 0xFF000000u) | (lane * 4));
+    const uint32_t meta0 = pin_u32(smem0 + 65536 + warp * (32 * C));
+    const uint32_t ends0 = smem0 + 65536 + WARPS * 32 * C + warp * kEndsBytes;
+    const uint32_t ring0 = smem0 + 65536 + WARPS * (32 * C + kEndsBytes) + warp * (C * RS);
+    const uint32_t rd0 = pin_u32(ring0 + lane * 4);
+    const uint32_t wr0 = pin_u32(ring0 + (lane >> 3) * RS + (lane & 7) * 16);
+    const uint32_t mcol = pin_u32(meta0 + (lane >> 3) * 4);
+    const uint32_t tl = pin_u32(lane >> 3);
+    const unsigned char* qlane = pin_ptr(q + (lane & 7) * 16);
+    // bytes this lane copies of group T-1 (groups < T-1 are whole)
+    const uint32_t offl = 128 * (T - 1) + (lane & 7) * 16, rowb = f4 * 4;
+    const uint32_t nbl = rowb > offl ? min(16u, rowb - offl) : 0u;
+    const bool stl = 32 * (T - 1) + lane < f4;  // this lane stores group T-1
+
+    uint64_t rb, re;
+    bal_range(srow, n_rows, (uint64_t)blockIdx.x * WARPS + warp, (uint64_t)gridDim.x * WARPS, rb, re);
+    while (rb < re) {
+        // slices with 32-bit slot offsets (one slice at the BASELINE shapes)
+        const uint64_t re1 = srow[re] - srow[rb] >= (1ull << 31) ? rb + 1 : re;
+        const uint64_t g0 = srow[rb];
+        const uint32_t total = (uint32_t)(srow[re1] - g0);
+        const uint32_t nrows = (uint32_t)(re1 - rb);
+        const uint64_t* rend = srow + rb + 1;  // end of row rb + i at rend[i]
+        auto window = [&](uint32_t w) -> uint32_t { return (uint32_t)(rend[min(w + lane, nrows - 1)] - g0); };
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(ends0 + lane * 4), "r"(window(0)) : "memory");
+        __syncwarp();
+
+        // metadata of round k -> buffer k & 3 (lanes 0..C-1: cols, 16..16+C-1: vals)
+        const char* const mbase = lane < 16 ? reinterpret_cast<const char*>(scol + g0 + (lane & 15))
+                                            : reinterpret_cast<const char*>(sval + g0 + (lane & 15));
+        const uint32_t mdst = meta0 + (lane >> 4) * (4 * C) + (lane & 15) * 4;
+        auto issue_meta = [&](uint32_t k) {
+            const uint32_t i = lane & 15, s = k * C + i;
+            if (i < (uint32_t)C && s < total)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(mdst + (k & 3) * (8 * C)),
+                             "l"(mbase + (uint64_t)(k * C) * 4)
+                             : "memory");
+        };
+        auto issue = [&](int p0, uint32_t k) {
+            if (k * C + p0 + tl < total) {
+                const uint32_t col = lds_u32(mcol + (k & 3) * (8 * C) + p0 * 4);
+                const unsigned char* src = qlane + (uint64_t)col * ldq;
+                const uint32_t dst = wr0 + p0 * RS;
+#pragma unroll
+                for (int t = 0; t < T - 1; ++t)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 128 * t),
+                                 "l"(src + 128 * t)
+                                 : "memory");
+                if (nbl != 0)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst + 128 * (T - 1)),
+                                 "l"(src + 128 * (T - 1)), "r"(nbl)
+                                 : "memory");
+            }
+        };
+        issue_meta(0);
+        issue_meta(1);
+        cp_commit();
+        cp_wait<0>();
+        __syncwarp();
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            issue(4 * b, 0);
+            cp_commit();
+        }
+
+        float4 acc[T];
+#pragma unroll
+        for (int t = 0; t < T; ++t) acc[t] = f4_zero();
+        uint32_t ri = 0;  // next row to store (relative to rb)
+        uint32_t wi = 0;  // its index in the window
+        uint32_t row_end = lds_u32(ends0);
+        float4* cptr = c + rb * ldc4 + lane;  // rows are stored in order: a running pointer
+        auto store_row = [&]() {
+#pragma unroll
+            for (int t = 0; t < T - 1; ++t) __stcs(cptr + 32 * t, acc[t]);
+            if (stl) __stcs(cptr + 32 * (T - 1), acc[T - 1]);
+            cptr += ldc4;
+#pragma unroll
+            for (int t = 0; t < T; ++t) acc[t] = f4_zero();
+        };
+        auto advance_rows = [&](uint32_t pos) {
+            do {
+                store_row();
+                ++ri;
+                if (++wi == 32) {  // enter the next 32-row window of row ends
+                    wi = 0;
+                    const uint32_t e = window(ri);
+                    __syncwarp();
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(ends0 + lane * 4), "r"(e) : "memory");
+                    __syncwarp();
+                }
+                row_end = lds_u32(ends0 + wi * 4);
+            } while (ri < nrows && row_end == pos);
+        };
+        if (row_end == 0) advance_rows(0);
+
+        auto consume = [&](int p, float v) {
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+                const uint32_t r = lds_u32(rd0 + p * RS + 128 * t);
+                const float d0 = lds_lut(__byte_perm(r, lane4, 0x7604u));
+                const float d1 = lds_lut(__byte_perm(r, lane4, 0x7614u));
+                const float d2 = lds_lut(__byte_perm(r, lane4, 0x7624u));
+                const float d3 = lds_lut(__byte_perm(r, lane4, 0x7634u));
+                add2_rn(acc[t].x, acc[t].y, __fmul_rn(v, d0), __fmul_rn(v, d1));
+                add2_rn(acc[t].z, acc[t].w, __fmul_rn(v, d2), __fmul_rn(v, d3));
+            }
+        };
+
+        // positions past `total` (last round only) accumulate garbage after
+        // the range's last row was stored — never written
+        for (uint32_t k = 0, t0 = 0; t0 < total; t0 += C, ++k) {
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                cp_wait<B - 1>();
+                __syncwarp();  // other lanes' copies of these four slots are visible
+                float4 v4;
+                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                             : "=f"(v4.x), "=f"(v4.y), "=f"(v4.z), "=f"(v4.w)
+                             : "r"(meta0 + (k & 3) * (8 * C) + 4 * C + 16 * b));
+                const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+                if (row_end > t0 + 4 * b + 4) {  // no row ends in this batch
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) consume(4 * b + u, vv[u]);
+                } else {
+                    const uint32_t base = t0 + 4 * b + 1;
+                    uint32_t rel = row_end - base;  // the row ends after slot 4b + rel
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        consume(4 * b + u, vv[u]);
+                        if (rel == (uint32_t)u) {
+                            advance_rows(base + u);
+                            rel = row_end - base;
+                        }
+                    }
+                }
+                __syncwarp();  // every lane is done reading these slots
+                if (b == 0) issue_meta(k + 2);
+                issue(4 * b, k + 1);
+                cp_commit();
+            }
+        }
+        cp_wait<0>();
+        for (; ri < nrows; ++ri) store_row();  // (only when the range has no slots)
+        __syncwarp();  // the next slice reuses this warp's ring, metadata and row ends
+        rb = re1;
+    }
+}
+
+template <int T, int C, int WARPS>
+int launch_q8_wide_t(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, const uint8_t* q,
+                     uint64_t ldq, uint32_t f4, float4* c, uint64_t ldc4, const float* lut, cudaStream_t st) {
+    const size_t smem = 256 * 256 + (size_t)WARPS * (32 * C + 144 + C * 128 * T);
+    static int occ_dev[kMaxDevices] = {};
+    int& occ = occ_dev[cur_device()];
+    if (occ == 0) {
+        AES_CUDA_TRY(cudaFuncSetAttribute(spmm_q8_wide_kernel<T, C, WARPS>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        AES_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmm_q8_wide_kernel<T, C, WARPS>,
+                                                                   WARPS * 32, smem));
+        if (occ < 1) occ = 1;
+    }
+    // one balanced wave (the 64 KB table filled once per CTA); small graphs
+    // keep at least 8 rows per warp
+    uint64_t grid = (uint64_t)num_sms() * occ;
+    const uint64_t cap = (n + (uint64_t)WARPS * 8 - 1) / ((uint64_t)WARPS * 8);
+    if (cap < grid) grid = cap ? cap : 1;
+    spmm_q8_wide_kernel<T, C, WARPS><<<(unsigned)grid, WARPS * 32, smem, st>>>(srow, scol, sval, n, q, (uint32_t)ldq,
+                                                                               f4, c, ldc4, lut);
+    AES_CUDA_TRY(cudaGetLastError());
+    return AES_OK;
+}
+
+// F in (128, 1024] codes: T = ceil(F / 128) groups per lane
+template <int C, int WARPS>
+int launch_q8_wide(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, const uint8_t* q,
+                   uint64_t ldq, uint32_t f4, float4* c, uint64_t ldc4, const float* lut, cudaStream_t st) {
+    switch ((f4 + 31) / 32) {
+        case 2: return launch_q8_wide_t<2, C, WARPS>(srow, scol, sval, n, q, ldq, f4, c, ldc4, lut, st);
+        case 3: return launch_q8_wide_t<3, C, WARPS>(srow, scol, sval, n, q, ldq, f4, c, ldc4, lut, st);
+        case 4: return launch_q8_wide_t<4, C, WARPS>(srow, scol, sval, n, q, ldq, f4, c, ldc4, lut, st);
+        case 5: return launch_q8_wide_t<5, C, WARPS>(srow, scol, sval, n, q, ldq, f4, c, ldc4, lut, st);
+        default: return AES_ERR_UNSUPPORTED;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // dispatch
 // ---------------------------------------------------------------------------
 int g_spmm_variant = 0;          // 0 = auto; see aes_dev_spmm_set_variant
@@ -2281,6 +2501,17 @@ int aes_dev_spmm_q8_ex(const uint64_t* srow_ptr, const uint32_t* scol, const flo
         f4 / 32 < 65535) {
         float4* c4 = reinterpret_cast<float4*>(c);
         const uint32_t f4u = (uint32_t)f4;
+        // 128 < F <= 640: one warp per whole code row (spmm_q8_wide_kernel)
+        if ((v == 0 || (v >= 46 && v <= 49)) && f4u > 32 && f4u <= 160) {
+            int rc;
+            switch (v) {
+                case 46: rc = launch_q8_wide<16, 12>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st); break;
+                case 48: rc = launch_q8_wide<12, 20>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st); break;
+                case 49: rc = launch_q8_wide<8, 16>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st); break;
+                default: rc = launch_q8_wide<12, 16>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st); break;
+            }
+            if (rc != AES_ERR_UNSUPPORTED) return rc;
+        }
         switch (v) {
             case 30: return launch_q8_batch<16, 16>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st, dyn);
             case 31: return launch_q8_batch<8, 16>(srow_ptr, scol, sval, n_rows, q, ldq, f4u, c4, ldc / 4, lut, st, dyn);

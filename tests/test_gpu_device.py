@@ -264,6 +264,35 @@ def test_q8_schedules_bit_exact(dev, sched, f):
     assert np.array_equal(bits(to_np(sampled)), bits(port.spmm_sampled(rp, col, val, deq, 32)))
 
 
+@pytest.mark.parametrize("variant", [0, 46, 48, 49, 30, 34])
+@pytest.mark.parametrize("f", [132, 200, 256, 300, 384, 511, 602, 640])
+def test_q8_wide_rows_bit_exact(dev, variant, f):
+    """int8 on rows wider than one 128-code tile: the wide-row kernel (one
+    warp per whole code row; default for 128 < F <= 640, variants 46/48/49)
+    and the batch kernel's column tiles (variants 30/34), exact (unbounded
+    hub rows) and sampled, every partial last group width."""
+    import torch
+
+    from paper_2503_18427_b200 import capi
+    L = capi.lib()
+    rp, col, val = graphs.power_law(7000, alpha=1.3, max_deg=5000, seed=f)
+    g = dev.Graph.from_numpy(rp, col, val)
+    x_np = np.random.default_rng(f).uniform(-1, 1, (7000, f)).astype(np.float32)
+    q = dev.quantize(torch.from_numpy(x_np).cuda())
+    lo, hi = port.fit_params(x_np)
+    deq = port.dequantize(port.quantize(x_np, lo, hi), lo, hi)
+    plan = dev.SampledPlan(g, 32)
+    try:
+        L.aes_dev_spmm_set_variant(variant)
+        exact = dev.spmm_q8(g.row_ptr, g.col, g.val, q)
+        sampled = dev.spmm_q8(plan.srow_ptr, plan.scol, plan.sval, q, max_row_slots=plan.row_bound)
+        torch.cuda.synchronize()
+    finally:
+        L.aes_dev_spmm_set_variant(0)
+    assert np.array_equal(bits(to_np(exact)), bits(port.spmm_csr(rp, col, val, deq)))
+    assert np.array_equal(bits(to_np(sampled)), bits(port.spmm_sampled(rp, col, val, deq, 32)))
+
+
 @pytest.mark.parametrize("f", [40, 128])
 def test_sharded_gcn_int8_exchange_cuda_ops(dev, f):
     """ShardedGCN(exchange_dtype="int8") on the CUDA ops (device fit_params,
