@@ -683,7 +683,7 @@ int aes_dev_spmm_q8_affine(const uint64_t* srow_ptr, const uint32_t* scol, const
     // LDS + 2 FMUL); with several tiles or fewer rows the batch kernel wins
     // (reddit 0.496 vs 0.593, arxiv 0.034 vs 0.058, pubmed 0.017 vs 0.029)
     const bool row_ring = mode == AES_QAFFINE_ROW && f <= 128 && n_rows >= (1u << 20);
-    if ((v == 0 || v == 55) && n_rows < (1ull << 31) && !(row_ring && v == 0)) {
+    if ((v == 0 || (v >= 55 && v <= 57)) && n_rows < (1ull << 31) && !(row_ring && v == 0)) {
         const int s = mode == AES_QAFFINE_FEATURE
                           ? launch_q8_feature_batch(srow_ptr, scol, sval, n_rows, q, ldq, f, p2, c, ldc, st)
                           : launch_q8_row_batch(srow_ptr, scol, sval, n_rows, q, ldq, f, p2, c, ldc, st);

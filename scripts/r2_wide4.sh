@@ -1,0 +1,19 @@
+#!/bin/bash
+# wide-row int8 kernel: ring / warp tuning for exact and fast modes + parity
+cd ${GRAFT_REPO_ROOT:-.}
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_device.py tests/test_gpu_affine.py -m gpu -q -x -k "wide or q8_schedules or every_spmm or affine or feature" 2>&1 | tail -3
+for w in 32 64; do
+  for v in 0 46 48 49; do
+    timeout 300 python bench.py --config reddit --width $w --dtype int8 --variant $v --no-cpu-baseline --no-e2e --no-layer --steps 20 --warmup 5 > /tmp/b.json 2>/tmp/b.err
+    python -c "import json;d=json.load(open('/tmp/b.json'));print('reddit W$w int8 v$v', d['ms_per_step'], d['roofline']['frac'], d['gpu_launches_per_step']['kernels'])" 2>/dev/null || tail -3 /tmp/b.err
+  done
+  for dt in int8-feature int8-row; do for v in 0 56 57; do
+    timeout 300 python bench.py --config reddit --width $w --dtype $dt --variant $v --no-cpu-baseline --no-e2e --no-layer --steps 20 --warmup 5 > /tmp/b.json 2>/tmp/b.err
+    python -c "import json;d=json.load(open('/tmp/b.json'));print('reddit W$w $dt v$v', d['ms_per_step'], d['roofline']['frac'], d['gpu_launches_per_step']['kernels'])" 2>/dev/null || tail -3 /tmp/b.err
+  done; done
+done
+timeout 300 python bench.py --config reddit --dtype int8 --no-layer > gpurun_out/r02_bench_reddit_int8.json 2>gpurun_out/r02_bench_reddit_int8.err
+bash scripts/ncu_capture.sh q8wide "spmm_q8_wide" 2 1 -- python bench.py --config reddit --dtype int8 --steps 2 --warmup 2 --no-e2e --no-cpu-baseline --no-layer
+python scripts/ncu_raw_summary.py gpurun_out/ncu_q8wide_raw.csv --json > gpurun_out/ncu_q8wide_summary.json
+head -c 1500 gpurun_out/ncu_q8wide_summary.json

@@ -147,7 +147,7 @@ def test_affine_handle_api(dev):
 
 
 @pytest.mark.parametrize("mode", ["feature", "row"])
-@pytest.mark.parametrize("f", [128, 130, 602])
+@pytest.mark.parametrize("f", [128, 130, 300, 602, 640])
 def test_feature_batch_kernel_equals_ring_kernel(dev, f, mode):
     """The per-feature affine decode runs in the batch kernel by default
     (spmm.cu, DEC 1) and in the cp.async ring kernel as variant 54: the same
@@ -167,7 +167,16 @@ def test_feature_batch_kernel_equals_ring_kernel(dev, f, mode):
     try:
         L.aes_dev_spmm_set_variant(54)
         ring = dev.spmm_q8_affine(plan.srow_ptr, plan.scol, plan.sval, q)
+        L.aes_dev_spmm_set_variant(55)  # batch kernel as 128-code column tiles
+        tiles = dev.spmm_q8_affine(plan.srow_ptr, plan.scol, plan.sval, q)
+        wide = []
+        for v in (56, 57):  # wide-row kernel (one warp per whole code row, F > 128), 8- / 12-slot rings
+            L.aes_dev_spmm_set_variant(v)
+            wide.append(dev.spmm_q8_affine(plan.srow_ptr, plan.scol, plan.sval, q))
         torch.cuda.synchronize()
     finally:
         L.aes_dev_spmm_set_variant(0)
     assert torch.equal(got.view(torch.int32), ring.view(torch.int32))
+    assert torch.equal(tiles.view(torch.int32), ring.view(torch.int32))
+    for w in wide:
+        assert torch.equal(w.view(torch.int32), ring.view(torch.int32))
