@@ -303,9 +303,13 @@ AES_API int aes_dev_spmm_f32_ex(const uint64_t* srow_ptr, const uint32_t* scol, 
                                 uint64_t n_rows, const float* b, uint64_t ldb, uint64_t f, float* c,
                                 uint64_t ldc, uint64_t max_row_slots, void* stream);
 
-/* Kernel-schedule override for F <= 128 (tuning/benchmarks; 0 = default):
+/* Kernel-schedule override (tuning/benchmarks; 0 = default).  fp32, F <= 128:
  * 1 register-staged batches, 2..8 shared-memory cp.async rings of different
- * depth x warps-per-CTA.  Results are bit-identical for every variant. */
+ * depth x warps-per-CTA.  int8: 21-24 dual-stream, 30-45 batch kernel ring x
+ * warps (F > 128 as 128-code column tiles), 40 TMA gather, 46/48/49 wide-row
+ * kernel ring x warps (128 < F <= 640; the default there), 50-57 fast-mode
+ * kernels (55 column tiles, 56/57 wide-row).  Results are bit-identical for
+ * every variant. */
 AES_API int aes_dev_spmm_set_variant(int variant);
 /* Row-group schedule of the SpMM kernels: 1 = static (warp w takes row
  * group w), 2 = heavy-first dynamic (groups with > 4096 slots first, then
