@@ -1606,6 +1606,7 @@ spmm_q8_wide_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restric
     static_assert(T >= 2 && T <= 8 && C % 4 == 0 && C >= 8 && C <= 16, "wide ring shape");
     constexpr int B = C / 4;               // batches per ring round
     constexpr uint32_t RS = 128 * T;       // ring slot stride (one whole code row)
+    constexpr bool kRolledEnds = true;     // batches holding a row end: rolled slot loop
     constexpr uint32_t kEndsBytes = 144;   // 33 row ends per warp
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (DEC == 0) {
@@ -1798,10 +1799,10 @@ spmm_q8_wide_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restric
                 if (row_end > t0 + 4 * b + 4) {  // no row ends in this batch
 #pragma unroll
                     for (int u = 0; u < 4; ++u) consume(4 * b + u, vv[u]);
-                } else if (DEC == 1) {
-                    // rolled: the per-feature epilogue in advance_rows is
-                    // large, so one copy per batch instead of four keeps the
-                    // kernel inside the instruction cache
+                } else if (kRolledEnds) {
+                    // rolled: advance_rows (the per-feature epilogue above
+                    // all) is inlined once per batch instead of four times,
+                    // which keeps the kernel inside the instruction cache
                     const uint32_t base = t0 + 4 * b + 1;
                     uint32_t rel = row_end - base;
                     const uint32_t va = meta0 + (k & 3) * (8 * C) + 4 * C + 16 * b;
@@ -2472,11 +2473,12 @@ int launch_q8_feature_batch(const uint64_t* srow, const uint32_t* scol, const fl
     if (f4 <= 16 || ldq % 16 != 0 || (uintptr_t)q % 16 != 0 || ldc % 4 != 0 || (uintptr_t)c % 16 != 0 ||
         f4 / 32 >= 65535 || f > 0xffffffffull)
         return AES_ERR_UNSUPPORTED;
-    // 128 < F <= 640, variants 56 / 57: one warp per whole code row.  Opt-in
-    // only: reddit W=32 0.557 / 0.993 ms vs 0.440 as column tiles (the
-    // per-feature epilogue, inlined at every row-end position of the unrolled
-    // batches, pushes the kernel out of the instruction cache)
-    if (f4 > 32 && f4 <= 160 && (g_spmm_variant == 56 || g_spmm_variant == 57))
+    // 128 < F <= 640: one warp per whole code row, 12-slot rings (variant 56:
+    // 8-slot; 55: the batch kernel's column tiles).  reddit W=32 0.440 ->
+    // 0.394 ms, W=64 0.662 -> 0.532 (with the row-end batches rolled: inlined
+    // at every row-end position, the per-feature epilogue had pushed the
+    // kernel out of the instruction cache, 0.557 / 0.993 ms)
+    if (f4 > 32 && f4 <= 160 && (g_spmm_variant == 0 || g_spmm_variant == 56 || g_spmm_variant == 57))
         return g_spmm_variant == 56
                    ? launch_q8_wide<8, 16, 1>(srow, scol, sval, n, q, ldq, (uint32_t)f4, reinterpret_cast<float4*>(c),
                                                 ldc / 4, nullptr, st, params, (uint32_t)f)

@@ -63,7 +63,7 @@ def test_exact_kernels_never_fuse_multiply_add():
         pytest.skip("cuobjdump missing")
     funcs = _sass_by_function()
     crit = [f for f in funcs if re.search(r"spmm|gemm|gcn_layer_fused|dequantize_kernel|(?<!fold_params_)lut_kernel|gcn_fill", f)
-            and not re.search(r"q8a|q8r|affine|q8t_kernelILi1E|q8_batch_kernel\w*ELi[12]EEEv", f)]  # int8 fast mode: bounded, not exact
+            and not re.search(r"q8a|q8r|affine|q8t_kernelILi1E|q8_(?:batch|wide)_kernel\w*ELi[12]EEEv", f)]  # int8 fast mode: bounded, not exact
     assert len(crit) >= 10
     # (HFMA2.MMA with RZ operands is ptxas's move-immediate idiom, not arithmetic)
     bad = {f: sorted(set(re.findall(r"\b(FFMA2?|DFMA)\b", "\n".join(funcs[f])))) for f in crit}
@@ -72,7 +72,7 @@ def test_exact_kernels_never_fuse_multiply_add():
     # the gather kernels really do stage through cp.async (LDGSTS)
     assert any("LDGSTS" in "\n".join(funcs[f]) for f in crit if "ring" in f)
     # and the fast mode does use packed FMAs (2 instructions per decoded code)
-    fast = [f for f in funcs if re.search(r"spmm_q8[ar]_|q8t_kernelILi1E|q8_batch_kernel\w*ELi[12]EEEv", f)]
+    fast = [f for f in funcs if re.search(r"spmm_q8[ar]_|q8t_kernelILi1E|q8_(?:batch|wide)_kernel\w*ELi[12]EEEv", f)]
     assert fast and all(re.search(r"\bFFMA2\b", "\n".join(funcs[f])) for f in fast)
 
 
