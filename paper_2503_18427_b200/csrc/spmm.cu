@@ -1603,7 +1603,7 @@ spmm_q8_wide_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restric
                     const float* __restrict__ lut_g, const float2* __restrict__ fparams = nullptr,
                     uint32_t fcols = 0) {
     static_assert(DEC >= 0 && DEC <= 2, "wide kernel decodes: global table, per-feature or per-row affine");
-    static_assert(T >= 2 && T <= 8 && C % 4 == 0 && C >= 8 && C <= 16, "wide ring shape");
+    static_assert(T >= 1 && T <= 8 && C % 4 == 0 && C >= 8 && C <= 16, "wide ring shape");
     constexpr int B = C / 4;               // batches per ring round
     constexpr uint32_t RS = 128 * T;       // ring slot stride (one whole code row)
     constexpr bool kRolledEnds = true;     // batches holding a row end: rolled slot loop
@@ -1873,6 +1873,7 @@ int launch_q8_wide(const uint64_t* srow, const uint32_t* scol, const float* sval
                    uint64_t ldq, uint32_t f4, float4* c, uint64_t ldc4, const float* lut, cudaStream_t st,
                    const float2* fparams = nullptr, uint32_t fcols = 0) {
     switch ((f4 + 31) / 32) {
+        case 1: return launch_q8_wide_t<1, C, WARPS, DEC>(srow, scol, sval, n, q, ldq, f4, c, ldc4, lut, st, fparams, fcols);
         case 2: return launch_q8_wide_t<2, C, WARPS, DEC>(srow, scol, sval, n, q, ldq, f4, c, ldc4, lut, st, fparams, fcols);
         case 3: return launch_q8_wide_t<3, C, WARPS, DEC>(srow, scol, sval, n, q, ldq, f4, c, ldc4, lut, st, fparams, fcols);
         case 4: return launch_q8_wide_t<4, C, WARPS, DEC>(srow, scol, sval, n, q, ldq, f4, c, ldc4, lut, st, fparams, fcols);
@@ -2478,7 +2479,7 @@ int launch_q8_feature_batch(const uint64_t* srow, const uint32_t* scol, const fl
     // 0.394 ms, W=64 0.662 -> 0.532 (with the row-end batches rolled: inlined
     // at every row-end position, the per-feature epilogue had pushed the
     // kernel out of the instruction cache, 0.557 / 0.993 ms)
-    if (f4 > 32 && f4 <= 160 && (g_spmm_variant == 0 || g_spmm_variant == 56 || g_spmm_variant == 57))
+    if (f4 <= 160 && ((f4 > 32 && g_spmm_variant == 0) || g_spmm_variant == 56 || g_spmm_variant == 57))
         return g_spmm_variant == 56
                    ? launch_q8_wide<8, 16, 1>(srow, scol, sval, n, q, ldq, (uint32_t)f4, reinterpret_cast<float4*>(c),
                                                 ldc / 4, nullptr, st, params, (uint32_t)f)
@@ -2499,7 +2500,7 @@ int launch_q8_row_batch(const uint64_t* srow, const uint32_t* scol, const float*
     // 128 < F <= 640: one warp per whole code row, 12-slot rings (variant 56:
     // 8-slot; 55: the batch kernel's column tiles).  reddit W=32 0.506 ->
     // 0.327 ms, W=64 0.775 -> 0.483
-    if (f4 > 32 && f4 <= 160 && (g_spmm_variant == 0 || g_spmm_variant == 56 || g_spmm_variant == 57))
+    if (f4 <= 160 && ((f4 > 32 && g_spmm_variant == 0) || g_spmm_variant == 56 || g_spmm_variant == 57))
         return g_spmm_variant == 56
                    ? launch_q8_wide<8, 16, 2>(srow, scol, sval, n, q, ldq, (uint32_t)f4, reinterpret_cast<float4*>(c),
                                                 ldc / 4, nullptr, st, params, (uint32_t)f)
@@ -2607,7 +2608,8 @@ int aes_dev_spmm_q8_ex(const uint64_t* srow_ptr, const uint32_t* scol, const flo
         float4* c4 = reinterpret_cast<float4*>(c);
         const uint32_t f4u = (uint32_t)f4;
         // 128 < F <= 640: one warp per whole code row (spmm_q8_wide_kernel)
-        if ((v == 0 || (v >= 46 && v <= 49)) && f4u > 32 && f4u <= 160) {
+        // (variants 46/48/49 also take one-tile rows, 64 < F <= 128: tuning)
+        if (((v == 0 && f4u > 32) || (v >= 46 && v <= 49)) && f4u <= 160) {
             int rc;
             switch (v) {
                 // measured on reddit W=32: 8-slot rings x 16 warps 0.431 ms;

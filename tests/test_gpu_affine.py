@@ -147,7 +147,7 @@ def test_affine_handle_api(dev):
 
 
 @pytest.mark.parametrize("mode", ["feature", "row"])
-@pytest.mark.parametrize("f", [128, 130, 300, 602, 640])
+@pytest.mark.parametrize("f", [100, 128, 130, 300, 602, 640])
 def test_feature_batch_kernel_equals_ring_kernel(dev, f, mode):
     """The per-feature affine decode runs in the batch kernel by default
     (spmm.cu, DEC 1) and in the cp.async ring kernel as variant 54: the same

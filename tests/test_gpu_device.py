@@ -63,7 +63,7 @@ def test_row_shards_equal_global(dev):
 @pytest.mark.parametrize("f", [72, 100, 128, 130, 256, 602])
 def test_device_q8(dev, f):
     """Device int8 path; F > 64 with 16-B aligned code rows runs the batch
-    kernel (128-code column tiles when F > 128)."""
+    kernel, F > 128 the wide-row kernel (one warp per whole code row)."""
     import torch
     rp, col, val = graphs.power_law(3000, alpha=1.5, max_deg=2000, seed=2)
     g = dev.Graph.from_numpy(rp, col, val)
@@ -265,7 +265,7 @@ def test_q8_schedules_bit_exact(dev, sched, f):
 
 
 @pytest.mark.parametrize("variant", [0, 46, 48, 49, 30, 34])
-@pytest.mark.parametrize("f", [132, 200, 256, 300, 384, 511, 602, 640])
+@pytest.mark.parametrize("f", [100, 128, 132, 200, 256, 300, 384, 511, 602, 640])
 def test_q8_wide_rows_bit_exact(dev, variant, f):
     """int8 on rows wider than one 128-code tile: the wide-row kernel (one
     warp per whole code row; default for 128 < F <= 640, variants 46/48/49)
