@@ -1592,7 +1592,7 @@ int launch_q8_batch(const uint64_t* srow, const uint32_t* scol, const float* sva
 // kernel's (SCHED 2); each output element is the same slot-order FMUL/FADD
 // chain, so the results are bit-identical to it.  DEC 1 (int8 FAST MODE,
 // per-feature codes) is the batch kernel's table-free decode and affine
-// epilogue, (s_j, m_j) read at each row store; DEC 2 (per-row codes) stages
+// epilogue, (s_j, m_j) staged in shared memory once per CTA; DEC 2 (per-row codes) stages
 // the gathered rows' (s, m) next to the slot metadata — again the same bits.
 // ---------------------------------------------------------------------------
 template <int T, int C, int WARPS, int DEC = 0>
@@ -1624,6 +1624,15 @@ spmm_q8_wide_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restric
     const uint32_t ring0 = smem0 + 65536 + WARPS * (32 * C + kEndsBytes) + warp * (C * RS);
     // DEC 2: the gathered rows' (s, m) pairs, 4 rounds x C slots x 8 B per warp
     const uint32_t par0 = smem0 + 65536 + WARPS * (32 * C + kEndsBytes + C * RS) + warp * (32 * C);
+    // DEC 1: (s_j, m_j) of every column, staged once per CTA (zero past F)
+    constexpr uint32_t kFparOff = 65536 + WARPS * (32 * C + kEndsBytes + C * RS);
+    const uint32_t fpar0 = smem0 + kFparOff;
+    if (DEC == 1) {
+        float2* fp = reinterpret_cast<float2*>(smem_raw + kFparOff);
+        for (uint32_t j = threadIdx.x; j < 128 * T; j += WARPS * 32)
+            fp[j] = j < fcols ? fparams[j] : make_float2(0.f, 0.f);
+        __syncthreads();
+    }
     const uint32_t rd0 = pin_u32(ring0 + lane * 4);
     const uint32_t wr0 = pin_u32(ring0 + (lane >> 3) * RS + (lane & 7) * 16);
     const uint32_t mcol = pin_u32(meta0 + (lane >> 3) * 4);
@@ -1710,14 +1719,12 @@ spmm_q8_wide_kernel(const uint64_t* __restrict__ srow, const uint32_t* __restric
             if (DEC == 2)
                 return make_float4(__fadd_rn(acc[t].x, bs), __fadd_rn(acc[t].y, bs), __fadd_rn(acc[t].z, bs),
                                    __fadd_rn(acc[t].w, bs));
-            float sj[4], mj[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t j = 128 * t + 4 * lane + u;
-                const float2 pj = j < fcols ? __ldg(fparams + j) : make_float2(0.f, 0.f);
-                sj[u] = pj.x;
-                mj[u] = pj.y;
-            }
+            float sj[4], mj[4];  // (s, m) of columns 128t + 4 lane .. + 3: two LDS.128
+            const uint32_t pa = fpar0 + (128 * t + 4 * lane) * 8;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(sj[0]), "=f"(mj[0]), "=f"(sj[1]), "=f"(mj[1]) : "r"(pa));
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(sj[2]), "=f"(mj[2]), "=f"(sj[3]), "=f"(mj[3]) : "r"(pa + 16));
             const float4& a = acc[t];
             return make_float4(fmaf(sj[0], a.x, mj[0] * bs), fmaf(sj[1], a.y, mj[1] * bs),
                                fmaf(sj[2], a.z, mj[2] * bs), fmaf(sj[3], a.w, mj[3] * bs));
@@ -1846,7 +1853,8 @@ template <int T, int C, int WARPS, int DEC>
 int launch_q8_wide_t(const uint64_t* srow, const uint32_t* scol, const float* sval, uint64_t n, const uint8_t* q,
                      uint64_t ldq, uint32_t f4, float4* c, uint64_t ldc4, const float* lut, cudaStream_t st,
                      const float2* fparams, uint32_t fcols) {
-    const size_t smem = 256 * 256 + (size_t)WARPS * (32 * C + 144 + C * 128 * T + (DEC == 2 ? 32 * C : 0));
+    const size_t smem = 256 * 256 + (size_t)WARPS * (32 * C + 144 + C * 128 * T + (DEC == 2 ? 32 * C : 0)) +
+                        (DEC == 1 ? (size_t)128 * T * 8 : 0);  // (+ the staged per-feature params)
     static int occ_dev[kMaxDevices] = {};
     int& occ = occ_dev[cur_device()];
     if (occ == 0) {
