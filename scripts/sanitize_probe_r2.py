@@ -2,8 +2,10 @@
 the fused GCN layer (plain and with the replica-broadcast epilogue + arrivals;
 its mbarrier hand-off between producer and consumer warps), the int8 batch
 kernel in its 32-warp / balanced form and its per-feature affine decode,
-the cooperative row scan (grid barrier) and the pinned staging ring of the
-handle tier (pageable host buffers).
+the cooperative row scan (grid barrier), the pinned staging ring of the
+handle tier (pageable host buffers) and the wide-row int8 kernel (F = 602:
+exact, per-feature and per-row decodes; cross-lane ring reads after
+__syncwarp).
 
     compute-sanitizer --tool racecheck python scripts/sanitize_probe_r2.py
 """
@@ -48,8 +50,9 @@ def main():
         q = device.quantize(xb)
         device.spmm_q8(plan.srow_ptr, plan.scol, plan.sval, q, max_row_slots=32)
         device.spmm_q8(g.row_ptr, g.col, g.val, q)  # exact: one balanced wave
-        qa = device.quantize_affine(xb, "feature")
-        device.spmm_q8_affine(plan.srow_ptr, plan.scol, plan.sval, qa)
+        for mode in ("feature", "row"):  # F = 602: the wide-row kernel (all three decodes)
+            qa = device.quantize_affine(xb, mode)
+            device.spmm_q8_affine(plan.srow_ptr, plan.scol, plan.sval, qa)
     # handle tier, pageable buffers above the 4 MB staging threshold
     a = m.CsrMatrix(n, n, rp, col, val)
     ps = m.build_plan_set(a, 32)
