@@ -508,3 +508,42 @@ def test_gemm_fused_fit_matches_fit_params(dev, m, k, n):
     out, res = dev.gemm_bias_act_fit(a, w2, b, False, finite_w=False)
     torch.cuda.synchronize()
     assert to_np(res).view(np.int32)[2] == 1  # NonFinite
+
+
+@pytest.mark.parametrize("variant", [0, 46, 49])
+@pytest.mark.parametrize("f", [300, 602])
+@pytest.mark.parametrize("degrees", [[0], [7], [0, 3], [0, 0, 5, 0, 2500, 1, 0, 33, 0, 0, 64, 65, 1200] * 3,
+                                     [0] * 40 + [9] + [0] * 40])
+def test_q8_wide_rows_edge_shapes(dev, variant, f, degrees):
+    """Wide-row int8 kernel on ragged shapes: empty rows (leading, trailing,
+    runs longer than its 32-row window of row ends), a single row, hub rows
+    next to empty ones, fewer rows than warps; exact and sampled, plus both
+    fast modes against their ring kernel (variant 54)."""
+    import torch
+
+    from paper_2503_18427_b200 import capi
+    L = capi.lib()
+    rp, col, val, n_cols = graphs.with_degrees(degrees, n_cols=3000, seed=f + len(degrees))
+    g = dev.Graph.from_numpy(rp, col, val, n_cols=n_cols)
+    x_np = np.random.default_rng(f).uniform(-1, 1, (n_cols, f)).astype(np.float32)
+    xt = torch.from_numpy(x_np).cuda()
+    q = dev.quantize(xt)
+    lo, hi = port.fit_params(x_np)
+    deq = port.dequantize(port.quantize(x_np, lo, hi), lo, hi)
+    plan = dev.SampledPlan(g, 32)
+    qa = {m_: dev.quantize_affine(xt, m_) for m_ in ("row", "feature")}
+    try:
+        L.aes_dev_spmm_set_variant(variant)
+        exact = dev.spmm_q8(g.row_ptr, g.col, g.val, q)
+        sampled = dev.spmm_q8(plan.srow_ptr, plan.scol, plan.sval, q, max_row_slots=plan.row_bound)
+        L.aes_dev_spmm_set_variant(0)
+        fast = {m_: dev.spmm_q8_affine(plan.srow_ptr, plan.scol, plan.sval, qa[m_]) for m_ in qa}
+        L.aes_dev_spmm_set_variant(54)
+        ring = {m_: dev.spmm_q8_affine(plan.srow_ptr, plan.scol, plan.sval, qa[m_]) for m_ in qa}
+        torch.cuda.synchronize()
+    finally:
+        L.aes_dev_spmm_set_variant(0)
+    assert np.array_equal(bits(to_np(exact)), bits(port.spmm_csr(rp, col, val, deq)))
+    assert np.array_equal(bits(to_np(sampled)), bits(port.spmm_sampled(rp, col, val, deq, 32)))
+    for m_ in qa:
+        assert torch.equal(fast[m_].view(torch.int32), ring[m_].view(torch.int32))
